@@ -1,0 +1,33 @@
+// ABI plumbing: version, thread-local error text, device queries.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace edgc {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int sm_count() {
+    static thread_local int cached = 0;
+    if (!cached) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || cached <= 0)
+            cached = 148;
+    }
+    return cached;
+}
+
+}  // namespace edgc
+
+extern "C" int edgc_abi_version(void) { return EDGC_ABI_VERSION; }
+
+extern "C" const char *edgc_last_error(void) { return edgc::g_err; }

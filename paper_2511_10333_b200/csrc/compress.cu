@@ -1,0 +1,773 @@
+// Low-rank compression with error feedback (compressor.py:94-151), batched
+// over a bucket set of gradient matrices, plus the (rank-averaged)
+// reconstruction (compressor.py:126-133, grad_source.py:404-408).
+//
+// One step for every matrix k (all matrices in one launch per phase):
+//   pass 1   w <- g + (w - p_res q_res^T)            (error feedback, in place)
+//            P_raw = w q_warm                         (row dots, fp64 partials
+//                                                      per column chunk)
+//   factor   P_raw = sum of chunk partials (fixed order), Gram = P_raw^T P_raw,
+//            Cholesky with MGS dead-column semantics -> T, twice (CholQR2);
+//            P = P_raw T  (== MGS(P_raw), compressor.py:74-91)
+//   pass 2   Q = w^T P                                (column sums, fp64
+//                                                      partials per row block)
+//   finalize Q = sum of row-block partials; dead columns <- fresh basis
+//            (compressor.py:113-114); q_warm <- Q
+// HBM traffic per element: pass 1 reads g, w and writes w (12 B); pass 2
+// reads w (4 B); the reconstruction writes out (4 B).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace edgc {
+namespace {
+
+struct MatDev {
+    const float *g;
+    float *w;
+    const float *p_res;
+    const float *q_res;
+    float *q_warm;
+    const float *basis;
+    float *p_out;
+    float *q_out;
+    int64_t m, n, ld_g;
+    int32_t r, r_res, ld_q, vec;
+    // scratch (workspace)
+    double *p_part;   // [nchunk1][m][r]
+    double *p_raw;    // [m][r]
+    double *q_part;   // [nblk2][n][r]
+    double *tmat;     // [r][r] combined T (column-major per column j: tmat[j*r + i])
+    int32_t *dead;    // [r]
+    int32_t nchunk1, nblk2;
+};
+
+// pass-1 / pass-2 tiles
+struct Tile {
+    int32_t mat;
+    int32_t chunk;   // column chunk index (pass 1) / row block index (pass 2)
+    int64_t slot0, slot1;  // [slot0, slot1) column slots (VEC columns each)
+    int64_t row0, row1;
+};
+
+constexpr int kP1Threads = 256;
+constexpr int kP1Rows = 64;     // rows per pass-1 tile
+constexpr int kP2Threads = 256;
+constexpr int kP2Rows = 256;    // rows per pass-2 tile (one fp64 partial per block)
+constexpr int kFactorThreads = 256;
+constexpr int kMaxRank = 32;
+
+template <int VEC> struct VecT;
+template <> struct VecT<4> {
+    typedef float4 T;
+    __device__ static float4 ld(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
+    __device__ static float4 ld_cs(const float *p) { return __ldcs(reinterpret_cast<const float4 *>(p)); }
+    __device__ static void st(float *p, const float (&v)[4]) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    __device__ static void unpack(const float4 &x, float (&v)[4]) { v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; }
+};
+template <> struct VecT<1> {
+    typedef float T;
+    __device__ static float ld(const float *p) { return __ldg(p); }
+    __device__ static float ld_cs(const float *p) { return __ldcs(p); }
+    __device__ static void st(float *p, const float (&v)[1]) { *p = v[0]; }
+    __device__ static void unpack(const float &x, float (&v)[1]) { v[0] = x; }
+};
+
+// ------------------------------------------------------------------ pass 1
+// RB rows at a time; per row the thread's VEC columns give RMAX partial dots,
+// reduced across the CTA in fp64 (butterfly within warps, fixed-order sum
+// across warps) and written as this column chunk's partial of P_raw.
+template <int VEC, int RMAX, int RB>
+__global__ void __launch_bounds__(kP1Threads) k_pass1(const MatDev *mats, const Tile *tiles, int32_t *status) {
+    constexpr int V = RB * RMAX;               // values reduced per row block
+    constexpr int VW = V < 32 ? V : 32;        // values per butterfly
+    constexpr int NB = V / VW;                 // butterflies per row block
+    constexpr int NWARP = kP1Threads / 32;
+    const Tile t = tiles[blockIdx.x];
+    const MatDev &M = mats[t.mat];
+    const int r = M.r, rr_res = M.r_res;
+    const int64_t n = M.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t slot = t.slot0 + tid;
+    const bool active = slot < t.slot1;
+    const int64_t col0 = slot * VEC;
+
+    __shared__ float s_pres[RB][RMAX];
+    __shared__ double s_red[NWARP][V];
+
+    float qw[VEC][RMAX], qr[VEC][RMAX];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v)
+#pragma unroll
+        for (int k = 0; k < RMAX; ++k) {
+            qw[v][k] = (active && k < r) ? M.q_warm[(col0 + v) * M.ld_q + k] : 0.f;
+            qr[v][k] = (active && k < rr_res) ? M.q_res[(col0 + v) * rr_res + k] : 0.f;
+        }
+    bool bad = false;
+    for (int64_t row = t.row0; row < t.row1; row += RB) {
+        __syncthreads();
+        if (tid < RB * RMAX) {
+            const int rr = tid / RMAX, k = tid % RMAX;
+            const int64_t i = row + rr;
+            s_pres[rr][k] = (k < rr_res && i < t.row1) ? M.p_res[i * rr_res + k] : 0.f;
+        }
+        __syncthreads();
+        double acc[V];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            const int64_t i = row + rr;
+            float pk[RMAX];
+#pragma unroll
+            for (int k = 0; k < RMAX; ++k) pk[k] = 0.f;
+            if (active && i < t.row1) {
+                float gv[VEC], wv[VEC];
+                VecT<VEC>::unpack(VecT<VEC>::ld_cs(M.g + i * M.ld_g + col0), gv);
+                VecT<VEC>::unpack(VecT<VEC>::ld_cs(M.w + i * n + col0), wv);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                    // residual = w - p_res q_res^T (compressor.py:112), then work = g + residual (:106)
+                    float dot = 0.f;
+#pragma unroll
+                    for (int k = 0; k < RMAX; ++k) dot = fmaf(s_pres[rr][k], qr[v][k], dot);
+                    const float x = gv[v] + (wv[v] - dot);
+                    bad |= !isfinite(x);
+                    wv[v] = x;
+#pragma unroll
+                    for (int k = 0; k < RMAX; ++k) pk[k] = fmaf(x, qw[v][k], pk[k]);
+                }
+                VecT<VEC>::st(M.w + i * n + col0, wv);
+            }
+#pragma unroll
+            for (int k = 0; k < RMAX; ++k) acc[rr * RMAX + k] = (double)pk[k];
+        }
+        // reduce acc across the CTA
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            double part[VW];
+#pragma unroll
+            for (int q = 0; q < VW; ++q) part[q] = acc[b * VW + q];
+            const double s = warp_reduce_scatter<VW>(part, lane);
+            const int owner = scatter_owner_index<VW>(lane);
+            if ((lane & ((32 / VW) - 1)) == 0) s_red[warp][b * VW + owner] = s;
+        }
+        __syncthreads();
+        if (tid < V) {
+            const int rr = tid / RMAX, k = tid % RMAX;
+            const int64_t i = row + rr;
+            if (i < t.row1 && k < r) {
+                double s = 0.0;
+#pragma unroll
+                for (int w = 0; w < NWARP; ++w) s += s_red[w][tid];
+                M.p_part[((int64_t)t.chunk * M.m + i) * r + k] = s;
+            }
+        }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
+}
+
+// ------------------------------------------------------------------ factor
+// One CTA per matrix.  Gram via per-thread (entry, row-group) sums reduced in
+// shared memory in fixed order; the r x r Cholesky runs on one thread.
+__device__ void gram_pass(const double *P, int64_t m, int r, double *s_gram, double *s_tmp) {
+    const int E = r * (r + 1) / 2;
+    const int tid = threadIdx.x;
+    for (int e0 = 0; e0 < E; e0 += kFactorThreads) {
+        const int ecount = min(E - e0, kFactorThreads);
+        const int ng = kFactorThreads / ecount;          // row groups
+        const int g = tid / ecount;
+        double acc = 0.0;
+        if (g < ng) {
+            // entry e -> (a, b), a <= b, row-major upper triangle
+            int a = 0, rem = e0 + tid % ecount;
+            while (rem >= r - a) { rem -= r - a; ++a; }
+            const int b = a + rem;
+            for (int64_t i = g; i < m; i += ng) acc += P[i * r + a] * P[i * r + b];
+        }
+        s_tmp[tid] = acc;
+        __syncthreads();
+        if (tid < ecount) {
+            double s = 0.0;
+            for (int gg = 0; gg < ng; ++gg) s += s_tmp[gg * ecount + tid];
+            int a = 0, rem = e0 + tid;
+            while (rem >= r - a) { rem -= r - a; ++a; }
+            const int b = a + rem;
+            s_gram[a * r + b] = s;
+            s_gram[b * r + a] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// Cholesky of the Gram with MGS dead-column semantics; returns T = R^{-1}
+// (dead columns zero) in s_t (column j at s_t[j*r .. j*r+r)).
+__device__ void chol_inverse(const double *s_gram, int r, double tol, int32_t *dead, double *s_R, double *s_t,
+                             bool detect) {
+    for (int j = 0; j < r; ++j) {
+        for (int i = 0; i < j; ++i) {
+            if (dead[i]) { s_R[i * r + j] = 0.0; continue; }
+            double v = s_gram[i * r + j];
+            for (int l = 0; l < i; ++l) v -= s_R[l * r + i] * s_R[l * r + j];
+            s_R[i * r + j] = v / s_R[i * r + i];
+        }
+        double d = s_gram[j * r + j];
+        for (int i = 0; i < j; ++i) d -= s_R[i * r + j] * s_R[i * r + j];
+        const double nrm = sqrt(fmax(d, 0.0));
+        if (detect) dead[j] = !(nrm > tol);
+        s_R[j * r + j] = dead[j] ? 0.0 : nrm;
+    }
+    for (int j = 0; j < r; ++j) {
+        for (int i = 0; i < r; ++i) s_t[j * r + i] = 0.0;
+        if (dead[j]) continue;
+        // T_j = (e_j - sum_{i<j} R_ij T_i) / R_jj
+        for (int i = 0; i < j; ++i) {
+            const double c = s_R[i * r + j];
+            if (c != 0.0)
+                for (int l = 0; l <= i; ++l) s_t[j * r + l] -= c * s_t[i * r + l];
+        }
+        s_t[j * r + j] += 1.0;
+        const double inv = 1.0 / s_R[j * r + j];
+        for (int l = 0; l <= j; ++l) s_t[j * r + l] *= inv;
+    }
+}
+
+__global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, const int32_t *status, double col_tol) {
+    const MatDev &M = mats[blockIdx.x];
+    if (status[blockIdx.x] & 1) return;
+    const int r = M.r;
+    const int64_t m = M.m;
+    __shared__ double s_gram[kMaxRank * kMaxRank];
+    __shared__ double s_R[kMaxRank * kMaxRank];
+    __shared__ double s_t1[kMaxRank * kMaxRank];
+    __shared__ double s_t2[kMaxRank * kMaxRank];
+    __shared__ double s_tmp[kFactorThreads];
+    __shared__ int32_t s_dead[kMaxRank];
+    // P_raw = sum over column chunks, fixed order
+    for (int64_t e = threadIdx.x; e < m * r; e += kFactorThreads) {
+        double s = 0.0;
+        for (int c = 0; c < M.nchunk1; ++c) s += M.p_part[(int64_t)c * m * r + e];
+        M.p_raw[e] = s;
+    }
+    __syncthreads();
+    gram_pass(M.p_raw, m, r, s_gram, s_tmp);
+    if (threadIdx.x == 0) {
+        double fro2 = 0.0;
+        for (int j = 0; j < r; ++j) fro2 += s_gram[j * r + j];
+        // compressor.py:79: tol = _COLUMN_TOL * ||P||_F, fixed before the sweep
+        const double tol = col_tol * sqrt(fro2);
+        for (int j = 0; j < r; ++j) s_dead[j] = 0;
+        chol_inverse(s_gram, r, tol, s_dead, s_R, s_t1, true);
+    }
+    __syncthreads();
+    // P1 = P_raw T1 in place (row-local)
+    for (int64_t i = threadIdx.x; i < m; i += kFactorThreads) {
+        double row[kMaxRank], out[kMaxRank];
+        for (int k = 0; k < r; ++k) row[k] = M.p_raw[i * r + k];
+        for (int j = 0; j < r; ++j) {
+            double s = 0.0;
+            for (int l = 0; l <= j; ++l) s += row[l] * s_t1[j * r + l];
+            out[j] = s;
+        }
+        for (int k = 0; k < r; ++k) M.p_raw[i * r + k] = out[k];
+    }
+    __syncthreads();
+    // second CholQR pass restores orthogonality to fp64 level
+    gram_pass(M.p_raw, m, r, s_gram, s_tmp);
+    if (threadIdx.x == 0) chol_inverse(s_gram, r, 0.0, s_dead, s_R, s_t2, false);
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < m; i += kFactorThreads) {
+        double row[kMaxRank];
+        for (int k = 0; k < r; ++k) row[k] = M.p_raw[i * r + k];
+        for (int j = 0; j < r; ++j) {
+            double s = 0.0;
+            for (int l = 0; l <= j; ++l) s += row[l] * s_t2[j * r + l];
+            M.p_out[i * r + j] = (float)s;
+        }
+    }
+    if (threadIdx.x < r) M.dead[threadIdx.x] = s_dead[threadIdx.x];
+}
+
+// ------------------------------------------------------------------ pass 2
+// Q partial over this tile's rows: thread owns VEC columns x RMAX ranks;
+// fp32 FMA over 32-row groups, fp64 across groups.
+template <int VEC, int RMAX>
+__global__ void __launch_bounds__(kP2Threads) k_pass2(const MatDev *mats, const Tile *tiles, const int32_t *status) {
+    const Tile t = tiles[blockIdx.x];
+    const MatDev &M = mats[t.mat];
+    if (status[t.mat] & 1) return;
+    const int r = M.r;
+    const int64_t n = M.n;
+    const int tid = threadIdx.x;
+    const int64_t slot = t.slot0 + tid;
+    const bool active = slot < t.slot1;
+    const int64_t col0 = slot * VEC;
+    __shared__ float s_p[32][RMAX];
+    double acc[VEC][RMAX];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v)
+#pragma unroll
+        for (int k = 0; k < RMAX; ++k) acc[v][k] = 0.0;
+    for (int64_t row = t.row0; row < t.row1; row += 32) {
+        __syncthreads();
+        for (int e = tid; e < 32 * RMAX; e += kP2Threads) {
+            const int rr = e / RMAX, k = e % RMAX;
+            const int64_t i = row + rr;
+            s_p[rr][k] = (i < t.row1 && k < r) ? M.p_out[i * r + k] : 0.f;
+        }
+        __syncthreads();
+        if (active) {
+            float part[VEC][RMAX];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+#pragma unroll
+                for (int k = 0; k < RMAX; ++k) part[v][k] = 0.f;
+            const int64_t rows = min((int64_t)32, t.row1 - row);
+            for (int rr = 0; rr < rows; ++rr) {
+                float wv[VEC];
+                VecT<VEC>::unpack(VecT<VEC>::ld(M.w + (row + rr) * n + col0), wv);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v)
+#pragma unroll
+                    for (int k = 0; k < RMAX; ++k) part[v][k] = fmaf(wv[v], s_p[rr][k], part[v][k]);
+            }
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+#pragma unroll
+                for (int k = 0; k < RMAX; ++k) acc[v][k] += (double)part[v][k];
+        }
+    }
+    if (active) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+#pragma unroll
+            for (int k = 0; k < RMAX; ++k)
+                if (k < r) M.q_part[((int64_t)t.chunk * n + col0 + v) * r + k] = acc[v][k];
+    }
+}
+
+// ---------------------------------------------------------------- finalize
+__global__ void k_finalize(const MatDev *mats, const int32_t *status) {
+    const MatDev &M = mats[blockIdx.y];
+    if (status[blockIdx.y] & 1) return;
+    const int r = M.r;
+    const int64_t n = M.n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * r; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / r;
+        const int k = (int)(e % r);
+        float q;
+        if (M.dead[k]) {
+            q = M.basis[j * M.ld_q + k];   // compressor.py:113-114
+        } else {
+            double s = 0.0;
+            for (int b = 0; b < M.nblk2; ++b) s += M.q_part[((int64_t)b * n + j) * r + k];
+            q = (float)s;
+        }
+        M.q_out[j * r + k] = q;
+        M.q_warm[j * M.ld_q + k] = q;
+    }
+}
+
+struct Plan {
+    std::vector<MatDev> mats;
+    std::vector<Tile> t1v4, t1v1, t2v4, t2v1;
+    int64_t bytes = 0;
+    MatDev *d_mats = nullptr;
+    Tile *d_t1v4 = nullptr, *d_t1v1 = nullptr, *d_t2v4 = nullptr, *d_t2v1 = nullptr;
+    int rmax4 = 0, rmax1 = 0;
+};
+
+int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes, Plan &P) {
+    Arena a(ws, ws_bytes);
+    P.mats.resize(n);
+    P.d_mats = a.take<MatDev>(n);
+    for (int k = 0; k < n; ++k) {
+        const edgc_compress_desc &d = descs[k];
+        EDGC_REQUIRE(d.m >= 1 && d.n >= 1, "compress desc %d: dims must be positive", k);
+        EDGC_REQUIRE(d.r >= 1 && d.r <= std::min<int64_t>(d.m, d.n), "compress desc %d: rank %d outside [1, %lld]",
+                     k, d.r, (long long)std::min(d.m, d.n));
+        EDGC_REQUIRE(d.r <= kMaxRank, "compress desc %d: rank %d > %d not supported by this build", k, d.r,
+                     kMaxRank);
+        EDGC_REQUIRE(d.r_res >= 0 && d.r_res <= kMaxRank, "compress desc %d: r_res %d", k, d.r_res);
+        EDGC_REQUIRE(d.r_res == 0 || (d.p_res && d.q_res), "compress desc %d: residual factors missing", k);
+        EDGC_REQUIRE(d.g && d.w && d.q_warm && d.basis && d.p_out && d.q_out && d.ld_q >= d.r && d.ld_g >= d.n,
+                     "compress desc %d: null pointer or bad leading dimension", k);
+        MatDev &M = P.mats[k];
+        M.g = d.g; M.w = d.w; M.p_res = d.p_res; M.q_res = d.q_res; M.q_warm = d.q_warm; M.basis = d.basis;
+        M.p_out = d.p_out; M.q_out = d.q_out;
+        M.m = d.m; M.n = d.n; M.ld_g = d.ld_g; M.r = d.r; M.r_res = d.r_res; M.ld_q = d.ld_q;
+        const bool v4 = (d.n % 4 == 0) && (d.ld_g % 4 == 0) && ((uintptr_t)d.g % 16 == 0) &&
+                        ((uintptr_t)d.w % 16 == 0) && std::max(d.r, d.r_res) <= 4;
+        M.vec = v4 ? 4 : 1;
+        const int64_t slots = d.n / M.vec;
+        const int64_t threads1 = kP1Threads;
+        M.nchunk1 = (int32_t)ceil_div(slots, threads1);
+        M.nblk2 = (int32_t)ceil_div(d.m, kP2Rows);
+        (v4 ? P.rmax4 : P.rmax1) = std::max(v4 ? P.rmax4 : P.rmax1, std::max(d.r, d.r_res));
+        for (int32_t c = 0; c < M.nchunk1; ++c)
+            for (int64_t r0 = 0; r0 < d.m; r0 += kP1Rows) {
+                Tile t{k, c, c * threads1, std::min(slots, (c + 1) * threads1), r0, std::min(d.m, r0 + kP1Rows)};
+                (v4 ? P.t1v4 : P.t1v1).push_back(t);
+            }
+        const int64_t slots2 = slots;
+        for (int32_t b = 0; b < M.nblk2; ++b)
+            for (int64_t s0 = 0; s0 < slots2; s0 += kP2Threads) {
+                Tile t{k, b, s0, std::min(slots2, s0 + kP2Threads), (int64_t)b * kP2Rows,
+                       std::min(d.m, (int64_t)(b + 1) * kP2Rows)};
+                (v4 ? P.t2v4 : P.t2v1).push_back(t);
+            }
+    }
+    for (int k = 0; k < n; ++k) {
+        MatDev &M = P.mats[k];
+        M.p_part = a.take<double>((int64_t)M.nchunk1 * M.m * M.r);
+        M.p_raw = a.take<double>(M.m * M.r);
+        M.q_part = a.take<double>((int64_t)M.nblk2 * M.n * M.r);
+        M.tmat = a.take<double>((int64_t)M.r * M.r);
+        M.dead = a.take<int32_t>(M.r);
+    }
+    P.d_t1v4 = a.take<Tile>(P.t1v4.size());
+    P.d_t1v1 = a.take<Tile>(P.t1v1.size());
+    P.d_t2v4 = a.take<Tile>(P.t2v4.size());
+    P.d_t2v1 = a.take<Tile>(P.t2v1.size());
+    P.bytes = a.off;
+    return EDGC_OK;
+}
+
+int launch_pass1(const Plan &P, bool v4, int32_t *status, cudaStream_t st) {
+    const std::vector<Tile> &h = v4 ? P.t1v4 : P.t1v1;
+    const Tile *d = v4 ? P.d_t1v4 : P.d_t1v1;
+    if (h.empty()) return EDGC_OK;
+    const unsigned grid = (unsigned)h.size();
+    const int rmax = v4 ? P.rmax4 : P.rmax1;
+    if (v4) k_pass1<4, 4, 4><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
+    else if (rmax <= 4) k_pass1<1, 4, 4><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
+    else if (rmax <= 8) k_pass1<1, 8, 2><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
+    else if (rmax <= 16) k_pass1<1, 16, 1><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
+    else k_pass1<1, 32, 1><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+int launch_pass2(const Plan &P, bool v4, const int32_t *status, cudaStream_t st) {
+    const std::vector<Tile> &h = v4 ? P.t2v4 : P.t2v1;
+    const Tile *d = v4 ? P.d_t2v4 : P.d_t2v1;
+    if (h.empty()) return EDGC_OK;
+    const unsigned grid = (unsigned)h.size();
+    const int rmax = v4 ? P.rmax4 : P.rmax1;
+    if (v4) k_pass2<4, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
+    else if (rmax <= 4) k_pass2<1, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
+    else if (rmax <= 8) k_pass2<1, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
+    else if (rmax <= 16) k_pass2<1, 16><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
+    else k_pass2<1, 32><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+// ---------------------------------------------------------- reconstruction
+struct ReconDev {
+    const float *p, *q;
+    float *out;
+    int64_t m, n, ld_out, p_stride, q_stride;
+    int32_t r, n_ranks;
+    float scale;
+};
+
+struct RTile {
+    int32_t d;
+    int64_t col0, col1, row0, row1;
+};
+
+constexpr int kRThreads = 128;
+constexpr int kRRows = 32;      // rows per register block
+constexpr int kRTileRows = 128;
+
+// out[i, j] = scale * sum_w sum_k P_w[i, k] Q_w[j, k], accumulated in rank order
+template <int kRChunk>  // (rank, k) pairs per register chunk
+__global__ void __launch_bounds__(kRThreads) k_recon(const ReconDev *descs, const RTile *tiles) {
+    const RTile t = tiles[blockIdx.x];
+    const ReconDev D = descs[t.d];
+    const int r = D.r, WR = D.r * D.n_ranks;
+    const int64_t j = t.col0 + threadIdx.x;
+    const bool active = j < t.col1;
+    __shared__ float s_p[kRRows][kRChunk];
+    for (int64_t row = t.row0; row < t.row1; row += kRRows) {
+        float acc[kRRows];
+#pragma unroll
+        for (int rr = 0; rr < kRRows; ++rr) acc[rr] = 0.f;
+        for (int c0 = 0; c0 < WR; c0 += kRChunk) {
+            const int cn = min(kRChunk, WR - c0);
+            float q[kRChunk];
+#pragma unroll
+            for (int c = 0; c < kRChunk; ++c) {
+                const int wk = c0 + c;
+                q[c] = (active && c < cn) ? __ldg(D.q + (int64_t)(wk / r) * D.q_stride + j * r + (wk % r)) : 0.f;
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < kRRows * kRChunk; e += kRThreads) {
+                const int rr = e / kRChunk, c = e % kRChunk;
+                const int64_t i = row + rr;
+                const int wk = c0 + c;
+                s_p[rr][c] = (i < t.row1 && c < cn) ? D.p[(int64_t)(wk / r) * D.p_stride + i * r + (wk % r)] : 0.f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int rr = 0; rr < kRRows; ++rr)
+#pragma unroll
+                for (int c = 0; c < kRChunk; ++c) acc[rr] = fmaf(s_p[rr][c], q[c], acc[rr]);
+        }
+        if (active) {
+#pragma unroll
+            for (int rr = 0; rr < kRRows; ++rr) {
+                const int64_t i = row + rr;
+                if (i < t.row1) __stcs(D.out + i * D.ld_out + j, acc[rr] * D.scale);
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------- misc kernels
+__global__ void k_residual(const float *w, const float *p, const float *q, int r, int64_t m, int64_t n, float *e) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < m * n; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = x / n, j = x % n;
+        float dot = 0.f;
+        for (int k = 0; k < r; ++k) dot = fmaf(p[i * r + k], q[j * r + k], dot);
+        e[x] = w[x] - dot;
+    }
+}
+
+__global__ void k_check_work(const float *g, int64_t ld_g, const float *w, const float *p, const float *q, int r,
+                             int64_t m, int64_t n, int32_t *flag) {
+    bool bad = false;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < m * n; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = x / n, j = x % n;
+        float dot = 0.f;
+        for (int k = 0; k < r; ++k) dot = fmaf(p[i * r + k], q[j * r + k], dot);
+        bad |= !isfinite(g[i * ld_g + j] + (w[x] - dot));
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+template <typename T>
+__global__ void k_check_finite(const T *x, int64_t count, int32_t *flag) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+int elementwise_blocks(int64_t count) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(count, 256), sm_count() * 8)); }
+
+}  // namespace
+}  // namespace edgc
+
+using namespace edgc;
+
+struct edgc_compress_plan {
+    std::vector<edgc_compress_desc> descs;
+    Plan P;
+    int64_t bytes = 0;
+};
+
+struct edgc_recon_plan;
+
+extern "C" int edgc_compress_plan_create(const edgc_compress_desc *descs, int n, edgc_compress_plan **out) {
+    EDGC_REQUIRE(out && n >= 1 && descs, "edgc_compress_plan_create: bad arguments");
+    auto *h = new edgc_compress_plan();
+    h->descs.assign(descs, descs + n);
+    int rc = make_plan(descs, n, nullptr, INT64_MAX, h->P);
+    if (rc != EDGC_OK) { delete h; return rc; }
+    h->bytes = h->P.bytes;
+    *out = h;
+    return EDGC_OK;
+}
+
+extern "C" int64_t edgc_compress_plan_workspace_bytes(const edgc_compress_plan *h) { return h ? h->bytes : -1; }
+
+extern "C" int edgc_compress_plan_bind(edgc_compress_plan *h, void *ws, int64_t ws_bytes, void *stream) {
+    EDGC_REQUIRE(h && ws && ws_bytes >= h->bytes, "edgc_compress_plan_bind: workspace %lld < needed %lld",
+                 (long long)ws_bytes, h ? (long long)h->bytes : -1LL);
+    Plan &P = h->P;
+    P = Plan();
+    int rc = make_plan(h->descs.data(), (int)h->descs.size(), ws, ws_bytes, P);
+    if (rc != EDGC_OK) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n = (int)h->descs.size();
+    EDGC_CUDA_TRY(cudaMemcpyAsync(P.d_mats, P.mats.data(), sizeof(MatDev) * n, cudaMemcpyHostToDevice, st));
+    auto up = [&](Tile *d, const std::vector<Tile> &v) -> cudaError_t {
+        return v.empty() ? cudaSuccess
+                         : cudaMemcpyAsync(d, v.data(), sizeof(Tile) * v.size(), cudaMemcpyHostToDevice, st);
+    };
+    EDGC_CUDA_TRY(up(P.d_t1v4, P.t1v4));
+    EDGC_CUDA_TRY(up(P.d_t1v1, P.t1v1));
+    EDGC_CUDA_TRY(up(P.d_t2v4, P.t2v4));
+    EDGC_CUDA_TRY(up(P.d_t2v1, P.t2v1));
+    // the host staging vectors stay alive in the plan; make the upload complete
+    // before the caller could destroy or rebind it
+    EDGC_CUDA_TRY(cudaStreamSynchronize(st));
+    return EDGC_OK;
+}
+
+extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int32_t *status_dev, void *stream) {
+    EDGC_REQUIRE(h && status_dev && h->P.d_mats, "edgc_compress_plan_run: plan not bound");
+    const Plan &P = h->P;
+    const int n = (int)h->descs.size();
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc;
+    EDGC_CUDA_TRY(cudaMemsetAsync(status_dev, 0, sizeof(int32_t) * n, st));
+    if ((rc = launch_pass1(P, true, status_dev, st))) return rc;
+    if ((rc = launch_pass1(P, false, status_dev, st))) return rc;
+    k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
+    EDGC_LAUNCH_CHECK();
+    if ((rc = launch_pass2(P, true, status_dev, st))) return rc;
+    if ((rc = launch_pass2(P, false, status_dev, st))) return rc;
+    k_finalize<<<dim3(16, n), 256, 0, st>>>(P.d_mats, status_dev);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+extern "C" void edgc_compress_plan_destroy(edgc_compress_plan *h) { delete h; }
+
+extern "C" int64_t edgc_compress_workspace_bytes(const edgc_compress_desc *descs, int n) {
+    Plan P;
+    if (n < 0 || make_plan(descs, n, nullptr, INT64_MAX, P) != EDGC_OK) return -1;
+    return P.bytes;
+}
+
+extern "C" int edgc_compress(const edgc_compress_desc *descs, int n, double col_tol, int32_t *status_dev, void *ws,
+                             int64_t ws_bytes, void *stream) {
+    if (n == 0) return EDGC_OK;
+    edgc_compress_plan *h = nullptr;
+    int rc = edgc_compress_plan_create(descs, n, &h);
+    if (rc != EDGC_OK) return rc;
+    rc = edgc_compress_plan_bind(h, ws, ws_bytes, stream);
+    if (rc == EDGC_OK) rc = edgc_compress_plan_run(h, col_tol, status_dev, stream);
+    edgc_compress_plan_destroy(h);
+    return rc;
+}
+
+namespace {
+struct RPlan {
+    std::vector<ReconDev> d;
+    std::vector<RTile> tiles;
+    int64_t bytes = 0;
+    ReconDev *dd = nullptr;
+    RTile *dt = nullptr;
+};
+int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
+    Arena a(ws, INT64_MAX);
+    P.tiles.clear();
+    P.d.resize(n);
+    P.dd = a.take<ReconDev>(n);
+    for (int k = 0; k < n; ++k) {
+        const edgc_recon_desc &s = descs[k];
+        EDGC_REQUIRE(s.m >= 1 && s.n >= 1 && s.r >= 1 && s.n_ranks >= 1 && s.p && s.q && s.out && s.ld_out >= s.n,
+                     "recon desc %d: bad arguments", k);
+        P.d[k] = ReconDev{s.p, s.q, s.out, s.m, s.n, s.ld_out, s.p_rank_stride, s.q_rank_stride, s.r, s.n_ranks,
+                          s.scale};
+        for (int64_t c0 = 0; c0 < s.n; c0 += kRThreads)
+            for (int64_t r0 = 0; r0 < s.m; r0 += kRTileRows)
+                P.tiles.push_back(RTile{k, c0, std::min(s.n, c0 + kRThreads), r0, std::min(s.m, r0 + kRTileRows)});
+    }
+    P.dt = a.take<RTile>(P.tiles.size());
+    P.bytes = a.off;
+    return EDGC_OK;
+}
+}  // namespace
+
+struct edgc_recon_plan {
+    std::vector<edgc_recon_desc> descs;
+    RPlan P;
+    int wr = 0;
+};
+
+extern "C" int edgc_recon_plan_create(const edgc_recon_desc *descs, int n, edgc_recon_plan **out) {
+    EDGC_REQUIRE(out && n >= 1 && descs, "edgc_recon_plan_create: bad arguments");
+    auto *h = new edgc_recon_plan();
+    h->descs.assign(descs, descs + n);
+    int rc = make_rplan(descs, n, nullptr, h->P);
+    if (rc != EDGC_OK) { delete h; return rc; }
+    for (int k = 0; k < n; ++k) h->wr = std::max(h->wr, descs[k].r * descs[k].n_ranks);
+    *out = h;
+    return EDGC_OK;
+}
+
+extern "C" int64_t edgc_recon_plan_workspace_bytes(const edgc_recon_plan *h) { return h ? h->P.bytes : -1; }
+
+extern "C" int edgc_recon_plan_bind(edgc_recon_plan *h, void *ws, int64_t ws_bytes, void *stream) {
+    EDGC_REQUIRE(h && ws && ws_bytes >= h->P.bytes, "edgc_recon_plan_bind: workspace");
+    RPlan &P = h->P;
+    P = RPlan();
+    int rc = make_rplan(h->descs.data(), (int)h->descs.size(), ws, P);
+    if (rc != EDGC_OK) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    EDGC_CUDA_TRY(cudaMemcpyAsync(P.dd, P.d.data(), sizeof(ReconDev) * P.d.size(), cudaMemcpyHostToDevice, st));
+    EDGC_CUDA_TRY(cudaMemcpyAsync(P.dt, P.tiles.data(), sizeof(RTile) * P.tiles.size(), cudaMemcpyHostToDevice, st));
+    EDGC_CUDA_TRY(cudaStreamSynchronize(st));
+    return EDGC_OK;
+}
+
+extern "C" int edgc_recon_plan_run(edgc_recon_plan *h, void *stream) {
+    EDGC_REQUIRE(h && h->P.dd, "edgc_recon_plan_run: plan not bound");
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned grid = (unsigned)h->P.tiles.size();
+    if (h->wr <= 4) k_recon<4><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
+    else if (h->wr <= 8) k_recon<8><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
+    else if (h->wr <= 16) k_recon<16><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
+    else k_recon<32><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+extern "C" void edgc_recon_plan_destroy(edgc_recon_plan *h) { delete h; }
+
+extern "C" int64_t edgc_reconstruct_workspace_bytes(const edgc_recon_desc *descs, int n) {
+    RPlan P;
+    if (n < 0 || make_rplan(descs, n, nullptr, P) != EDGC_OK) return -1;
+    return P.bytes;
+}
+
+extern "C" int edgc_reconstruct(const edgc_recon_desc *descs, int n, void *ws, int64_t ws_bytes, void *stream) {
+    if (n == 0) return EDGC_OK;
+    edgc_recon_plan *h = nullptr;
+    int rc = edgc_recon_plan_create(descs, n, &h);
+    if (rc != EDGC_OK) return rc;
+    rc = edgc_recon_plan_bind(h, ws, ws_bytes, stream);
+    if (rc == EDGC_OK) rc = edgc_recon_plan_run(h, stream);
+    edgc_recon_plan_destroy(h);
+    return rc;
+}
+
+extern "C" int edgc_residual(const float *w, const float *p_res, const float *q_res, int32_t r_res, int64_t m,
+                             int64_t n, float *e_out, void *stream) {
+    EDGC_REQUIRE(w && e_out && m >= 1 && n >= 1 && r_res >= 0 && (r_res == 0 || (p_res && q_res)),
+                 "edgc_residual: bad arguments");
+    k_residual<<<elementwise_blocks(m * n), 256, 0, (cudaStream_t)stream>>>(w, p_res, q_res, r_res, m, n, e_out);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+extern "C" int edgc_check_work_finite(const float *g, int64_t ld_g, const float *w, const float *p_res,
+                                      const float *q_res, int32_t r_res, int64_t m, int64_t n, int32_t *flag_dev,
+                                      void *stream) {
+    EDGC_REQUIRE(g && w && flag_dev && m >= 1 && n >= 1 && ld_g >= n && (r_res == 0 || (p_res && q_res)),
+                 "edgc_check_work_finite: bad arguments");
+    k_check_work<<<elementwise_blocks(m * n), 256, 0, (cudaStream_t)stream>>>(g, ld_g, w, p_res, q_res, r_res, m, n,
+                                                                             flag_dev);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+extern "C" int edgc_check_finite(int dtype, const void *x, int64_t count, int32_t *flag_dev, void *stream) {
+    EDGC_REQUIRE((dtype == 0 || dtype == 1) && flag_dev && count >= 0, "edgc_check_finite: bad arguments");
+    if (count == 0) return EDGC_OK;
+    if (dtype == 0)
+        k_check_finite<float><<<elementwise_blocks(count), 256, 0, (cudaStream_t)stream>>>((const float *)x, count,
+                                                                                          flag_dev);
+    else
+        k_check_finite<double><<<elementwise_blocks(count), 256, 0, (cudaStream_t)stream>>>((const double *)x, count,
+                                                                                           flag_dev);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}

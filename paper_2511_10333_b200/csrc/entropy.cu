@@ -1,0 +1,491 @@
+// Entropy estimators on the device.
+//
+// Gaussian plug-in (default estimator, entropy.py:82-90 / :143): fused
+// gather + fp64 reduction, batched over all layers of one sampled iteration.
+// FD histogram (entropy.py:93-107 -> np.histogram(x, bins="fd")): order
+// statistics by 4-target radix select, NumPy's fp64 edge/index arithmetic with
+// separately rounded operations (no FMA contraction), warp-aggregated shared-
+// memory atomics for the counts, fp64 entropy reduction.  Counts and edges are
+// bit-exact with NumPy 2.3.5 (restated in oracle/oracle.py:fd_histogram).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace edgc {
+namespace {
+
+constexpr double kGaussConst = 1.4189385332046727;  // 0.5 * ln(2*pi*e), entropy.py:24
+constexpr int kRedThreads = 256;
+constexpr int kGaussBlocksPerDesc = 64;
+
+// ---------------------------------------------------------------- Gaussian
+struct GaussDev {
+    const void *src;
+    const int32_t *idx;
+    int64_t count;
+};
+
+template <typename T>
+__device__ __forceinline__ double load_sample(const GaussDev &d, int64_t i) {
+    const int64_t k = d.idx ? (int64_t)__ldg(d.idx + i) : i;
+    return (double)__ldg(reinterpret_cast<const T *>(d.src) + k);
+}
+
+// partial[desc][block] = {sum(x-K), sum((x-K)^2)} with the shift K = first sample
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_gauss_partial(const GaussDev *descs, double2 *partial) {
+    const GaussDev d = descs[blockIdx.y];
+    __shared__ double2 s_red[kRedThreads / 32];
+    double s1 = 0.0, s2 = 0.0;
+    if (d.count > 0) {
+        const double K = load_sample<T>(d, 0);
+        const int64_t stride = (int64_t)gridDim.x * kRedThreads;
+        int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+        // 4 independent loads in flight per thread
+        for (; i + 3 * stride < d.count; i += 4 * stride) {
+            double v0 = load_sample<T>(d, i) - K, v1 = load_sample<T>(d, i + stride) - K;
+            double v2 = load_sample<T>(d, i + 2 * stride) - K, v3 = load_sample<T>(d, i + 3 * stride) - K;
+            s1 += (v0 + v1) + (v2 + v3);
+            s2 += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
+        }
+        for (; i < d.count; i += stride) {
+            double v = load_sample<T>(d, i) - K;
+            s1 += v;
+            s2 += v * v;
+        }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_red[warp] = make_double2(s1, s2);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) { a += s_red[w].x; b += s_red[w].y; }
+        partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = make_double2(a, b);
+    }
+}
+
+__global__ void k_gauss_finish(const GaussDev *descs, int n, const double2 *partial, int nblk, double *h_out,
+                               int32_t *status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t cnt = descs[i].count;
+    if (cnt < 2) { status[i] = EDGC_EINVAL; h_out[i] = NAN; return; }
+    double s1 = 0.0, s2 = 0.0;
+    for (int b = 0; b < nblk; ++b) { s1 += partial[(int64_t)i * nblk + b].x; s2 += partial[(int64_t)i * nblk + b].y; }
+    const double nn = (double)cnt;
+    double var = (s2 - s1 * (s1 / nn)) / (nn - 1.0);
+    if (var < 0.0) var = 0.0;
+    const double sigma = sqrt(var);
+    if (sigma == 0.0) { status[i] = EDGC_EDEGENERATE; h_out[i] = NAN; return; }
+    status[i] = EDGC_OK;
+    h_out[i] = log(sigma) + kGaussConst;
+}
+
+// --------------------------------------------------------------- histogram
+template <typename T> struct KeyOf;
+template <> struct KeyOf<float> {
+    typedef uint32_t K;
+    static constexpr int kBits = 32;
+    __device__ static K key(float x) {
+        uint32_t b = __float_as_uint(x);
+        return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    }
+    __device__ static double value(K k) {
+        uint32_t b = (k & 0x80000000u) ? (k ^ 0x80000000u) : ~k;
+        return (double)__uint_as_float(b);
+    }
+};
+template <> struct KeyOf<double> {
+    typedef unsigned long long K;
+    static constexpr int kBits = 64;
+    __device__ static K key(double x) {
+        unsigned long long b = (unsigned long long)__double_as_longlong(x);
+        return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    }
+    __device__ static double value(K k) {
+        unsigned long long b = (k >> 63) ? (k ^ 0x8000000000000000ull) : ~k;
+        return __longlong_as_double((long long)b);
+    }
+};
+
+struct HistState {
+    // order statistics: targets 0..3 = ranks lo25, lo25+1, lo75, lo75+1
+    unsigned long long prefix[4];
+    long long rank[4];
+    double minv, maxv;
+    double first, last, delta, step, width;
+    long long nb;
+    int fixed;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_minmax(const T *x, int64_t n, double2 *partial) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kRedThreads) {
+        const double v = (double)x[i];
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    __shared__ double2 s[kRedThreads / 32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = make_double2(lo, hi);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kRedThreads / 32; ++w) { lo = fmin(lo, s[w].x); hi = fmax(hi, s[w].y); }
+        lo = fmin(lo, s[0].x);
+        hi = fmax(hi, s[0].y);
+        partial[blockIdx.x] = make_double2(lo, hi);
+    }
+}
+
+__global__ void k_hist_init(HistState *st, const double2 *mm, int nblk, int64_t n, int fixed, int32_t *status,
+                            double *result) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int b = 0; b < nblk; ++b) { lo = fmin(lo, mm[b].x); hi = fmax(hi, mm[b].y); }
+    st->minv = lo;
+    st->maxv = hi;
+    st->fixed = fixed;
+    // numpy percentile 'linear': virtual index (n-1)*q, floor, +1
+    const double v25 = (double)(n - 1) * 0.25, v75 = (double)(n - 1) * 0.75;
+    const long long l25 = (long long)floor(v25), l75 = (long long)floor(v75);
+    st->rank[0] = l25;
+    st->rank[1] = min(l25 + 1, (long long)n - 1);
+    st->rank[2] = l75;
+    st->rank[3] = min(l75 + 1, (long long)n - 1);
+    for (int t = 0; t < 4; ++t) st->prefix[t] = 0ull;
+    *status = EDGC_OK;
+    if (n < 2) *status = EDGC_EINVAL;
+    else if (lo == hi) *status = EDGC_EDEGENERATE;
+    for (int i = 0; i < 5; ++i) result[i] = NAN;
+}
+
+// one radix-select digit pass (8-bit digits, most significant first)
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t n, const HistState *st, int shift,
+                                                           unsigned int *ghist /*[4][256]*/) {
+    typedef typename KeyOf<T>::K K;
+    __shared__ unsigned int h[4][256];
+    for (int i = threadIdx.x; i < 4 * 256; i += kRedThreads) (&h[0][0])[i] = 0u;
+    __syncthreads();
+    const int kbits = KeyOf<T>::kBits;
+    const K hi_mask = (shift + 8 >= kbits) ? (K)0 : (K)(~(K)0) << (shift + 8);
+    K pre[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) pre[t] = (K)st->prefix[t];
+    for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kRedThreads) {
+        const K k = KeyOf<T>::key(x[i]);
+        const unsigned dig = (unsigned)((k >> shift) & 0xFF);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (((k ^ pre[t]) & hi_mask) == 0) atomicAdd(&h[t][dig], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * 256; i += kRedThreads) {
+        const unsigned v = (&h[0][0])[i];
+        if (v) atomicAdd(ghist + i, v);
+    }
+}
+
+__global__ void k_radix_pick(HistState *st, unsigned int *ghist, int shift) {
+    const int t = threadIdx.x;
+    if (t < 4) {
+        long long r = st->rank[t];
+        long long cum = 0;
+        int d = 0;
+        for (; d < 256; ++d) {
+            const long long c = ghist[t * 256 + d];
+            if (r < cum + c) break;
+            cum += c;
+        }
+        st->prefix[t] |= ((unsigned long long)d) << shift;
+        st->rank[t] = r - cum;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) ghist[i] = 0u;
+}
+
+__device__ __forceinline__ double np_lerp(double a, double b, double t) {
+    // numpy/lib/_function_base_impl.py:4657-4678, each op rounded separately
+    const double diff = __dsub_rn(b, a);
+    double out = __dadd_rn(a, __dmul_rn(diff, t));
+    if (t >= 0.5) out = __dsub_rn(b, __dmul_rn(diff, __dsub_rn(1.0, t)));
+    return out;
+}
+
+__device__ __forceinline__ double edge_at(const HistState &s, long long k) {
+    // numpy/_core/function_base.py:139-172 (linspace): y = k*step + start, last = stop
+    if (k >= s.nb) return s.last;
+    if (s.step == 0.0) return __dadd_rn(__dmul_rn(__ddiv_rn((double)k, (double)s.nb), s.delta), s.first);
+    return __dadd_rn(__dmul_rn((double)k, s.step), s.first);
+}
+
+template <typename T>
+__global__ void k_hist_params(HistState *st, int64_t n, double inv_cbrt_n, long long fixed_bins, long long cap,
+                              int32_t *status, double *result) {
+    if (*status != EDGC_OK) return;
+    typedef KeyOf<T> KO;
+    double q[4];
+    for (int t = 0; t < 4; ++t) q[t] = KO::value((typename KO::K)st->prefix[t]);
+    const double v25 = __dmul_rn((double)(n - 1), 0.25), v75 = __dmul_rn((double)(n - 1), 0.75);
+    const double g25 = __dsub_rn(v25, floor(v25)), g75 = __dsub_rn(v75, floor(v75));
+    const double p25 = (v25 >= (double)(n - 1)) ? st->maxv : np_lerp(q[0], q[1], g25);
+    const double p75 = (v75 >= (double)(n - 1)) ? st->maxv : np_lerp(q[2], q[3], g75);
+    double first = st->minv, last = st->maxv;
+    if (first == last) { first = __dsub_rn(first, 0.5); last = __dadd_rn(last, 0.5); }
+    const double delta = __dsub_rn(last, first);
+    long long nb;
+    double width = 0.0;
+    if (fixed_bins > 0) {
+        nb = fixed_bins;
+    } else {
+        const double iqr = __dsub_rn(p75, p25);
+        width = __dmul_rn(__dmul_rn(2.0, iqr), inv_cbrt_n);
+        nb = (width != 0.0) ? (long long)ceil(__ddiv_rn(delta, width)) : 1;
+    }
+    st->first = first;
+    st->last = last;
+    st->delta = delta;
+    st->nb = nb;
+    st->width = width;
+    st->step = __ddiv_rn(delta, (double)nb);
+    result[1] = first;
+    result[2] = last;
+    result[3] = width;
+    result[4] = (double)nb;
+    if (nb > cap) *status = EDGC_ECAPACITY;
+}
+
+__global__ void k_hist_edges(const HistState *st, const int32_t *status, double *edges_out, int32_t *status_w) {
+    if (*status != EDGC_OK) return;
+    const HistState s = *st;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k <= s.nb;
+         k += (long long)gridDim.x * blockDim.x) {
+        const double e = edge_at(s, k);
+        if (edges_out) edges_out[k] = e;
+        if (k < s.nb && !(e < edge_at(s, k + 1))) *status_w = EDGC_ETOOMANYBINS;
+    }
+}
+
+// numpy/lib/_histograms_impl.py:836-863: index, edge correction, bincount
+template <typename T>
+__device__ __forceinline__ long long bin_of(const HistState &s, double v) {
+    const double f = __dmul_rn(__ddiv_rn(__dsub_rn(v, s.first), s.delta), (double)s.nb);
+    long long idx = (long long)f;
+    if (idx == s.nb) --idx;
+    if (v < edge_at(s, idx)) --idx;
+    if (idx != s.nb - 1 && v >= edge_at(s, idx + 1)) ++idx;
+    return idx;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_hist_count_smem(const T *x, int64_t n, const HistState *st,
+                                                                 const int32_t *status, long long *counts) {
+    if (*status != EDGC_OK) return;
+    extern __shared__ unsigned int sh[];
+    const HistState s = *st;
+    for (long long i = threadIdx.x; i < s.nb; i += kRedThreads) sh[i] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * kRedThreads;
+    const int64_t n_iter = (n + stride - 1) / stride;
+    for (int64_t it = 0; it < n_iter; ++it) {
+        const int64_t i = it * stride + (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+        const bool live = i < n;
+        const int b = live ? (int)bin_of<T>(s, (double)x[i]) : -1;
+        // warp-aggregated: one shared atomic per distinct bin per warp
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        if (live && lane == leader) atomicAdd(&sh[b], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    for (long long i = threadIdx.x; i < s.nb; i += kRedThreads) {
+        const unsigned v = sh[i];
+        if (v) atomicAdd(reinterpret_cast<unsigned long long *>(counts) + i, (unsigned long long)v);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_hist_count_global(const T *x, int64_t n, const HistState *st,
+                                                                   const int32_t *status, long long *counts) {
+    if (*status != EDGC_OK) return;
+    const HistState s = *st;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * kRedThreads;
+    const int64_t n_iter = (n + stride - 1) / stride;
+    for (int64_t it = 0; it < n_iter; ++it) {
+        const int64_t i = it * stride + (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+        const bool live = i < n;
+        const long long b = live ? bin_of<T>(s, (double)x[i]) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        if (live && lane == leader)
+            atomicAdd(reinterpret_cast<unsigned long long *>(counts) + b, (unsigned long long)__popc(peers));
+    }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_hist_entropy_partial(const HistState *st, const int32_t *status,
+                                                                      const long long *counts, int64_t total,
+                                                                      double *partial) {
+    double acc = 0.0;
+    if (*status == EDGC_OK) {
+        const HistState s = *st;
+        const double tot = (double)total;
+        for (long long k = (long long)blockIdx.x * kRedThreads + threadIdx.x; k < s.nb;
+             k += (long long)gridDim.x * kRedThreads) {
+            const long long c = counts[k];
+            if (c > 0) {
+                const double p = __ddiv_rn((double)c, tot);
+                const double w = __dsub_rn(edge_at(s, k + 1), edge_at(s, k));
+                acc += p * log(__ddiv_rn(p, w));
+            }
+        }
+    }
+    acc = warp_sum(acc);
+    __shared__ double s_red[kRedThreads / 32];
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) a += s_red[w];
+        partial[blockIdx.x] = a;
+    }
+}
+
+__global__ void k_hist_entropy_final(const double *partial, int nblk, const int32_t *status, double *result) {
+    if (*status != EDGC_OK) return;
+    double a = 0.0;
+    for (int b = 0; b < nblk; ++b) a += partial[b];
+    result[0] = -a;
+}
+
+constexpr int kMinMaxBlocks = 296;
+constexpr int kHistBlocks = 592;
+constexpr int kEntBlocks = 148;
+
+struct HistLayout {
+    HistState *st;
+    double2 *mm;
+    unsigned int *ghist;
+    double *ent;
+    int64_t bytes;
+};
+
+HistLayout hist_layout(void *ws) {
+    Arena a(ws, INT64_MAX);
+    HistLayout L;
+    L.st = a.take<HistState>(1);
+    L.mm = a.take<double2>(kMinMaxBlocks);
+    L.ghist = a.take<unsigned int>(4 * 256);
+    L.ent = a.take<double>(kEntBlocks);
+    L.bytes = a.off;
+    return L;
+}
+
+template <typename T>
+int run_histogram(const T *x, int64_t n, double inv_cbrt_n, int64_t fixed_bins, int64_t cap, long long *counts,
+                  double *edges, double *result, int32_t *status, void *ws, cudaStream_t st) {
+    HistLayout L = hist_layout(ws);
+    const int sms = sm_count();
+    const int mmb = (int)std::max<int64_t>(1, std::min<int64_t>(kMinMaxBlocks, ceil_div(n, kRedThreads)));
+    k_minmax<T><<<mmb, kRedThreads, 0, st>>>(x, n, L.mm);
+    EDGC_LAUNCH_CHECK();
+    k_hist_init<<<1, 1, 0, st>>>(L.st, L.mm, mmb, n, fixed_bins > 0, status, result);
+    EDGC_LAUNCH_CHECK();
+    EDGC_CUDA_TRY(cudaMemsetAsync(L.ghist, 0, 4 * 256 * sizeof(unsigned int), st));
+    const int kbits = KeyOf<T>::kBits;
+    const int hb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 4, ceil_div(n, kRedThreads)));
+    if (fixed_bins <= 0) {
+        for (int shift = kbits - 8; shift >= 0; shift -= 8) {
+            k_radix_hist<T><<<hb, kRedThreads, 0, st>>>(x, n, L.st, shift, L.ghist);
+            EDGC_LAUNCH_CHECK();
+            k_radix_pick<<<1, 256, 0, st>>>(L.st, L.ghist, shift);
+            EDGC_LAUNCH_CHECK();
+        }
+    }
+    k_hist_params<T><<<1, 1, 0, st>>>(L.st, n, inv_cbrt_n, fixed_bins, cap, status, result);
+    EDGC_LAUNCH_CHECK();
+    k_hist_edges<<<sms, 256, 0, st>>>(L.st, status, edges, status);
+    EDGC_LAUNCH_CHECK();
+    EDGC_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(long long) * cap, st));
+    // counts go to shared memory when they fit (<= 48K bins), else global atomics
+    const int64_t smem_bins = 48 * 1024;
+    const int cb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 2, ceil_div(n, kRedThreads)));
+    if (cap <= smem_bins) {
+        const size_t smem = sizeof(unsigned int) * (size_t)std::max<int64_t>(cap, 1);
+        EDGC_CUDA_TRY(cudaFuncSetAttribute(k_hist_count_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(smem_bins * sizeof(unsigned int))));
+        k_hist_count_smem<T><<<cb, kRedThreads, smem, st>>>(x, n, L.st, status, counts);
+    } else {
+        k_hist_count_global<T><<<cb * 4, kRedThreads, 0, st>>>(x, n, L.st, status, counts);
+    }
+    EDGC_LAUNCH_CHECK();
+    k_hist_entropy_partial<<<kEntBlocks, kRedThreads, 0, st>>>(L.st, status, counts, n, L.ent);
+    EDGC_LAUNCH_CHECK();
+    k_hist_entropy_final<<<1, 1, 0, st>>>(L.ent, kEntBlocks, status, result);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+}  // namespace
+}  // namespace edgc
+
+using namespace edgc;
+
+extern "C" int64_t edgc_entropy_gaussian_workspace_bytes(const edgc_gauss_desc *descs, int n) {
+    (void)descs;
+    return align256(sizeof(GaussDev) * (int64_t)std::max(n, 1)) +
+           align256(sizeof(double2) * (int64_t)std::max(n, 1) * kGaussBlocksPerDesc);
+}
+
+extern "C" int edgc_entropy_gaussian(int src_dtype, const edgc_gauss_desc *descs, int n, double *h_out,
+                                     int32_t *status_dev, void *ws, int64_t ws_bytes, void *stream) {
+    if (n == 0) return EDGC_OK;
+    EDGC_REQUIRE(n > 0 && descs && h_out && status_dev && (src_dtype == 0 || src_dtype == 1),
+                 "edgc_entropy_gaussian: bad arguments");
+    EDGC_REQUIRE(ws_bytes >= edgc_entropy_gaussian_workspace_bytes(descs, n), "edgc_entropy_gaussian: workspace");
+    Arena a(ws, ws_bytes);
+    GaussDev *d = a.take<GaussDev>(n);
+    double2 *part = a.take<double2>((int64_t)n * kGaussBlocksPerDesc);
+    std::vector<GaussDev> h(n);
+    for (int i = 0; i < n; ++i) h[i] = GaussDev{descs[i].src, descs[i].idx, descs[i].count};
+    cudaStream_t st = (cudaStream_t)stream;
+    EDGC_CUDA_TRY(cudaMemcpyAsync(d, h.data(), sizeof(GaussDev) * n, cudaMemcpyHostToDevice, st));
+    dim3 grid(kGaussBlocksPerDesc, n);
+    if (src_dtype == 0)
+        k_gauss_partial<float><<<grid, kRedThreads, 0, st>>>(d, part);
+    else
+        k_gauss_partial<double><<<grid, kRedThreads, 0, st>>>(d, part);
+    EDGC_LAUNCH_CHECK();
+    k_gauss_finish<<<(n + 127) / 128, 128, 0, st>>>(d, n, part, kGaussBlocksPerDesc, h_out, status_dev);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+extern "C" int64_t edgc_entropy_histogram_workspace_bytes(int64_t count) {
+    (void)count;
+    return hist_layout(nullptr).bytes;
+}
+
+extern "C" int edgc_entropy_histogram(int dtype, const void *samples, int64_t count, double inv_cbrt_n,
+                                      int64_t fixed_bins, int64_t bins_cap, int64_t *counts_dev, double *edges_dev,
+                                      double *result_dev, int32_t *status_dev, void *ws, int64_t ws_bytes,
+                                      void *stream) {
+    EDGC_REQUIRE((dtype == 0 || dtype == 1) && samples && count >= 1 && bins_cap >= 1 && counts_dev &&
+                     result_dev && status_dev,
+                 "edgc_entropy_histogram: bad arguments");
+    EDGC_REQUIRE(ws_bytes >= edgc_entropy_histogram_workspace_bytes(count), "edgc_entropy_histogram: workspace");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == 0)
+        return run_histogram<float>((const float *)samples, count, inv_cbrt_n, fixed_bins, bins_cap,
+                                    (long long *)counts_dev, edges_dev, result_dev, status_dev, ws, st);
+    return run_histogram<double>((const double *)samples, count, inv_cbrt_n, fixed_bins, bins_cap,
+                                 (long long *)counts_dev, edges_dev, result_dev, status_dev, ws, st);
+}

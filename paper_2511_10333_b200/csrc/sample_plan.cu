@@ -1,0 +1,410 @@
+// Sample plan: NumPy-exact sampled indices on the device.
+//
+// Replaces np.random.default_rng(seed).choice(N, count, replace=False,
+// shuffle=False) at /root/reference/pkg/src/edgc/entropy.py:78.  The NumPy
+// algorithm (restated in oracle/npchoice.c) is sequential: a partial
+// Fisher-Yates over arange(N) ("tail", N > 10000 and count > N//20) or
+// Floyd's algorithm, each step consuming Lemire-bounded 32-bit draws from
+// PCG64 with rare, value-dependent rejections.  The device plan splits it
+// into four data-parallel phases:
+//   P1 draws    every thread jumps PCG64 ahead to its own chunk and writes the
+//               u32 stream (low half first, as next_uint32 buffers it);
+//   P2 walk     one CTA per plan assigns draws to steps: 1024 lanes test 1024
+//               consecutive steps against their draws in parallel, a CTA-wide
+//               vote finds the first Lemire rejection, and the window slides
+//               past it (rejections are ~1e-3 per step at GPT-2 sizes);
+//   P3 index    (key = bounded value, step) pairs go into an open-addressing
+//               hash table with per-key step lists;
+//   P4 resolve  tail: out[i] = value at position j just before step i, found
+//               by following "last earlier writer" links (chains are a few
+//               links deep); Floyd: a draw collides iff it equals an earlier
+//               draw or an earlier collided step's j.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace edgc {
+namespace {
+
+typedef unsigned __int128 u128;
+
+__host__ __device__ __forceinline__ u128 pcg_mult() {
+    return (((u128)0x2360ED051FC65DA4ULL) << 64) | (u128)0x4385DF649FCCF645ULL;
+}
+
+__device__ __forceinline__ uint64_t pcg_output(u128 s) {
+    const uint64_t x = (uint64_t)(s >> 64) ^ (uint64_t)s;
+    const unsigned rot = (unsigned)(s >> 122);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+// state after `delta` LCG steps (pcg_advance_lcg_128)
+__device__ __forceinline__ u128 pcg_jump(u128 state, u128 inc, uint64_t delta) {
+    u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
+    while (delta) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    return acc_mult * state + acc_plus;
+}
+
+struct PlanDev {
+    u128 state, inc;
+    int64_t n_elems, count;
+    int32_t *idx;
+    uint32_t *draws;   // [n_draws]
+    int64_t n_draws;   // even
+    int32_t *rv;       // [count] bounded values
+    int32_t *next;     // [count]
+    int32_t *keys;     // [cap]
+    int32_t *heads;    // [cap]
+    int64_t cap;       // power of two
+    int32_t log2cap;
+    int32_t tail;      // 1 = tail shuffle, 0 = Floyd
+    int64_t draw_chunk0;  // first P1 chunk index of this plan
+    int64_t step_block0;  // first P3/P4 block index of this plan
+};
+
+constexpr int kDrawsPerThread = 64;  // 64-bit outputs per P1 thread
+constexpr int kP1Threads = 256;
+constexpr int kWalkThreads = 1024;
+constexpr int kStepThreads = 256;
+
+__device__ __forceinline__ int find_plan(const PlanDev *plans, int n, int64_t blk, bool by_draw) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        int64_t b0 = by_draw ? plans[mid].draw_chunk0 : plans[mid].step_block0;
+        if (b0 <= blk) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// ---- P1: u32 draw stream ---------------------------------------------------
+__global__ void __launch_bounds__(kP1Threads) k_draws(const PlanDev *plans, int n_plans) {
+    const int64_t chunk = (int64_t)blockIdx.x * kP1Threads + threadIdx.x;
+    const PlanDev &P = plans[find_plan(plans, n_plans, chunk, true)];
+    const int64_t local = chunk - P.draw_chunk0;
+    const int64_t n64 = P.n_draws / 2;
+    const int64_t o0 = local * kDrawsPerThread;
+    if (local < 0 || o0 >= n64) return;
+    u128 s = pcg_jump(P.state, P.inc, (uint64_t)o0);
+    const int64_t o1 = min(o0 + kDrawsPerThread, n64);
+    uint2 *out = reinterpret_cast<uint2 *>(P.draws);
+    for (int64_t o = o0; o < o1; ++o) {
+        s = s * pcg_mult() + P.inc;
+        const uint64_t v = pcg_output(s);
+        out[o] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
+    }
+}
+
+// Lemire 32-bit bounded draw check (NumPy bounded_lemire_uint32).
+__device__ __forceinline__ bool lemire_accept(uint32_t x, uint32_t rng, uint32_t &val) {
+    const uint32_t excl = rng + 1u;
+    const uint64_t m = (uint64_t)x * excl;
+    val = (uint32_t)(m >> 32);
+    const uint32_t left = (uint32_t)m;
+    if (left >= excl) return true;
+    const uint32_t thr = (0xFFFFFFFFu - rng) % excl;
+    return left >= thr;
+}
+
+__device__ __forceinline__ uint32_t step_rng(const PlanDev &P, int64_t s) {
+    // tail: i = N-1-s (bounded(0..i)); Floyd: j = N-count+s (bounded(0..j))
+    return P.tail ? (uint32_t)(P.n_elems - 1 - s) : (uint32_t)(P.n_elems - P.count + s);
+}
+
+// ---- P2: assign draws to steps --------------------------------------------
+__global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int32_t *status) {
+    const PlanDev &P = plans[blockIdx.x];
+    __shared__ int s_warp_first[kWalkThreads / 32];
+    __shared__ int s_first;
+    __shared__ long long s_next_u;
+    __shared__ int s_err;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_err = 0;
+    __syncthreads();
+    int64_t s = 0, u = 0;
+    const int64_t count = P.count, nd = P.n_draws;
+    uint32_t x_pref = (tid < nd) ? P.draws[tid] : 0u;
+    while (s < count) {
+        const int64_t st = s + tid, pos = u + tid;
+        const bool valid = st < count;
+        uint32_t x = x_pref;
+        // prefetch the next window assuming this one has no rejection
+        const int64_t pnext = u + kWalkThreads + tid;
+        x_pref = (pnext < nd) ? __ldg(P.draws + pnext) : 0u;
+        bool rej = false;
+        uint32_t val = 0;
+        if (valid) {
+            if (pos >= nd) {
+                rej = true;  // out of draws: handled below as an error
+            } else {
+                rej = !lemire_accept(x, step_rng(P, st), val);
+            }
+        }
+        if (__syncthreads_or(rej) == 0) {
+            if (valid) P.rv[st] = (int32_t)val;
+            s += kWalkThreads;
+            u += kWalkThreads;
+            continue;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, rej);
+        if (lane == 0) s_warp_first[warp] = bal ? (warp * 32 + __ffs(bal) - 1) : 0x7fffffff;
+        __syncthreads();
+        if (tid < 32) {
+            int f = s_warp_first[tid];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
+            if (tid == 0) s_first = f;
+        }
+        __syncthreads();
+        const int f = s_first;
+        if (valid && tid < f) P.rv[st] = (int32_t)val;
+        if (tid == f) {
+            // the rejected step keeps drawing sequentially (rare: p ~ rng/2^32)
+            const uint32_t rng = step_rng(P, st);
+            int64_t p = pos + 1;
+            uint32_t v2 = 0;
+            bool ok = false;
+            while (p < nd) {
+                if (lemire_accept(P.draws[p], rng, v2)) { ok = true; break; }
+                ++p;
+            }
+            if (!ok || pos >= nd) {
+                s_err = 1;
+            } else {
+                P.rv[st] = (int32_t)v2;
+            }
+            s_next_u = p + 1;
+        }
+        __syncthreads();
+        if (s_err) break;
+        s = s + f + 1;
+        u = s_next_u;
+        x_pref = (u + tid < nd) ? P.draws[u + tid] : 0u;
+    }
+    if (tid == 0) status[blockIdx.x] = s_err ? EDGC_EDRAWS : EDGC_OK;
+}
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t key, int log2cap) {
+    return (uint32_t)((key * 2654435761u) >> (32 - log2cap));
+}
+
+__device__ __forceinline__ int find_plan_steps(const PlanDev *plans, int n, int64_t blk) {
+    return find_plan(plans, n, blk, false);
+}
+
+// ---- P3: hash (key = bounded value) -> list of steps ----------------------
+__global__ void __launch_bounds__(kStepThreads) k_index(const PlanDev *plans, int n_plans) {
+    const int p = find_plan_steps(plans, n_plans, blockIdx.x);
+    const PlanDev &P = plans[p];
+    const int64_t s = (int64_t)(blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
+    if (s >= P.count) return;
+    const int32_t key = P.rv[s];
+    const uint32_t mask = (uint32_t)(P.cap - 1);
+    uint32_t slot = P.log2cap ? hash_slot((uint32_t)key, P.log2cap) : 0u;
+    while (true) {
+        const int32_t k = atomicCAS(P.keys + slot, -1, key);
+        if (k == -1 || k == key) break;
+        slot = (slot + 1) & mask;
+    }
+    P.next[s] = atomicExch(P.heads + slot, (int32_t)s);
+}
+
+__device__ __forceinline__ int32_t lookup_head(const PlanDev &P, int32_t key) {
+    const uint32_t mask = (uint32_t)(P.cap - 1);
+    uint32_t slot = P.log2cap ? hash_slot((uint32_t)key, P.log2cap) : 0u;
+    while (true) {
+        const int32_t k = P.keys[slot];
+        if (k == key) return P.heads[slot];
+        if (k == -1) return -1;
+        slot = (slot + 1) & mask;
+    }
+}
+
+// largest step < before in the list of `key` (or -1)
+__device__ __forceinline__ int32_t latest_before(const PlanDev &P, int32_t key, int32_t before) {
+    int32_t best = -1;
+    for (int32_t e = lookup_head(P, key); e >= 0; e = P.next[e])
+        if (e < before && e > best) best = e;
+    return best;
+}
+
+// ---- P4: resolve chains / collisions ---------------------------------------
+__global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, int n_plans) {
+    const int p = find_plan_steps(plans, n_plans, blockIdx.x);
+    const PlanDev &P = plans[p];
+    const int64_t s64 = (int64_t)(blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
+    if (s64 >= P.count) return;
+    const int32_t s = (int32_t)s64;
+    const int64_t N = P.n_elems, count = P.count;
+    if (P.tail) {
+        // step s swaps positions i = N-1-s and j = rv[s]; out[count-1-s] is the
+        // value sitting at j just before step s.
+        const int32_t j = P.rv[s];
+        int32_t t = latest_before(P, j, s);
+        int64_t val = j;
+        if (t >= 0) {
+            // value deposited at j by step t = value at position i_t before step t
+            while (true) {
+                const int32_t pos_t = (int32_t)(N - 1 - t);
+                const int32_t t2 = latest_before(P, pos_t, t);
+                if (t2 < 0) { val = pos_t; break; }
+                t = t2;
+            }
+        }
+        P.idx[count - 1 - s] = (int32_t)val;
+    } else {
+        const int64_t base = N - count;
+        int32_t cur = s;
+        bool collide = false;
+        while (true) {
+            const int32_t v = P.rv[cur];
+            if (latest_before(P, v, cur) >= 0) { collide = true; break; }
+            if (v < base) break;
+            cur = (int32_t)(v - base);
+        }
+        P.idx[s] = collide ? (int32_t)(base + s) : P.rv[s];
+    }
+}
+
+struct PlanLayout {
+    std::vector<PlanDev> dev;
+    int64_t ws_bytes = 0;
+    int64_t draw_chunks = 0, step_blocks = 0;
+    int64_t table_bytes = 0;
+    char *table_base = nullptr;
+};
+
+int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes, PlanLayout &L) {
+    Arena a(ws, ws_bytes);
+    L.dev.resize(n);
+    PlanDev *descs_dev = a.take<PlanDev>(n);
+    (void)descs_dev;
+    int64_t chunk = 0, blocks = 0;
+    // tables are contiguous so one memset clears them
+    std::vector<int64_t> caps(n);
+    for (int i = 0; i < n; ++i) {
+        const edgc_plan_desc &d = plans[i];
+        EDGC_REQUIRE(d.n_elems >= 2 && d.n_elems < (int64_t(1) << 31), "plan %d: N=%lld outside [2, 2^31)", i,
+                     (long long)d.n_elems);
+        EDGC_REQUIRE(d.count >= 1 && d.count < d.n_elems, "plan %d: count=%lld must be in [1, N)", i,
+                     (long long)d.count);
+        PlanDev &P = L.dev[i];
+        P.state = (((u128)d.state_hi) << 64) | d.state_lo;
+        P.inc = (((u128)d.inc_hi) << 64) | d.inc_lo;
+        P.n_elems = d.n_elems;
+        P.count = d.count;
+        P.idx = d.idx;
+        P.tail = (d.n_elems > 10000 && d.count > d.n_elems / 20) ? 1 : 0;
+        // expected rejections ~ count * N / 2^33 (threshold ~ uniform below rng+1)
+        const double lam = (double)d.count * (double)d.n_elems / 4294967296.0;
+        int64_t slack = (int64_t)(2.0 * lam + 16.0 * std::sqrt(lam + 1.0)) + 4096;
+        int64_t nd = d.count + slack;
+        nd = (nd + 1) & ~int64_t(1);
+        P.n_draws = nd;
+        P.draw_chunk0 = chunk;
+        chunk += ceil_div(nd / 2, kDrawsPerThread);
+        P.step_block0 = blocks;
+        blocks += ceil_div(d.count, kStepThreads);
+        int64_t cap = 1;
+        int lg = 0;
+        while (cap < 2 * d.count) { cap <<= 1; ++lg; }
+        P.cap = cap;
+        P.log2cap = lg;
+        caps[i] = cap;
+    }
+    // round the P1 chunk index up so blocks never straddle more than needed
+    L.draw_chunks = chunk;
+    L.step_blocks = blocks;
+    for (int i = 0; i < n; ++i) {
+        PlanDev &P = L.dev[i];
+        P.draws = a.take<uint32_t>(P.n_draws);
+        P.rv = a.take<int32_t>(P.count);
+        P.next = a.take<int32_t>(P.count);
+    }
+    a.off = align256(a.off);
+    const int64_t t0 = a.off;
+    for (int i = 0; i < n; ++i) {
+        PlanDev &P = L.dev[i];
+        P.keys = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
+        a.off += caps[i] * 4;
+        P.heads = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
+        a.off += caps[i] * 4;
+    }
+    L.table_bytes = a.off - t0;
+    L.table_base = a.base ? a.base + t0 : nullptr;
+    L.ws_bytes = a.off;
+    return EDGC_OK;
+}
+
+__global__ void k_gather(int src_dtype, const void *src, const int32_t *idx, int64_t count, int dst_dtype,
+                         void *dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = idx ? (int64_t)idx[i] : i;
+        const double v = src_dtype == 0 ? (double)reinterpret_cast<const float *>(src)[k]
+                                        : reinterpret_cast<const double *>(src)[k];
+        if (dst_dtype == 0)
+            reinterpret_cast<float *>(dst)[i] = (float)v;
+        else
+            reinterpret_cast<double *>(dst)[i] = v;
+    }
+}
+
+}  // namespace
+}  // namespace edgc
+
+using namespace edgc;
+
+extern "C" int64_t edgc_sample_plan_workspace_bytes(const edgc_plan_desc *plans, int n_plans) {
+    PlanLayout L;
+    if (n_plans < 0) return -1;
+    if (layout_plans(plans, n_plans, nullptr, INT64_MAX, L) != EDGC_OK) return -1;
+    return L.ws_bytes;
+}
+
+extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_t *status_dev, void *ws,
+                                int64_t ws_bytes, void *stream) {
+    if (n_plans == 0) return EDGC_OK;
+    EDGC_REQUIRE(n_plans > 0 && plans && status_dev, "edgc_sample_plan: bad arguments");
+    PlanLayout L;
+    int rc = layout_plans(plans, n_plans, ws, ws_bytes, L);
+    if (rc != EDGC_OK) return rc;
+    EDGC_REQUIRE(L.ws_bytes <= ws_bytes, "edgc_sample_plan: workspace %lld < needed %lld", (long long)ws_bytes,
+                 (long long)L.ws_bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    PlanDev *d_plans = reinterpret_cast<PlanDev *>(ws);
+    EDGC_CUDA_TRY(cudaMemcpyAsync(d_plans, L.dev.data(), sizeof(PlanDev) * n_plans, cudaMemcpyHostToDevice, st));
+    EDGC_CUDA_TRY(cudaMemsetAsync(L.table_base, 0xFF, L.table_bytes, st));
+    const int64_t p1_blocks = ceil_div(L.draw_chunks, kP1Threads);
+    k_draws<<<(unsigned)p1_blocks, kP1Threads, 0, st>>>(d_plans, n_plans);
+    EDGC_LAUNCH_CHECK();
+    k_walk<<<n_plans, kWalkThreads, 0, st>>>(d_plans, status_dev);
+    EDGC_LAUNCH_CHECK();
+    k_index<<<(unsigned)L.step_blocks, kStepThreads, 0, st>>>(d_plans, n_plans);
+    EDGC_LAUNCH_CHECK();
+    k_resolve<<<(unsigned)L.step_blocks, kStepThreads, 0, st>>>(d_plans, n_plans);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+extern "C" int edgc_gather(int src_dtype, const void *src, const int32_t *idx, int64_t count, int dst_dtype,
+                           void *dst, void *stream) {
+    EDGC_REQUIRE((src_dtype == 0 || src_dtype == 1) && (dst_dtype == 0 || dst_dtype == 1) && count >= 0,
+                 "edgc_gather: bad dtype/count");
+    if (count == 0) return EDGC_OK;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>(ceil_div(count, threads), (int64_t)sm_count() * 16);
+    k_gather<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(src_dtype, src, idx, count, dst_dtype, dst);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}

@@ -1,0 +1,295 @@
+"""Data-parallel bucket engine: the B200 form of train_toy's EDGC step.
+
+One process per GPU.  Each rank owns its gradient matrices and one
+CompressorState per matrix, seeded exactly as the reference seeds worker w's
+states (grad_source.py:440-447).  A step is (grad_source.py:389-419):
+
+  1. compress every matrix of this rank (one grouped launch per phase:
+     pass 1, factor, pass 2, finalize) into a packed factor buffer
+     [P_0 | Q_0 | P_1 | Q_1 | ...];
+  2. exchange: one all-gather of the packed buffers over NCCL (W > 1);
+  3. reconstruct the DP average out_k = (1/W) sum_w P_{k,w} Q_{k,w}^T in
+     worker order (grad_source.py:404-408) — one grouped launch.
+
+Rank decisions come from the worker-0 entropy tracker (rank 0) and are
+broadcast; every rank then applies set_rank (grad_source.py:416-418, 469-471).
+
+Memory (per rank, fp32): gradients, the error-feedback base w and the output
+are m*n each; factors are 2 x sum (m + n) r_cap, basis and warm start
+sum n r_cap each.  Kernel plans (descriptor + tile tables) are uploaded once
+per rank configuration and reused, so a steady-state step is launches only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .compressor import DEVICE_COLUMN_TOL, basis_columns
+from .errors import DivergenceError
+from .seeds import state_seeds
+
+__all__ = ["BucketEngine", "GPT2_2P5B_LAYER", "GPT2_12P1B_LAYER", "gpt2_shapes"]
+
+# per-layer weight gradients (QKV, proj, fc1, fc2)
+GPT2_2P5B_LAYER = ((1920, 5760), (1920, 1920), (1920, 7680), (7680, 1920))
+GPT2_12P1B_LAYER = ((3584, 10752), (3584, 3584), (3584, 14336), (14336, 3584))
+
+
+def gpt2_shapes(which: str = "2.5B", layers: int | None = None):
+    layer, default = {"2.5B": (GPT2_2P5B_LAYER, 52), "12.1B": (GPT2_12P1B_LAYER, 76)}[which]
+    return [s for _ in range(default if layers is None else layers) for s in layer]
+
+
+class _Plan:
+    """Owns one bound C plan (compress or reconstruct) and its workspace."""
+
+    def __init__(self, kind: str, descs, device):
+        L = _lib.lib()
+        self.kind = kind
+        self.L = L
+        h = ctypes.c_void_p()
+        n = len(descs)
+        if kind == "compress":
+            arr = (_lib.CompressDesc * n)(*descs)
+            _lib.check(L.edgc_compress_plan_create(arr, n, ctypes.byref(h)), "compress plan")
+            nbytes = L.edgc_compress_plan_workspace_bytes(h)
+            self.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            _lib.check(L.edgc_compress_plan_bind(h, _lib.ptr(self.ws), self.ws.numel(), _lib.stream_ptr(device)),
+                       "compress plan bind")
+        else:
+            arr = (_lib.ReconDesc * n)(*descs)
+            _lib.check(L.edgc_recon_plan_create(arr, n, ctypes.byref(h)), "recon plan")
+            nbytes = L.edgc_recon_plan_workspace_bytes(h)
+            self.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            _lib.check(L.edgc_recon_plan_bind(h, _lib.ptr(self.ws), self.ws.numel(), _lib.stream_ptr(device)),
+                       "recon plan bind")
+        self.h = h
+        self.descs = arr
+
+    def run(self, stream, *, col_tol=None, status=None):
+        if self.kind == "compress":
+            _lib.check(self.L.edgc_compress_plan_run(self.h, col_tol, _lib.ptr(status), stream), "compress run")
+        else:
+            _lib.check(self.L.edgc_recon_plan_run(self.h, stream), "recon run")
+
+    def __del__(self):
+        try:
+            if self.h:
+                (self.L.edgc_compress_plan_destroy if self.kind == "compress" else self.L.edgc_recon_plan_destroy)(
+                    self.h)
+        except Exception:
+            pass
+
+
+class BucketEngine:
+    """One DP rank's bucket set: compress + exchange + averaged reconstruction."""
+
+    def __init__(self, shapes, rank: int, seed: int = 0, *, world_size: int = 1, rank_id: int = 0, group=None,
+                 rank_cap: int | None = None, col_tol: float = DEVICE_COLUMN_TOL, device=None):
+        self.L = _lib.lib()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.shapes = [(int(m), int(n)) for m, n in shapes]
+        if not self.shapes:
+            raise ValueError("need at least one matrix")
+        self.world, self.me, self.group = int(world_size), int(rank_id), group
+        self.col_tol = float(col_tol)
+        self.cap = max(int(rank), int(rank_cap or rank))
+        seeds = state_seeds(seed, self.world, len(self.shapes))
+        self.basis_seeds = [seeds[(self.me, k)] for k in range(len(self.shapes))]
+        dev = self.device
+        numel = [m * n for m, n in self.shapes]
+        self._mat_off = np.concatenate([[0], np.cumsum(numel)]).astype(np.int64)
+        total = int(self._mat_off[-1])
+        self.total_elems = total
+        self.grad_arena = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.w_arena = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.out_arena = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.grads = [self.grad_arena[a:b].view(m, n) for (a, b), (m, n) in zip(self._spans(), self.shapes)]
+        self.outs = [self.out_arena[a:b].view(m, n) for (a, b), (m, n) in zip(self._spans(), self.shapes)]
+        self.ws_views = [self.w_arena[a:b].view(m, n) for (a, b), (m, n) in zip(self._spans(), self.shapes)]
+        self._alloc_rank_buffers(self.cap)
+        self.ranks = [min(int(rank), min(m, n)) for m, n in self.shapes]
+        self._res = None            # (parity, ranks, offsets) of the residual factor pair
+        self._parity = 0
+        self._plans = {}
+        self.status = torch.zeros(len(self.shapes), dtype=torch.int32, device=dev)
+        self.steps = 0
+
+    # ------------------------------------------------------------ buffers
+    def _spans(self):
+        return [(int(self._mat_off[k]), int(self._mat_off[k + 1])) for k in range(len(self.shapes))]
+
+    def _alloc_rank_buffers(self, cap: int, old=None):
+        dev = self.device
+        bsz = sum(n * cap for _, n in self.shapes)
+        basis = torch.empty(bsz, dtype=torch.float32, device=dev)
+        qwarm = torch.empty(bsz, dtype=torch.float32, device=dev)
+        offs, cur = [], 0
+        for k, (m, n) in enumerate(self.shapes):
+            offs.append(cur)
+            old_cap = 0 if old is None else old["cap"]
+            view_b = basis[cur:cur + n * cap].view(n, cap)
+            view_q = qwarm[cur:cur + n * cap].view(n, cap)
+            if old is not None:
+                view_b[:, :old_cap] = old["basis"][k]
+                view_q[:, :old_cap] = old["q_warm"][k]
+            if cap > old_cap:
+                fresh = torch.from_numpy(basis_columns(self.basis_seeds[k], n, old_cap, cap)).to(dev)
+                view_b[:, old_cap:] = fresh
+                view_q[:, old_cap:] = fresh
+            cur += n * cap
+        self._basis_arena, self._qwarm_arena = basis, qwarm
+        self.basis = [basis[o:o + n * cap].view(n, cap) for o, (_, n) in zip(offs, self.shapes)]
+        self.q_warm = [qwarm[o:o + n * cap].view(n, cap) for o, (_, n) in zip(offs, self.shapes)]
+        fsz = sum((m + n) * cap for m, n in self.shapes)
+        new_fac = [torch.zeros(fsz, dtype=torch.float32, device=dev) for _ in range(2)]
+        if old is not None:
+            for i in range(2):
+                new_fac[i][:old["factors"][i].numel()] = old["factors"][i]
+        self.factors = new_fac
+        self.cap = cap
+        self._gathered = None
+        if self.world > 1:
+            self._gathered = torch.empty(self.world * fsz, dtype=torch.float32, device=dev)
+
+    def _packed_offsets(self, ranks):
+        offs, cur = [], 0
+        for (m, n), r in zip(self.shapes, ranks):
+            offs.append((cur, cur + m * r))
+            cur += (m + n) * r
+        return offs, cur
+
+    # -------------------------------------------------------------- plans
+    def _compress_plan(self):
+        ranks = tuple(self.ranks)
+        res = self._res
+        key = ("c", self._parity, ranks, None if res is None else (res[0], res[1]),
+               tuple(g.data_ptr() for g in self.grads))
+        plan = self._plans.get(key)
+        if plan is not None:
+            return plan
+        offs, _ = self._packed_offsets(ranks)
+        out_buf = self.factors[self._parity]
+        descs = []
+        for k, ((m, n), r) in enumerate(zip(self.shapes, ranks)):
+            p_res = q_res = None
+            r_res = 0
+            if res is not None:
+                rbuf = self.factors[res[0]]
+                (po, qo), r_res = res[2][k], res[1][k]
+                p_res = rbuf[po:]
+                q_res = rbuf[qo:]
+            po, qo = offs[k]
+            g = self.grads[k]
+            descs.append(_lib.CompressDesc(_lib.ptr(g), _lib.ptr(self.ws_views[k]), _lib.ptr(p_res), _lib.ptr(q_res),
+                                           _lib.ptr(self.q_warm[k]), _lib.ptr(self.basis[k]),
+                                           _lib.ptr(out_buf[po:]), _lib.ptr(out_buf[qo:]), m, n, g.stride(0), r,
+                                           r_res, self.cap, 0))
+        plan = _Plan("compress", descs, self.device)
+        self._plans[key] = plan
+        return plan
+
+    def _recon_plan(self):
+        ranks = tuple(self.ranks)
+        key = ("r", self._parity, ranks, tuple(o.data_ptr() for o in self.outs))
+        plan = self._plans.get(key)
+        if plan is not None:
+            return plan
+        offs, size = self._packed_offsets(ranks)
+        src = self.factors[self._parity] if self.world == 1 else self._gathered
+        descs = []
+        for k, ((m, n), r) in enumerate(zip(self.shapes, ranks)):
+            po, qo = offs[k]
+            o = self.outs[k]
+            descs.append(_lib.ReconDesc(_lib.ptr(src[po:]), _lib.ptr(src[qo:]), _lib.ptr(o), m, n, o.stride(0),
+                                        size, size, r, self.world, 1.0 / self.world, 0))
+        plan = _Plan("recon", descs, self.device)
+        self._plans[key] = plan
+        return plan
+
+    # --------------------------------------------------------------- step
+    def compress(self):
+        """Phase 1: compress every matrix of this rank into the packed factor buffer."""
+        stream = _lib.stream_ptr(self.device)
+        self._compress_plan().run(stream, col_tol=self.col_tol, status=self.status)
+
+    def exchange(self):
+        """Phase 2: all-gather the packed factors of every rank (NCCL); no-op at W = 1."""
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        _, size = self._packed_offsets(self.ranks)
+        dist.all_gather_into_tensor(self._gathered[:self.world * size].view(self.world, size),
+                                    self.factors[self._parity][:size], group=self.group)
+
+    def reconstruct(self):
+        """Phase 3: out_k = (1/W) sum_w P_kw Q_kw^T in worker order."""
+        self._recon_plan().run(_lib.stream_ptr(self.device))
+
+    def step(self, grads=None, check: bool = False):
+        """One DP step; returns the per-matrix averaged reconstructions (views of out_arena)."""
+        if grads is not None:
+            for dst, src in zip(self.grads, grads):
+                if dst.data_ptr() != src.data_ptr():
+                    dst.copy_(src, non_blocking=True)
+        self.compress()
+        self.exchange()
+        self.reconstruct()
+        offs, _ = self._packed_offsets(self.ranks)
+        self._res = (self._parity, tuple(self.ranks), offs)
+        self._parity ^= 1
+        self.steps += 1
+        if check:
+            self.check_status()
+        return self.outs
+
+    def check_status(self):
+        """Raise DivergenceError if any matrix saw a non-finite work entry (synchronises)."""
+        bad = torch.nonzero(self.status).flatten().tolist()
+        if bad:
+            raise DivergenceError(f"non-finite gradient or residual in matrices {bad[:8]}")
+
+    # ---------------------------------------------------------- state API
+    def set_rank(self, r: int):
+        """Apply a controller decision to every matrix: r_k = min(r, min(m, n)) (grad_source.py:469-471)."""
+        if r < 1:
+            raise ValueError(f"rank must be >= 1, got {r}")
+        if r > self.cap:
+            old = {"cap": self.cap, "basis": [b.clone() for b in self.basis],
+                   "q_warm": [q.clone() for q in self.q_warm], "factors": self.factors}
+            self._alloc_rank_buffers(r, old)
+            self._plans.clear()
+        new = [min(int(r), min(m, n)) for m, n in self.shapes]
+        for k, (ro, rn) in enumerate(zip(self.ranks, new)):
+            if rn > ro:
+                self.q_warm[k][:, ro:rn].copy_(self.basis[k][:, ro:rn])
+        self.ranks = new
+
+    def factors_of(self, k: int):
+        """(P, Q) of matrix k from the last step (views)."""
+        if self._res is None:
+            raise ValueError("no step has run yet")
+        parity, ranks, offs = self._res
+        buf = self.factors[parity]
+        (m, n), r, (po, qo) = self.shapes[k], ranks[k], offs[k]
+        return buf[po:po + m * r].view(m, r), buf[qo:qo + n * r].view(n, r)
+
+    def residual(self, k: int) -> torch.Tensor:
+        """Materialised error-feedback residual of matrix k (compressor.py:112)."""
+        m, n = self.shapes[k]
+        w = self.ws_views[k]
+        if self._res is None:
+            return w.clone()
+        p, q = self.factors_of(k)
+        out = torch.empty_like(w)
+        _lib.check(self.L.edgc_residual(_lib.ptr(w), _lib.ptr(p), _lib.ptr(q), p.shape[1], m, n, _lib.ptr(out),
+                                        _lib.stream_ptr(self.device)), "edgc_residual")
+        return out
+
+    def wire_bytes(self) -> int:
+        """Logical bytes this worker sends per step: 4 r (m + n) per matrix (grad_source.py:398-403)."""
+        return sum(4 * r * (m + n) for (m, n), r in zip(self.shapes, self.ranks))

@@ -1,0 +1,363 @@
+"""Gradient down-sampling (GDS) and entropy estimation on the device.
+
+Mirrors pkg/src/edgc/entropy.py name for name.  What runs where:
+
+* iteration gate, window bookkeeping, per-iteration layer mean: host Python,
+  identical arithmetic to the reference (entropy.py:53-64, 110-121, 158-192);
+* sampler seeds and PCG64 words: host NumPy (seeds.py);
+* sampled indices (NumPy ``Generator.choice`` rule), gather, Gaussian plug-in
+  and FD-histogram estimators: libedgc_b200.so kernels.  Indices and
+  histogram counts are bit-exact with the reference; entropies agree to fp64
+  reduction order (<1e-12 nats).
+"""
+
+from __future__ import annotations
+
+import csv
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DegenerateInputError
+from .matrix_core import as_device_array, as_device_matrix
+from .seeds import pcg64_words, subsample_seed
+
+__all__ = ["GAUSSIAN_ENTROPY_CONST", "SamplerConfig", "EntropyWindow", "should_sample_iteration",
+           "sampling_period", "sample_count", "sample_indices", "sample_plans", "subsample_entries",
+           "entropy_gaussian_plugin", "entropy_histogram", "histogram_fd", "close_window",
+           "relative_change_rate", "EntropyTracker", "write_window_csv"]
+
+GAUSSIAN_ENTROPY_CONST = 0.5 * math.log(2.0 * math.pi * math.e)
+
+# a single edgc_sample_plan call is capped at this much workspace; larger
+# bucket sets are planned in several calls
+_PLAN_WS_CAP = 3 << 30
+
+
+@dataclass(frozen=True)
+class SamplerConfig:
+    """Iteration-level rate alpha and element-level rate beta, both in (0, 1]."""
+
+    alpha: float = 0.1
+    beta: float = 0.25
+    rng_seed: int = 0
+
+    def __post_init__(self) -> None:
+        for name in ("alpha", "beta"):
+            v = getattr(self, name)
+            if not 0.0 < v <= 1.0:
+                raise ValueError(f"{name} must be in (0, 1], got {v}")
+
+
+@dataclass
+class EntropyWindow:
+    window_index: int
+    window_size: int
+    mean_entropy: float
+    samples_used: int
+    per_iteration_entropies: list = field(default_factory=list)
+
+
+def sampling_period(alpha: float) -> int:
+    return max(1, round(1.0 / alpha))
+
+
+def should_sample_iteration(iteration: int, alpha: float) -> bool:
+    """True on every round(1/alpha)-th iteration (Python's banker's rounding, as the reference)."""
+    if iteration < 0:
+        raise ValueError(f"iteration must be non-negative, got {iteration}")
+    if not 0.0 < alpha <= 1.0:
+        raise ValueError(f"alpha must be in (0, 1], got {alpha}")
+    return iteration % sampling_period(alpha) == 0
+
+
+def sample_count(n_elems: int, beta: float) -> int:
+    return min(n_elems, math.ceil(beta * n_elems))
+
+
+def sample_plans(specs, device=None):
+    """Device index plans for many (n_elems, count, seed) at once.
+
+    Returns a list of int32 CUDA tensors (None where count == n_elems, i.e. the
+    reference's full copy).  Order of each plan = NumPy's output order.
+    """
+    L = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    out = [None] * len(specs)
+    todo = []
+    for i, (n_elems, count, seed) in enumerate(specs):
+        if count == n_elems:
+            continue
+        if n_elems >= 2**31:
+            raise ValueError(f"sampling over {n_elems} >= 2^31 elements is outside the device plan's range")
+        out[i] = torch.empty(count, dtype=torch.int32, device=dev)
+        todo.append(i)
+    k = 0
+    while k < len(todo):
+        # grow the batch while the workspace stays under the cap
+        batch = []
+        while k < len(todo):
+            i = todo[k]
+            n_elems, count, seed = specs[i]
+            d = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]))
+            trial = (_lib.PlanDesc * (len(batch) + 1))(*(batch + [d]))
+            need = L.edgc_sample_plan_workspace_bytes(trial, len(batch) + 1)
+            if batch and need > _PLAN_WS_CAP:
+                break
+            batch.append(d)
+            k += 1
+        arr = (_lib.PlanDesc * len(batch))(*batch)
+        need = L.edgc_sample_plan_workspace_bytes(arr, len(batch))
+        if need < 0:
+            _lib.check(_lib.EDGC_EINVAL, "sample plan layout")
+        ws = _lib.WORKSPACE.get(need, dev)
+        status = torch.zeros(len(batch), dtype=torch.int32, device=dev)
+        _lib.check(L.edgc_sample_plan(arr, len(batch), _lib.ptr(status), _lib.ptr(ws), ws.numel(),
+                                      _lib.stream_ptr(dev)), "edgc_sample_plan")
+        bad = status.nonzero()
+        if bad.numel():
+            raise RuntimeError("sample plan exhausted its pre-generated draws")
+    return out
+
+
+def sample_indices(n_elems: int, beta: float, seed: int, device=None) -> torch.Tensor:
+    """The int64 flat indices subsample_entries draws (entropy.py:75-78), on the device."""
+    if not 0.0 < beta <= 1.0:
+        raise ValueError(f"beta must be in (0, 1], got {beta}")
+    count = sample_count(n_elems, beta)
+    plan = sample_plans([(n_elems, count, seed)], device)[0]
+    if plan is None:
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        return torch.arange(n_elems, dtype=torch.int64, device=dev)
+    return plan.to(torch.int64)
+
+
+def subsample_entries(matrix, beta: float, seed: int) -> torch.Tensor:
+    """ceil(beta*m*n) row-major entries without replacement, NumPy's order (entropy.py:67-79).
+
+    Returns a float64 CUDA tensor (values are the fp32 device entries, exactly).
+    """
+    if not 0.0 < beta <= 1.0:
+        raise ValueError(f"beta must be in (0, 1], got {beta}")
+    flat = as_device_matrix(matrix).reshape(-1)
+    count = sample_count(flat.numel(), beta)
+    if count == flat.numel():
+        return flat.to(torch.float64)
+    idx = sample_plans([(flat.numel(), count, seed)], flat.device)[0]
+    out = torch.empty(count, dtype=torch.float64, device=flat.device)
+    L = _lib.lib()
+    _lib.check(L.edgc_gather(0, _lib.ptr(flat), _lib.ptr(idx), count, 1, _lib.ptr(out), _lib.stream_ptr()),
+               "edgc_gather")
+    return out
+
+
+def _samples_tensor(samples) -> torch.Tensor:
+    if isinstance(samples, torch.Tensor) and samples.is_cuda and samples.dtype in (torch.float32, torch.float64):
+        return samples.reshape(-1).contiguous()
+    return as_device_array(np.asarray(samples, dtype=np.float64).ravel()
+                           if not isinstance(samples, torch.Tensor) else samples.double().reshape(-1),
+                           torch.float64)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    return 0 if t.dtype == torch.float32 else 1
+
+
+def _gaussian_batch(items, dtype_code: int, device) -> list:
+    """items: list of (src tensor, idx tensor or None, count) -> list of device entropies (float)."""
+    L = _lib.lib()
+    n = len(items)
+    descs = (_lib.GaussDesc * n)(*[_lib.GaussDesc(_lib.ptr(s), _lib.ptr(i), c) for s, i, c in items])
+    need = L.edgc_entropy_gaussian_workspace_bytes(descs, n)
+    ws = _lib.WORKSPACE.get(need, device)
+    h = torch.empty(n, dtype=torch.float64, device=device)
+    status = torch.empty(n, dtype=torch.int32, device=device)
+    _lib.check(L.edgc_entropy_gaussian(dtype_code, descs, n, _lib.ptr(h), _lib.ptr(status), _lib.ptr(ws),
+                                       ws.numel(), _lib.stream_ptr(device)), "edgc_entropy_gaussian")
+    h_host = h.cpu().tolist()
+    st_host = status.cpu().tolist()
+    for code in st_host:
+        if code == _lib.EDGC_EINVAL:
+            raise ValueError("need at least 2 samples")
+        if code == _lib.EDGC_EDEGENERATE:
+            raise DegenerateInputError("zero-variance sample has no differential entropy")
+        _lib.raise_device_status(code, "entropy_gaussian_plugin")
+    return h_host
+
+
+def entropy_gaussian_plugin(samples) -> float:
+    """ln(sigma_hat) + 0.5 ln(2 pi e) with the ddof=1 deviation (entropy.py:82-90)."""
+    x = _samples_tensor(samples)
+    if x.numel() < 2:
+        raise ValueError(f"need at least 2 samples, got {x.numel()}")
+    return _gaussian_batch([(x, None, x.numel())], _dtype_code(x), x.device)[0]
+
+
+def histogram_fd(samples, bins="fd"):
+    """Device np.histogram(x, bins) for bins == "fd" or an int: (counts int64, edges float64, H).
+
+    Counts and edges are bit-exact with NumPy 2.3.5.
+    """
+    x = _samples_tensor(samples)
+    n = x.numel()
+    if n < 2:
+        raise ValueError(f"need at least 2 samples, got {n}")
+    if isinstance(bins, str):
+        if bins != "fd":
+            raise NotImplementedError(f"bins={bins!r}: the device histogram implements 'fd' and integer bins")
+        fixed = 0
+    else:
+        fixed = int(bins)
+        if fixed < 1:
+            raise ValueError("`bins` must be positive, when an integer")
+    L = _lib.lib()
+    dev = x.device
+    ws = _lib.WORKSPACE.get(L.edgc_entropy_histogram_workspace_bytes(n), dev)
+    inv_cbrt = float(n) ** (-1.0 / 3.0) if n else 0.0  # x.size ** (-1/3): same libm pow as NumPy
+    cap = max(fixed, 1 << 16)
+    for _ in range(2):
+        counts = torch.empty(cap, dtype=torch.int64, device=dev)
+        edges = torch.empty(cap + 1, dtype=torch.float64, device=dev)
+        result = torch.empty(5, dtype=torch.float64, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.check(L.edgc_entropy_histogram(_dtype_code(x), _lib.ptr(x), n, inv_cbrt, fixed, cap, _lib.ptr(counts),
+                                            _lib.ptr(edges), _lib.ptr(result), _lib.ptr(status), _lib.ptr(ws),
+                                            ws.numel(), _lib.stream_ptr(dev)), "edgc_entropy_histogram")
+        code = int(status.item())
+        res = result.cpu().tolist()
+        if code == _lib.EDGC_ECAPACITY:
+            cap = int(res[4])
+            continue
+        if code == _lib.EDGC_EDEGENERATE:
+            raise DegenerateInputError("zero-range sample has no histogram entropy")
+        if code == _lib.EDGC_ETOOMANYBINS:
+            raise ValueError(f"Too many bins for data range. Cannot create {int(res[4])} finite-sized bins.")
+        _lib.raise_device_status(code, "entropy_histogram")
+        nb = int(res[4])
+        return counts[:nb], edges[:nb + 1], res[0]
+    raise RuntimeError("histogram bin capacity retry failed")
+
+
+def entropy_histogram(samples, bins="fd") -> float:
+    """-sum p ln(p / width) over the histogram (entropy.py:93-107)."""
+    return histogram_fd(samples, bins)[2]
+
+
+def close_window(records, window_index: int = 0, window_size: int | None = None) -> EntropyWindow:
+    values = [float(v) for v in records]
+    if not values:
+        raise DegenerateInputError("cannot close a window with no sampled iterations")
+    return EntropyWindow(window_index=window_index,
+                         window_size=len(values) if window_size is None else window_size,
+                         mean_entropy=float(np.mean(values)), samples_used=len(values),
+                         per_iteration_entropies=values)
+
+
+def relative_change_rate(series_sampled, series_full) -> np.ndarray:
+    """|H_sampled - H_full| / |H_full| per window (analysis metric, host)."""
+    a = np.asarray(series_sampled, dtype=np.float64)
+    b = np.asarray(series_full, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError(f"window series lengths differ: {a.shape} vs {b.shape}")
+    if np.any(b == 0.0):
+        raise DegenerateInputError("zero baseline entropy in relative change rate")
+    return np.abs(a - b) / np.abs(b)
+
+
+def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=None) -> list:
+    """Per-layer entropies of one sampled iteration, all layers batched on the device."""
+    estimator = entropy_gaussian_plugin if estimator is None else estimator
+    flats = [as_device_matrix(m).reshape(-1) for m in matrices]
+    if not flats:
+        return []
+    specs = []
+    for k, f in enumerate(flats):
+        n = f.numel()
+        specs.append((n, sample_count(n, config.beta), subsample_seed(config.rng_seed, iteration, k)))
+    plans = sample_plans(specs, flats[0].device)
+    if estimator is entropy_gaussian_plugin:
+        for f, (n, c, _) in zip(flats, specs):
+            if c < 2:
+                raise ValueError(f"need at least 2 samples, got {c}")
+        items = [(f, p, c) for f, p, (_, c, _) in zip(flats, plans, specs)]
+        return _gaussian_batch(items, 0, flats[0].device)
+    out = []
+    L = _lib.lib()
+    for f, p, (n, c, _) in zip(flats, plans, specs):
+        if estimator is entropy_histogram:
+            if p is None:
+                sub = f
+            else:
+                sub = torch.empty(c, dtype=torch.float32, device=f.device)
+                _lib.check(L.edgc_gather(0, _lib.ptr(f), _lib.ptr(p), c, 0, _lib.ptr(sub), _lib.stream_ptr()),
+                           "edgc_gather")
+            out.append(entropy_histogram(sub))
+        else:
+            sub = f.double() if p is None else f.double()[p.long()]
+            out.append(float(estimator(sub)))
+    return out
+
+
+class EntropyTracker:
+    """Per-iteration layer matrices -> fixed-size entropy windows (entropy.py:135-192).
+
+    Sampled iterations run one batched device pipeline over all layers (plans,
+    fused gather + estimator) and one device-to-host copy of the per-layer
+    entropies; the layer mean and window logic are the reference's, on the host.
+    """
+
+    def __init__(self, config: SamplerConfig, window: int, estimator=entropy_gaussian_plugin):
+        if window < 1:
+            raise ValueError(f"window must be positive, got {window}")
+        period = sampling_period(config.alpha)
+        if window < period:
+            raise ValueError(f"window {window} shorter than the sampling period {period}: "
+                             "windows could close empty")
+        self.config = config
+        self.window = window
+        self.estimator = estimator
+        self.windows: list[EntropyWindow] = []
+        self._pending: list[float] = []
+        self._current = 0
+
+    def observe(self, iteration: int, matrices) -> EntropyWindow | None:
+        closed = None
+        win = iteration // self.window
+        if win < self._current:
+            raise ValueError(f"iteration {iteration} precedes window {self._current}")
+        if win > self._current:
+            closed = self._close()
+            self._current = win
+        if should_sample_iteration(iteration, self.config.alpha):
+            per_layer = layer_entropies(list(matrices), iteration, self.config, self.estimator)
+            if per_layer:
+                self._pending.append(float(np.mean(per_layer)))
+        return closed
+
+    def flush(self) -> EntropyWindow | None:
+        if not self._pending:
+            return None
+        out = self._close()
+        self._current += 1
+        return out
+
+    def _close(self) -> EntropyWindow:
+        rec = close_window(self._pending, window_index=self._current, window_size=self.window)
+        self.windows.append(rec)
+        self._pending = []
+        return rec
+
+
+def write_window_csv(path, windows) -> None:
+    with open(path, "w", newline="") as fh:
+        out = csv.writer(fh, lineterminator="\n")
+        out.writerow(["window_index", "mean_entropy", "samples_used"])
+        for w in windows:
+            out.writerow([w.window_index, repr(w.mean_entropy), w.samples_used])
+
+
+_ = ctypes  # ctypes structures are built in _lib

@@ -1,0 +1,84 @@
+"""GPU: the bucket engine (grouped compress + reconstruct) against the oracle's DP step.
+
+W = 1 here (multi-rank exchange is covered by tests/test_dist.py on CPU/gloo
+and by the multi-GPU bench).  Worker-w states are seeded as the reference
+seeds them (grad_source.py:440-447), so a W-rank engine's rank-w factors are
+the reference worker w's.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from tests.helpers import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _shapes():
+    return [(256, 768), (256, 256), (256, 1024), (1024, 256), (48, 36), (7, 9)]
+
+
+@pytest.mark.parametrize("rank", [1, 4, 8, 16, 32])
+def test_engine_matches_oracle_dp_step_chained(rank):
+    from paper_2511_10333_b200.engine import BucketEngine
+    shapes = _shapes()
+    eng = BucketEngine(shapes, rank=rank, seed=3)
+    seeds = oracle.state_seeds(3, 1, len(shapes))
+    ost = [[oracle.OracleState(m, n, min(rank, m, n), seeds[(0, k)]) for k, (m, n) in enumerate(shapes)]]
+    worst = 0.0
+    for t in range(6):
+        gs = [oracle.synth_matrix(1, t, k, 0, m, n, 1e-2) for k, (m, n) in enumerate(shapes)]
+        for dst, g in zip(eng.grads, gs):
+            dst.copy_(torch.from_numpy(g))
+        outs = eng.step(check=True)
+        ref = oracle.dp_step([[g.astype(np.float64) for g in gs]], ost)
+        for k, (o, r) in enumerate(zip(outs, ref)):
+            worst = max(worst, rel_err(o, r))
+            if t == 5:
+                worst = max(worst, rel_err(eng.residual(k), ost[0][k].residual))
+    assert worst <= 5e-5, worst
+
+
+def test_engine_set_rank_matches_oracle():
+    from paper_2511_10333_b200.engine import BucketEngine
+    shapes = [(128, 384), (384, 128)]
+    eng = BucketEngine(shapes, rank=8, seed=0, rank_cap=8)
+    seeds = oracle.state_seeds(0, 1, 2)
+    ost = [[oracle.OracleState(m, n, 8, seeds[(0, k)]) for k, (m, n) in enumerate(shapes)]]
+    schedule = {2: 4, 4: 12, 5: 6}
+    for t in range(7):
+        if t in schedule:
+            eng.set_rank(schedule[t])
+            for s in ost[0]:
+                oracle.set_rank(s, schedule[t])
+        gs = [oracle.synth_matrix(2, t, k, 0, m, n, 1e-2) for k, (m, n) in enumerate(shapes)]
+        outs = eng.step([torch.from_numpy(g).cuda() for g in gs], check=True)
+        ref = oracle.dp_step([[g.astype(np.float64) for g in gs]], ost)
+        for o, r in zip(outs, ref):
+            assert rel_err(o, r) <= 5e-5
+
+
+def test_engine_nonfinite_raises_divergence():
+    from paper_2511_10333_b200.engine import BucketEngine
+    from paper_2511_10333_b200.errors import DivergenceError
+    eng = BucketEngine([(64, 64)], rank=4)
+    eng.grads[0].fill_(1.0)
+    eng.grads[0][3, 3] = float("nan")
+    with pytest.raises(DivergenceError):
+        eng.step(check=True)
+
+
+def test_engine_gpt2_layer_one_step():
+    """One full GPT2-2.5B layer (4 matrices, 30.7M elements) against the oracle."""
+    from paper_2511_10333_b200.engine import GPT2_2P5B_LAYER, BucketEngine
+    eng = BucketEngine(list(GPT2_2P5B_LAYER), rank=4, seed=0)
+    seeds = oracle.state_seeds(0, 1, 4)
+    ost = [[oracle.OracleState(m, n, 4, seeds[(0, k)]) for k, (m, n) in enumerate(GPT2_2P5B_LAYER)]]
+    for t in range(2):
+        gs = [oracle.synth_matrix(0, t, k, 0, m, n, 1e-2) for k, (m, n) in enumerate(GPT2_2P5B_LAYER)]
+        outs = eng.step([torch.from_numpy(g).cuda() for g in gs], check=True)
+        ref = oracle.dp_step([[g.astype(np.float64) for g in gs]], ost)
+        for o, r in zip(outs, ref):
+            assert rel_err(o, r) <= 1e-4

@@ -1,0 +1,78 @@
+"""GPU: NumPy-exact sampled indices (entropy.py:67-79) through the CUDA C-ABI.
+
+Bit-exact against the golden checksums made by NumPy 2.3.5 itself and against
+the C restatement (oracle/npchoice.c) on extra seeds.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from tests.helpers import load_json, sha, to_np
+
+pytestmark = pytest.mark.gpu
+
+CASES = load_json("choice.json")["cases"]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"N{c['N']}-b{c['beta']}-s{c['seed']}-{c['branch']}")
+def test_sample_indices_bit_exact_vs_numpy_golden(case):
+    from paper_2511_10333_b200.entropy import sample_indices
+    idx = to_np(sample_indices(case["N"], case["beta"], case["seed"])).astype(np.int64)
+    assert idx.size == case["count"]
+    assert idx[:16].tolist() == case["head"]
+    assert idx[-16:].tolist() == case["tail"]
+    assert sha(idx) == case["sha256"]
+
+
+def test_batched_plans_match_oracle_on_many_seeds():
+    """Both branches, several seeds per shape, all planned in ONE batched device call."""
+    from paper_2511_10333_b200.entropy import sample_count, sample_plans
+    specs = []
+    for n_elems in (12_345, 65_536, 1_000_000, 3_686_400):
+        for beta in (0.05, 0.051, 0.25, 0.5, 0.9):
+            for seed in (0, 7, 2**31 - 1):
+                specs.append((n_elems, sample_count(n_elems, beta), seed))
+    plans = sample_plans(specs)
+    for (n_elems, count, seed), p in zip(specs, plans):
+        ref = oracle.choice_indices(seed, n_elems, count)
+        assert np.array_equal(to_np(p).astype(np.int64), ref), (n_elems, count, seed)
+
+
+def test_subsample_entries_values_and_order():
+    from paper_2511_10333_b200.entropy import subsample_entries
+    rng = np.random.default_rng(5)
+    m = rng.standard_normal((300, 200)).astype(np.float32)
+    got = to_np(subsample_entries(m, 0.25, seed=77))
+    ref = oracle.subsample(m.astype(np.float64), 0.25, 77)
+    assert got.dtype == np.float64
+    assert np.array_equal(got, ref)
+    full = to_np(subsample_entries(m, 1.0, seed=0))
+    assert np.array_equal(full, m.astype(np.float64).ravel())
+
+
+def test_subsample_count_and_without_replacement():
+    from paper_2511_10333_b200.entropy import subsample_entries
+    m = np.arange(100.0, dtype=np.float32).reshape(10, 10)
+    out = to_np(subsample_entries(m, 0.5, seed=3))
+    assert out.size == 50 and len(set(out.tolist())) == 50
+    m = np.random.default_rng(0).standard_normal((64, 64)).astype(np.float32)
+    for beta in (0.1, 0.25, 0.333, 0.5, 0.999):
+        assert subsample_entries(m, beta, seed=1).numel() == math.ceil(beta * 4096)
+
+
+def test_bad_beta_raises():
+    from paper_2511_10333_b200.entropy import subsample_entries
+    with pytest.raises(ValueError):
+        subsample_entries(np.zeros((4, 4), np.float32), 0.0, 1)
+    with pytest.raises(ValueError):
+        subsample_entries(np.zeros((4, 4), np.float32), 1.5, 1)
+
+
+def test_native_library_is_loaded():
+    import paper_2511_10333_b200._lib as L
+    L.lib()
+    assert L._lib is not None and torch.cuda.is_available()
