@@ -1,0 +1,383 @@
+"""EDGC data-parallel hot-path benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric (BASELINE.json): EDGC grad GB/s — gradient bytes (4 B per fp32
+element, all ranks) pushed through entropy + compress + exchange + decompress
+per second, plus the fraction of the HBM roofline.  Workload (BASELINE.json
+configs[1]): the GPT2-2.5B-shaped bucket set (52 layers x {QKV 1920x5760,
+proj 1920x1920, fc1 1920x7680, fc2 7680x1920} = 208 matrices, 2.30e9 fp32
+elements = 9.2 GB per GPU) at rank 4, GSR beta = 0.25, ISR alpha = 0.1
+(entropy on every 10th iteration, as the reference's default SamplerConfig).
+
+A step = (sampled iterations only) device entropy of the worker-0 raw
+gradients [sampled indices -> fused gather + Gaussian plug-in], then the
+bucket engine: grouped compress with error feedback, NCCL all-gather of the
+packed factors (N > 1), averaged reconstruction.  Inputs are resident in HBM
+and 9.2 GB per GPU >> the 126 MB L2, so no flush is needed between steps.
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  `e2e` repeats the step through the same public API
+with the gradients copied in from pinned host memory and the averaged
+gradients copied back every step.
+
+`--impl reference` times the reference's CPU path (the oracle port: NumPy
+float64 compress/decompress + Generator.choice + std, exactly the calls
+train_toy makes) on the host cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EDGC grad GB/s (entropy+compress+AR+decompress) @1/2/4/8 B200; % HBM roofline"
+UNIT = "GB/s"
+SMI_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+REASON_NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", choices=["2.5B", "12.1B"], default="2.5B")
+    ap.add_argument("--layers", type=int, default=None, help="layers of the model shape set (default: all)")
+    ap.add_argument("--rank", type=int, default=4)
+    ap.add_argument("--alpha", type=float, default=0.1)
+    ap.add_argument("--beta", type=float, default=0.25)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=6, help="EF steps in the bounded CPU sample")
+    return ap.parse_args()
+
+
+def load_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(kernel: str):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            rec = json.load(fh)
+        return rec["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.proc = None
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={SMI_FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(gpu_index)], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "note": "nvidia-smi unavailable"}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons, n = [], None, set(), 0
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                n += 1
+                for name, val in zip(REASON_NAMES, parts[5:9]):
+                    if val.lower().startswith("active"):
+                        reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": n}
+
+
+# ----------------------------------------------------------------- CPU side
+
+def cpu_reference_sample(shapes, rank, alpha, beta, seed, steps):
+    """Time the reference's CPU path (oracle port) on one layer; returns (GB/s, detail)."""
+    import numpy as np
+
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    layer = shapes[:4]
+    elems = sum(m * n for m, n in layer)
+    grads = [oracle.synth_matrix(seed, 0, k, 0, m, n, 1e-2).astype(np.float64) for k, (m, n) in enumerate(layer)]
+    seeds = oracle.state_seeds(seed, 1, len(layer))
+    states = [[oracle.OracleState(m, n, min(rank, m, n), seeds[(0, k)]) for k, (m, n) in enumerate(layer)]]
+    oracle.dp_step([grads], states)  # warm call (BLAS thread pool, page faults)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.dp_step([grads], states)
+    t_step = (time.perf_counter() - t0) / steps
+    # worker-0 entropy of one sampled iteration: NumPy Generator.choice + gather + std (entropy.py:67-90)
+    t0 = time.perf_counter()
+    for k, g in enumerate(grads):
+        n_el = g.size
+        cnt = oracle.sample_count(n_el, beta)
+        sub = g.ravel() if cnt == n_el else g.ravel()[
+            np.random.default_rng(oracle.subsample_seed(seed, 0, k)).choice(n_el, size=cnt, replace=False,
+                                                                          shuffle=False)]
+        oracle.gaussian_entropy(sub)
+    t_ent = time.perf_counter() - t0
+    per_step = t_step + alpha * t_ent
+    gbs = 4.0 * elems / per_step / 1e9
+    sample = (f"1 GPT-2 layer ({len(layer)} matrices, {elems / 1e6:.1f}M fp32 elements) of the bucket set: "
+              f"{steps} error-feedback steps of compress+decompress (NumPy f64/OpenBLAS) at r={rank}, plus one "
+              f"sampled-iteration entropy pass (Generator.choice + std, beta={beta}) weighted by alpha={alpha}; "
+              f"{t_step * 1e3:.0f} ms/step + {t_ent * 1e3:.0f} ms/entropy pass")
+    return gbs, {"cores": cores, "sample": sample, "t_step_s": t_step, "t_entropy_s": t_ent}
+
+
+def run_reference(args):
+    rank_env = int(os.environ.get("RANK", "0"))
+    if rank_env != 0:
+        return 0
+    from paper_2511_10333_b200.engine import gpt2_shapes
+    shapes = gpt2_shapes(args.model, args.layers)
+    total = sum(m * n for m, n in shapes)
+    vals = []
+    det = None
+    for _ in range(max(1, args.warmup and 1)):
+        cpu_reference_sample(shapes, args.rank, args.alpha, args.beta, args.seed, 1)
+    for _ in range(max(1, min(args.steps, 3))):
+        v, det = cpu_reference_sample(shapes, args.rank, args.alpha, args.beta, args.seed, args.cpu_steps)
+        vals.append(v)
+    value = statistics.median(vals)
+    ms = 4.0 * total / (value * 1e9) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, shapes),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": det["cores"], "kind": "port",
+                         "sample": det["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference CPU path = oracle port (NumPy float64, OpenBLAS on all host cores; choice/MGS "
+                "single-threaded as in NumPy); ms_per_step scaled from the one-layer sample to the full set",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, shapes):
+    total = sum(m * n for m, n in shapes)
+    return {"workload": f"GPT2-{args.model} bucket set: {len(shapes)} matrices, {total / 1e9:.3f}e9 fp32 "
+                        f"elements ({4 * total / 1e9:.2f} GB) per GPU",
+            "rank": args.rank, "alpha": args.alpha, "beta": args.beta, "estimator": "gaussian_plugin",
+            "l2": "inputs 9.2 GB/GPU >> 126 MB L2 (no flush needed)" if args.model == "2.5B" and args.layers is None
+            else "inputs larger than L2", "parallelism": f"dp{args.gpus}"}
+
+
+# ------------------------------------------------------------------ GPU side
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_10333_b200 import _lib
+    from paper_2511_10333_b200.engine import BucketEngine, gpt2_shapes
+    from paper_2511_10333_b200.entropy import EntropyTracker, SamplerConfig, sample_count
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    me = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.lib()
+    shapes = gpt2_shapes(args.model, args.layers)
+    total = sum(m * n for m, n in shapes)
+    eng = BucketEngine(shapes, rank=args.rank, seed=args.seed, world_size=world, rank_id=me)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + me)
+    chunk = 1 << 28
+    for a in range(0, total, chunk):
+        b = min(total, a + chunk)
+        eng.grad_arena[a:b].normal_(0.0, 1e-2, generator=gen)
+    cfg = SamplerConfig(alpha=args.alpha, beta=args.beta, rng_seed=args.seed)
+    tracker = EntropyTracker(cfg, window=max(100, args.steps + args.warmup + 10)) if me == 0 else None
+    period = max(1, round(1.0 / args.alpha))
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    def one_step(t, ev=None):
+        if tracker is not None and t % period == 0:
+            if ev is not None:
+                ev["ent0"].append(torch.cuda.Event(enable_timing=True))
+                ev["ent0"][-1].record(stream)
+            tracker.observe(t, eng.grads)
+            if ev is not None:
+                ev["ent1"].append(torch.cuda.Event(enable_timing=True))
+                ev["ent1"][-1].record(stream)
+        marks = []
+        if ev is not None:
+            marks = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            marks[0].record(stream)
+        eng.compress(_lib.PHASE_PASS1)
+        if ev is not None:
+            marks[1].record(stream)
+        eng.compress(_lib.PHASE_FACTOR)
+        if ev is not None:
+            marks[2].record(stream)
+        eng.compress(_lib.PHASE_PASS2 | _lib.PHASE_FINALIZE)
+        if ev is not None:
+            marks[3].record(stream)
+        eng.exchange()
+        if ev is not None:
+            marks[4].record(stream)
+        eng.reconstruct()
+        if ev is not None:
+            marks[5].record(stream)
+            ev["marks"].append(marks)
+        eng.advance()
+
+    for t in range(args.warmup):
+        one_step(t)
+    eng.check_status()
+    barrier()
+    clocks = ClockSampler(local) if me == 0 else None
+    launches0 = L.edgc_launch_count()
+    ev = {"ent0": [], "ent1": [], "marks": []}
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    start.record(stream)
+    for t in range(args.warmup, args.warmup + args.steps):
+        one_step(t, ev)
+    stop.record(stream)
+    barrier()
+    launches = L.edgc_launch_count() - launches0
+    clk = clocks.stop() if clocks is not None else None
+    eng.check_status()
+    elapsed = start.elapsed_time(stop) / 1e3
+    t_max = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_all = float(t_max.item())
+    value = world * 4.0 * total * args.steps / t_all / 1e9
+    # per-phase device times (ms, mean over timed steps)
+    names = ["pass1", "factor", "pass2_finalize", "exchange", "reconstruct"]
+    ph = {n: 0.0 for n in names}
+    for mk in ev["marks"]:
+        for i, n in enumerate(names):
+            ph[n] += mk[i].elapsed_time(mk[i + 1]) / len(ev["marks"])
+    ent_ms = [a.elapsed_time(b) for a, b in zip(ev["ent0"], ev["ent1"])]
+    ph["entropy_per_sampled_step"] = statistics.mean(ent_ms) if ent_ms else 0.0
+    ph["entropy_sampled_steps"] = len(ent_ms)
+    peak, peak_src = load_peak()
+    # dominant kernel: pass 1 (error feedback + P = W Q): reads g and w, writes w: 12 B per element
+    alg_bytes = {"pass1": 12.0 * total, "pass2_finalize": 4.0 * total, "reconstruct": 4.0 * total}
+    dom = max(alg_bytes, key=lambda k: ph[k])
+    dom_ms = ph[dom]
+    achieved = alg_bytes[dom] / (dom_ms / 1e3) / 1e9
+    traffic = load_traffic({"pass1": "k_pass1", "pass2_finalize": "k_pass2", "reconstruct": "k_recon"}[dom])
+    n_sampled = len(ent_ms)
+    ent_bytes = 4.0 * sum(sample_count(m * n, args.beta) for m, n in shapes) * n_sampled / max(1, args.steps)
+    step_frac = (16.0 * total + ent_bytes) / (t_all / args.steps) / 1e9 / peak
+    line = None
+    if me == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_all / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(args, shapes),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": alg_bytes[dom], "peak_source": peak_src,
+                         "step_hbm_frac": step_frac,
+                         "step_alg_bytes": "16 B/elem (read g, read e, write e', write out) + 4 B/sample on "
+                                           "sampled iterations (SURVEY.md 8(d))"},
+            "phases_ms": ph,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+    # ---------------------------------------------------------------- e2e
+    if not args.no_e2e:
+        ke = max(1, args.e2e_steps)
+        host_g = torch.empty(total, dtype=torch.float32, pin_memory=True)
+        host_out = torch.empty(total, dtype=torch.float32, pin_memory=True)
+        host_g.copy_(eng.grad_arena)
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = args.warmup + args.steps
+        s0.record(stream)
+        for t in range(t0, t0 + ke):
+            eng.grad_arena.copy_(host_g, non_blocking=True)
+            if tracker is not None and t % period == 0:
+                tracker.observe(t, eng.grads)
+            eng.step()
+            host_out.copy_(eng.out_arena, non_blocking=True)
+        s1.record(stream)
+        barrier()
+        te = torch.tensor([s0.elapsed_time(s1) / 1e3], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        if line is not None:
+            line["e2e"] = {"value": world * 4.0 * total * ke / float(te.item()) / 1e9, "unit": UNIT,
+                           "h2d_bytes_per_step": 4 * total, "d2h_bytes_per_step": 4 * total, "steps": ke,
+                           "path": "BucketEngine.step with gradients H2D from pinned host memory and the averaged "
+                                   "gradients D2H every step"}
+        del host_g, host_out
+    # ------------------------------------------------------- CPU baseline
+    if line is not None and world == 1 and not args.no_cpu_baseline:
+        v, det = cpu_reference_sample(shapes, args.rank, args.alpha, args.beta, args.seed, args.cpu_steps)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": det["cores"], "kind": "port",
+                                "sample": det["sample"]}
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    _ = np
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -50,6 +50,8 @@ typedef enum {
 int edgc_abi_version(void);
 /* Message for the last non-OK status returned on the calling thread. */
 const char *edgc_last_error(void);
+/* Number of kernels this library has launched in the process so far. */
+int64_t edgc_launch_count(void);
 
 /* ------------------------------------------------------------------------
  * Sample plan — replaces np.random.default_rng(seed).choice(N, count,
@@ -131,8 +133,13 @@ typedef struct {
     const float *basis;   /* n x r (ld ld_q): fresh columns, compressor.py:63-66 */
     float *p_out;         /* m x r (ld r): orthonormal P (dead columns = 0)     */
     float *q_out;         /* n x r (ld r): W^T P, dead columns reseeded         */
+    double *precond;      /* state, r_cap x r_cap (ld ld_s) upper-triangular warm-start
+                             preconditioner, identity at creation; NULL = none.  Any
+                             such right factor leaves MGS(w q_warm) unchanged; the
+                             library keeps it equal to the last step's transform so
+                             the one-sweep Q = Z T path stays well conditioned.  */
     int64_t m, n, ld_g;
-    int32_t r, r_res, ld_q, pad_;
+    int32_t r, r_res, ld_q, ld_s;
 } edgc_compress_desc;
 
 /* Persistent plan: descriptors and tile tables are uploaded into the
@@ -143,7 +150,17 @@ typedef struct edgc_compress_plan edgc_compress_plan;
 int edgc_compress_plan_create(const edgc_compress_desc *descs, int n, edgc_compress_plan **out);
 int64_t edgc_compress_plan_workspace_bytes(const edgc_compress_plan *plan);
 int edgc_compress_plan_bind(edgc_compress_plan *plan, void *ws, int64_t ws_bytes, void *stream);
-int edgc_compress_plan_run(edgc_compress_plan *plan, double col_tol, int32_t *status_dev, void *stream);
+/* phases: bit mask of the EDGC_PHASE_* steps to launch (EDGC_PHASE_ALL for a
+ * full step); running them in order in separate calls is equivalent. */
+enum {
+    EDGC_PHASE_PASS1 = 1,     /* error feedback + P_raw partials (clears status) */
+    EDGC_PHASE_FACTOR = 2,    /* P_raw reduce + CholQR2 -> P                     */
+    EDGC_PHASE_PASS2 = 4,     /* Q partials = w^T P                               */
+    EDGC_PHASE_FINALIZE = 8,  /* Q reduce, dead-column reseed, warm start        */
+    EDGC_PHASE_ALL = 15
+};
+int edgc_compress_plan_run(edgc_compress_plan *plan, double col_tol, int32_t *status_dev, int phases,
+                           void *stream);
 void edgc_compress_plan_destroy(edgc_compress_plan *plan);
 
 int64_t edgc_compress_workspace_bytes(const edgc_compress_desc *descs, int n);

@@ -27,6 +27,8 @@ EDGC_ETOOMANYBINS = 6
 EDGC_ECAPACITY = 7
 EDGC_EDRAWS = 8
 
+PHASE_PASS1, PHASE_FACTOR, PHASE_PASS2, PHASE_FINALIZE, PHASE_ALL = 1, 2, 4, 8, 15
+
 c_i32, c_i64, c_u64, c_f32, c_f64, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float,
                                            ctypes.c_double, ctypes.c_void_p)
 
@@ -42,8 +44,8 @@ class GaussDesc(ctypes.Structure):
 
 class CompressDesc(ctypes.Structure):
     _fields_ = [("g", c_vp), ("w", c_vp), ("p_res", c_vp), ("q_res", c_vp), ("q_warm", c_vp), ("basis", c_vp),
-                ("p_out", c_vp), ("q_out", c_vp), ("m", c_i64), ("n", c_i64), ("ld_g", c_i64),
-                ("r", c_i32), ("r_res", c_i32), ("ld_q", c_i32), ("pad_", c_i32)]
+                ("p_out", c_vp), ("q_out", c_vp), ("precond", c_vp), ("m", c_i64), ("n", c_i64), ("ld_g", c_i64),
+                ("r", c_i32), ("r_res", c_i32), ("ld_q", c_i32), ("ld_s", c_i32)]
 
 
 class ReconDesc(ctypes.Structure):
@@ -56,6 +58,7 @@ class ReconDesc(ctypes.Structure):
 SIGNATURES = {
     "edgc_abi_version": (c_i32, []),
     "edgc_last_error": (ctypes.c_char_p, []),
+    "edgc_launch_count": (c_i64, []),
     "edgc_sample_plan_workspace_bytes": (c_i64, [ctypes.POINTER(PlanDesc), c_i32]),
     "edgc_sample_plan": (c_i32, [ctypes.POINTER(PlanDesc), c_i32, c_vp, c_vp, c_i64, c_vp]),
     "edgc_gather": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
@@ -67,7 +70,7 @@ SIGNATURES = {
     "edgc_compress_plan_create": (c_i32, [ctypes.POINTER(CompressDesc), c_i32, ctypes.POINTER(c_vp)]),
     "edgc_compress_plan_workspace_bytes": (c_i64, [c_vp]),
     "edgc_compress_plan_bind": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
-    "edgc_compress_plan_run": (c_i32, [c_vp, c_f64, c_vp, c_vp]),
+    "edgc_compress_plan_run": (c_i32, [c_vp, c_f64, c_vp, c_i32, c_vp]),
     "edgc_compress_plan_destroy": (None, [c_vp]),
     "edgc_compress_workspace_bytes": (c_i64, [ctypes.POINTER(CompressDesc), c_i32]),
     "edgc_compress": (c_i32, [ctypes.POINTER(CompressDesc), c_i32, c_f64, c_vp, c_vp, c_i64, c_vp]),

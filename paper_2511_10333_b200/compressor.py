@@ -77,6 +77,7 @@ class CompressorState:
         self._cap = 0
         self._basis = torch.empty((n, 0), dtype=torch.float32, device=dev)
         self._q_warm = torch.empty((n, 0), dtype=torch.float32, device=dev)
+        self._precond = torch.empty((0, 0), dtype=torch.float64, device=dev)
         self._grow(rank)
         self._q_warm[:, :rank].copy_(self._basis[:, :rank])
         # residual factor pair of the last compress (None: residual == w)
@@ -93,7 +94,9 @@ class CompressorState:
         basis[:, self._cap:] = fresh
         qw[:, :self._cap] = self._q_warm
         qw[:, self._cap:] = fresh
-        self._basis, self._q_warm, self._cap = basis, qw, cap
+        pre = torch.eye(cap, dtype=torch.float64, device=self.device)
+        pre[:self._cap, :self._cap] = self._precond
+        self._basis, self._q_warm, self._precond, self._cap = basis, qw, pre, cap
 
     @property
     def q_warm(self) -> torch.Tensor:
@@ -136,7 +139,8 @@ def compress(matrix, state: CompressorState) -> LowRankFactors:
     q = torch.empty((state.n, r), dtype=torch.float32, device=state.device)
     desc = _lib.CompressDesc(_lib.ptr(g), _lib.ptr(state._w), _lib.ptr(p_res), _lib.ptr(q_res),
                              _lib.ptr(state._q_warm), _lib.ptr(state._basis), _lib.ptr(p), _lib.ptr(q),
-                             state.m, state.n, g.stride(0), r, r_res, state._cap, 0)
+                             _lib.ptr(state._precond), state.m, state.n, g.stride(0), r, r_res, state._cap,
+                             state._cap)
     arr = (_lib.CompressDesc * 1)(desc)
     need = L.edgc_compress_workspace_bytes(arr, 1)
     if need < 0:
@@ -186,6 +190,10 @@ def set_rank(state: CompressorState, r_new: int) -> None:
     if r_new > r_old:
         state._grow(r_new)
         state._q_warm[:, r_old:r_new].copy_(state._basis[:, r_old:r_new])
+        # fresh warm-start columns restart unpreconditioned
+        state._precond[:, r_old:r_new] = 0.0
+        state._precond[r_old:r_new, r_old:r_new] = torch.eye(r_new - r_old, dtype=torch.float64,
+                                                             device=state.device)
     state.rank = r_new
 
 

@@ -1,4 +1,5 @@
 // ABI plumbing: version, thread-local error text, device queries.
+#include <atomic>
 #include <stdarg.h>
 #include <stdio.h>
 
@@ -14,6 +15,10 @@ void set_error(const char *fmt, ...) {
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
 }
+
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int sm_count() {
     static thread_local int cached = 0;
@@ -31,3 +36,5 @@ int sm_count() {
 extern "C" int edgc_abi_version(void) { return EDGC_ABI_VERSION; }
 
 extern "C" const char *edgc_last_error(void) { return edgc::g_err; }
+
+extern "C" int64_t edgc_launch_count(void) { return (int64_t)edgc::g_launches.load(); }

@@ -11,6 +11,8 @@ namespace edgc {
 
 // Thread-local message for edgc_last_error().
 void set_error(const char *fmt, ...);
+// Process-wide count of kernels this library has launched (edgc_launch_count).
+void count_launch();
 
 #define EDGC_CUDA_TRY(expr)                                                          \
     do {                                                                              \
@@ -24,6 +26,7 @@ void set_error(const char *fmt, ...);
 
 #define EDGC_LAUNCH_CHECK()                                                          \
     do {                                                                              \
+        ::edgc::count_launch();                                                       \
         cudaError_t _e = cudaGetLastError();                                          \
         if (_e != cudaSuccess) {                                                      \
             ::edgc::set_error("%s:%d launch: %s", __FILE__, __LINE__,               \
@@ -74,8 +77,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 // two, V <= 32), in a butterfly that halves the live set each step: after the
 // call lane l holds the full warp sum of value index (l / (32 / V)) in v[0]...
 // Fixed association order => deterministic.
-template <int V>
-__device__ __forceinline__ double warp_reduce_scatter(double (&v)[V], int lane) {
+template <int V, typename T>
+__device__ __forceinline__ T warp_reduce_scatter(T (&v)[V], int lane) {
     int cur = V;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -85,8 +88,8 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[V], int lane) 
 #pragma unroll
             for (int i = 0; i < V / 2; ++i) {
                 if (i < half) {
-                    double send = upper ? v[i] : v[i + half];
-                    double keep = upper ? v[i + half] : v[i];
+                    T send = upper ? v[i] : v[i + half];
+                    T keep = upper ? v[i + half] : v[i];
                     v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
             }

@@ -15,8 +15,22 @@
 //            (compressor.py:113-114); q_warm <- Q
 // HBM traffic per element: pass 1 reads g, w and writes w (12 B); pass 2
 // reads w (4 B); the reconstruction writes out (4 B).
+//
+// Z path (r <= 4, n <= 8192, float4-aligned): pass 1 runs as thread-block
+// clusters, one cluster per row strip, one CTA per 1024-column chunk.  Row
+// dots are exchanged through distributed shared memory each 8-row round, so
+// every CTA knows P_raw rows while their w values are still in registers and
+// accumulates Z = w^T P_raw in the same sweep.  Then Q = w^T P = Z T with the
+// CholQR transform T, and pass 2 is skipped: 16 B/elem for the whole step.
+// The warm start is preconditioned by the previous step's transform (any
+// upper-triangular right factor leaves MGS(P) unchanged), which keeps T well
+// conditioned; if cond(R) still exceeds kappa_max the matrix falls back to
+// the re-read pass 2 on the device (status bit 1).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -39,9 +53,18 @@ struct MatDev {
     double *p_part;   // [nchunk1][m][r]
     double *p_raw;    // [m][r]
     double *q_part;   // [nblk2][n][r]
-    double *tmat;     // [r][r] combined T (column-major per column j: tmat[j*r + i])
+    double *tmat;     // [r][r] combined T (column j at tmat[j*r .. j*r+r))
     int32_t *dead;    // [r]
     int32_t nchunk1, nblk2;
+    double *precond;  // state: r_cap x r_cap upper-triangular warm-start preconditioner (or NULL)
+    double *zpart;    // [nitems][n][r] Z partials (Z path)
+    int32_t ld_s, zmode, nitems, zc;   // zc = cluster size (column chunks) on the Z path
+};
+
+// Z-path work item: one row strip of one matrix, processed by one cluster
+struct ZTile {
+    int32_t mat, item;
+    int64_t row0, row1;
 };
 
 // pass-1 / pass-2 tiles
@@ -58,6 +81,10 @@ constexpr int kP2Threads = 256;
 constexpr int kP2Rows = 256;    // rows per pass-2 tile (one fp64 partial per block)
 constexpr int kFactorThreads = 256;
 constexpr int kMaxRank = 32;
+constexpr int kZThreads = 256;
+constexpr int kZRB = 8;        // rows per DSMEM exchange round
+constexpr int kZRows = 512;    // rows per cluster work item
+constexpr double kKappaMax = 64.0;
 
 template <int VEC> struct VecT;
 template <> struct VecT<4> {
@@ -169,6 +196,148 @@ __global__ void __launch_bounds__(kP1Threads) k_pass1(const MatDev *mats, const 
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
 }
 
+// ------------------------------------------------------------ pass 1 (Z)
+template <int RMAX>
+__global__ void __launch_bounds__(kZThreads, 2) k_pass1z(const MatDev *mats, const ZTile *tiles, int32_t *status) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int C = (int)cluster.num_blocks();
+    const int c = (int)cluster.block_rank();
+    const ZTile t = tiles[blockIdx.x / C];
+    const MatDev &M = mats[t.mat];
+    constexpr int RB = kZRB;
+    constexpr int V = RB * RMAX;
+    constexpr int VW = V < 32 ? V : 32;
+    constexpr int NB = V / VW;
+    constexpr int NWARP = kZThreads / 32;
+    const int r = M.r, rr_res = M.r_res;
+    const int64_t n = M.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t col0 = ((int64_t)c * kZThreads + tid) * 4;
+    const bool active = col0 < n;
+
+    __shared__ double s_S[RMAX * RMAX];
+    __shared__ float s_pres[RB][RMAX];
+    __shared__ double s_red[NWARP][V];
+    __shared__ double s_part[2][V];
+    __shared__ float s_prow[RB][RMAX];
+
+    if (tid < RMAX * RMAX) {
+        const int i = tid / RMAX, k = tid % RMAX;
+        double v = (i == k) ? 1.0 : 0.0;
+        if (M.precond && i < r && k < r) v = M.precond[(int64_t)i * M.ld_s + k];
+        s_S[tid] = v;
+    }
+    __syncthreads();
+    // preconditioned warm start qw = q_warm S (S upper triangular), residual factor qr
+    float qw[4][RMAX], qr[4][RMAX];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        double raw[RMAX];
+#pragma unroll
+        for (int k = 0; k < RMAX; ++k) raw[k] = (active && k < r) ? (double)M.q_warm[(col0 + v) * M.ld_q + k] : 0.0;
+#pragma unroll
+        for (int k = 0; k < RMAX; ++k) {
+            double a = 0.0;
+#pragma unroll
+            for (int i = 0; i <= k; ++i) a += raw[i] * s_S[i * RMAX + k];
+            qw[v][k] = (float)a;
+            qr[v][k] = (active && k < rr_res) ? M.q_res[(col0 + v) * rr_res + k] : 0.f;
+        }
+    }
+    float zacc[4][RMAX];
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int k = 0; k < RMAX; ++k) zacc[v][k] = 0.f;
+    bool bad = false;
+    int buf = 0;
+    for (int64_t row = t.row0; row < t.row1; row += RB, buf ^= 1) {
+        if (tid < RB * RMAX) {
+            const int rr = tid / RMAX, k = tid % RMAX;
+            const int64_t i = row + rr;
+            s_pres[rr][k] = (k < rr_res && i < t.row1) ? M.p_res[i * rr_res + k] : 0.f;
+        }
+        __syncthreads();
+        float x[RB][4];
+        float acc[V];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            const int64_t i = row + rr;
+            float pk[RMAX];
+#pragma unroll
+            for (int k = 0; k < RMAX; ++k) pk[k] = 0.f;
+            if (active && i < t.row1) {
+                float gv[4], wv[4];
+                VecT<4>::unpack(VecT<4>::ld_cs(M.g + i * M.ld_g + col0), gv);
+                VecT<4>::unpack(VecT<4>::ld_cs(M.w + i * n + col0), wv);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    float dot = 0.f;
+#pragma unroll
+                    for (int k = 0; k < RMAX; ++k) dot = fmaf(s_pres[rr][k], qr[v][k], dot);
+                    const float xv = gv[v] + (wv[v] - dot);
+                    bad |= !isfinite(xv);
+                    wv[v] = xv;
+                    x[rr][v] = xv;
+#pragma unroll
+                    for (int k = 0; k < RMAX; ++k) pk[k] = fmaf(xv, qw[v][k], pk[k]);
+                }
+                VecT<4>::st(M.w + i * n + col0, wv);
+            } else {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) x[rr][v] = 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < RMAX; ++k) acc[rr * RMAX + k] = pk[k];
+        }
+        // CTA partial of this round's row dots: fp32 butterfly in the warp, fp64 across warps
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            float part[VW];
+#pragma unroll
+            for (int q = 0; q < VW; ++q) part[q] = acc[b * VW + q];
+            const float sv = warp_reduce_scatter<VW>(part, lane);
+            const int owner = scatter_owner_index<VW>(lane);
+            if ((lane & ((32 / VW) - 1)) == 0) s_red[warp][b * VW + owner] = (double)sv;
+        }
+        __syncthreads();
+        if (tid < V) {
+            double a = 0.0;
+#pragma unroll
+            for (int w = 0; w < NWARP; ++w) a += s_red[w][tid];
+            s_part[buf][tid] = a;
+        }
+        // exchange through distributed shared memory: every CTA sums the C
+        // column-chunk partials in the same order -> identical P_raw rows
+        cluster.sync();
+        if (tid < V) {
+            double a = 0.0;
+            for (int cc = 0; cc < C; ++cc) a += cluster.map_shared_rank(&s_part[buf][0], cc)[tid];
+            const int rr = tid / RMAX, k = tid % RMAX;
+            const int64_t i = row + rr;
+            s_prow[rr][k] = (float)a;
+            if (c == 0 && i < t.row1 && k < r) M.p_raw[i * r + k] = a;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr)
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+                for (int k = 0; k < RMAX; ++k) zacc[v][k] = fmaf(x[rr][v], s_prow[rr][k], zacc[v][k]);
+    }
+    if (active) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+            for (int k = 0; k < RMAX; ++k)
+                if (k < r) M.zpart[((int64_t)t.item * n + col0 + v) * r + k] = (double)zacc[v][k];
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
+    cluster.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
 // ------------------------------------------------------------------ factor
 // One CTA per matrix.  Gram via per-thread (entry, row-group) sums reduced in
 // shared memory in fixed order; the r x r Cholesky runs on one thread.
@@ -205,7 +374,7 @@ __device__ void gram_pass(const double *P, int64_t m, int r, double *s_gram, dou
 // Cholesky of the Gram with MGS dead-column semantics; returns T = R^{-1}
 // (dead columns zero) in s_t (column j at s_t[j*r .. j*r+r)).
 __device__ void chol_inverse(const double *s_gram, int r, double tol, int32_t *dead, double *s_R, double *s_t,
-                             bool detect) {
+                             bool detect, const double *col_scale = nullptr) {
     for (int j = 0; j < r; ++j) {
         for (int i = 0; i < j; ++i) {
             if (dead[i]) { s_R[i * r + j] = 0.0; continue; }
@@ -216,7 +385,7 @@ __device__ void chol_inverse(const double *s_gram, int r, double tol, int32_t *d
         double d = s_gram[j * r + j];
         for (int i = 0; i < j; ++i) d -= s_R[i * r + j] * s_R[i * r + j];
         const double nrm = sqrt(fmax(d, 0.0));
-        if (detect) dead[j] = !(nrm > tol);
+        if (detect) dead[j] = !(nrm > tol * (col_scale ? col_scale[j] : 1.0));
         s_R[j * r + j] = dead[j] ? 0.0 : nrm;
     }
     for (int j = 0; j < r; ++j) {
@@ -234,7 +403,7 @@ __device__ void chol_inverse(const double *s_gram, int r, double tol, int32_t *d
     }
 }
 
-__global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, const int32_t *status, double col_tol) {
+__global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, int32_t *status, double col_tol) {
     const MatDev &M = mats[blockIdx.x];
     if (status[blockIdx.x] & 1) return;
     const int r = M.r;
@@ -243,23 +412,64 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, c
     __shared__ double s_R[kMaxRank * kMaxRank];
     __shared__ double s_t1[kMaxRank * kMaxRank];
     __shared__ double s_t2[kMaxRank * kMaxRank];
+    __shared__ double s_S[kMaxRank * kMaxRank];    // preconditioner S[i][k] at i*r + k
     __shared__ double s_tmp[kFactorThreads];
+    __shared__ double s_scale[kMaxRank];
     __shared__ int32_t s_dead[kMaxRank];
-    // P_raw = sum over column chunks, fixed order
-    for (int64_t e = threadIdx.x; e < m * r; e += kFactorThreads) {
-        double s = 0.0;
-        for (int c = 0; c < M.nchunk1; ++c) s += M.p_part[(int64_t)c * m * r + e];
-        M.p_raw[e] = s;
+    const bool pre = M.zmode && M.precond;
+    if (!M.zmode) {
+        // P_raw = sum over column chunks, fixed order
+        for (int64_t e = threadIdx.x; e < m * r; e += kFactorThreads) {
+            double s = 0.0;
+            for (int c = 0; c < M.nchunk1; ++c) s += M.p_part[(int64_t)c * m * r + e];
+            M.p_raw[e] = s;
+        }
+    }
+    for (int e = threadIdx.x; e < r * r; e += kFactorThreads) {
+        const int i = e / r, k = e % r;
+        s_S[e] = pre ? M.precond[(int64_t)i * M.ld_s + k] : (i == k ? 1.0 : 0.0);
     }
     __syncthreads();
     gram_pass(M.p_raw, m, r, s_gram, s_tmp);
     if (threadIdx.x == 0) {
+        // P_raw = P_orig S with P_orig = w q_warm.  The reference's tolerance is
+        // relative to ||P_orig||_F (compressor.py:79) and its column test uses
+        // the P_orig projection norms = R_jj / S_jj.
         double fro2 = 0.0;
-        for (int j = 0; j < r; ++j) fro2 += s_gram[j * r + j];
-        // compressor.py:79: tol = _COLUMN_TOL * ||P||_F, fixed before the sweep
-        const double tol = col_tol * sqrt(fro2);
-        for (int j = 0; j < r; ++j) s_dead[j] = 0;
-        chol_inverse(s_gram, r, tol, s_dead, s_R, s_t1, true);
+        if (pre) {
+            // Sinv (upper triangular), column j at s_t2[j*r..]
+            for (int j = 0; j < r; ++j) {
+                for (int l = 0; l < r; ++l) s_t2[j * r + l] = 0.0;
+                for (int l = j; l >= 0; --l) {
+                    double v = (l == j) ? 1.0 : 0.0;
+                    for (int q = l + 1; q <= j; ++q) v -= s_S[l * r + q] * s_t2[j * r + q];
+                    s_t2[j * r + l] = v / s_S[l * r + l];
+                }
+            }
+            for (int j = 0; j < r; ++j) {
+                double a = 0.0;
+                for (int u = 0; u <= j; ++u)
+                    for (int v = 0; v <= j; ++v) a += s_t2[j * r + u] * s_gram[u * r + v] * s_t2[j * r + v];
+                fro2 += a;
+            }
+        } else {
+            for (int j = 0; j < r; ++j) fro2 += s_gram[j * r + j];
+        }
+        for (int j = 0; j < r; ++j) { s_dead[j] = 0; s_scale[j] = s_S[j * r + j]; }
+        const double tol = col_tol * sqrt(fro2);   // fixed before the sweep, compressor.py:79
+        chol_inverse(s_gram, r, tol, s_dead, s_R, s_t1, true, s_scale);
+        if (M.zmode) {
+            double rn = 0.0, tn = 0.0;
+            for (int j = 0; j < r; ++j) {
+                if (s_dead[j]) continue;
+                for (int i = 0; i <= j; ++i) {
+                    if (s_dead[i]) continue;
+                    rn += s_R[i * r + j] * s_R[i * r + j];
+                    tn += s_t1[j * r + i] * s_t1[j * r + i];
+                }
+            }
+            if (sqrt(rn * tn) > kKappaMax) atomicOr(status + blockIdx.x, 2);
+        }
     }
     __syncthreads();
     // P1 = P_raw T1 in place (row-local)
@@ -288,6 +498,28 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, c
         }
     }
     if (threadIdx.x < r) M.dead[threadIdx.x] = s_dead[threadIdx.x];
+    if (threadIdx.x == 0) {
+        // T = T1 T2: P = P_raw T, and on the Z path Q = Z T
+        for (int j = 0; j < r; ++j)
+            for (int l = 0; l < r; ++l) {
+                double a = 0.0;
+                for (int i = l; i <= j; ++i) a += s_t1[i * r + l] * s_t2[j * r + i];
+                M.tmat[j * r + l] = a;
+            }
+        if (pre) {
+            // next preconditioner A = S T (dead columns restart from e_j)
+            for (int j = 0; j < r; ++j)
+                for (int i = 0; i < r; ++i) {
+                    double a = 0.0;
+                    if (s_dead[j]) {
+                        a = (i == j) ? 1.0 : 0.0;
+                    } else {
+                        for (int l = i; l <= j; ++l) a += s_S[i * r + l] * M.tmat[j * r + l];
+                    }
+                    M.precond[(int64_t)i * M.ld_s + j] = a;
+                }
+        }
+    }
 }
 
 // ------------------------------------------------------------------ pass 2
@@ -297,7 +529,8 @@ template <int VEC, int RMAX>
 __global__ void __launch_bounds__(kP2Threads) k_pass2(const MatDev *mats, const Tile *tiles, const int32_t *status) {
     const Tile t = tiles[blockIdx.x];
     const MatDev &M = mats[t.mat];
-    if (status[t.mat] & 1) return;
+    const int st = status[t.mat];
+    if ((st & 1) || (M.zmode && !(st & 2))) return;   // Z path: only on the kappa fallback
     const int r = M.r;
     const int64_t n = M.n;
     const int tid = threadIdx.x;
@@ -351,31 +584,46 @@ __global__ void __launch_bounds__(kP2Threads) k_pass2(const MatDev *mats, const 
 // ---------------------------------------------------------------- finalize
 __global__ void k_finalize(const MatDev *mats, const int32_t *status) {
     const MatDev &M = mats[blockIdx.y];
-    if (status[blockIdx.y] & 1) return;
+    const int st = status[blockIdx.y];
+    if (st & 1) return;
     const int r = M.r;
     const int64_t n = M.n;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * r; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = e / r;
-        const int k = (int)(e % r);
-        float q;
-        if (M.dead[k]) {
-            q = M.basis[j * M.ld_q + k];   // compressor.py:113-114
-        } else {
+    const bool zq = M.zmode && !(st & 2);
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        double z[kMaxRank];
+        for (int k = 0; k < r; ++k) {
             double s = 0.0;
-            for (int b = 0; b < M.nblk2; ++b) s += M.q_part[((int64_t)b * n + j) * r + k];
-            q = (float)s;
+            if (zq)
+                for (int b = 0; b < M.nitems; ++b) s += M.zpart[((int64_t)b * n + j) * r + k];
+            else
+                for (int b = 0; b < M.nblk2; ++b) s += M.q_part[((int64_t)b * n + j) * r + k];
+            z[k] = s;
         }
-        M.q_out[j * r + k] = q;
-        M.q_warm[j * M.ld_q + k] = q;
+        for (int k = 0; k < r; ++k) {
+            float q;
+            if (M.dead[k]) {
+                q = M.basis[j * M.ld_q + k];   // compressor.py:113-114
+            } else if (zq) {
+                double a = 0.0;
+                for (int l = 0; l <= k; ++l) a += z[l] * M.tmat[k * r + l];
+                q = (float)a;
+            } else {
+                q = (float)z[k];
+            }
+            M.q_out[j * r + k] = q;
+            M.q_warm[j * M.ld_q + k] = q;
+        }
     }
 }
 
 struct Plan {
     std::vector<MatDev> mats;
     std::vector<Tile> t1v4, t1v1, t2v4, t2v1;
+    std::vector<ZTile> tz[9];          // Z-path items grouped by cluster size 1..8
     int64_t bytes = 0;
     MatDev *d_mats = nullptr;
     Tile *d_t1v4 = nullptr, *d_t1v1 = nullptr, *d_t2v4 = nullptr, *d_t2v1 = nullptr;
+    ZTile *d_tz[9] = {};
     int rmax4 = 0, rmax1 = 0;
 };
 
@@ -398,15 +646,24 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.g = d.g; M.w = d.w; M.p_res = d.p_res; M.q_res = d.q_res; M.q_warm = d.q_warm; M.basis = d.basis;
         M.p_out = d.p_out; M.q_out = d.q_out;
         M.m = d.m; M.n = d.n; M.ld_g = d.ld_g; M.r = d.r; M.r_res = d.r_res; M.ld_q = d.ld_q;
+        M.precond = d.precond; M.ld_s = d.ld_s;
         const bool v4 = (d.n % 4 == 0) && (d.ld_g % 4 == 0) && ((uintptr_t)d.g % 16 == 0) &&
                         ((uintptr_t)d.w % 16 == 0) && std::max(d.r, d.r_res) <= 4;
         M.vec = v4 ? 4 : 1;
+        static const bool z_off = std::getenv("EDGC_NO_ZPATH") != nullptr;
+        const int zc = (int)ceil_div(d.n, 4 * kZThreads);
+        M.zmode = (!z_off && v4 && std::max(d.r, d.r_res) <= 4 && zc <= 8) ? 1 : 0;
+        M.zc = zc;
+        M.nitems = M.zmode ? (int32_t)ceil_div(d.m, kZRows) : 0;
+        if (M.zmode)
+            for (int32_t it = 0; it < M.nitems; ++it)
+                P.tz[zc].push_back(ZTile{k, it, (int64_t)it * kZRows, std::min(d.m, (int64_t)(it + 1) * kZRows)});
         const int64_t slots = d.n / M.vec;
         const int64_t threads1 = kP1Threads;
         M.nchunk1 = (int32_t)ceil_div(slots, threads1);
         M.nblk2 = (int32_t)ceil_div(d.m, kP2Rows);
         (v4 ? P.rmax4 : P.rmax1) = std::max(v4 ? P.rmax4 : P.rmax1, std::max(d.r, d.r_res));
-        for (int32_t c = 0; c < M.nchunk1; ++c)
+        for (int32_t c = 0; c < (M.zmode ? 0 : M.nchunk1); ++c)
             for (int64_t r0 = 0; r0 < d.m; r0 += kP1Rows) {
                 Tile t{k, c, c * threads1, std::min(slots, (c + 1) * threads1), r0, std::min(d.m, r0 + kP1Rows)};
                 (v4 ? P.t1v4 : P.t1v1).push_back(t);
@@ -421,7 +678,8 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     }
     for (int k = 0; k < n; ++k) {
         MatDev &M = P.mats[k];
-        M.p_part = a.take<double>((int64_t)M.nchunk1 * M.m * M.r);
+        M.p_part = a.take<double>(M.zmode ? 0 : (int64_t)M.nchunk1 * M.m * M.r);
+        M.zpart = a.take<double>((int64_t)M.nitems * M.n * M.r);
         M.p_raw = a.take<double>(M.m * M.r);
         M.q_part = a.take<double>((int64_t)M.nblk2 * M.n * M.r);
         M.tmat = a.take<double>((int64_t)M.r * M.r);
@@ -431,6 +689,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     P.d_t1v1 = a.take<Tile>(P.t1v1.size());
     P.d_t2v4 = a.take<Tile>(P.t2v4.size());
     P.d_t2v1 = a.take<Tile>(P.t2v1.size());
+    for (int c = 1; c <= 8; ++c) P.d_tz[c] = a.take<ZTile>(P.tz[c].size());
     P.bytes = a.off;
     return EDGC_OK;
 }
@@ -447,6 +706,27 @@ int launch_pass1(const Plan &P, bool v4, int32_t *status, cudaStream_t st) {
     else if (rmax <= 16) k_pass1<1, 16, 1><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
     else k_pass1<1, 32, 1><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
     EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+int launch_pass1z(const Plan &P, int32_t *status, cudaStream_t st) {
+    for (int c = 1; c <= 8; ++c) {
+        if (P.tz[c].empty()) continue;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(P.tz[c].size() * c));
+        cfg.blockDim = dim3(kZThreads);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = c;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1z<4>, (const MatDev *)P.d_mats, (const ZTile *)P.d_tz[c], status));
+        EDGC_LAUNCH_CHECK();
+    }
     return EDGC_OK;
 }
 
@@ -603,27 +883,41 @@ extern "C" int edgc_compress_plan_bind(edgc_compress_plan *h, void *ws, int64_t 
     EDGC_CUDA_TRY(up(P.d_t1v1, P.t1v1));
     EDGC_CUDA_TRY(up(P.d_t2v4, P.t2v4));
     EDGC_CUDA_TRY(up(P.d_t2v1, P.t2v1));
+    for (int c = 1; c <= 8; ++c)
+        if (!P.tz[c].empty())
+            EDGC_CUDA_TRY(cudaMemcpyAsync(P.d_tz[c], P.tz[c].data(), sizeof(ZTile) * P.tz[c].size(),
+                                          cudaMemcpyHostToDevice, st));
     // the host staging vectors stay alive in the plan; make the upload complete
     // before the caller could destroy or rebind it
     EDGC_CUDA_TRY(cudaStreamSynchronize(st));
     return EDGC_OK;
 }
 
-extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int32_t *status_dev, void *stream) {
+extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int32_t *status_dev, int phases,
+                                      void *stream) {
     EDGC_REQUIRE(h && status_dev && h->P.d_mats, "edgc_compress_plan_run: plan not bound");
     const Plan &P = h->P;
     const int n = (int)h->descs.size();
     cudaStream_t st = (cudaStream_t)stream;
     int rc;
-    EDGC_CUDA_TRY(cudaMemsetAsync(status_dev, 0, sizeof(int32_t) * n, st));
-    if ((rc = launch_pass1(P, true, status_dev, st))) return rc;
-    if ((rc = launch_pass1(P, false, status_dev, st))) return rc;
-    k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
-    EDGC_LAUNCH_CHECK();
-    if ((rc = launch_pass2(P, true, status_dev, st))) return rc;
-    if ((rc = launch_pass2(P, false, status_dev, st))) return rc;
-    k_finalize<<<dim3(16, n), 256, 0, st>>>(P.d_mats, status_dev);
-    EDGC_LAUNCH_CHECK();
+    if (phases & EDGC_PHASE_PASS1) {
+        EDGC_CUDA_TRY(cudaMemsetAsync(status_dev, 0, sizeof(int32_t) * n, st));
+        if ((rc = launch_pass1(P, true, status_dev, st))) return rc;
+        if ((rc = launch_pass1(P, false, status_dev, st))) return rc;
+        if ((rc = launch_pass1z(P, status_dev, st))) return rc;
+    }
+    if (phases & EDGC_PHASE_FACTOR) {
+        k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
+        EDGC_LAUNCH_CHECK();
+    }
+    if (phases & EDGC_PHASE_PASS2) {
+        if ((rc = launch_pass2(P, true, status_dev, st))) return rc;
+        if ((rc = launch_pass2(P, false, status_dev, st))) return rc;
+    }
+    if (phases & EDGC_PHASE_FINALIZE) {
+        k_finalize<<<dim3(16, n), 256, 0, st>>>(P.d_mats, status_dev);
+        EDGC_LAUNCH_CHECK();
+    }
     return EDGC_OK;
 }
 
@@ -642,7 +936,7 @@ extern "C" int edgc_compress(const edgc_compress_desc *descs, int n, double col_
     int rc = edgc_compress_plan_create(descs, n, &h);
     if (rc != EDGC_OK) return rc;
     rc = edgc_compress_plan_bind(h, ws, ws_bytes, stream);
-    if (rc == EDGC_OK) rc = edgc_compress_plan_run(h, col_tol, status_dev, stream);
+    if (rc == EDGC_OK) rc = edgc_compress_plan_run(h, col_tol, status_dev, EDGC_PHASE_ALL, stream);
     edgc_compress_plan_destroy(h);
     return rc;
 }

@@ -317,7 +317,7 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
         blocks += ceil_div(d.count, kStepThreads);
         int64_t cap = 1;
         int lg = 0;
-        while (cap < 2 * d.count) { cap <<= 1; ++lg; }
+        while (cap < d.count + d.count / 2) { cap <<= 1; ++lg; }
         P.cap = cap;
         P.log2cap = lg;
         caps[i] = cap;

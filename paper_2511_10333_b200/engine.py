@@ -44,6 +44,43 @@ def gpt2_shapes(which: str = "2.5B", layers: int | None = None):
     return [s for _ in range(default if layers is None else layers) for s in layer]
 
 
+def packed_offsets(shapes, ranks):
+    """Offsets of (P_k, Q_k) in one rank's packed factor buffer and its total size (elements).
+
+    Layout: [P_0 (m_0 x r_0) | Q_0 (n_0 x r_0) | P_1 | Q_1 | ...], row-major, ld = r_k.
+    """
+    offs, cur = [], 0
+    for (m, n), r in zip(shapes, ranks):
+        offs.append((cur, cur + m * r))
+        cur += (m + n) * r
+    return offs, cur
+
+
+def gather_packed(send, gathered, world: int, group=None) -> None:
+    """All-gather every rank's packed factors into gathered[w * size:(w + 1) * size] (rank order).
+
+    NCCL: one all_gather_into_tensor.  Other backends (gloo in the CPU tests):
+    all_gather into views of the same buffer, so the layout is identical.
+    """
+    import torch.distributed as dist
+    size = send.numel()
+    out = gathered[:world * size]
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out.view(world, size), send, group=group)
+    else:
+        views = list(out.view(world, size).unbind(0))
+        dist.all_gather(views, send, group=group)
+
+
+def broadcast_decision(rank, device, group=None, src: int = 0):
+    """Rank `src`'s window decision (an int or None) on every rank (grad_source.py:469-471 on all workers)."""
+    import torch.distributed as dist
+    t = torch.tensor([-1 if rank is None else int(rank)], dtype=torch.int64, device=device)
+    dist.broadcast(t, src=src, group=group)
+    v = int(t.item())
+    return None if v < 0 else v
+
+
 class _Plan:
     """Owns one bound C plan (compress or reconstruct) and its workspace."""
 
@@ -70,9 +107,10 @@ class _Plan:
         self.h = h
         self.descs = arr
 
-    def run(self, stream, *, col_tol=None, status=None):
+    def run(self, stream, *, col_tol=None, status=None, phases=_lib.PHASE_ALL):
         if self.kind == "compress":
-            _lib.check(self.L.edgc_compress_plan_run(self.h, col_tol, _lib.ptr(status), stream), "compress run")
+            _lib.check(self.L.edgc_compress_plan_run(self.h, col_tol, _lib.ptr(status), phases, stream),
+                       "compress run")
         else:
             _lib.check(self.L.edgc_recon_plan_run(self.h, stream), "recon run")
 
@@ -143,6 +181,11 @@ class BucketEngine:
                 view_q[:, old_cap:] = fresh
             cur += n * cap
         self._basis_arena, self._qwarm_arena = basis, qwarm
+        pre = torch.zeros(len(self.shapes), cap, cap, dtype=torch.float64, device=dev)
+        pre[:] = torch.eye(cap, dtype=torch.float64, device=dev)
+        if old is not None:
+            pre[:, :old["cap"], :old["cap"]] = old["precond"]
+        self.precond = pre
         self.basis = [basis[o:o + n * cap].view(n, cap) for o, (_, n) in zip(offs, self.shapes)]
         self.q_warm = [qwarm[o:o + n * cap].view(n, cap) for o, (_, n) in zip(offs, self.shapes)]
         fsz = sum((m + n) * cap for m, n in self.shapes)
@@ -157,11 +200,7 @@ class BucketEngine:
             self._gathered = torch.empty(self.world * fsz, dtype=torch.float32, device=dev)
 
     def _packed_offsets(self, ranks):
-        offs, cur = [], 0
-        for (m, n), r in zip(self.shapes, ranks):
-            offs.append((cur, cur + m * r))
-            cur += (m + n) * r
-        return offs, cur
+        return packed_offsets(self.shapes, ranks)
 
     # -------------------------------------------------------------- plans
     def _compress_plan(self):
@@ -187,8 +226,9 @@ class BucketEngine:
             g = self.grads[k]
             descs.append(_lib.CompressDesc(_lib.ptr(g), _lib.ptr(self.ws_views[k]), _lib.ptr(p_res), _lib.ptr(q_res),
                                            _lib.ptr(self.q_warm[k]), _lib.ptr(self.basis[k]),
-                                           _lib.ptr(out_buf[po:]), _lib.ptr(out_buf[qo:]), m, n, g.stride(0), r,
-                                           r_res, self.cap, 0))
+                                           _lib.ptr(out_buf[po:]), _lib.ptr(out_buf[qo:]),
+                                           _lib.ptr(self.precond[k]), m, n, g.stride(0), r, r_res, self.cap,
+                                           self.cap))
         plan = _Plan("compress", descs, self.device)
         self._plans[key] = plan
         return plan
@@ -212,19 +252,21 @@ class BucketEngine:
         return plan
 
     # --------------------------------------------------------------- step
-    def compress(self):
-        """Phase 1: compress every matrix of this rank into the packed factor buffer."""
+    def compress(self, phases: int = _lib.PHASE_ALL):
+        """Phase 1: compress every matrix of this rank into the packed factor buffer.
+
+        `phases` selects sub-steps (pass 1, factor, pass 2, finalize) so a caller
+        can bracket each with CUDA events; issuing them in order == PHASE_ALL.
+        """
         stream = _lib.stream_ptr(self.device)
-        self._compress_plan().run(stream, col_tol=self.col_tol, status=self.status)
+        self._compress_plan().run(stream, col_tol=self.col_tol, status=self.status, phases=phases)
 
     def exchange(self):
         """Phase 2: all-gather the packed factors of every rank (NCCL); no-op at W = 1."""
         if self.world == 1:
             return
-        import torch.distributed as dist
         _, size = self._packed_offsets(self.ranks)
-        dist.all_gather_into_tensor(self._gathered[:self.world * size].view(self.world, size),
-                                    self.factors[self._parity][:size], group=self.group)
+        gather_packed(self.factors[self._parity][:size], self._gathered, self.world, self.group)
 
     def reconstruct(self):
         """Phase 3: out_k = (1/W) sum_w P_kw Q_kw^T in worker order."""
@@ -239,13 +281,17 @@ class BucketEngine:
         self.compress()
         self.exchange()
         self.reconstruct()
+        self.advance()
+        if check:
+            self.check_status()
+        return self.outs
+
+    def advance(self):
+        """Close a step issued phase by phase: the factors just written become the residual pair."""
         offs, _ = self._packed_offsets(self.ranks)
         self._res = (self._parity, tuple(self.ranks), offs)
         self._parity ^= 1
         self.steps += 1
-        if check:
-            self.check_status()
-        return self.outs
 
     def check_status(self):
         """Raise DivergenceError if any matrix saw a non-finite work entry (synchronises)."""
@@ -260,13 +306,16 @@ class BucketEngine:
             raise ValueError(f"rank must be >= 1, got {r}")
         if r > self.cap:
             old = {"cap": self.cap, "basis": [b.clone() for b in self.basis],
-                   "q_warm": [q.clone() for q in self.q_warm], "factors": self.factors}
+                   "q_warm": [q.clone() for q in self.q_warm], "factors": self.factors,
+                   "precond": self.precond.clone()}
             self._alloc_rank_buffers(r, old)
             self._plans.clear()
         new = [min(int(r), min(m, n)) for m, n in self.shapes]
         for k, (ro, rn) in enumerate(zip(self.ranks, new)):
             if rn > ro:
                 self.q_warm[k][:, ro:rn].copy_(self.basis[k][:, ro:rn])
+                self.precond[k][:, ro:rn] = 0.0
+                self.precond[k][ro:rn, ro:rn] = torch.eye(rn - ro, dtype=torch.float64, device=self.device)
         self.ranks = new
 
     def factors_of(self, k: int):

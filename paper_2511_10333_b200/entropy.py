@@ -33,9 +33,16 @@ __all__ = ["GAUSSIAN_ENTROPY_CONST", "SamplerConfig", "EntropyWindow", "should_s
 
 GAUSSIAN_ENTROPY_CONST = 0.5 * math.log(2.0 * math.pi * math.e)
 
-# a single edgc_sample_plan call is capped at this much workspace; larger
-# bucket sets are planned in several calls
-_PLAN_WS_CAP = 3 << 30
+
+
+def _plan_ws_cap(device) -> int:
+    """Workspace cap of one edgc_sample_plan call: half the free HBM (>= 2 GiB).
+
+    All plans of a batch walk concurrently (one CTA each), so fewer, larger
+    batches are faster; bucket sets beyond the cap are planned in several calls.
+    """
+    free, _ = torch.cuda.mem_get_info(device)
+    return max(2 << 30, free // 2)
 
 
 @dataclass(frozen=True)
@@ -96,6 +103,7 @@ def sample_plans(specs, device=None):
             raise ValueError(f"sampling over {n_elems} >= 2^31 elements is outside the device plan's range")
         out[i] = torch.empty(count, dtype=torch.int32, device=dev)
         todo.append(i)
+    cap_bytes = _plan_ws_cap(dev)
     k = 0
     while k < len(todo):
         # grow the batch while the workspace stays under the cap
@@ -106,7 +114,7 @@ def sample_plans(specs, device=None):
             d = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]))
             trial = (_lib.PlanDesc * (len(batch) + 1))(*(batch + [d]))
             need = L.edgc_sample_plan_workspace_bytes(trial, len(batch) + 1)
-            if batch and need > _PLAN_WS_CAP:
+            if batch and need > cap_bytes:
                 break
             batch.append(d)
             k += 1

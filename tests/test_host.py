@@ -38,7 +38,7 @@ def test_workspace_queries_need_no_device():
     assert lib.edgc_sample_plan_workspace_bytes(plans, 2) > 4 * (1_048_576 + 552_960)
     bad = (_lib.PlanDesc * 1)(_lib.PlanDesc(1, 2, 3, 5, 10, 10, None))
     assert lib.edgc_sample_plan_workspace_bytes(bad, 1) == -1
-    d = (_lib.CompressDesc * 1)(_lib.CompressDesc(1, 1, 0, 0, 1, 1, 1, 1, 1920, 7680, 7680, 4, 0, 4, 0))
+    d = (_lib.CompressDesc * 1)(_lib.CompressDesc(1, 1, 0, 0, 1, 1, 1, 1, 0, 1920, 7680, 7680, 4, 0, 4, 4))
     assert lib.edgc_compress_workspace_bytes(d, 1) > 1920 * 4 * 8
 
 
