@@ -59,6 +59,9 @@ struct MatDev {
     double *precond;  // state: r_cap x r_cap upper-triangular warm-start preconditioner (or NULL)
     double *zpart;    // [nitems][n][r] Z partials (Z path)
     int32_t ld_s, zmode, nitems, zc;   // zc = cluster size (column chunks) on the Z path
+    double *fwork;    // 5 r^2 factor scratch
+    double *p_tmp;    // [m][r] CholQR intermediate
+    int32_t wide, pad_;   // wide = 1: tiled GEMM path (r > 8 or unaligned)
 };
 
 // Z-path work item: one row strip of one matrix, processed by one cluster
@@ -80,7 +83,9 @@ constexpr int kP1Rows = 64;     // rows per pass-1 tile
 constexpr int kP2Threads = 256;
 constexpr int kP2Rows = 256;    // rows per pass-2 tile (one fp64 partial per block)
 constexpr int kFactorThreads = 256;
-constexpr int kMaxRank = 32;
+constexpr int kMaxRank = 1024;     // device limit (TMEM-free fp32 path)
+constexpr int kNarrow = 8;         // register kernels up to this rank
+constexpr int64_t kWideSplitK = 2048;
 constexpr int kZThreads = 256;
 constexpr int kZRB = 8;        // rows per DSMEM exchange round
 constexpr int kZRows = 512;    // rows per cluster work item
@@ -339,9 +344,13 @@ __global__ void __launch_bounds__(kZThreads, 2) k_pass1z(const MatDev *mats, con
 }
 
 // ------------------------------------------------------------------ factor
-// One CTA per matrix.  Gram via per-thread (entry, row-group) sums reduced in
-// shared memory in fixed order; the r x r Cholesky runs on one thread.
-__device__ void gram_pass(const double *P, int64_t m, int r, double *s_gram, double *s_tmp) {
+// One CTA per matrix; r x r work matrices live in the matrix's workspace slice
+// (L1/L2 resident).  Gram by (entry, row-group) partial sums reduced in fixed
+// order; right-looking Cholesky with the MGS dead-column rule (a column whose
+// projected norm -- the Schur-complement diagonal -- is <= tol is zeroed and
+// drops out of later projections, compressor.py:80-90); triangular inverse by
+// independent column back-substitutions; everything fp64 and deterministic.
+__device__ void gram_pass(const double *P, int64_t m, int r, double *gram, double *s_tmp) {
     const int E = r * (r + 1) / 2;
     const int tid = threadIdx.x;
     for (int e0 = 0; e0 < E; e0 += kFactorThreads) {
@@ -349,58 +358,80 @@ __device__ void gram_pass(const double *P, int64_t m, int r, double *s_gram, dou
         const int ng = kFactorThreads / ecount;          // row groups
         const int g = tid / ecount;
         double acc = 0.0;
+        int a = 0, b = 0;
         if (g < ng) {
-            // entry e -> (a, b), a <= b, row-major upper triangle
-            int a = 0, rem = e0 + tid % ecount;
+            int rem = e0 + tid % ecount;
             while (rem >= r - a) { rem -= r - a; ++a; }
-            const int b = a + rem;
+            b = a + rem;
             for (int64_t i = g; i < m; i += ng) acc += P[i * r + a] * P[i * r + b];
         }
         s_tmp[tid] = acc;
         __syncthreads();
         if (tid < ecount) {
-            double s = 0.0;
-            for (int gg = 0; gg < ng; ++gg) s += s_tmp[gg * ecount + tid];
-            int a = 0, rem = e0 + tid;
-            while (rem >= r - a) { rem -= r - a; ++a; }
-            const int b = a + rem;
-            s_gram[a * r + b] = s;
-            s_gram[b * r + a] = s;
+            double sum = 0.0;
+            for (int gg = 0; gg < ng; ++gg) sum += s_tmp[gg * ecount + tid];
+            gram[a * r + b] = sum;
+            gram[b * r + a] = sum;
         }
         __syncthreads();
     }
 }
 
-// Cholesky of the Gram with MGS dead-column semantics; returns T = R^{-1}
-// (dead columns zero) in s_t (column j at s_t[j*r .. j*r+r)).
-__device__ void chol_inverse(const double *s_gram, int r, double tol, int32_t *dead, double *s_R, double *s_t,
-                             bool detect, const double *col_scale = nullptr) {
-    for (int j = 0; j < r; ++j) {
-        for (int i = 0; i < j; ++i) {
-            if (dead[i]) { s_R[i * r + j] = 0.0; continue; }
-            double v = s_gram[i * r + j];
-            for (int l = 0; l < i; ++l) v -= s_R[l * r + i] * s_R[l * r + j];
-            s_R[i * r + j] = v / s_R[i * r + i];
+// A (r x r, destroyed) -> R (upper, row-major R[i*r+j]); dead[] updated when detect.
+// tol_k = tol * scale[k] (scale = NULL -> 1).
+__device__ void chol_dead(double *A, int r, double tol, const double *scale, int32_t *dead, double *R, bool detect) {
+    const int tid = threadIdx.x;
+    for (int e = tid; e < r * r; e += kFactorThreads) R[e] = 0.0;
+    __syncthreads();
+    for (int k = 0; k < r; ++k) {
+        if (tid == 0) {
+            const double nrm = sqrt(fmax(A[k * r + k], 0.0));
+            if (detect) dead[k] = !(nrm > tol * (scale ? scale[k] : 1.0));
+            R[k * r + k] = dead[k] ? 0.0 : nrm;
         }
-        double d = s_gram[j * r + j];
-        for (int i = 0; i < j; ++i) d -= s_R[i * r + j] * s_R[i * r + j];
-        const double nrm = sqrt(fmax(d, 0.0));
-        if (detect) dead[j] = !(nrm > tol * (col_scale ? col_scale[j] : 1.0));
-        s_R[j * r + j] = dead[j] ? 0.0 : nrm;
+        __syncthreads();
+        if (!dead[k]) {
+            const double piv = R[k * r + k];
+            for (int j = k + 1 + tid; j < r; j += kFactorThreads) R[k * r + j] = A[k * r + j] / piv;
+            __syncthreads();
+            const int rem = r - k - 1;
+            for (int e = tid; e < rem * rem; e += kFactorThreads) {
+                const int i = k + 1 + e / rem, j = k + 1 + e % rem;
+                if (j >= i) A[i * r + j] -= R[k * r + i] * R[k * r + j];
+            }
+        }
+        __syncthreads();
     }
-    for (int j = 0; j < r; ++j) {
-        for (int i = 0; i < r; ++i) s_t[j * r + i] = 0.0;
+}
+
+// T = R^{-1} over the live columns (dead rows/columns zero); T column j at T[j*r + i].
+__device__ void tri_inverse(const double *R, const int32_t *dead, int r, double *T) {
+    for (int j = threadIdx.x; j < r; j += kFactorThreads) {
+        double *x = T + (int64_t)j * r;
+        for (int i = 0; i < r; ++i) x[i] = 0.0;
         if (dead[j]) continue;
-        // T_j = (e_j - sum_{i<j} R_ij T_i) / R_jj
-        for (int i = 0; i < j; ++i) {
-            const double c = s_R[i * r + j];
-            if (c != 0.0)
-                for (int l = 0; l <= i; ++l) s_t[j * r + l] -= c * s_t[i * r + l];
+        x[j] = 1.0 / R[j * r + j];
+        for (int i = j - 1; i >= 0; --i) {
+            if (dead[i]) continue;
+            double acc = 0.0;
+            for (int l = i + 1; l <= j; ++l) acc += R[i * r + l] * x[l];
+            x[i] = -acc / R[i * r + i];
         }
-        s_t[j * r + j] += 1.0;
-        const double inv = 1.0 / s_R[j * r + j];
-        for (int l = 0; l <= j; ++l) s_t[j * r + l] *= inv;
     }
+    __syncthreads();
+}
+
+// dst (m x r) = src (m x r) * T (upper, column-major by column)
+__device__ void right_mul(const double *src, const double *T, int64_t m, int r, double *dst, float *dst_f) {
+    for (int64_t e = threadIdx.x; e < m * r; e += kFactorThreads) {
+        const int64_t i = e / r;
+        const int j = (int)(e % r);
+        double acc = 0.0;
+        for (int l = 0; l <= j; ++l) acc += src[i * r + l] * T[(int64_t)j * r + l];
+        if (dst) dst[e] = acc;
+        if (dst_f) dst_f[e] = (float)acc;
+    }
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, int32_t *status, double col_tol) {
@@ -408,118 +439,187 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, i
     if (status[blockIdx.x] & 1) return;
     const int r = M.r;
     const int64_t m = M.m;
-    __shared__ double s_gram[kMaxRank * kMaxRank];
-    __shared__ double s_R[kMaxRank * kMaxRank];
-    __shared__ double s_t1[kMaxRank * kMaxRank];
-    __shared__ double s_t2[kMaxRank * kMaxRank];
-    __shared__ double s_S[kMaxRank * kMaxRank];    // preconditioner S[i][k] at i*r + k
+    const int tid = threadIdx.x;
+    double *gram = M.fwork, *R = gram + r * r, *T1 = R + r * r, *T2 = T1 + r * r, *S = T2 + r * r;
     __shared__ double s_tmp[kFactorThreads];
-    __shared__ double s_scale[kMaxRank];
-    __shared__ int32_t s_dead[kMaxRank];
+    __shared__ double s_tol;
+    int32_t *dead = M.dead;
     const bool pre = M.zmode && M.precond;
     if (!M.zmode) {
         // P_raw = sum over column chunks, fixed order
-        for (int64_t e = threadIdx.x; e < m * r; e += kFactorThreads) {
-            double s = 0.0;
-            for (int c = 0; c < M.nchunk1; ++c) s += M.p_part[(int64_t)c * m * r + e];
-            M.p_raw[e] = s;
+        for (int64_t e = tid; e < m * r; e += kFactorThreads) {
+            double acc = 0.0;
+            for (int c = 0; c < M.nchunk1; ++c) acc += M.p_part[(int64_t)c * m * r + e];
+            M.p_raw[e] = acc;
         }
     }
-    for (int e = threadIdx.x; e < r * r; e += kFactorThreads) {
+    for (int e = tid; e < r * r; e += kFactorThreads) {
         const int i = e / r, k = e % r;
-        s_S[e] = pre ? M.precond[(int64_t)i * M.ld_s + k] : (i == k ? 1.0 : 0.0);
+        S[e] = pre ? M.precond[(int64_t)i * M.ld_s + k] : (i == k ? 1.0 : 0.0);
     }
+    for (int j = tid; j < r; j += kFactorThreads) dead[j] = 0;
     __syncthreads();
-    gram_pass(M.p_raw, m, r, s_gram, s_tmp);
-    if (threadIdx.x == 0) {
-        // P_raw = P_orig S with P_orig = w q_warm.  The reference's tolerance is
-        // relative to ||P_orig||_F (compressor.py:79) and its column test uses
-        // the P_orig projection norms = R_jj / S_jj.
+    gram_pass(M.p_raw, m, r, gram, s_tmp);
+    if (tid == 0) {
+        // tolerance relative to ||P_orig||_F with P_raw = P_orig S (compressor.py:79)
         double fro2 = 0.0;
         if (pre) {
-            // Sinv (upper triangular), column j at s_t2[j*r..]
-            for (int j = 0; j < r; ++j) {
-                for (int l = 0; l < r; ++l) s_t2[j * r + l] = 0.0;
+            for (int j = 0; j < r; ++j) {          // Sinv column j into T2 (scratch)
+                for (int l = 0; l < r; ++l) T2[j * r + l] = 0.0;
                 for (int l = j; l >= 0; --l) {
                     double v = (l == j) ? 1.0 : 0.0;
-                    for (int q = l + 1; q <= j; ++q) v -= s_S[l * r + q] * s_t2[j * r + q];
-                    s_t2[j * r + l] = v / s_S[l * r + l];
+                    for (int q = l + 1; q <= j; ++q) v -= S[l * r + q] * T2[j * r + q];
+                    T2[j * r + l] = v / S[l * r + l];
                 }
             }
-            for (int j = 0; j < r; ++j) {
-                double a = 0.0;
-                for (int u = 0; u <= j; ++u)
-                    for (int v = 0; v <= j; ++v) a += s_t2[j * r + u] * s_gram[u * r + v] * s_t2[j * r + v];
-                fro2 += a;
-            }
-        } else {
-            for (int j = 0; j < r; ++j) fro2 += s_gram[j * r + j];
-        }
-        for (int j = 0; j < r; ++j) { s_dead[j] = 0; s_scale[j] = s_S[j * r + j]; }
-        const double tol = col_tol * sqrt(fro2);   // fixed before the sweep, compressor.py:79
-        chol_inverse(s_gram, r, tol, s_dead, s_R, s_t1, true, s_scale);
-        if (M.zmode) {
-            double rn = 0.0, tn = 0.0;
-            for (int j = 0; j < r; ++j) {
-                if (s_dead[j]) continue;
-                for (int i = 0; i <= j; ++i) {
-                    if (s_dead[i]) continue;
-                    rn += s_R[i * r + j] * s_R[i * r + j];
-                    tn += s_t1[j * r + i] * s_t1[j * r + i];
-                }
-            }
-            if (sqrt(rn * tn) > kKappaMax) atomicOr(status + blockIdx.x, 2);
-        }
-    }
-    __syncthreads();
-    // P1 = P_raw T1 in place (row-local)
-    for (int64_t i = threadIdx.x; i < m; i += kFactorThreads) {
-        double row[kMaxRank], out[kMaxRank];
-        for (int k = 0; k < r; ++k) row[k] = M.p_raw[i * r + k];
-        for (int j = 0; j < r; ++j) {
-            double s = 0.0;
-            for (int l = 0; l <= j; ++l) s += row[l] * s_t1[j * r + l];
-            out[j] = s;
-        }
-        for (int k = 0; k < r; ++k) M.p_raw[i * r + k] = out[k];
-    }
-    __syncthreads();
-    // second CholQR pass restores orthogonality to fp64 level
-    gram_pass(M.p_raw, m, r, s_gram, s_tmp);
-    if (threadIdx.x == 0) chol_inverse(s_gram, r, 0.0, s_dead, s_R, s_t2, false);
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < m; i += kFactorThreads) {
-        double row[kMaxRank];
-        for (int k = 0; k < r; ++k) row[k] = M.p_raw[i * r + k];
-        for (int j = 0; j < r; ++j) {
-            double s = 0.0;
-            for (int l = 0; l <= j; ++l) s += row[l] * s_t2[j * r + l];
-            M.p_out[i * r + j] = (float)s;
-        }
-    }
-    if (threadIdx.x < r) M.dead[threadIdx.x] = s_dead[threadIdx.x];
-    if (threadIdx.x == 0) {
-        // T = T1 T2: P = P_raw T, and on the Z path Q = Z T
-        for (int j = 0; j < r; ++j)
-            for (int l = 0; l < r; ++l) {
-                double a = 0.0;
-                for (int i = l; i <= j; ++i) a += s_t1[i * r + l] * s_t2[j * r + i];
-                M.tmat[j * r + l] = a;
-            }
-        if (pre) {
-            // next preconditioner A = S T (dead columns restart from e_j)
             for (int j = 0; j < r; ++j)
-                for (int i = 0; i < r; ++i) {
-                    double a = 0.0;
-                    if (s_dead[j]) {
-                        a = (i == j) ? 1.0 : 0.0;
-                    } else {
-                        for (int l = i; l <= j; ++l) a += s_S[i * r + l] * M.tmat[j * r + l];
-                    }
-                    M.precond[(int64_t)i * M.ld_s + j] = a;
-                }
+                for (int u = 0; u <= j; ++u)
+                    for (int v = 0; v <= j; ++v) fro2 += T2[j * r + u] * gram[u * r + v] * T2[j * r + v];
+        } else {
+            for (int j = 0; j < r; ++j) fro2 += gram[j * r + j];
+        }
+        s_tol = col_tol * sqrt(fro2);
+        for (int j = 0; j < r; ++j) T1[j] = S[j * r + j];   // column scales (P_orig norms = R_jj / S_jj)
+    }
+    __syncthreads();
+    // scales must survive chol_dead (which uses R); copy to the tail of T2's region is not needed:
+    // chol_dead reads scale[k] only at step k before R row k is written.
+    double *scale = T2;  // reuse: T2 is free again
+    for (int j = tid; j < r; j += kFactorThreads) scale[j] = T1[j];
+    __syncthreads();
+    chol_dead(gram, r, s_tol, scale, dead, R, true);
+    if (M.zmode && tid == 0) {
+        double rn = 0.0;
+        for (int i = 0; i < r; ++i)
+            for (int j = i; j < r; ++j) rn += R[i * r + j] * R[i * r + j];
+        // ||R^{-1}||_F is computed after tri_inverse below; stash ||R||_F^2
+        s_tmp[0] = rn;
+    }
+    __syncthreads();
+    const double rn2 = s_tmp[0];
+    __syncthreads();
+    tri_inverse(R, dead, r, T1);
+    if (M.zmode && tid == 0) {
+        double tn = 0.0;
+        for (int e = 0; e < r * r; ++e) tn += T1[e] * T1[e];
+        if (sqrt(rn2 * tn) > kKappaMax) atomicOr(status + blockIdx.x, 2);
+    }
+    // P1 = P_raw T1, then a second CholQR pass restores orthogonality to fp64 level
+    right_mul(M.p_raw, T1, m, r, M.p_tmp, nullptr);
+    gram_pass(M.p_tmp, m, r, gram, s_tmp);
+    chol_dead(gram, r, 0.0, nullptr, dead, R, false);
+    tri_inverse(R, dead, r, T2);
+    right_mul(M.p_tmp, T2, m, r, nullptr, M.p_out);
+    // T = T1 T2: P = P_raw T, and on the Z path Q = Z T
+    for (int e = tid; e < r * r; e += kFactorThreads) {
+        const int j = e / r, l = e % r;
+        double a = 0.0;
+        for (int i = l; i <= j; ++i) a += T1[(int64_t)i * r + l] * T2[(int64_t)j * r + i];
+        M.tmat[(int64_t)j * r + l] = a;
+    }
+    __syncthreads();
+    if (pre) {
+        // next preconditioner A = S T (dead columns restart from e_j)
+        for (int e = tid; e < r * r; e += kFactorThreads) {
+            const int i = e / r, j = e % r;
+            double a = 0.0;
+            if (dead[j]) {
+                a = (i == j) ? 1.0 : 0.0;
+            } else {
+                for (int l = i; l <= j; ++l) a += S[i * r + l] * M.tmat[(int64_t)j * r + l];
+            }
+            M.precond[(int64_t)i * M.ld_s + j] = a;
         }
     }
+}
+
+// --------------------------------------------------------- wide-rank path
+// r > 8 (and unaligned shapes): a 64x64x16 smem-tiled fp32 GEMM with strided
+// operands and fp64 split-K partials, used for P_raw = w q_warm and
+// Q = w^T P, plus a tiled error-feedback update w <- g + (w - p_res q_res^T).
+struct GemmTile {
+    int32_t mat, split;
+    int64_t i0, j0;        // output tile origin
+    int64_t k0, k1;        // K range of this split
+};
+
+constexpr int kGT = 64, kGK = 16, kGThreads = 256;
+
+// op 0: P_raw partial (M = m, N = r, K = n):  A(i,k) = w[i*n + k], B(k,j) = q_warm[k*ld_q + j]
+// op 1: Q partial     (M = n, N = r, K = m):  A(i,k) = w[k*n + i], B(k,j) = p_out[k*r + j]
+// op 2: EF update     (M = m, N = n, K = r_res): C = p_res q_res^T; w <- g + (w - C)
+template <int OP>
+__global__ void __launch_bounds__(kGThreads) k_gemm(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
+    const GemmTile t = tiles[blockIdx.x];
+    const MatDev &M = mats[t.mat];
+    if (OP == 1) {
+        const int st = status[t.mat];
+        if ((st & 1) || (M.zmode && !(st & 2))) return;
+    }
+    const int64_t n = M.n, m = M.m;
+    const int r = M.r, rres = M.r_res;
+    const int64_t MM = OP == 0 ? m : (OP == 1 ? n : m);
+    const int64_t NN = OP == 2 ? n : r;
+    __shared__ float As[kGK][kGT + 4];
+    __shared__ float Bs[kGK][kGT + 4];
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    float acc[4][4] = {};
+    for (int64_t k0 = t.k0; k0 < t.k1; k0 += kGK) {
+        // A tile: kGT rows x kGK cols
+        for (int e = tid; e < kGT * kGK; e += kGThreads) {
+            int ii, kk;
+            if (OP == 1) { ii = e % kGT; kk = e / kGT; } else { kk = e % kGK; ii = e / kGK; }
+            const int64_t gi = t.i0 + ii, gk = k0 + kk;
+            float v = 0.f;
+            if (gi < MM && gk < t.k1) {
+                if (OP == 0) v = M.w[gi * n + gk];
+                else if (OP == 1) v = M.w[gk * n + gi];
+                else v = M.p_res[gi * rres + gk];
+            }
+            As[kk][ii] = v;
+        }
+        for (int e = tid; e < kGT * kGK; e += kGThreads) {
+            const int jj = e % kGT, kk = e / kGT;
+            const int64_t gj = t.j0 + jj, gk = k0 + kk;
+            float v = 0.f;
+            if (gj < NN && gk < t.k1) {
+                if (OP == 0) v = M.q_warm[gk * M.ld_q + gj];
+                else if (OP == 1) v = M.p_out[gk * r + gj];
+                else v = M.q_res[gj * rres + gk];
+            }
+            Bs[kk][jj] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kGK; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { a[u] = As[kk][ty * 4 + u]; b[u] = Bs[kk][tx * 4 + u]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t gi = t.i0 + ty * 4 + u, gj = t.j0 + tx * 4 + v;
+            if (gi >= MM || gj >= NN) continue;
+            if (OP == 0) {
+                M.p_part[((int64_t)t.split * m + gi) * r + gj] = (double)acc[u][v];
+            } else if (OP == 1) {
+                M.q_part[((int64_t)t.split * n + gi) * r + gj] = (double)acc[u][v];
+            } else {
+                const float x = M.g[gi * M.ld_g + gj] + (M.w[gi * n + gj] - acc[u][v]);
+                bad |= !isfinite(x);
+                M.w[gi * n + gj] = x;
+            }
+        }
+    if (OP == 2 && __syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
 }
 
 // ------------------------------------------------------------------ pass 2
@@ -589,30 +689,28 @@ __global__ void k_finalize(const MatDev *mats, const int32_t *status) {
     const int r = M.r;
     const int64_t n = M.n;
     const bool zq = M.zmode && !(st & 2);
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        double z[kMaxRank];
-        for (int k = 0; k < r; ++k) {
-            double s = 0.0;
-            if (zq)
-                for (int b = 0; b < M.nitems; ++b) s += M.zpart[((int64_t)b * n + j) * r + k];
-            else
-                for (int b = 0; b < M.nblk2; ++b) s += M.q_part[((int64_t)b * n + j) * r + k];
-            z[k] = s;
-        }
-        for (int k = 0; k < r; ++k) {
-            float q;
-            if (M.dead[k]) {
-                q = M.basis[j * M.ld_q + k];   // compressor.py:113-114
-            } else if (zq) {
-                double a = 0.0;
-                for (int l = 0; l <= k; ++l) a += z[l] * M.tmat[k * r + l];
-                q = (float)a;
-            } else {
-                q = (float)z[k];
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * r; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / r;
+        const int k = (int)(e % r);
+        float q;
+        if (M.dead[k]) {
+            q = M.basis[j * M.ld_q + k];   // compressor.py:113-114
+        } else if (zq) {
+            // Q = Z T (T upper triangular): sum_l Z[j, l] T[l, k]
+            double a = 0.0;
+            for (int l = 0; l <= k; ++l) {
+                double z = 0.0;
+                for (int b = 0; b < M.nitems; ++b) z += M.zpart[((int64_t)b * n + j) * r + l];
+                a += z * M.tmat[(int64_t)k * r + l];
             }
-            M.q_out[j * r + k] = q;
-            M.q_warm[j * M.ld_q + k] = q;
+            q = (float)a;
+        } else {
+            double a = 0.0;
+            for (int b = 0; b < M.nblk2; ++b) a += M.q_part[((int64_t)b * n + j) * r + k];
+            q = (float)a;
         }
+        M.q_out[j * r + k] = q;
+        M.q_warm[j * M.ld_q + k] = q;
     }
 }
 
@@ -620,10 +718,12 @@ struct Plan {
     std::vector<MatDev> mats;
     std::vector<Tile> t1v4, t1v1, t2v4, t2v1;
     std::vector<ZTile> tz[9];          // Z-path items grouped by cluster size 1..8
+    std::vector<GemmTile> gw, gp, gq;  // wide path: EF update, P_raw, Q tiles
     int64_t bytes = 0;
     MatDev *d_mats = nullptr;
     Tile *d_t1v4 = nullptr, *d_t1v1 = nullptr, *d_t2v4 = nullptr, *d_t2v1 = nullptr;
     ZTile *d_tz[9] = {};
+    GemmTile *d_gw = nullptr, *d_gp = nullptr, *d_gq = nullptr;
     int rmax4 = 0, rmax1 = 0;
 };
 
@@ -639,6 +739,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         EDGC_REQUIRE(d.r <= kMaxRank, "compress desc %d: rank %d > %d not supported by this build", k, d.r,
                      kMaxRank);
         EDGC_REQUIRE(d.r_res >= 0 && d.r_res <= kMaxRank, "compress desc %d: r_res %d", k, d.r_res);
+        EDGC_REQUIRE(!d.precond || d.ld_s >= d.r, "compress desc %d: ld_s %d < r", k, d.ld_s);
         EDGC_REQUIRE(d.r_res == 0 || (d.p_res && d.q_res), "compress desc %d: residual factors missing", k);
         EDGC_REQUIRE(d.g && d.w && d.q_warm && d.basis && d.p_out && d.q_out && d.ld_q >= d.r && d.ld_g >= d.n,
                      "compress desc %d: null pointer or bad leading dimension", k);
@@ -660,8 +761,23 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                 P.tz[zc].push_back(ZTile{k, it, (int64_t)it * kZRows, std::min(d.m, (int64_t)(it + 1) * kZRows)});
         const int64_t slots = d.n / M.vec;
         const int64_t threads1 = kP1Threads;
-        M.nchunk1 = (int32_t)ceil_div(slots, threads1);
+        M.wide = std::max(d.r, d.r_res) > kNarrow ? 1 : 0;
+        M.nchunk1 = M.wide ? (int32_t)ceil_div(d.n, kWideSplitK) : (int32_t)ceil_div(slots, threads1);
         M.nblk2 = (int32_t)ceil_div(d.m, kP2Rows);
+        if (M.wide) {
+            for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
+                for (int64_t j0 = 0; j0 < d.n; j0 += kGT) P.gw.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
+            for (int32_t c = 0; c < M.nchunk1; ++c)
+                for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
+                    for (int64_t j0 = 0; j0 < d.r; j0 += kGT)
+                        P.gp.push_back(GemmTile{k, c, i0, j0, c * kWideSplitK, std::min(d.n, (c + 1) * kWideSplitK)});
+            for (int32_t b = 0; b < M.nblk2; ++b)
+                for (int64_t i0 = 0; i0 < d.n; i0 += kGT)
+                    for (int64_t j0 = 0; j0 < d.r; j0 += kGT)
+                        P.gq.push_back(GemmTile{k, b, i0, j0, (int64_t)b * kP2Rows,
+                                                std::min(d.m, (int64_t)(b + 1) * kP2Rows)});
+            continue;
+        }
         (v4 ? P.rmax4 : P.rmax1) = std::max(v4 ? P.rmax4 : P.rmax1, std::max(d.r, d.r_res));
         for (int32_t c = 0; c < (M.zmode ? 0 : M.nchunk1); ++c)
             for (int64_t r0 = 0; r0 < d.m; r0 += kP1Rows) {
@@ -684,12 +800,17 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.q_part = a.take<double>((int64_t)M.nblk2 * M.n * M.r);
         M.tmat = a.take<double>((int64_t)M.r * M.r);
         M.dead = a.take<int32_t>(M.r);
+        M.fwork = a.take<double>(5 * (int64_t)M.r * M.r);
+        M.p_tmp = a.take<double>(M.m * M.r);
     }
     P.d_t1v4 = a.take<Tile>(P.t1v4.size());
     P.d_t1v1 = a.take<Tile>(P.t1v1.size());
     P.d_t2v4 = a.take<Tile>(P.t2v4.size());
     P.d_t2v1 = a.take<Tile>(P.t2v1.size());
     for (int c = 1; c <= 8; ++c) P.d_tz[c] = a.take<ZTile>(P.tz[c].size());
+    P.d_gw = a.take<GemmTile>(P.gw.size());
+    P.d_gp = a.take<GemmTile>(P.gp.size());
+    P.d_gq = a.take<GemmTile>(P.gq.size());
     P.bytes = a.off;
     return EDGC_OK;
 }
@@ -702,9 +823,15 @@ int launch_pass1(const Plan &P, bool v4, int32_t *status, cudaStream_t st) {
     const int rmax = v4 ? P.rmax4 : P.rmax1;
     if (v4) k_pass1<4, 4, 4><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
     else if (rmax <= 4) k_pass1<1, 4, 4><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
-    else if (rmax <= 8) k_pass1<1, 8, 2><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
-    else if (rmax <= 16) k_pass1<1, 16, 1><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
-    else k_pass1<1, 32, 1><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
+    else k_pass1<1, 8, 2><<<grid, kP1Threads, 0, st>>>(P.d_mats, d, status);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+template <int OP>
+int launch_gemm(const Plan &P, const std::vector<GemmTile> &h, const GemmTile *d, int32_t *status, cudaStream_t st) {
+    if (h.empty()) return EDGC_OK;
+    k_gemm<OP><<<(unsigned)h.size(), kGThreads, 0, st>>>(P.d_mats, d, status);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }
@@ -738,9 +865,7 @@ int launch_pass2(const Plan &P, bool v4, const int32_t *status, cudaStream_t st)
     const int rmax = v4 ? P.rmax4 : P.rmax1;
     if (v4) k_pass2<4, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
     else if (rmax <= 4) k_pass2<1, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
-    else if (rmax <= 8) k_pass2<1, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
-    else if (rmax <= 16) k_pass2<1, 16><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
-    else k_pass2<1, 32><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
+    else k_pass2<1, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }
@@ -887,6 +1012,13 @@ extern "C" int edgc_compress_plan_bind(edgc_compress_plan *h, void *ws, int64_t 
         if (!P.tz[c].empty())
             EDGC_CUDA_TRY(cudaMemcpyAsync(P.d_tz[c], P.tz[c].data(), sizeof(ZTile) * P.tz[c].size(),
                                           cudaMemcpyHostToDevice, st));
+    auto upg = [&](GemmTile *d, const std::vector<GemmTile> &v) -> cudaError_t {
+        return v.empty() ? cudaSuccess
+                         : cudaMemcpyAsync(d, v.data(), sizeof(GemmTile) * v.size(), cudaMemcpyHostToDevice, st);
+    };
+    EDGC_CUDA_TRY(upg(P.d_gw, P.gw));
+    EDGC_CUDA_TRY(upg(P.d_gp, P.gp));
+    EDGC_CUDA_TRY(upg(P.d_gq, P.gq));
     // the host staging vectors stay alive in the plan; make the upload complete
     // before the caller could destroy or rebind it
     EDGC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -905,6 +1037,8 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if ((rc = launch_pass1(P, true, status_dev, st))) return rc;
         if ((rc = launch_pass1(P, false, status_dev, st))) return rc;
         if ((rc = launch_pass1z(P, status_dev, st))) return rc;
+        if ((rc = launch_gemm<2>(P, P.gw, P.d_gw, status_dev, st))) return rc;
+        if ((rc = launch_gemm<0>(P, P.gp, P.d_gp, status_dev, st))) return rc;
     }
     if (phases & EDGC_PHASE_FACTOR) {
         k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
@@ -913,6 +1047,7 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
     if (phases & EDGC_PHASE_PASS2) {
         if ((rc = launch_pass2(P, true, status_dev, st))) return rc;
         if ((rc = launch_pass2(P, false, status_dev, st))) return rc;
+        if ((rc = launch_gemm<1>(P, P.gq, P.d_gq, status_dev, st))) return rc;
     }
     if (phases & EDGC_PHASE_FINALIZE) {
         k_finalize<<<dim3(16, n), 256, 0, st>>>(P.d_mats, status_dev);

@@ -210,3 +210,27 @@ def test_error_sandwich():
     f = e.compress(m, e.CompressorState(64, 64, 16, rng_seed=1))
     err = float(torch.linalg.norm(torch.from_numpy(m).cuda() - f.p @ f.q.T))
     assert e.optimal_rank_r_error(m, 16) <= err <= e.frobenius_norm(m)
+
+
+def _graded_matrix(m, n, sigmas, seed):
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(rng.standard_normal((m, len(sigmas))))
+    v, _ = np.linalg.qr(rng.standard_normal((n, len(sigmas))))
+    a = (u * np.asarray(sigmas)) @ v.T + 1e-4 * rng.standard_normal((m, n))
+    return a.astype(np.float32)
+
+
+@pytest.mark.parametrize("sigmas", [(1e3, 1e2, 10.0, 1.0, 0.5), (1.0, 1.0, 1.0, 1.0), (1e4, 1.0, 1e-1, 1e-2)])
+def test_graded_spectrum_chained_vs_oracle(sigmas):
+    """Ill-conditioned warm starts (the one-sweep path's kappa fallback) stay within tolerance."""
+    e = _api()
+    m, n, r = 256, 512, 4
+    st = e.CompressorState(m, n, r, rng_seed=4)
+    ost = oracle.OracleState(m, n, r, 4)
+    for t in range(4):
+        g = _graded_matrix(m, n, sigmas, 100 + t)
+        f = e.compress(g, st)
+        p, q, _ = oracle.compress(g.astype(np.float64), ost)
+        out = p @ q.T
+        assert rel_err(e.decompress(f).data, out) <= 1e-4, (t, rel_err(e.decompress(f).data, out))
+        assert rel_err(f.q, q) <= 1e-4
