@@ -266,11 +266,15 @@ __global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, 
         const int64_t base = N - count;
         int32_t cur = s;
         bool collide = false;
+        // collision(t) = [v_t drawn at an earlier step] or [v_t == j_t' of an
+        // earlier step t' that itself collided]; v_t == j_t (t' == t) is a fresh value
         while (true) {
             const int32_t v = P.rv[cur];
             if (latest_before(P, v, cur) >= 0) { collide = true; break; }
             if (v < base) break;
-            cur = (int32_t)(v - base);
+            const int32_t prev = (int32_t)(v - base);
+            if (prev >= cur) break;
+            cur = prev;
         }
         P.idx[s] = collide ? (int32_t)(base + s) : P.rv[s];
     }

@@ -1,0 +1,106 @@
+"""CPU: the device sample-plan ALGORITHM (csrc/sample_plan.cu phases P2-P4),
+emulated step for step in Python on the oracle's u32 stream, against NumPy.
+
+This pins the parallel decomposition (walk with first-rejection windows, hash
+lists, tail-shuffle chains, Floyd collision chains) independently of the GPU.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+
+
+def lemire(x, rng):
+    excl = rng + 1
+    m = x * excl
+    val, left = m >> 32, m & 0xFFFFFFFF
+    if left >= excl:
+        return True, val
+    thr = (0xFFFFFFFF - rng) % excl
+    return left >= thr, val
+
+
+def emulate(seed, n_elems, count, window=64):
+    tail = n_elems > 10000 and count > n_elems // 20
+    draws = oracle.pcg64_u32(seed, count + 4096 + 2 * count).astype(np.int64)
+    step_rng = (lambda s: n_elems - 1 - s) if tail else (lambda s: n_elems - count + s)
+    rv = [0] * count
+    s = u = 0
+    while s < count:                      # k_walk
+        res = []
+        for lane in range(window):
+            st, pos = s + lane, u + lane
+            if st >= count:
+                res.append((False, 0))
+                continue
+            ok, val = lemire(int(draws[pos]), step_rng(st))
+            res.append((not ok, val))
+        rejs = [i for i, (rj, _) in enumerate(res) if rj]
+        if not rejs:
+            for lane in range(window):
+                if s + lane < count:
+                    rv[s + lane] = res[lane][1]
+            s += window
+            u += window
+            continue
+        f = rejs[0]
+        for lane in range(f):
+            rv[s + lane] = res[lane][1]
+        p = u + f + 1
+        while True:
+            ok, val = lemire(int(draws[p]), step_rng(s + f))
+            if ok:
+                break
+            p += 1
+        rv[s + f] = val
+        s, u = s + f + 1, p + 1
+    lists = {}                            # k_index (hash lists)
+    for st in range(count):
+        lists.setdefault(rv[st], []).append(st)
+
+    def latest_before(key, before):
+        c = [e for e in lists.get(key, []) if e < before]
+        return max(c) if c else -1
+
+    out = [0] * count                     # k_resolve
+    base = n_elems - count
+    for st in range(count):
+        if tail:
+            j = rv[st]
+            t = latest_before(j, st)
+            val = j
+            if t >= 0:
+                while True:
+                    pos_t = n_elems - 1 - t
+                    t2 = latest_before(pos_t, t)
+                    if t2 < 0:
+                        val = pos_t
+                        break
+                    t = t2
+            out[count - 1 - st] = val
+        else:
+            cur, collide = st, False
+            while True:
+                v = rv[cur]
+                if latest_before(v, cur) >= 0:
+                    collide = True
+                    break
+                if v < base or v - base >= cur:
+                    break
+                cur = v - base
+            out[st] = base + st if collide else rv[st]
+    return np.asarray(out, dtype=np.int64)
+
+
+@pytest.mark.parametrize("n_elems,beta,seed", [
+    (100, 0.5, 3), (101, 0.9, 1), (4096, 0.25, 1), (10000, 0.5, 4), (10001, 0.06, 4), (12000, 0.25, 5),
+    (20000, 0.05, 9), (20000, 0.0501, 11), (40000, 0.999, 2), (7, 0.3, 5), (2, 0.5, 0), (300, 0.99, 8)])
+def test_plan_algorithm_matches_numpy(n_elems, beta, seed):
+    count = min(n_elems, math.ceil(beta * n_elems))
+    if count == n_elems:
+        pytest.skip("copy branch")
+    ref = np.random.default_rng(seed).choice(n_elems, size=count, replace=False, shuffle=False)
+    assert np.array_equal(emulate(seed, n_elems, count), ref)
