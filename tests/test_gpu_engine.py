@@ -37,7 +37,11 @@ def test_engine_matches_oracle_dp_step_chained(rank):
         for k, (o, r) in enumerate(zip(outs, ref)):
             worst = max(worst, rel_err(o, r))
             if t == 5:
-                worst = max(worst, rel_err(eng.residual(k), ost[0][k].residual))
+                ref_res = ost[0][k].residual
+                if np.linalg.norm(ref_res) > 1e-9 * np.linalg.norm(gs[k]):
+                    worst = max(worst, rel_err(eng.residual(k), ref_res))
+                else:  # full-rank compression: the reference residual is fp64 round-off
+                    assert float(torch.linalg.norm(eng.residual(k))) <= 1e-5 * np.linalg.norm(gs[k])
     assert worst <= 5e-5, worst
 
 
