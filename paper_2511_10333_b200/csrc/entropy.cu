@@ -18,7 +18,11 @@ namespace {
 
 constexpr double kGaussConst = 1.4189385332046727;  // 0.5 * ln(2*pi*e), entropy.py:24
 constexpr int kRedThreads = 256;
-constexpr int kGaussBlocksPerDesc = 64;
+// Many blocks per layer, layers in blockIdx.y order: the whole GPU gathers from
+// one or two matrices at a time, so their sectors stay in L2 and each matrix is
+// read from DRAM about once (a scattered gather over all layers at once thrashes
+// L2 and moves ~30x the algorithmic bytes).
+constexpr int kGaussBlocksPerDesc = 1184;
 
 // ---------------------------------------------------------------- Gaussian
 struct GaussDev {

@@ -40,8 +40,8 @@ __device__ __forceinline__ uint64_t pcg_output(u128 s) {
     return (x >> rot) | (x << ((64u - rot) & 63u));
 }
 
-// state after `delta` LCG steps (pcg_advance_lcg_128)
-__device__ __forceinline__ u128 pcg_jump(u128 state, u128 inc, uint64_t delta) {
+// affine map of `delta` LCG steps: state -> mult * state + plus (pcg_advance_lcg_128)
+__device__ __forceinline__ void pcg_affine(u128 inc, uint64_t delta, u128 &mult, u128 &plus) {
     u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
     while (delta) {
         if (delta & 1) {
@@ -52,7 +52,14 @@ __device__ __forceinline__ u128 pcg_jump(u128 state, u128 inc, uint64_t delta) {
         cur_mult *= cur_mult;
         delta >>= 1;
     }
-    return acc_mult * state + acc_plus;
+    mult = acc_mult;
+    plus = acc_plus;
+}
+
+__device__ __forceinline__ u128 pcg_jump(u128 state, u128 inc, uint64_t delta) {
+    u128 a, c;
+    pcg_affine(inc, delta, a, c);
+    return a * state + c;
 }
 
 struct PlanDev {
@@ -74,6 +81,7 @@ struct PlanDev {
 
 constexpr int kDrawsPerThread = 64;  // 64-bit outputs per P1 thread
 constexpr int kP1Threads = 256;
+constexpr int64_t kDrawsPerBlock = (int64_t)kDrawsPerThread * kP1Threads;
 constexpr int kWalkThreads = 1024;
 constexpr int kStepThreads = 256;
 
@@ -88,20 +96,25 @@ __device__ __forceinline__ int find_plan(const PlanDev *plans, int n, int64_t bl
 }
 
 // ---- P1: u32 draw stream ---------------------------------------------------
+// Block b of a plan owns 64-bit outputs [b*64*256, (b+1)*64*256); thread t
+// produces outputs t, t+256, t+512, ... of that range (one jump-ahead, then a
+// 256-step affine LCG map per output), so every warp store is coalesced.
 __global__ void __launch_bounds__(kP1Threads) k_draws(const PlanDev *plans, int n_plans) {
-    const int64_t chunk = (int64_t)blockIdx.x * kP1Threads + threadIdx.x;
-    const PlanDev &P = plans[find_plan(plans, n_plans, chunk, true)];
-    const int64_t local = chunk - P.draw_chunk0;
+    const PlanDev &P = plans[find_plan(plans, n_plans, blockIdx.x, true)];
+    const int64_t o_base = (int64_t)(blockIdx.x - P.draw_chunk0) * kDrawsPerBlock;
     const int64_t n64 = P.n_draws / 2;
-    const int64_t o0 = local * kDrawsPerThread;
-    if (local < 0 || o0 >= n64) return;
-    u128 s = pcg_jump(P.state, P.inc, (uint64_t)o0);
-    const int64_t o1 = min(o0 + kDrawsPerThread, n64);
+    if (o_base >= n64) return;
+    u128 s = pcg_jump(P.state, P.inc, (uint64_t)(o_base + threadIdx.x));
+    u128 a_t, c_t;
+    pcg_affine(P.inc, kP1Threads, a_t, c_t);
     uint2 *out = reinterpret_cast<uint2 *>(P.draws);
-    for (int64_t o = o0; o < o1; ++o) {
-        s = s * pcg_mult() + P.inc;
-        const uint64_t v = pcg_output(s);
+    const u128 m1 = pcg_mult();
+    for (int k = 0; k < kDrawsPerThread; ++k) {
+        const int64_t o = o_base + threadIdx.x + (int64_t)k * kP1Threads;
+        if (o >= n64) break;
+        const uint64_t v = pcg_output(s * m1 + P.inc);   // output o = XSL-RR(state after o+1 steps)
         out[o] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
+        s = a_t * s + c_t;
     }
 }
 
@@ -122,80 +135,110 @@ __device__ __forceinline__ uint32_t step_rng(const PlanDev &P, int64_t s) {
 }
 
 // ---- P2: assign draws to steps --------------------------------------------
-__global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int32_t *status) {
+// One CTA per plan walks windows of kWT steps.  Lane l tests its step against
+// the draws at shifts 0..kWK-1 (draw u+l+j): a Lemire rejection at lane f and
+// shift d moves every later step one draw further, so the window resolves by
+// scanning rejection events in lane order (warp 0, ballots) and accepting each
+// lane at shift #events at lanes <= l.  Up to kWK-1 rejections fit in one
+// window; rarer bursts end the window early.  The draw window lives in shared
+// memory and the next one is prefetched while the current one resolves.
+constexpr int kWT = kWalkThreads;
+constexpr int kWK = 4;
+constexpr int kWBuf = kWT + 2 * kWK;
+
+__global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *status) {
     const PlanDev &P = plans[blockIdx.x];
-    __shared__ int s_warp_first[kWalkThreads / 32];
-    __shared__ int s_first;
-    __shared__ long long s_next_u;
-    __shared__ int s_err;
+    __shared__ uint32_t s_draw[2][kWBuf];
+    __shared__ uint32_t s_mask[kWK][kWT / 32];
+    __shared__ uint32_t s_val[kWK][kWT];
+    __shared__ int s_ev[kWK];
+    __shared__ int s_ne, s_len, s_err;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t count = P.count, nd = P.n_draws;
+    int64_t s = 0, u = 0, base = 0;
+    int buf = 0;
+    for (int i = tid; i < kWBuf; i += kWT) s_draw[0][i] = (i < nd) ? P.draws[i] : 0u;
     if (tid == 0) s_err = 0;
     __syncthreads();
-    int64_t s = 0, u = 0;
-    const int64_t count = P.count, nd = P.n_draws;
-    uint32_t x_pref = (tid < nd) ? P.draws[tid] : 0u;
     while (s < count) {
-        const int64_t st = s + tid, pos = u + tid;
+        // prefetch the window that follows if this one resolves with shift < kWK
+        const int64_t nb = u + kWT;
+        const uint32_t pre0 = (nb + tid < nd) ? __ldg(P.draws + nb + tid) : 0u;
+        const uint32_t pre1 = (tid < 2 * kWK && nb + kWT + tid < nd) ? __ldg(P.draws + nb + kWT + tid) : 0u;
+        const int off = (int)(u - base);
+        const int64_t st = s + tid;
         const bool valid = st < count;
-        uint32_t x = x_pref;
-        // prefetch the next window assuming this one has no rejection
-        const int64_t pnext = u + kWalkThreads + tid;
-        x_pref = (pnext < nd) ? __ldg(P.draws + pnext) : 0u;
-        bool rej = false;
-        uint32_t val = 0;
-        if (valid) {
-            if (pos >= nd) {
-                rej = true;  // out of draws: handled below as an error
-            } else {
-                rej = !lemire_accept(x, step_rng(P, st), val);
-            }
-        }
-        if (__syncthreads_or(rej) == 0) {
-            if (valid) P.rv[st] = (int32_t)val;
-            s += kWalkThreads;
-            u += kWalkThreads;
-            continue;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, rej);
-        if (lane == 0) s_warp_first[warp] = bal ? (warp * 32 + __ffs(bal) - 1) : 0x7fffffff;
-        __syncthreads();
-        if (tid < 32) {
-            int f = s_warp_first[tid];
+        const uint32_t rng = valid ? step_rng(P, st) : 0u;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
-            if (tid == 0) s_first = f;
+        for (int j = 0; j < kWK; ++j) {
+            uint32_t val = 0;
+            bool rej = false;
+            if (valid) {
+                if (u + tid + j >= nd) {
+                    rej = true;
+                } else {
+                    rej = !lemire_accept(s_draw[buf][off + tid + j], rng, val);
+                }
+            }
+            s_val[j][tid] = val;
+            const unsigned bal = __ballot_sync(0xffffffffu, rej);
+            if (lane == 0) s_mask[j][warp] = bal;
         }
         __syncthreads();
-        const int f = s_first;
-        if (valid && tid < f) P.rv[st] = (int32_t)val;
-        if (tid == f) {
-            // the rejected step keeps drawing sequentially (rare: p ~ rng/2^32)
-            const uint32_t rng = step_rng(P, st);
-            int64_t p = pos + 1;
-            uint32_t v2 = 0;
-            bool ok = false;
-            while (p < nd) {
-                if (lemire_accept(P.draws[p], rng, v2)) { ok = true; break; }
-                ++p;
+        if (warp == 0) {
+            const int nvalid = (int)min((int64_t)kWT, count - s);
+            int cur = 0, d = 0, ne = 0, len = nvalid;
+            while (true) {
+                // first lane >= cur (and < nvalid) rejected at shift d
+                uint32_t bits = s_mask[d][lane];
+                const int lo = lane * 32;
+                if (lo + 32 <= cur) bits = 0u;
+                else if (lo < cur) bits &= ~((1u << (cur - lo)) - 1u);
+                if (lo >= nvalid) bits = 0u;
+                else if (lo + 32 > nvalid) bits &= (nvalid - lo == 32) ? 0xffffffffu : ((1u << (nvalid - lo)) - 1u);
+                const unsigned any = __ballot_sync(0xffffffffu, bits != 0u);
+                if (!any) break;
+                const int wi = __ffs(any) - 1;
+                const uint32_t wbits = __shfl_sync(0xffffffffu, bits, wi);
+                const int f = wi * 32 + __ffs(wbits) - 1;
+                if (lane == 0) s_ev[ne] = f;
+                ++ne;
+                ++d;
+                if (d == kWK) { len = f; break; }
+                cur = f;
             }
-            if (!ok || pos >= nd) {
-                s_err = 1;
-            } else {
-                P.rv[st] = (int32_t)v2;
-            }
-            s_next_u = p + 1;
+            if (lane == 0) { s_ne = ne; s_len = len; }
         }
         __syncthreads();
-        if (s_err) break;
-        s = s + f + 1;
-        u = s_next_u;
-        x_pref = (u + tid < nd) ? P.draws[u + tid] : 0u;
+        const int ne = s_ne, len = s_len;
+        if (tid < len) {
+            int sh = 0;
+            for (int e = 0; e < ne; ++e) sh += (s_ev[e] <= tid);
+            P.rv[s + tid] = (int32_t)s_val[sh][tid];
+        }
+        if (tid == 0 && u + len + ne > nd) s_err = 1;   // consumed draws past the generated stream
+        s += len;
+        u += len + ne;
+        const int nbuf = buf ^ 1;
+        if (u - nb >= 0 && u - nb <= kWK) {
+            s_draw[nbuf][tid] = pre0;
+            if (tid < 2 * kWK) s_draw[nbuf][kWT + tid] = pre1;
+            base = nb;
+        } else {
+            for (int i = tid; i < kWBuf; i += kWT) s_draw[nbuf][i] = (u + i < nd) ? P.draws[u + i] : 0u;
+            base = u;
+        }
+        buf = nbuf;
+        __syncthreads();
+        if (s_err || (len == 0 && ne == 0)) break;
     }
-    if (tid == 0) status[blockIdx.x] = s_err ? EDGC_EDRAWS : EDGC_OK;
+    if (tid == 0) status[blockIdx.x] = (s_err || s < count) ? EDGC_EDRAWS : EDGC_OK;
 }
 
-__device__ __forceinline__ uint32_t hash_slot(uint32_t key, int log2cap) {
-    return (uint32_t)((key * 2654435761u) >> (32 - log2cap));
+__device__ __forceinline__ uint32_t hash_slot(uint32_t key, uint32_t cap) {
+    // murmur3 finaliser, then multiply-shift range reduction onto [0, cap)
+    key ^= key >> 16; key *= 0x85ebca6bu; key ^= key >> 13; key *= 0xc2b2ae35u; key ^= key >> 16;
+    return (uint32_t)(((uint64_t)key * cap) >> 32);
 }
 
 __device__ __forceinline__ int find_plan_steps(const PlanDev *plans, int n, int64_t blk) {
@@ -209,24 +252,24 @@ __global__ void __launch_bounds__(kStepThreads) k_index(const PlanDev *plans, in
     const int64_t s = (int64_t)(blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
     if (s >= P.count) return;
     const int32_t key = P.rv[s];
-    const uint32_t mask = (uint32_t)(P.cap - 1);
-    uint32_t slot = P.log2cap ? hash_slot((uint32_t)key, P.log2cap) : 0u;
+    const uint32_t cap = (uint32_t)P.cap;
+    uint32_t slot = hash_slot((uint32_t)key, cap);
     while (true) {
         const int32_t k = atomicCAS(P.keys + slot, -1, key);
         if (k == -1 || k == key) break;
-        slot = (slot + 1) & mask;
+        if (++slot == cap) slot = 0;
     }
     P.next[s] = atomicExch(P.heads + slot, (int32_t)s);
 }
 
 __device__ __forceinline__ int32_t lookup_head(const PlanDev &P, int32_t key) {
-    const uint32_t mask = (uint32_t)(P.cap - 1);
-    uint32_t slot = P.log2cap ? hash_slot((uint32_t)key, P.log2cap) : 0u;
+    const uint32_t cap = (uint32_t)P.cap;
+    uint32_t slot = hash_slot((uint32_t)key, cap);
     while (true) {
         const int32_t k = P.keys[slot];
         if (k == key) return P.heads[slot];
         if (k == -1) return -1;
-        slot = (slot + 1) & mask;
+        if (++slot == cap) slot = 0;
     }
 }
 
@@ -316,14 +359,12 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
         nd = (nd + 1) & ~int64_t(1);
         P.n_draws = nd;
         P.draw_chunk0 = chunk;
-        chunk += ceil_div(nd / 2, kDrawsPerThread);
+        chunk += ceil_div(nd / 2, kDrawsPerBlock);
         P.step_block0 = blocks;
         blocks += ceil_div(d.count, kStepThreads);
-        int64_t cap = 1;
-        int lg = 0;
-        while (cap < d.count + d.count / 2) { cap <<= 1; ++lg; }
+        const int64_t cap = ((d.count * 4 / 3 + 256) + 255) & ~int64_t(255);   // load <= 0.75
         P.cap = cap;
-        P.log2cap = lg;
+        P.log2cap = 0;
         caps[i] = cap;
     }
     // round the P1 chunk index up so blocks never straddle more than needed
@@ -389,8 +430,7 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
     PlanDev *d_plans = reinterpret_cast<PlanDev *>(ws);
     EDGC_CUDA_TRY(cudaMemcpyAsync(d_plans, L.dev.data(), sizeof(PlanDev) * n_plans, cudaMemcpyHostToDevice, st));
     EDGC_CUDA_TRY(cudaMemsetAsync(L.table_base, 0xFF, L.table_bytes, st));
-    const int64_t p1_blocks = ceil_div(L.draw_chunks, kP1Threads);
-    k_draws<<<(unsigned)p1_blocks, kP1Threads, 0, st>>>(d_plans, n_plans);
+    k_draws<<<(unsigned)L.draw_chunks, kP1Threads, 0, st>>>(d_plans, n_plans);
     EDGC_LAUNCH_CHECK();
     k_walk<<<n_plans, kWalkThreads, 0, st>>>(d_plans, status_dev);
     EDGC_LAUNCH_CHECK();

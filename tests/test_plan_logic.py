@@ -29,34 +29,31 @@ def emulate(seed, n_elems, count, window=64):
     step_rng = (lambda s: n_elems - 1 - s) if tail else (lambda s: n_elems - count + s)
     rv = [0] * count
     s = u = 0
-    while s < count:                      # k_walk
-        res = []
-        for lane in range(window):
-            st, pos = s + lane, u + lane
-            if st >= count:
-                res.append((False, 0))
-                continue
-            ok, val = lemire(int(draws[pos]), step_rng(st))
-            res.append((not ok, val))
-        rejs = [i for i, (rj, _) in enumerate(res) if rj]
-        if not rejs:
-            for lane in range(window):
-                if s + lane < count:
-                    rv[s + lane] = res[lane][1]
-            s += window
-            u += window
-            continue
-        f = rejs[0]
-        for lane in range(f):
-            rv[s + lane] = res[lane][1]
-        p = u + f + 1
+    K = 4
+    while s < count:                      # k_walk (speculative shifts 0..K-1)
+        nvalid = min(window, count - s)
+        vals = [[0] * window for _ in range(K)]
+        rej = [[False] * window for _ in range(K)]
+        for lane in range(nvalid):
+            for j in range(K):
+                ok, v = lemire(int(draws[u + lane + j]), step_rng(s + lane))
+                vals[j][lane], rej[j][lane] = v, not ok
+        cur, d, events, length = 0, 0, [], nvalid
         while True:
-            ok, val = lemire(int(draws[p]), step_rng(s + f))
-            if ok:
+            f = next((l for l in range(cur, nvalid) if rej[d][l]), None)
+            if f is None:
                 break
-            p += 1
-        rv[s + f] = val
-        s, u = s + f + 1, p + 1
+            events.append(f)
+            d += 1
+            if d == K:
+                length = f
+                break
+            cur = f
+        for lane in range(length):
+            sh = sum(1 for e in events if e <= lane)
+            rv[s + lane] = vals[sh][lane]
+        s += length
+        u += length + len(events)
     lists = {}                            # k_index (hash lists)
     for st in range(count):
         lists.setdefault(rv[st], []).append(st)
@@ -95,12 +92,13 @@ def emulate(seed, n_elems, count, window=64):
     return np.asarray(out, dtype=np.int64)
 
 
+@pytest.mark.parametrize("window", [64, 7])
 @pytest.mark.parametrize("n_elems,beta,seed", [
     (100, 0.5, 3), (101, 0.9, 1), (4096, 0.25, 1), (10000, 0.5, 4), (10001, 0.06, 4), (12000, 0.25, 5),
     (20000, 0.05, 9), (20000, 0.0501, 11), (40000, 0.999, 2), (7, 0.3, 5), (2, 0.5, 0), (300, 0.99, 8)])
-def test_plan_algorithm_matches_numpy(n_elems, beta, seed):
+def test_plan_algorithm_matches_numpy(n_elems, beta, seed, window):
     count = min(n_elems, math.ceil(beta * n_elems))
     if count == n_elems:
         pytest.skip("copy branch")
     ref = np.random.default_rng(seed).choice(n_elems, size=count, replace=False, shuffle=False)
-    assert np.array_equal(emulate(seed, n_elems, count), ref)
+    assert np.array_equal(emulate(seed, n_elems, count, window), ref)

@@ -89,7 +89,10 @@ def parse_report(path):
                     u = units[head.index(mname)]
                     v = float(rec[mname].replace(",", ""))
                     mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                            "msecond": 1e-3}.get(u, 1)
+                            "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}.get(u, 1)
+                    if mname == "gpu__time_duration.sum" and u not in ("nsecond", "usecond", "msecond", "ns", "us",
+                                                                       "ms", "second"):
+                        mult = 1e-9
                     vals[mname] = v * mult
                 except (ValueError, IndexError):
                     pass
