@@ -31,9 +31,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace edgc {
 namespace {
@@ -343,6 +345,207 @@ __global__ void __launch_bounds__(kZThreads, 2) k_pass1z(const MatDev *mats, con
     cluster.sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
+// ------------------------------------------- pass 1 (Z, TMA-pipelined)
+// Same math as k_pass1z, restructured for bandwidth:
+//  * a producer warp streams the cluster CTA's [4 rows x 1024 cols] tiles of g
+//    and w into a 3-stage shared-memory ring with 1-D bulk async copies (TMA
+//    engine, mbarrier complete_tx); consumer warps never stall on loads;
+//  * row dots are accumulated in fp64 (exact fp32 x fp32 products);
+//  * the cluster exchange is a push: each CTA stores its partial row dots
+//    into every peer's shared memory (st.shared::cluster) and release-arrives
+//    on the peer's mbarrier; the receive side is consumed one round later,
+//    so the exchange latency overlaps the next round's work (3 slots keep the
+//    lagged buffers race-free).
+constexpr int kTCons = 256;
+constexpr int kTThreads = kTCons + 32;
+constexpr int kTRB = 4;
+constexpr int kTStages = 3;
+constexpr int kTCW = 4 * kTCons;
+constexpr int kTSlots = 3;
+constexpr int kTV = kTRB * 4;   // row-dot values per round (RMAX = 4)
+
+struct TSmem {
+    float g[kTStages][kTRB][kTCW];
+    float w[kTStages][kTRB][kTCW];
+    double recv[kTSlots][8][kTV];
+    double red[kTCons / 32][kTV];
+    double S[16];
+    float prow[kTV];
+    alignas(8) uint64_t full[kTStages];
+    alignas(8) uint64_t empty[kTStages];
+    alignas(8) uint64_t xfull[kTSlots];
+};
+
+__global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, const ZTile *tiles, int32_t *status) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TSmem &sm = *reinterpret_cast<TSmem *>(smem_raw);
+    const uint32_t C = ptx::cluster_nctarank();
+    const uint32_t me = ptx::cluster_ctarank();
+    const ZTile t = tiles[blockIdx.x / C];
+    const MatDev &M = mats[t.mat];
+    const int r = M.r, rr_res = M.r_res;
+    const int64_t n = M.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t col_base = (int64_t)me * kTCW;
+    const int64_t chunk_cols = min((int64_t)kTCW, n - col_base);
+    const int nrounds = (int)((t.row1 - t.row0 + kTRB - 1) / kTRB);
+
+    if (tid == 0) {
+        for (int s = 0; s < kTStages; ++s) {
+            ptx::mbar_init(&sm.full[s], 1);
+            ptx::mbar_init(&sm.empty[s], kTCons / 32);
+        }
+        for (int s = 0; s < kTSlots; ++s) ptx::mbar_init(&sm.xfull[s], C);
+        ptx::fence_mbar_init();
+    }
+    if (tid < 16) {
+        const int i = tid / 4, k = tid % 4;
+        double v = (i == k) ? 1.0 : 0.0;
+        if (M.precond && i < r && k < r) v = M.precond[(int64_t)i * M.ld_s + k];
+        sm.S[tid] = v;
+    }
+    ptx::cluster_sync();
+
+    if (warp == kTCons / 32) {
+        // ---------------- producer warp
+        if (lane == 0 && chunk_cols > 0) {
+            const uint32_t bytes = (uint32_t)(chunk_cols * 4);
+            for (int b = 0; b < nrounds; ++b) {
+                const int s = b % kTStages;
+                if (b >= kTStages) ptx::mbar_wait(&sm.empty[s], ((b / kTStages) - 1) & 1);
+                const int64_t i0 = t.row0 + (int64_t)b * kTRB;
+                const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
+                ptx::mbar_arrive_expect_tx(&sm.full[s], 2u * bytes * (uint32_t)rows);
+                for (int rr = 0; rr < rows; ++rr) {
+                    ptx::bulk_g2s(&sm.g[s][rr][0], M.g + (i0 + rr) * M.ld_g + col_base, bytes, &sm.full[s]);
+                    ptx::bulk_g2s(&sm.w[s][rr][0], M.w + (i0 + rr) * n + col_base, bytes, &sm.full[s]);
+                }
+            }
+        }
+    } else {
+        // ---------------- consumer warps
+        const int64_t col0 = col_base + 4 * tid;
+        const bool active = 4 * tid < chunk_cols;
+        double qw[4][4];
+        float qr[4][4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            double raw[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) raw[k] = (active && k < r) ? (double)M.q_warm[(col0 + v) * M.ld_q + k] : 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                double a = 0.0;
+#pragma unroll
+                for (int i = 0; i <= k; ++i) a += raw[i] * sm.S[i * 4 + k];
+                qw[v][k] = a;
+                qr[v][k] = (active && k < rr_res) ? M.q_res[(col0 + v) * rr_res + k] : 0.f;
+            }
+        }
+        float zacc[4][4], xprev[kTRB][4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) zacc[v][k] = 0.f;
+        bool bad = false;
+        auto consume = [&](int bb) {
+            const int slot = bb % kTSlots;
+            const int64_t i0 = t.row0 + (int64_t)bb * kTRB;
+            if (tid < kTV) {
+                ptx::mbar_wait_cluster(&sm.xfull[slot], (bb / kTSlots) & 1);
+                double a = 0.0;
+                for (uint32_t cc = 0; cc < C; ++cc) a += sm.recv[slot][cc][tid];
+                sm.prow[tid] = (float)a;
+                const int rr = tid / 4, k = tid % 4;
+                if (me == 0 && i0 + rr < t.row1 && k < r) M.p_raw[(i0 + rr) * r + k] = a;
+            }
+            ptx::named_bar_sync(1, kTCons);
+#pragma unroll
+            for (int rr = 0; rr < kTRB; ++rr)
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) zacc[v][k] = fmaf(xprev[rr][v], sm.prow[rr * 4 + k], zacc[v][k]);
+        };
+        for (int b = 0; b < nrounds; ++b) {
+            const int s = b % kTStages;
+            const int64_t i0 = t.row0 + (int64_t)b * kTRB;
+            const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
+            if (chunk_cols > 0) ptx::mbar_wait(&sm.full[s], (b / kTStages) & 1);
+            double acc[kTV];
+            float x[kTRB][4];
+#pragma unroll
+            for (int rr = 0; rr < kTRB; ++rr) {
+                float pres[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    pres[k] = (k < rr_res && rr < rows) ? __ldg(M.p_res + (i0 + rr) * rr_res + k) : 0.f;
+                double pk[4] = {0.0, 0.0, 0.0, 0.0};
+                if (active && rr < rows) {
+                    const float4 gv = *reinterpret_cast<const float4 *>(&sm.g[s][rr][4 * tid]);
+                    const float4 wv = *reinterpret_cast<const float4 *>(&sm.w[s][rr][4 * tid]);
+                    const float gg[4] = {gv.x, gv.y, gv.z, gv.w}, ww[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        float dot = 0.f;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) dot = fmaf(pres[k], qr[v][k], dot);
+                        const float xv = gg[v] + (ww[v] - dot);
+                        bad |= !isfinite(xv);
+                        x[rr][v] = xv;
+                        const double xd = (double)xv;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) pk[k] = fma(xd, qw[v][k], pk[k]);
+                    }
+                    ptx::st_global_v4(M.w + (i0 + rr) * n + col0, x[rr][0], x[rr][1], x[rr][2], x[rr][3]);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) x[rr][v] = 0.f;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[rr * 4 + k] = pk[k];
+            }
+            // stage s fully read by this warp
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&sm.empty[s]);
+            const double part = warp_reduce_scatter<kTV>(acc, lane);
+            if ((lane & 1) == 0) sm.red[warp][scatter_owner_index<kTV>(lane)] = part;
+            ptx::named_bar_sync(1, kTCons);
+            const int slot = b % kTSlots;
+            if (tid < kTV) {
+                double a = 0.0;
+#pragma unroll
+                for (int w = 0; w < kTCons / 32; ++w) a += sm.red[w][tid];
+                const uint32_t dst = ptx::smem_addr(&sm.recv[slot][me][tid]);
+                for (uint32_t cc = 0; cc < C; ++cc) ptx::st_cluster_f64(ptx::mapa(dst, cc), a);
+            }
+            if (warp == 0) {
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::fence_cluster();
+                    const uint32_t bar = ptx::smem_addr(&sm.xfull[slot]);
+                    for (uint32_t cc = 0; cc < C; ++cc) ptx::mbar_arrive_remote(ptx::mapa(bar, cc));
+                }
+            }
+            if (b >= 1) consume(b - 1);
+#pragma unroll
+            for (int rr = 0; rr < kTRB; ++rr)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) xprev[rr][v] = x[rr][v];
+        }
+        if (nrounds >= 1) consume(nrounds - 1);
+        if (active) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < r) M.zpart[((int64_t)t.item * n + col0 + v) * r + k] = (double)zacc[v][k];
+        }
+        if (bad) atomicOr(status + t.mat, 1);
+    }
+    ptx::cluster_sync();  // no CTA leaves while a peer may still push into it
+}
+
 // ------------------------------------------------------------------ factor
 // One CTA per matrix; r x r work matrices live in the matrix's workspace slice
 // (L1/L2 resident).  Gram by (entry, row-group) partial sums reduced in fixed
@@ -563,7 +766,10 @@ __global__ void __launch_bounds__(kGThreads) k_gemm(const MatDev *mats, const Ge
     __shared__ float As[kGK][kGT + 4];
     __shared__ float Bs[kGK][kGT + 4];
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-    float acc[4][4] = {};
+    // P_raw and Q partials accumulate exact fp32 products in fp64: at high rank
+    // P_raw can be ill-conditioned and its rounding is amplified by cond(R)
+    typedef typename std::conditional<OP == 2, float, double>::type AccT;
+    AccT acc[4][4] = {};
     for (int64_t k0 = t.k0; k0 < t.k1; k0 += kGK) {
         // A tile: kGT rows x kGK cols
         for (int e = tid; e < kGT * kGK; e += kGThreads) {
@@ -598,7 +804,7 @@ __global__ void __launch_bounds__(kGThreads) k_gemm(const MatDev *mats, const Ge
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
+                for (int v = 0; v < 4; ++v) acc[u][v] = (AccT)a[u] * (AccT)b[v] + acc[u][v];
         }
         __syncthreads();
     }
@@ -614,7 +820,7 @@ __global__ void __launch_bounds__(kGThreads) k_gemm(const MatDev *mats, const Ge
             } else if (OP == 1) {
                 M.q_part[((int64_t)t.split * n + gi) * r + gj] = (double)acc[u][v];
             } else {
-                const float x = M.g[gi * M.ld_g + gj] + (M.w[gi * n + gj] - acc[u][v]);
+                const float x = M.g[gi * M.ld_g + gj] + (M.w[gi * n + gj] - (float)acc[u][v]);
                 bad |= !isfinite(x);
                 M.w[gi * n + gj] = x;
             }
@@ -851,7 +1057,22 @@ int launch_pass1z(const Plan &P, int32_t *status, cudaStream_t st) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1z<4>, (const MatDev *)P.d_mats, (const ZTile *)P.d_tz[c], status));
+        static const bool legacy = std::getenv("EDGC_PASS1Z") != nullptr;
+        if (legacy) {
+            EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1z<4>, (const MatDev *)P.d_mats, (const ZTile *)P.d_tz[c],
+                                             status));
+        } else {
+            static bool attr_set = false;
+            if (!attr_set) {
+                EDGC_CUDA_TRY(cudaFuncSetAttribute(k_pass1t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)sizeof(TSmem)));
+                attr_set = true;
+            }
+            cfg.blockDim = dim3(kTThreads);
+            cfg.dynamicSmemBytes = sizeof(TSmem);
+            EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1t, (const MatDev *)P.d_mats, (const ZTile *)P.d_tz[c],
+                                             status));
+        }
         EDGC_LAUNCH_CHECK();
     }
     return EDGC_OK;

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace edgc {
 namespace {
@@ -144,28 +145,45 @@ __device__ __forceinline__ uint32_t step_rng(const PlanDev &P, int64_t s) {
 // memory and the next one is prefetched while the current one resolves.
 constexpr int kWT = kWalkThreads;
 constexpr int kWK = 4;
-constexpr int kWBuf = kWT + 2 * kWK;
+constexpr int kRingBlk = 1024;            // draws per ring block (4 KB bulk copy)
+constexpr int kRingN = 8;                 // blocks in flight
+constexpr int kRing = kRingBlk * kRingN;  // ring size (draws), power of two
 
 __global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *status) {
     const PlanDev &P = plans[blockIdx.x];
-    __shared__ uint32_t s_draw[2][kWBuf];
+    extern __shared__ __align__(128) uint32_t s_ring[];   // kRing draws (dynamic: 32 KB)
     __shared__ uint32_t s_mask[kWK][kWT / 32];
     __shared__ uint32_t s_val[kWK][kWT];
     __shared__ int s_ev[kWK];
     __shared__ int s_ne, s_len, s_err;
+    __shared__ __align__(8) uint64_t s_full[kRingN];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t count = P.count, nd = P.n_draws;
-    int64_t s = 0, u = 0, base = 0;
-    int buf = 0;
-    for (int i = tid; i < kWBuf; i += kWT) s_draw[0][i] = (i < nd) ? P.draws[i] : 0u;
-    if (tid == 0) s_err = 0;
+    const int64_t nblocks = (nd + kRingBlk - 1) / kRingBlk;
+    int64_t next_blk = 0;   // first block not yet requested (used by thread 0)
+    auto request = [&](int64_t upto) {
+        while (next_blk < upto && next_blk < nblocks) {
+            const int slot = (int)(next_blk % kRingN);
+            const int64_t first = next_blk * kRingBlk;
+            const uint32_t bytes = (uint32_t)(min((int64_t)kRingBlk, nd - first) * 4);
+            ptx::mbar_arrive_expect_tx(&s_full[slot], bytes);
+            ptx::bulk_g2s(&s_ring[slot * kRingBlk], P.draws + first, bytes, &s_full[slot]);
+            ++next_blk;
+        }
+    };
+    if (tid == 0) {
+        for (int i = 0; i < kRingN; ++i) ptx::mbar_init(&s_full[i], 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        s_err = 0;
+    }
     __syncthreads();
+    if (tid == 0) request(kRingN);
+    int64_t s = 0, u = 0;
     while (s < count) {
-        // prefetch the window that follows if this one resolves with shift < kWK
-        const int64_t nb = u + kWT;
-        const uint32_t pre0 = (nb + tid < nd) ? __ldg(P.draws + nb + tid) : 0u;
-        const uint32_t pre1 = (tid < 2 * kWK && nb + kWT + tid < nd) ? __ldg(P.draws + nb + kWT + tid) : 0u;
-        const int off = (int)(u - base);
+        // this window reads draws [u, u + kWT + kWK): ring blocks u / kRingBlk and the next one
+        const int64_t b0 = u / kRingBlk;
+        for (int64_t bb = b0; bb <= b0 + 1 && bb < nblocks; ++bb)
+            ptx::mbar_wait(&s_full[bb % kRingN], (uint32_t)((bb / kRingN) & 1));
         const int64_t st = s + tid;
         const bool valid = st < count;
         const uint32_t rng = valid ? step_rng(P, st) : 0u;
@@ -174,11 +192,9 @@ __global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *sta
             uint32_t val = 0;
             bool rej = false;
             if (valid) {
-                if (u + tid + j >= nd) {
-                    rej = true;
-                } else {
-                    rej = !lemire_accept(s_draw[buf][off + tid + j], rng, val);
-                }
+                const int64_t pos = u + tid + j;
+                if (pos >= nd) rej = true;
+                else rej = !lemire_accept(s_ring[pos & (kRing - 1)], rng, val);
             }
             s_val[j][tid] = val;
             const unsigned bal = __ballot_sync(0xffffffffu, rej);
@@ -189,7 +205,6 @@ __global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *sta
             const int nvalid = (int)min((int64_t)kWT, count - s);
             int cur = 0, d = 0, ne = 0, len = nvalid;
             while (true) {
-                // first lane >= cur (and < nvalid) rejected at shift d
                 uint32_t bits = s_mask[d][lane];
                 const int lo = lane * 32;
                 if (lo + 32 <= cur) bits = 0u;
@@ -219,17 +234,8 @@ __global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *sta
         if (tid == 0 && u + len + ne > nd) s_err = 1;   // consumed draws past the generated stream
         s += len;
         u += len + ne;
-        const int nbuf = buf ^ 1;
-        if (u - nb >= 0 && u - nb <= kWK) {
-            s_draw[nbuf][tid] = pre0;
-            if (tid < 2 * kWK) s_draw[nbuf][kWT + tid] = pre1;
-            base = nb;
-        } else {
-            for (int i = tid; i < kWBuf; i += kWT) s_draw[nbuf][i] = (u + i < nd) ? P.draws[u + i] : 0u;
-            base = u;
-        }
-        buf = nbuf;
-        __syncthreads();
+        __syncthreads();   // every read of ring blocks below u / kRingBlk is done
+        if (tid == 0) request(u / kRingBlk + kRingN);
         if (s_err || (len == 0 && ne == 0)) break;
     }
     if (tid == 0) status[blockIdx.x] = (s_err || s < count) ? EDGC_EDRAWS : EDGC_OK;
@@ -246,10 +252,10 @@ __device__ __forceinline__ int find_plan_steps(const PlanDev *plans, int n, int6
 }
 
 // ---- P3: hash (key = bounded value) -> list of steps ----------------------
-__global__ void __launch_bounds__(kStepThreads) k_index(const PlanDev *plans, int n_plans) {
-    const int p = find_plan_steps(plans, n_plans, blockIdx.x);
+__global__ void __launch_bounds__(kStepThreads) k_index(const PlanDev *plans, int p0, int p1, int64_t blk0) {
+    const int p = p0 + find_plan_steps(plans + p0, p1 - p0, blk0 + blockIdx.x);
     const PlanDev &P = plans[p];
-    const int64_t s = (int64_t)(blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
+    const int64_t s = (int64_t)(blk0 + blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
     if (s >= P.count) return;
     const int32_t key = P.rv[s];
     const uint32_t cap = (uint32_t)P.cap;
@@ -282,10 +288,10 @@ __device__ __forceinline__ int32_t latest_before(const PlanDev &P, int32_t key, 
 }
 
 // ---- P4: resolve chains / collisions ---------------------------------------
-__global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, int n_plans) {
-    const int p = find_plan_steps(plans, n_plans, blockIdx.x);
+__global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, int p0, int p1, int64_t blk0) {
+    const int p = p0 + find_plan_steps(plans + p0, p1 - p0, blk0 + blockIdx.x);
     const PlanDev &P = plans[p];
-    const int64_t s64 = (int64_t)(blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
+    const int64_t s64 = (int64_t)(blk0 + blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
     if (s64 >= P.count) return;
     const int32_t s = (int32_t)s64;
     const int64_t N = P.n_elems, count = P.count;
@@ -329,6 +335,7 @@ struct PlanLayout {
     int64_t draw_chunks = 0, step_blocks = 0;
     int64_t table_bytes = 0;
     char *table_base = nullptr;
+    std::vector<int64_t> table_off;   // per plan, relative to table_base (plan tables are contiguous)
 };
 
 int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes, PlanLayout &L) {
@@ -356,7 +363,7 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
         const double lam = (double)d.count * (double)d.n_elems / 4294967296.0;
         int64_t slack = (int64_t)(2.0 * lam + 16.0 * std::sqrt(lam + 1.0)) + 4096;
         int64_t nd = d.count + slack;
-        nd = (nd + 1) & ~int64_t(1);
+        nd = (nd + 3) & ~int64_t(3);
         P.n_draws = nd;
         P.draw_chunk0 = chunk;
         chunk += ceil_div(nd / 2, kDrawsPerBlock);
@@ -378,13 +385,16 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
     }
     a.off = align256(a.off);
     const int64_t t0 = a.off;
+    L.table_off.assign(n + 1, 0);
     for (int i = 0; i < n; ++i) {
         PlanDev &P = L.dev[i];
+        L.table_off[i] = a.off - t0;
         P.keys = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
         a.off += caps[i] * 4;
         P.heads = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
         a.off += caps[i] * 4;
     }
+    L.table_off[n] = a.off - t0;
     L.table_bytes = a.off - t0;
     L.table_base = a.base ? a.base + t0 : nullptr;
     L.ws_bytes = a.off;
@@ -429,15 +439,38 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
     cudaStream_t st = (cudaStream_t)stream;
     PlanDev *d_plans = reinterpret_cast<PlanDev *>(ws);
     EDGC_CUDA_TRY(cudaMemcpyAsync(d_plans, L.dev.data(), sizeof(PlanDev) * n_plans, cudaMemcpyHostToDevice, st));
-    EDGC_CUDA_TRY(cudaMemsetAsync(L.table_base, 0xFF, L.table_bytes, st));
     k_draws<<<(unsigned)L.draw_chunks, kP1Threads, 0, st>>>(d_plans, n_plans);
     EDGC_LAUNCH_CHECK();
-    k_walk<<<n_plans, kWalkThreads, 0, st>>>(d_plans, status_dev);
+    static bool walk_attr = false;
+    if (!walk_attr) {
+        EDGC_CUDA_TRY(cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(kRing * sizeof(uint32_t))));
+        walk_attr = true;
+    }
+    k_walk<<<n_plans, kWalkThreads, kRing * sizeof(uint32_t), st>>>(d_plans, status_dev);
     EDGC_LAUNCH_CHECK();
-    k_index<<<(unsigned)L.step_blocks, kStepThreads, 0, st>>>(d_plans, n_plans);
-    EDGC_LAUNCH_CHECK();
-    k_resolve<<<(unsigned)L.step_blocks, kStepThreads, 0, st>>>(d_plans, n_plans);
-    EDGC_LAUNCH_CHECK();
+    // index + resolve plan groups whose hash tables, links and bounded values
+    // fit in L2 together, so the random table traffic stays on chip
+    const int64_t kGroupBytes = 48ll << 20;
+    int p0 = 0;
+    while (p0 < n_plans) {
+        int p1 = p0 + 1;
+        int64_t bytes = (L.table_off[p0 + 1] - L.table_off[p0]) + 8 * L.dev[p0].count;
+        while (p1 < n_plans) {
+            const int64_t more = (L.table_off[p1 + 1] - L.table_off[p1]) + 8 * L.dev[p1].count;
+            if (bytes + more > kGroupBytes) break;
+            bytes += more;
+            ++p1;
+        }
+        EDGC_CUDA_TRY(cudaMemsetAsync(L.table_base + L.table_off[p0], 0xFF, L.table_off[p1] - L.table_off[p0], st));
+        const int64_t blk0 = L.dev[p0].step_block0;
+        const int64_t blk1 = (p1 < n_plans) ? L.dev[p1].step_block0 : L.step_blocks;
+        k_index<<<(unsigned)(blk1 - blk0), kStepThreads, 0, st>>>(d_plans, p0, p1, blk0);
+        EDGC_LAUNCH_CHECK();
+        k_resolve<<<(unsigned)(blk1 - blk0), kStepThreads, 0, st>>>(d_plans, p0, p1, blk0);
+        EDGC_LAUNCH_CHECK();
+        p0 = p1;
+    }
     return EDGC_OK;
 }
 

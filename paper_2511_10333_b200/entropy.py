@@ -104,19 +104,19 @@ def sample_plans(specs, device=None):
         out[i] = torch.empty(count, dtype=torch.int32, device=dev)
         todo.append(i)
     cap_bytes = _plan_ws_cap(dev)
+    descs = {}
+    sizes = {}
+    for i in todo:
+        n_elems, count, seed = specs[i]
+        descs[i] = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]))
+        sizes[i] = L.edgc_sample_plan_workspace_bytes((_lib.PlanDesc * 1)(descs[i]), 1) + 4096
     k = 0
     while k < len(todo):
-        # grow the batch while the workspace stays under the cap
-        batch = []
-        while k < len(todo):
-            i = todo[k]
-            n_elems, count, seed = specs[i]
-            d = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]))
-            trial = (_lib.PlanDesc * (len(batch) + 1))(*(batch + [d]))
-            need = L.edgc_sample_plan_workspace_bytes(trial, len(batch) + 1)
-            if batch and need > cap_bytes:
-                break
-            batch.append(d)
+        # greedy batches under the workspace cap (per-plan sizes add up, plus slack)
+        batch, acc = [], 0
+        while k < len(todo) and (not batch or acc + sizes[todo[k]] <= cap_bytes):
+            batch.append(descs[todo[k]])
+            acc += sizes[todo[k]]
             k += 1
         arr = (_lib.PlanDesc * len(batch))(*batch)
         need = L.edgc_sample_plan_workspace_bytes(arr, len(batch))
@@ -126,8 +126,7 @@ def sample_plans(specs, device=None):
         status = torch.zeros(len(batch), dtype=torch.int32, device=dev)
         _lib.check(L.edgc_sample_plan(arr, len(batch), _lib.ptr(status), _lib.ptr(ws), ws.numel(),
                                       _lib.stream_ptr(dev)), "edgc_sample_plan")
-        bad = status.nonzero()
-        if bad.numel():
+        if int(status.max().item()) != 0:
             raise RuntimeError("sample plan exhausted its pre-generated draws")
     return out
 
