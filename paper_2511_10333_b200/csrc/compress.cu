@@ -1153,6 +1153,57 @@ __global__ void __launch_bounds__(kRThreads) k_recon(const ReconDev *descs, cons
     }
 }
 
+// float4 variant for W*r <= 8 (the DP-average hot case): each thread owns 4
+// adjacent columns and kV4Rows rows per pass, with Q (4 x W*r) in registers and
+// P rows broadcast from shared memory; 512-byte coalesced streaming stores.
+constexpr int kV4Threads = 128;
+constexpr int kV4Cols = 4 * kV4Threads;
+constexpr int kV4Rows = 8;
+constexpr int kV4TileRows = 64;
+
+template <int WR>
+__global__ void __launch_bounds__(kV4Threads) k_recon4(const ReconDev *descs, const RTile *tiles) {
+    const RTile t = tiles[blockIdx.x];
+    const ReconDev D = descs[t.d];
+    const int r = D.r, wr = D.r * D.n_ranks;
+    const int64_t j0 = t.col0 + 4 * threadIdx.x;
+    const bool active = j0 < t.col1;
+    __shared__ float s_p[kV4TileRows][WR];
+    for (int e = threadIdx.x; e < kV4TileRows * WR; e += kV4Threads) {
+        const int rr = e / WR, c = e % WR;
+        const int64_t i = t.row0 + rr;
+        s_p[rr][c] = (i < t.row1 && c < wr) ? D.p[(int64_t)(c / r) * D.p_stride + i * r + (c % r)] : 0.f;
+    }
+    float q[4][WR];
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int c = 0; c < WR; ++c)
+            q[v][c] = (active && c < wr) ? __ldg(D.q + (int64_t)(c / r) * D.q_stride + (j0 + v) * r + (c % r)) : 0.f;
+    __syncthreads();
+    if (!active) return;
+    for (int64_t row = t.row0; row < t.row1; row += kV4Rows) {
+        float acc[kV4Rows][4];
+#pragma unroll
+        for (int rr = 0; rr < kV4Rows; ++rr) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                float a = 0.f;
+#pragma unroll
+                for (int c = 0; c < WR; ++c) a = fmaf(s_p[row - t.row0 + rr][c], q[v][c], a);
+                acc[rr][v] = a * D.scale;
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < kV4Rows; ++rr) {
+            const int64_t i = row + rr;
+            if (i < t.row1)
+                __stcs(reinterpret_cast<float4 *>(D.out + i * D.ld_out + j0),
+                       make_float4(acc[rr][0], acc[rr][1], acc[rr][2], acc[rr][3]));
+        }
+    }
+}
+
 // ----------------------------------------------------------- misc kernels
 __global__ void k_residual(const float *w, const float *p, const float *q, int r, int64_t m, int64_t n, float *e) {
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < m * n; x += (int64_t)gridDim.x * blockDim.x) {
@@ -1300,14 +1351,15 @@ extern "C" int edgc_compress(const edgc_compress_desc *descs, int n, double col_
 namespace {
 struct RPlan {
     std::vector<ReconDev> d;
-    std::vector<RTile> tiles;
+    std::vector<RTile> tiles, tiles4;
     int64_t bytes = 0;
     ReconDev *dd = nullptr;
-    RTile *dt = nullptr;
+    RTile *dt = nullptr, *dt4 = nullptr;
 };
 int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
     Arena a(ws, INT64_MAX);
     P.tiles.clear();
+    P.tiles4.clear();
     P.d.resize(n);
     P.dd = a.take<ReconDev>(n);
     for (int k = 0; k < n; ++k) {
@@ -1316,11 +1368,19 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
                      "recon desc %d: bad arguments", k);
         P.d[k] = ReconDev{s.p, s.q, s.out, s.m, s.n, s.ld_out, s.p_rank_stride, s.q_rank_stride, s.r, s.n_ranks,
                           s.scale};
-        for (int64_t c0 = 0; c0 < s.n; c0 += kRThreads)
-            for (int64_t r0 = 0; r0 < s.m; r0 += kRTileRows)
-                P.tiles.push_back(RTile{k, c0, std::min(s.n, c0 + kRThreads), r0, std::min(s.m, r0 + kRTileRows)});
+        const bool v4 = s.r * s.n_ranks <= 8 && s.n % 4 == 0 && s.ld_out % 4 == 0 && ((uintptr_t)s.out % 16 == 0);
+        if (v4) {
+            for (int64_t c0 = 0; c0 < s.n; c0 += kV4Cols)
+                for (int64_t r0 = 0; r0 < s.m; r0 += kV4TileRows)
+                    P.tiles4.push_back(RTile{k, c0, std::min(s.n, c0 + kV4Cols), r0, std::min(s.m, r0 + kV4TileRows)});
+        } else {
+            for (int64_t c0 = 0; c0 < s.n; c0 += kRThreads)
+                for (int64_t r0 = 0; r0 < s.m; r0 += kRTileRows)
+                    P.tiles.push_back(RTile{k, c0, std::min(s.n, c0 + kRThreads), r0, std::min(s.m, r0 + kRTileRows)});
+        }
     }
     P.dt = a.take<RTile>(P.tiles.size());
+    P.dt4 = a.take<RTile>(P.tiles4.size());
     P.bytes = a.off;
     return EDGC_OK;
 }
@@ -1329,7 +1389,7 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
 struct edgc_recon_plan {
     std::vector<edgc_recon_desc> descs;
     RPlan P;
-    int wr = 0;
+    int wr = 0, wr4 = 0;
 };
 
 extern "C" int edgc_recon_plan_create(const edgc_recon_desc *descs, int n, edgc_recon_plan **out) {
@@ -1338,7 +1398,11 @@ extern "C" int edgc_recon_plan_create(const edgc_recon_desc *descs, int n, edgc_
     h->descs.assign(descs, descs + n);
     int rc = make_rplan(descs, n, nullptr, h->P);
     if (rc != EDGC_OK) { delete h; return rc; }
-    for (int k = 0; k < n; ++k) h->wr = std::max(h->wr, descs[k].r * descs[k].n_ranks);
+    for (int k = 0; k < n; ++k) {
+        const int wr = descs[k].r * descs[k].n_ranks;
+        if (wr <= 8) h->wr4 = std::max(h->wr4, wr);
+        h->wr = std::max(h->wr, wr);
+    }
     *out = h;
     return EDGC_OK;
 }
@@ -1353,7 +1417,12 @@ extern "C" int edgc_recon_plan_bind(edgc_recon_plan *h, void *ws, int64_t ws_byt
     if (rc != EDGC_OK) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     EDGC_CUDA_TRY(cudaMemcpyAsync(P.dd, P.d.data(), sizeof(ReconDev) * P.d.size(), cudaMemcpyHostToDevice, st));
-    EDGC_CUDA_TRY(cudaMemcpyAsync(P.dt, P.tiles.data(), sizeof(RTile) * P.tiles.size(), cudaMemcpyHostToDevice, st));
+    if (!P.tiles.empty())
+        EDGC_CUDA_TRY(
+            cudaMemcpyAsync(P.dt, P.tiles.data(), sizeof(RTile) * P.tiles.size(), cudaMemcpyHostToDevice, st));
+    if (!P.tiles4.empty())
+        EDGC_CUDA_TRY(
+            cudaMemcpyAsync(P.dt4, P.tiles4.data(), sizeof(RTile) * P.tiles4.size(), cudaMemcpyHostToDevice, st));
     EDGC_CUDA_TRY(cudaStreamSynchronize(st));
     return EDGC_OK;
 }
@@ -1361,12 +1430,20 @@ extern "C" int edgc_recon_plan_bind(edgc_recon_plan *h, void *ws, int64_t ws_byt
 extern "C" int edgc_recon_plan_run(edgc_recon_plan *h, void *stream) {
     EDGC_REQUIRE(h && h->P.dd, "edgc_recon_plan_run: plan not bound");
     cudaStream_t st = (cudaStream_t)stream;
-    const unsigned grid = (unsigned)h->P.tiles.size();
-    if (h->wr <= 4) k_recon<4><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
-    else if (h->wr <= 8) k_recon<8><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
-    else if (h->wr <= 16) k_recon<16><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
-    else k_recon<32><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
-    EDGC_LAUNCH_CHECK();
+    if (!h->P.tiles4.empty()) {
+        const unsigned g4 = (unsigned)h->P.tiles4.size();
+        if (h->wr4 <= 4) k_recon4<4><<<g4, kV4Threads, 0, st>>>(h->P.dd, h->P.dt4);
+        else k_recon4<8><<<g4, kV4Threads, 0, st>>>(h->P.dd, h->P.dt4);
+        EDGC_LAUNCH_CHECK();
+    }
+    if (!h->P.tiles.empty()) {
+        const unsigned grid = (unsigned)h->P.tiles.size();
+        if (h->wr <= 4) k_recon<4><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
+        else if (h->wr <= 8) k_recon<8><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
+        else if (h->wr <= 16) k_recon<16><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
+        else k_recon<32><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
+        EDGC_LAUNCH_CHECK();
+    }
     return EDGC_OK;
 }
 
