@@ -346,34 +346,42 @@ __global__ void __launch_bounds__(kZThreads, 2) k_pass1z(const MatDev *mats, con
 }
 
 // ------------------------------------------- pass 1 (Z, TMA-pipelined)
-// Same math as k_pass1z, restructured for bandwidth:
-//  * a producer warp streams the cluster CTA's [4 rows x 1024 cols] tiles of g
-//    and w into a 3-stage shared-memory ring with 1-D bulk async copies (TMA
-//    engine, mbarrier complete_tx); consumer warps never stall on loads;
-//  * row dots are accumulated in fp64 (exact fp32 x fp32 products);
-//  * the cluster exchange is a push: each CTA stores its partial row dots
-//    into every peer's shared memory (st.shared::cluster) and release-arrives
-//    on the peer's mbarrier; the receive side is consumed one round later,
-//    so the exchange latency overlaps the next round's work (3 slots keep the
-//    lagged buffers race-free).
+// Same math as k_pass1z, warp-specialised for bandwidth.  Per CTA (one per
+// 1024-column chunk of a cluster's row strip):
+//   producer warp  streams [4 rows x 1024 cols] tiles of g and w into a
+//                  3-stage shared-memory ring with 1-D bulk async copies
+//                  (TMA engine, mbarrier complete_tx);
+//   8 consumer warps  error feedback, w write-back, fp64 row dots (exact
+//                  fp32 x fp32 products), per-warp butterfly -> red[] ring;
+//                  then, two rounds later, Z += x * P_raw with that round's
+//                  rows -- they never wait on the cluster;
+//   exchange warp  sums the 8 warp partials, pushes them into every peer's
+//                  shared memory (st.shared::cluster) and release-arrives on
+//                  the peer's mbarrier, waits for all peers, writes P_raw
+//                  rows to shared memory and signals the consumers.
+// All hand-offs are mbarriers; no block-wide barrier in the steady state.
 constexpr int kTCons = 256;
-constexpr int kTThreads = kTCons + 32;
+constexpr int kTThreads = kTCons + 64;   // + producer warp + exchange warp
 constexpr int kTRB = 4;
 constexpr int kTStages = 3;
 constexpr int kTCW = 4 * kTCons;
-constexpr int kTSlots = 3;
-constexpr int kTV = kTRB * 4;   // row-dot values per round (RMAX = 4)
+constexpr int kTLag = 2;                 // consumer Z update lags the exchange by 2 rounds
+constexpr int kTRing = kTLag + 1;        // red / prow ring depth
+constexpr int kTSlots = 3;               // DSMEM receive slots
+constexpr int kTV = kTRB * 4;            // row-dot values per round (RMAX = 4)
 
 struct TSmem {
     float g[kTStages][kTRB][kTCW];
     float w[kTStages][kTRB][kTCW];
     double recv[kTSlots][8][kTV];
-    double red[kTCons / 32][kTV];
+    double red[kTRing][kTCons / 32][kTV];
+    double prow[kTRing][kTV];
     double S[16];
-    float prow[kTV];
     alignas(8) uint64_t full[kTStages];
     alignas(8) uint64_t empty[kTStages];
     alignas(8) uint64_t xfull[kTSlots];
+    alignas(8) uint64_t redfull[kTRing];
+    alignas(8) uint64_t prowready[kTRing];
 };
 
 __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, const ZTile *tiles, int32_t *status) {
@@ -389,6 +397,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
     const int64_t col_base = (int64_t)me * kTCW;
     const int64_t chunk_cols = min((int64_t)kTCW, n - col_base);
     const int nrounds = (int)((t.row1 - t.row0 + kTRB - 1) / kTRB);
+    constexpr int kProducer = kTCons / 32, kExchange = kTCons / 32 + 1;
 
     if (tid == 0) {
         for (int s = 0; s < kTStages; ++s) {
@@ -396,6 +405,10 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             ptx::mbar_init(&sm.empty[s], kTCons / 32);
         }
         for (int s = 0; s < kTSlots; ++s) ptx::mbar_init(&sm.xfull[s], C);
+        for (int s = 0; s < kTRing; ++s) {
+            ptx::mbar_init(&sm.redfull[s], kTCons / 32);
+            ptx::mbar_init(&sm.prowready[s], 1);
+        }
         ptx::fence_mbar_init();
     }
     if (tid < 16) {
@@ -406,8 +419,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
     }
     ptx::cluster_sync();
 
-    if (warp == kTCons / 32) {
-        // ---------------- producer warp
+    if (warp == kProducer) {
         if (lane == 0 && chunk_cols > 0) {
             const uint32_t bytes = (uint32_t)(chunk_cols * 4);
             for (int b = 0; b < nrounds; ++b) {
@@ -421,6 +433,31 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                     ptx::bulk_g2s(&sm.w[s][rr][0], M.w + (i0 + rr) * n + col_base, bytes, &sm.full[s]);
                 }
             }
+        }
+    } else if (warp == kExchange) {
+        for (int b = 0; b < nrounds; ++b) {
+            const int q = b % kTRing, slot = b % kTSlots;
+            ptx::mbar_wait(&sm.redfull[q], (b / kTRing) & 1);
+            if (lane < kTV) {
+                double a = 0.0;
+#pragma unroll
+                for (int w = 0; w < kTCons / 32; ++w) a += sm.red[q][w][lane];
+                const uint32_t dst = ptx::smem_addr(&sm.recv[slot][me][lane]);
+                for (uint32_t cc = 0; cc < C; ++cc) ptx::st_cluster_f64(ptx::mapa(dst, cc), a);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t bar = ptx::smem_addr(&sm.xfull[slot]);
+                for (uint32_t cc = 0; cc < C; ++cc) ptx::mbar_arrive_remote(ptx::mapa(bar, cc));
+            }
+            ptx::mbar_wait_cluster(&sm.xfull[slot], (b / kTSlots) & 1);
+            if (lane < kTV) {
+                double a = 0.0;
+                for (uint32_t cc = 0; cc < C; ++cc) a += sm.recv[slot][cc][lane];
+                sm.prow[q][lane] = a;
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cta(&sm.prowready[q]);
         }
     } else {
         // ---------------- consumer warps
@@ -442,33 +479,32 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 qr[v][k] = (active && k < rr_res) ? M.q_res[(col0 + v) * rr_res + k] : 0.f;
             }
         }
-        float zacc[4][4], xprev[kTRB][4];
+        float zacc[4][4], x1[kTRB][4], x2[kTRB][4];   // x of rounds b-1 and b-2
 #pragma unroll
         for (int v = 0; v < 4; ++v)
 #pragma unroll
             for (int k = 0; k < 4; ++k) zacc[v][k] = 0.f;
         bool bad = false;
-        auto consume = [&](int bb) {
-            const int slot = bb % kTSlots;
+        auto consume = [&](int bb, const float (&xp)[kTRB][4]) {
+            const int q = bb % kTRing;
+            ptx::mbar_wait(&sm.prowready[q], (bb / kTRing) & 1);
             const int64_t i0 = t.row0 + (int64_t)bb * kTRB;
-            if (tid < kTV) {
-                ptx::mbar_wait_cluster(&sm.xfull[slot], (bb / kTSlots) & 1);
-                double a = 0.0;
-                for (uint32_t cc = 0; cc < C; ++cc) a += sm.recv[slot][cc][tid];
-                sm.prow[tid] = (float)a;
+            if (me == 0 && tid < kTV) {
                 const int rr = tid / 4, k = tid % 4;
-                if (me == 0 && i0 + rr < t.row1 && k < r) M.p_raw[(i0 + rr) * r + k] = a;
+                if (i0 + rr < t.row1 && k < r) M.p_raw[(i0 + rr) * r + k] = sm.prow[q][tid];
             }
-            ptx::named_bar_sync(1, kTCons);
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr)
 #pragma unroll
-                for (int v = 0; v < 4; ++v)
+                for (int k = 0; k < 4; ++k) {
+                    const float pv = (float)sm.prow[q][rr * 4 + k];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) zacc[v][k] = fmaf(xprev[rr][v], sm.prow[rr * 4 + k], zacc[v][k]);
+                    for (int v = 0; v < 4; ++v) zacc[v][k] = fmaf(xp[rr][v], pv, zacc[v][k]);
+                }
         };
+#pragma unroll 1
         for (int b = 0; b < nrounds; ++b) {
-            const int s = b % kTStages;
+            const int s = b % kTStages, q = b % kTRing;
             const int64_t i0 = t.row0 + (int64_t)b * kTRB;
             const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
             if (chunk_cols > 0) ptx::mbar_wait(&sm.full[s], (b / kTStages) & 1);
@@ -505,35 +541,24 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[rr * 4 + k] = pk[k];
             }
-            // stage s fully read by this warp
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&sm.empty[s]);
+            if (lane == 0) ptx::mbar_arrive(&sm.empty[s]);   // stage s read by this warp
             const double part = warp_reduce_scatter<kTV>(acc, lane);
-            if ((lane & 1) == 0) sm.red[warp][scatter_owner_index<kTV>(lane)] = part;
-            ptx::named_bar_sync(1, kTCons);
-            const int slot = b % kTSlots;
-            if (tid < kTV) {
-                double a = 0.0;
-#pragma unroll
-                for (int w = 0; w < kTCons / 32; ++w) a += sm.red[w][tid];
-                const uint32_t dst = ptx::smem_addr(&sm.recv[slot][me][tid]);
-                for (uint32_t cc = 0; cc < C; ++cc) ptx::st_cluster_f64(ptx::mapa(dst, cc), a);
-            }
-            if (warp == 0) {
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::fence_cluster();
-                    const uint32_t bar = ptx::smem_addr(&sm.xfull[slot]);
-                    for (uint32_t cc = 0; cc < C; ++cc) ptx::mbar_arrive_remote(ptx::mapa(bar, cc));
-                }
-            }
-            if (b >= 1) consume(b - 1);
+            if ((lane & 1) == 0) sm.red[q][warp][scatter_owner_index<kTV>(lane)] = part;
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cta(&sm.redfull[q]);
+            if (b >= kTLag) consume(b - kTLag, x2);
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) xprev[rr][v] = x[rr][v];
+                for (int v = 0; v < 4; ++v) {
+                    x2[rr][v] = x1[rr][v];
+                    x1[rr][v] = x[rr][v];
+                }
         }
-        if (nrounds >= 1) consume(nrounds - 1);
+        // drain: rounds nrounds-2 (in x2) and nrounds-1 (in x1)
+        if (nrounds >= 2) consume(nrounds - 2, x2);
+        if (nrounds >= 1) consume(nrounds - 1, x1);
         if (active) {
 #pragma unroll
             for (int v = 0; v < 4; ++v)

@@ -102,3 +102,12 @@ __device__ __forceinline__ void st_global_v4(float *p, float a, float b, float c
 
 }  // namespace ptx
 }  // namespace edgc
+
+namespace edgc {
+namespace ptx {
+// arrive on a local mbarrier with release at cluster scope (consumer -> exchange warp handoff)
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+}  // namespace ptx
+}  // namespace edgc

@@ -143,8 +143,10 @@ __device__ __forceinline__ uint32_t step_rng(const PlanDev &P, int64_t s) {
 // lane at shift #events at lanes <= l.  Up to kWK-1 rejections fit in one
 // window; rarer bursts end the window early.  The draw window lives in shared
 // memory and the next one is prefetched while the current one resolves.
-constexpr int kWT = kWalkThreads;
-constexpr int kWK = 4;
+constexpr int kWT = 256;                  // threads per walk CTA
+constexpr int kWQ = 4;                    // consecutive steps per thread
+constexpr int kWW = kWT * kWQ;            // steps per window
+constexpr int kWK = 4;                    // speculative shifts
 constexpr int kRingBlk = 1024;            // draws per ring block (4 KB bulk copy)
 constexpr int kRingN = 8;                 // blocks in flight
 constexpr int kRing = kRingBlk * kRingN;  // ring size (draws), power of two
@@ -152,22 +154,25 @@ constexpr int kRing = kRingBlk * kRingN;  // ring size (draws), power of two
 __global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *status) {
     const PlanDev &P = plans[blockIdx.x];
     extern __shared__ __align__(128) uint32_t s_ring[];   // kRing draws (dynamic: 32 KB)
-    __shared__ uint32_t s_mask[kWK][kWT / 32];
-    __shared__ uint32_t s_val[kWK][kWT];
+    __shared__ uint32_t s_mask[kWK][kWW / 32];
     __shared__ int s_ev[kWK];
     __shared__ int s_ne, s_len, s_err;
     __shared__ __align__(8) uint64_t s_full[kRingN];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t count = P.count, nd = P.n_draws;
     const int64_t nblocks = (nd + kRingBlk - 1) / kRingBlk;
-    int64_t next_blk = 0;   // first block not yet requested (used by thread 0)
+    const uint32_t tail = (uint32_t)P.tail;
+    const uint32_t rng_hi = tail ? (uint32_t)(P.n_elems - 1) : (uint32_t)(P.n_elems - P.count);
+    int32_t *rv = P.rv;
+    const uint32_t *draws = P.draws;
+    int64_t next_blk = 0;   // first block not yet requested (thread 0)
     auto request = [&](int64_t upto) {
         while (next_blk < upto && next_blk < nblocks) {
             const int slot = (int)(next_blk % kRingN);
             const int64_t first = next_blk * kRingBlk;
             const uint32_t bytes = (uint32_t)(min((int64_t)kRingBlk, nd - first) * 4);
             ptx::mbar_arrive_expect_tx(&s_full[slot], bytes);
-            ptx::bulk_g2s(&s_ring[slot * kRingBlk], P.draws + first, bytes, &s_full[slot]);
+            ptx::bulk_g2s(&s_ring[slot * kRingBlk], draws + first, bytes, &s_full[slot]);
             ++next_blk;
         }
     };
@@ -180,37 +185,53 @@ __global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *sta
     if (tid == 0) request(kRingN);
     int64_t s = 0, u = 0;
     while (s < count) {
-        // this window reads draws [u, u + kWT + kWK): ring blocks u / kRingBlk and the next one
         const int64_t b0 = u / kRingBlk;
         for (int64_t bb = b0; bb <= b0 + 1 && bb < nblocks; ++bb)
             ptx::mbar_wait(&s_full[bb % kRingN], (uint32_t)((bb / kRingN) & 1));
-        const int64_t st = s + tid;
-        const bool valid = st < count;
-        const uint32_t rng = valid ? step_rng(P, st) : 0u;
+        // this thread's steps s + 4 tid + q use draws u + 4 tid + q + j
+        const int nvalid = (int)min((int64_t)kWW, count - s);
+        const uint32_t ubase = (uint32_t)(u & (kRing - 1)) + 4u * tid;
+        const int64_t dleft = nd - u - 4 * tid;   // draws generated from this thread's first one on
+        uint32_t d[kWQ + kWK - 1];
+#pragma unroll
+        for (int e = 0; e < kWQ + kWK - 1; ++e) d[e] = s_ring[(ubase + e) & (kRing - 1)];
+        uint32_t val[kWQ][kWK];
+        uint32_t nib[kWK] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int q = 0; q < kWQ; ++q) {
+            const int step = 4 * tid + q;
+            // rng of step s + step: tail i = N-1-(s+step); Floyd j = N-count+(s+step)
+            const uint32_t off = (uint32_t)s + (uint32_t)step;
+            const uint32_t rng = tail ? rng_hi - off : rng_hi + off;
+            const uint32_t excl = rng + 1u;
+#pragma unroll
+            for (int j = 0; j < kWK; ++j) {
+                const uint64_t m = (uint64_t)d[q + j] * excl;
+                val[q][j] = (uint32_t)(m >> 32);
+                bool rej = false;
+                const uint32_t left = (uint32_t)m;
+                if (left < excl) rej = left < (0xFFFFFFFFu - rng) % excl;
+                if ((int64_t)(q + j) >= dleft) rej = true;   // past the generated stream
+                if (step < nvalid && rej) nib[j] |= 1u << q;
+            }
+        }
+        // assemble per-shift 32-bit words: word (8 warp + lane/8) holds steps 32 w .. 32 w + 31
 #pragma unroll
         for (int j = 0; j < kWK; ++j) {
-            uint32_t val = 0;
-            bool rej = false;
-            if (valid) {
-                const int64_t pos = u + tid + j;
-                if (pos >= nd) rej = true;
-                else rej = !lemire_accept(s_ring[pos & (kRing - 1)], rng, val);
-            }
-            s_val[j][tid] = val;
-            const unsigned bal = __ballot_sync(0xffffffffu, rej);
-            if (lane == 0) s_mask[j][warp] = bal;
+            uint32_t wv = nib[j] << (4 * (lane & 7));
+            wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
+            wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
+            wv |= __shfl_xor_sync(0xffffffffu, wv, 4);
+            if ((lane & 7) == 0) s_mask[j][warp * 4 + (lane >> 3)] = wv;
         }
         __syncthreads();
         if (warp == 0) {
-            const int nvalid = (int)min((int64_t)kWT, count - s);
-            int cur = 0, d = 0, ne = 0, len = nvalid;
+            int cur = 0, dd = 0, ne = 0, len = nvalid;
             while (true) {
-                uint32_t bits = s_mask[d][lane];
+                uint32_t bits = s_mask[dd][lane];
                 const int lo = lane * 32;
                 if (lo + 32 <= cur) bits = 0u;
                 else if (lo < cur) bits &= ~((1u << (cur - lo)) - 1u);
-                if (lo >= nvalid) bits = 0u;
-                else if (lo + 32 > nvalid) bits &= (nvalid - lo == 32) ? 0xffffffffu : ((1u << (nvalid - lo)) - 1u);
                 const unsigned any = __ballot_sync(0xffffffffu, bits != 0u);
                 if (!any) break;
                 const int wi = __ffs(any) - 1;
@@ -218,20 +239,38 @@ __global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *sta
                 const int f = wi * 32 + __ffs(wbits) - 1;
                 if (lane == 0) s_ev[ne] = f;
                 ++ne;
-                ++d;
-                if (d == kWK) { len = f; break; }
+                ++dd;
+                if (dd == kWK) { len = f; break; }
                 cur = f;
             }
             if (lane == 0) { s_ne = ne; s_len = len; }
         }
         __syncthreads();
         const int ne = s_ne, len = s_len;
-        if (tid < len) {
+        int ev[kWK];
+#pragma unroll
+        for (int e = 0; e < kWK; ++e) ev[e] = (e < ne) ? s_ev[e] : 0x7fffffff;
+        uint32_t out[kWQ];
+#pragma unroll
+        for (int q = 0; q < kWQ; ++q) {
+            const int step = 4 * tid + q;
             int sh = 0;
-            for (int e = 0; e < ne; ++e) sh += (s_ev[e] <= tid);
-            P.rv[s + tid] = (int32_t)s_val[sh][tid];
+#pragma unroll
+            for (int e = 0; e < kWK; ++e) sh += (ev[e] <= step);
+            uint32_t v = val[q][0];
+#pragma unroll
+            for (int j = 1; j < kWK; ++j) v = (sh == j) ? val[q][j] : v;
+            out[q] = v;
         }
-        if (tid == 0 && u + len + ne > nd) s_err = 1;   // consumed draws past the generated stream
+        const int first = 4 * tid;
+        if (first + kWQ <= len && ((s & 3) == 0)) {
+            *reinterpret_cast<int4 *>(rv + s + first) = make_int4(out[0], out[1], out[2], out[3]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kWQ; ++q)
+                if (first + q < len) rv[s + first + q] = (int32_t)out[q];
+        }
+        if (tid == 0 && u + len + ne > nd) s_err = 1;
         s += len;
         u += len + ne;
         __syncthreads();   // every read of ring blocks below u / kRingBlk is done
@@ -447,7 +486,7 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
                                            (int)(kRing * sizeof(uint32_t))));
         walk_attr = true;
     }
-    k_walk<<<n_plans, kWalkThreads, kRing * sizeof(uint32_t), st>>>(d_plans, status_dev);
+    k_walk<<<n_plans, kWT, kRing * sizeof(uint32_t), st>>>(d_plans, status_dev);
     EDGC_LAUNCH_CHECK();
     // index + resolve plan groups whose hash tables, links and bounded values
     // fit in L2 together, so the random table traffic stays on chip

