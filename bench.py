@@ -242,12 +242,13 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
 
     def one_step(t, ev=None):
-        if tracker is not None and t % period == 0:
-            if ev is not None:
+        if tracker is not None:
+            sampled = t % period == 0
+            if ev is not None and sampled:
                 ev["ent0"].append(torch.cuda.Event(enable_timing=True))
                 ev["ent0"][-1].record(stream)
-            tracker.observe(t, eng.grads)
-            if ev is not None:
+            tracker.observe(t, eng.grads)   # non-sampled iterations only schedule the next plan
+            if ev is not None and sampled:
                 ev["ent1"].append(torch.cuda.Event(enable_timing=True))
                 ev["ent1"][-1].record(stream)
         marks = []
@@ -343,7 +344,7 @@ def run_ours(args):
         s0.record(stream)
         for t in range(t0, t0 + ke):
             eng.grad_arena.copy_(host_g, non_blocking=True)
-            if tracker is not None and t % period == 0:
+            if tracker is not None:
                 tracker.observe(t, eng.grads)
             eng.step()
             host_out.copy_(eng.out_arena, non_blocking=True)

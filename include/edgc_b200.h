@@ -65,6 +65,8 @@ typedef struct {
     int64_t n_elems;   /* N = m * n                       */
     int64_t count;     /* ceil(beta * N); 1 <= count < N  */
     int32_t *idx;      /* device out [count], NumPy order */
+    uint32_t *bitmap;  /* optional device out [ceil(N/32)] membership bits
+                          (caller zeroes; bit e set iff e is sampled) or NULL */
 } edgc_plan_desc;
 
 int64_t edgc_sample_plan_workspace_bytes(const edgc_plan_desc *plans, int n_plans);
@@ -84,9 +86,13 @@ int edgc_gather(int src_dtype, const void *src, const int32_t *idx, int64_t coun
  * EntropyTracker.observe (entropy.py:168-177).
  * ---------------------------------------------------------------------- */
 typedef struct {
-    const void *src;       /* fp32 or fp64 (src_dtype), device            */
-    const int32_t *idx;    /* device [count] or NULL (contiguous src)     */
+    const void *src;        /* fp32 or fp64 (src_dtype), device                       */
+    const int32_t *idx;     /* device [count] or NULL (contiguous src)                */
     int64_t count;
+    const uint32_t *bitmap; /* optional: stream src[0..n_elems) and keep the elements
+                               whose bit is set (the set the plan's idx enumerates);
+                               idx must then be given (its first entry is the shift) */
+    int64_t n_elems;
 } edgc_gauss_desc;
 
 int64_t edgc_entropy_gaussian_workspace_bytes(const edgc_gauss_desc *descs, int n);

@@ -35,11 +35,11 @@ c_i32, c_i64, c_u64, c_f32, c_f64, c_vp = (ctypes.c_int32, ctypes.c_int64, ctype
 
 class PlanDesc(ctypes.Structure):
     _fields_ = [("state_hi", c_u64), ("state_lo", c_u64), ("inc_hi", c_u64), ("inc_lo", c_u64),
-                ("n_elems", c_i64), ("count", c_i64), ("idx", c_vp)]
+                ("n_elems", c_i64), ("count", c_i64), ("idx", c_vp), ("bitmap", c_vp)]
 
 
 class GaussDesc(ctypes.Structure):
-    _fields_ = [("src", c_vp), ("idx", c_vp), ("count", c_i64)]
+    _fields_ = [("src", c_vp), ("idx", c_vp), ("count", c_i64), ("bitmap", c_vp), ("n_elems", c_i64)]
 
 
 class CompressDesc(ctypes.Structure):

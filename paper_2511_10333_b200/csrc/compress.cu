@@ -391,8 +391,19 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
     const uint32_t me = ptx::cluster_ctarank();
     const ZTile t = tiles[blockIdx.x / C];
     const MatDev &M = mats[t.mat];
+    // descriptor fields in registers: the asm memory clobbers below would
+    // otherwise force a global reload of every field each round
     const int r = M.r, rr_res = M.r_res;
-    const int64_t n = M.n;
+    const int64_t n = M.n, ld_g = M.ld_g, ld_q = M.ld_q;
+    const float *__restrict__ gptr = M.g;
+    float *wptr = M.w;
+    const float *__restrict__ pres_ptr = M.p_res;
+    const float *__restrict__ qres_ptr = M.q_res;
+    const float *__restrict__ qwarm_ptr = M.q_warm;
+    double *praw_ptr = M.p_raw;
+    double *zpart_ptr = M.zpart;
+    const double *precond_ptr = M.precond;
+    const int ld_s = M.ld_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t col_base = (int64_t)me * kTCW;
     const int64_t chunk_cols = min((int64_t)kTCW, n - col_base);
@@ -414,7 +425,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
     if (tid < 16) {
         const int i = tid / 4, k = tid % 4;
         double v = (i == k) ? 1.0 : 0.0;
-        if (M.precond && i < r && k < r) v = M.precond[(int64_t)i * M.ld_s + k];
+        if (precond_ptr && i < r && k < r) v = precond_ptr[(int64_t)i * ld_s + k];
         sm.S[tid] = v;
     }
     ptx::cluster_sync();
@@ -429,15 +440,15 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
                 ptx::mbar_arrive_expect_tx(&sm.full[s], 2u * bytes * (uint32_t)rows);
                 for (int rr = 0; rr < rows; ++rr) {
-                    ptx::bulk_g2s(&sm.g[s][rr][0], M.g + (i0 + rr) * M.ld_g + col_base, bytes, &sm.full[s]);
-                    ptx::bulk_g2s(&sm.w[s][rr][0], M.w + (i0 + rr) * n + col_base, bytes, &sm.full[s]);
+                    ptx::bulk_g2s(&sm.g[s][rr][0], gptr + (i0 + rr) * ld_g + col_base, bytes, &sm.full[s]);
+                    ptx::bulk_g2s(&sm.w[s][rr][0], wptr + (i0 + rr) * n + col_base, bytes, &sm.full[s]);
                 }
             }
         }
     } else if (warp == kExchange) {
         for (int b = 0; b < nrounds; ++b) {
             const int q = b % kTRing, slot = b % kTSlots;
-            ptx::mbar_wait(&sm.redfull[q], (b / kTRing) & 1);
+            ptx::named_bar_sync(2 + q, kTCons + 32);   // the 8 consumer warps wrote red[q]
             if (lane < kTV) {
                 double a = 0.0;
 #pragma unroll
@@ -469,14 +480,14 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
         for (int v = 0; v < 4; ++v) {
             double raw[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) raw[k] = (active && k < r) ? (double)M.q_warm[(col0 + v) * M.ld_q + k] : 0.0;
+            for (int k = 0; k < 4; ++k) raw[k] = (active && k < r) ? (double)qwarm_ptr[(col0 + v) * ld_q + k] : 0.0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 double a = 0.0;
 #pragma unroll
                 for (int i = 0; i <= k; ++i) a += raw[i] * sm.S[i * 4 + k];
                 qw[v][k] = a;
-                qr[v][k] = (active && k < rr_res) ? M.q_res[(col0 + v) * rr_res + k] : 0.f;
+                qr[v][k] = (active && k < rr_res) ? qres_ptr[(col0 + v) * rr_res + k] : 0.f;
             }
         }
         float zacc[4][4], x1[kTRB][4], x2[kTRB][4];   // x of rounds b-1 and b-2
@@ -491,7 +502,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             const int64_t i0 = t.row0 + (int64_t)bb * kTRB;
             if (me == 0 && tid < kTV) {
                 const int rr = tid / 4, k = tid % 4;
-                if (i0 + rr < t.row1 && k < r) M.p_raw[(i0 + rr) * r + k] = sm.prow[q][tid];
+                if (i0 + rr < t.row1 && k < r) praw_ptr[(i0 + rr) * r + k] = sm.prow[q][tid];
             }
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr)
@@ -507,6 +518,12 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             const int s = b % kTStages, q = b % kTRing;
             const int64_t i0 = t.row0 + (int64_t)b * kTRB;
             const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
+            float presr[kTRB][4];
+#pragma unroll
+            for (int rr = 0; rr < kTRB; ++rr)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    presr[rr][k] = (k < rr_res && rr < rows) ? __ldg(pres_ptr + (i0 + rr) * rr_res + k) : 0.f;
             if (chunk_cols > 0) ptx::mbar_wait(&sm.full[s], (b / kTStages) & 1);
             double acc[kTV];
             float x[kTRB][4];
@@ -514,8 +531,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             for (int rr = 0; rr < kTRB; ++rr) {
                 float pres[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    pres[k] = (k < rr_res && rr < rows) ? __ldg(M.p_res + (i0 + rr) * rr_res + k) : 0.f;
+                for (int k = 0; k < 4; ++k) pres[k] = presr[rr][k];
                 double pk[4] = {0.0, 0.0, 0.0, 0.0};
                 if (active && rr < rows) {
                     const float4 gv = *reinterpret_cast<const float4 *>(&sm.g[s][rr][4 * tid]);
@@ -533,7 +549,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
 #pragma unroll
                         for (int k = 0; k < 4; ++k) pk[k] = fma(xd, qw[v][k], pk[k]);
                     }
-                    ptx::st_global_v4(M.w + (i0 + rr) * n + col0, x[rr][0], x[rr][1], x[rr][2], x[rr][3]);
+                    ptx::st_global_v4(wptr + (i0 + rr) * n + col0, x[rr][0], x[rr][1], x[rr][2], x[rr][3]);
                 } else {
 #pragma unroll
                     for (int v = 0; v < 4; ++v) x[rr][v] = 0.f;
@@ -542,11 +558,10 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 for (int k = 0; k < 4; ++k) acc[rr * 4 + k] = pk[k];
             }
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&sm.empty[s]);   // stage s read by this warp
+            if (lane == 0) ptx::mbar_arrive_relaxed(&sm.empty[s]);   // stage s read by this warp
             const double part = warp_reduce_scatter<kTV>(acc, lane);
             if ((lane & 1) == 0) sm.red[q][warp][scatter_owner_index<kTV>(lane)] = part;
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cta(&sm.redfull[q]);
+            ptx::named_bar_arrive(2 + q, kTCons + 32);   // hand red[q] to the exchange warp
             if (b >= kTLag) consume(b - kTLag, x2);
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr)
@@ -564,7 +579,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             for (int v = 0; v < 4; ++v)
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if (k < r) M.zpart[((int64_t)t.item * n + col0 + v) * r + k] = (double)zacc[v][k];
+                    if (k < r) zpart_ptr[((int64_t)t.item * n + col0 + v) * r + k] = (double)zacc[v][k];
         }
         if (bad) atomicOr(status + t.mat, 1);
     }

@@ -29,6 +29,8 @@ struct GaussDev {
     const void *src;
     const int32_t *idx;
     int64_t count;
+    const uint32_t *bitmap;
+    int64_t n_elems;
 };
 
 template <typename T>
@@ -43,7 +45,44 @@ __global__ void __launch_bounds__(kRedThreads) k_gauss_partial(const GaussDev *d
     const GaussDev d = descs[blockIdx.y];
     __shared__ double2 s_red[kRedThreads / 32];
     double s1 = 0.0, s2 = 0.0;
-    if (d.count > 0) {
+    if (d.count > 0 && d.bitmap) {
+        // stream the whole matrix, keep the plan's members: coalesced reads
+        // instead of a random gather (a 4-byte gather moves ~64-128 bytes of DRAM)
+        const double K = load_sample<T>(d, 0);
+        const T *src = reinterpret_cast<const T *>(d.src);
+        const int64_t nw = (d.n_elems + 31) / 32;
+        const int lane = threadIdx.x & 31;
+        const int64_t wstride = (int64_t)gridDim.x * (kRedThreads / 32);
+        int64_t wi = (int64_t)blockIdx.x * (kRedThreads / 32) + (threadIdx.x >> 5);
+        // one bitmap word per warp iteration: lane l owns element 32 wi + l (coalesced 128-byte reads)
+        for (; wi + 3 * wstride < nw; wi += 4 * wstride) {
+            uint32_t bw[4];
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t w = wi + q * wstride;
+                bw[q] = __ldg(d.bitmap + w);
+                const int64_t e = w * 32 + lane;
+                v[q] = (e < d.n_elems) ? (double)__ldg(src + e) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if ((bw[q] >> lane) & 1u) {
+                    const double x = v[q] - K;
+                    s1 += x;
+                    s2 += x * x;
+                }
+        }
+        for (; wi < nw; wi += wstride) {
+            const uint32_t bw = __ldg(d.bitmap + wi);
+            const int64_t e = wi * 32 + lane;
+            if (e < d.n_elems && ((bw >> lane) & 1u)) {
+                const double x = (double)__ldg(src + e) - K;
+                s1 += x;
+                s2 += x * x;
+            }
+        }
+    } else if (d.count > 0) {
         const double K = load_sample<T>(d, 0);
         const int64_t stride = (int64_t)gridDim.x * kRedThreads;
         int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
@@ -459,7 +498,10 @@ extern "C" int edgc_entropy_gaussian(int src_dtype, const edgc_gauss_desc *descs
     GaussDev *d = a.take<GaussDev>(n);
     double2 *part = a.take<double2>((int64_t)n * kGaussBlocksPerDesc);
     std::vector<GaussDev> h(n);
-    for (int i = 0; i < n; ++i) h[i] = GaussDev{descs[i].src, descs[i].idx, descs[i].count};
+    for (int i = 0; i < n; ++i) {
+        EDGC_REQUIRE(!descs[i].bitmap || descs[i].idx, "gauss desc %d: a bitmap needs idx (for the shift)", i);
+        h[i] = GaussDev{descs[i].src, descs[i].idx, descs[i].count, descs[i].bitmap, descs[i].n_elems};
+    }
     cudaStream_t st = (cudaStream_t)stream;
     EDGC_CUDA_TRY(cudaMemcpyAsync(d, h.data(), sizeof(GaussDev) * n, cudaMemcpyHostToDevice, st));
     dim3 grid(kGaussBlocksPerDesc, n);

@@ -111,3 +111,15 @@ __device__ __forceinline__ void mbar_arrive_cta(uint64_t *bar) {
 }
 }  // namespace ptx
 }  // namespace edgc
+
+namespace edgc {
+namespace ptx {
+// arrive without release semantics (the caller only signals that its reads are done)
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int threads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+}  // namespace ptx
+}  // namespace edgc

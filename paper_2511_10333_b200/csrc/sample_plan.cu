@@ -67,6 +67,7 @@ struct PlanDev {
     u128 state, inc;
     int64_t n_elems, count;
     int32_t *idx;
+    uint32_t *bitmap;  // optional membership bits
     uint32_t *draws;   // [n_draws]
     int64_t n_draws;   // even
     int32_t *rv;       // [count] bounded values
@@ -350,6 +351,7 @@ __global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, 
             }
         }
         P.idx[count - 1 - s] = (int32_t)val;
+        if (P.bitmap) atomicOr(P.bitmap + (val >> 5), 1u << (val & 31));
     } else {
         const int64_t base = N - count;
         int32_t cur = s;
@@ -364,7 +366,9 @@ __global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, 
             if (prev >= cur) break;
             cur = prev;
         }
-        P.idx[s] = collide ? (int32_t)(base + s) : P.rv[s];
+        const int32_t outv = collide ? (int32_t)(base + s) : P.rv[s];
+        P.idx[s] = outv;
+        if (P.bitmap) atomicOr(P.bitmap + (outv >> 5), 1u << (outv & 31));
     }
 }
 
@@ -397,6 +401,7 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
         P.n_elems = d.n_elems;
         P.count = d.count;
         P.idx = d.idx;
+        P.bitmap = d.bitmap;
         P.tail = (d.n_elems > 10000 && d.count > d.n_elems / 20) ? 1 : 0;
         // expected rejections ~ count * N / 2^33 (threshold ~ uniform below rng+1)
         const double lam = (double)d.count * (double)d.n_elems / 4294967296.0;

@@ -86,48 +86,60 @@ def sample_count(n_elems: int, beta: float) -> int:
     return min(n_elems, math.ceil(beta * n_elems))
 
 
-def sample_plans(specs, device=None):
+def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, workspace=None, check: bool = True):
     """Device index plans for many (n_elems, count, seed) at once.
 
     Returns a list of int32 CUDA tensors (None where count == n_elems, i.e. the
-    reference's full copy).  Order of each plan = NumPy's output order.
+    reference's full copy).  Order of each plan = NumPy's output order.  With
+    ``bitmaps=True`` returns (plans, bitmaps, status): per-plan int32 words with
+    bit e set iff element e is sampled.  ``stream`` / ``workspace`` let the
+    tracker build the next sampled iteration's plans on a side stream;
+    ``check=False`` skips the synchronising status check (the caller checks
+    ``status`` later).
     """
     L = _lib.lib()
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    st = torch.cuda.current_stream(dev) if stream is None else stream
+    ws_pool = _lib.WORKSPACE if workspace is None else workspace
     out = [None] * len(specs)
+    bms = [None] * len(specs)
     todo = []
-    for i, (n_elems, count, seed) in enumerate(specs):
-        if count == n_elems:
-            continue
-        if n_elems >= 2**31:
-            raise ValueError(f"sampling over {n_elems} >= 2^31 elements is outside the device plan's range")
-        out[i] = torch.empty(count, dtype=torch.int32, device=dev)
-        todo.append(i)
-    cap_bytes = _plan_ws_cap(dev)
-    descs = {}
-    sizes = {}
-    for i in todo:
-        n_elems, count, seed = specs[i]
-        descs[i] = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]))
-        sizes[i] = L.edgc_sample_plan_workspace_bytes((_lib.PlanDesc * 1)(descs[i]), 1) + 4096
-    k = 0
-    while k < len(todo):
-        # greedy batches under the workspace cap (per-plan sizes add up, plus slack)
-        batch, acc = [], 0
-        while k < len(todo) and (not batch or acc + sizes[todo[k]] <= cap_bytes):
-            batch.append(descs[todo[k]])
-            acc += sizes[todo[k]]
-            k += 1
-        arr = (_lib.PlanDesc * len(batch))(*batch)
-        need = L.edgc_sample_plan_workspace_bytes(arr, len(batch))
-        if need < 0:
-            _lib.check(_lib.EDGC_EINVAL, "sample plan layout")
-        ws = _lib.WORKSPACE.get(need, dev)
-        status = torch.zeros(len(batch), dtype=torch.int32, device=dev)
-        _lib.check(L.edgc_sample_plan(arr, len(batch), _lib.ptr(status), _lib.ptr(ws), ws.numel(),
-                                      _lib.stream_ptr(dev)), "edgc_sample_plan")
-        if int(status.max().item()) != 0:
-            raise RuntimeError("sample plan exhausted its pre-generated draws")
+    with torch.cuda.stream(st):
+        for i, (n_elems, count, seed) in enumerate(specs):
+            if count == n_elems:
+                continue
+            if n_elems >= 2**31:
+                raise ValueError(f"sampling over {n_elems} >= 2^31 elements is outside the device plan's range")
+            out[i] = torch.empty(count, dtype=torch.int32, device=dev)
+            if bitmaps:
+                bms[i] = torch.zeros((n_elems + 31) // 32, dtype=torch.int32, device=dev)
+            todo.append(i)
+        cap_bytes = _plan_ws_cap(dev)
+        descs, sizes = {}, {}
+        for i in todo:
+            n_elems, count, seed = specs[i]
+            descs[i] = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]), _lib.ptr(bms[i]))
+            sizes[i] = L.edgc_sample_plan_workspace_bytes((_lib.PlanDesc * 1)(descs[i]), 1) + 4096
+        status_all = torch.zeros(max(1, len(todo)), dtype=torch.int32, device=dev)
+        k = 0
+        while k < len(todo):
+            batch, acc = [], 0
+            while k < len(todo) and (not batch or acc + sizes[todo[k]] <= cap_bytes):
+                batch.append(descs[todo[k]])
+                acc += sizes[todo[k]]
+                k += 1
+            arr = (_lib.PlanDesc * len(batch))(*batch)
+            need = L.edgc_sample_plan_workspace_bytes(arr, len(batch))
+            if need < 0:
+                _lib.check(_lib.EDGC_EINVAL, "sample plan layout")
+            ws = ws_pool.get(need, dev)
+            status = status_all[k - len(batch):k]
+            _lib.check(L.edgc_sample_plan(arr, len(batch), _lib.ptr(status), _lib.ptr(ws), ws.numel(),
+                                          st.cuda_stream), "edgc_sample_plan")
+    if check and todo and int(status_all.max().item()) != 0:
+        raise RuntimeError("sample plan exhausted its pre-generated draws")
+    if bitmaps:
+        return out, bms, status_all
     return out
 
 
@@ -175,10 +187,15 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 
 def _gaussian_batch(items, dtype_code: int, device) -> list:
-    """items: list of (src tensor, idx tensor or None, count) -> list of device entropies (float)."""
+    """items: (src, idx or None, count[, bitmap]) -> per-item entropies (floats; synchronises)."""
     L = _lib.lib()
     n = len(items)
-    descs = (_lib.GaussDesc * n)(*[_lib.GaussDesc(_lib.ptr(s), _lib.ptr(i), c) for s, i, c in items])
+    rows = []
+    for it in items:
+        src, idx, cnt = it[:3]
+        bm = it[3] if len(it) > 3 else None
+        rows.append(_lib.GaussDesc(_lib.ptr(src), _lib.ptr(idx), cnt, _lib.ptr(bm), src.numel() if bm is not None else 0))
+    descs = (_lib.GaussDesc * n)(*rows)
     need = L.edgc_entropy_gaussian_workspace_bytes(descs, n)
     ws = _lib.WORKSPACE.get(need, device)
     h = torch.empty(n, dtype=torch.float64, device=device)
@@ -275,23 +292,38 @@ def relative_change_rate(series_sampled, series_full) -> np.ndarray:
     return np.abs(a - b) / np.abs(b)
 
 
-def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=None) -> list:
-    """Per-layer entropies of one sampled iteration, all layers batched on the device."""
+def _layer_specs(flats, iteration: int, config: SamplerConfig):
+    return [(f.numel(), sample_count(f.numel(), config.beta), subsample_seed(config.rng_seed, iteration, k))
+            for k, f in enumerate(flats)]
+
+
+def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=None, prefetched=None) -> list:
+    """Per-layer entropies of one sampled iteration, all layers batched on the device.
+
+    Gaussian plug-in (the default): each matrix is streamed once against the
+    plan's membership bitmap (coalesced) instead of gathered at random.
+    ``prefetched`` = (specs, plans, bitmaps, status) built earlier on a side stream.
+    """
     estimator = entropy_gaussian_plugin if estimator is None else estimator
     flats = [as_device_matrix(m).reshape(-1) for m in matrices]
     if not flats:
         return []
-    specs = []
-    for k, f in enumerate(flats):
-        n = f.numel()
-        specs.append((n, sample_count(n, config.beta), subsample_seed(config.rng_seed, iteration, k)))
-    plans = sample_plans(specs, flats[0].device)
+    specs = _layer_specs(flats, iteration, config)
+    dev = flats[0].device
     if estimator is entropy_gaussian_plugin:
-        for f, (n, c, _) in zip(flats, specs):
+        for (n, c, _) in specs:
             if c < 2:
                 raise ValueError(f"need at least 2 samples, got {c}")
-        items = [(f, p, c) for f, p, (_, c, _) in zip(flats, plans, specs)]
-        return _gaussian_batch(items, 0, flats[0].device)
+        if prefetched is not None and prefetched[0] == specs:
+            _, plans, bms, status = prefetched
+        else:
+            plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False)
+        items = [(f, p, c) if p is None else (f, p, c, bm) for f, p, bm, (_, c, _) in zip(flats, plans, bms, specs)]
+        out = _gaussian_batch(items, 0, dev)
+        if int(status.max().item()) != 0:
+            raise RuntimeError("sample plan exhausted its pre-generated draws")
+        return out
+    plans = sample_plans(specs, dev)
     out = []
     L = _lib.lib()
     for f, p, (n, c, _) in zip(flats, plans, specs):
@@ -312,12 +344,16 @@ def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=N
 class EntropyTracker:
     """Per-iteration layer matrices -> fixed-size entropy windows (entropy.py:135-192).
 
-    Sampled iterations run one batched device pipeline over all layers (plans,
-    fused gather + estimator) and one device-to-host copy of the per-layer
-    entropies; the layer mean and window logic are the reference's, on the host.
+    Sampled iterations run one batched device pipeline over all layers and one
+    device-to-host copy of the per-layer entropies; the layer mean and window
+    logic are the reference's, on the host.  Because sampled indices do not
+    depend on the gradients, the plans (and membership bitmaps) of the next
+    sampled iteration are built on a side stream while the intervening
+    iterations run (``prefetch=True``); results are unchanged.
     """
 
-    def __init__(self, config: SamplerConfig, window: int, estimator=entropy_gaussian_plugin):
+    def __init__(self, config: SamplerConfig, window: int, estimator=entropy_gaussian_plugin,
+                 prefetch: bool = True):
         if window < 1:
             raise ValueError(f"window must be positive, got {window}")
         period = sampling_period(config.alpha)
@@ -330,6 +366,38 @@ class EntropyTracker:
         self.windows: list[EntropyWindow] = []
         self._pending: list[float] = []
         self._current = 0
+        self.prefetch = prefetch and estimator is entropy_gaussian_plugin
+        self._pf = {}              # iteration -> (specs, plans, bitmaps, status, event)
+        self._pf_stream = None
+        self._pf_ws = _lib.Workspace()
+
+    def _launch_prefetch(self, iteration: int, matrices) -> None:
+        flats = [as_device_matrix(m).reshape(-1) for m in matrices]
+        if not flats:
+            return
+        dev = flats[0].device
+        if self._pf_stream is None:
+            self._pf_stream = torch.cuda.Stream(dev)
+        specs = _layer_specs(flats, iteration, self.config)
+        if any(c < 2 for _, c, _ in specs):
+            return
+        plans, bms, status = sample_plans(specs, dev, bitmaps=True, stream=self._pf_stream,
+                                          workspace=self._pf_ws, check=False)
+        ev = torch.cuda.Event()
+        ev.record(self._pf_stream)
+        self._pf[iteration] = (specs, plans, bms, status, ev)
+
+    def _take_prefetch(self, iteration: int):
+        rec = self._pf.pop(iteration, None)
+        if rec is None:
+            return None
+        specs, plans, bms, status, ev = rec
+        cur = torch.cuda.current_stream(status.device)
+        cur.wait_event(ev)
+        for t in list(plans) + list(bms) + [status]:
+            if t is not None:
+                t.record_stream(cur)
+        return specs, plans, bms, status
 
     def observe(self, iteration: int, matrices) -> EntropyWindow | None:
         closed = None
@@ -339,10 +407,17 @@ class EntropyTracker:
         if win > self._current:
             closed = self._close()
             self._current = win
+        mats = list(matrices)
         if should_sample_iteration(iteration, self.config.alpha):
-            per_layer = layer_entropies(list(matrices), iteration, self.config, self.estimator)
+            pre = self._take_prefetch(iteration)
+            per_layer = layer_entropies(mats, iteration, self.config, self.estimator, prefetched=pre)
             if per_layer:
                 self._pending.append(float(np.mean(per_layer)))
+        if self.prefetch and mats:
+            period = sampling_period(self.config.alpha)
+            nxt = (iteration // period + 1) * period
+            if nxt not in self._pf:
+                self._launch_prefetch(nxt, mats)
         return closed
 
     def flush(self) -> EntropyWindow | None:
