@@ -363,10 +363,10 @@ __global__ void __launch_bounds__(kZThreads, 2) k_pass1z(const MatDev *mats, con
 constexpr int kTCons = 256;
 constexpr int kTThreads = kTCons + 64;   // + producer warp + exchange warp
 constexpr int kTRB = 4;
-constexpr int kTStages = 3;
+constexpr int kTStages = 6;              // 6 x 32 KB: lag + 1 held by consumers, the rest prefetched
 constexpr int kTCW = 4 * kTCons;
-constexpr int kTLag = 2;                 // consumer Z update lags the exchange by 2 rounds
-constexpr int kTRing = kTLag + 1;        // red / prow ring depth
+constexpr int kTLag = 3;                 // consumer Z update lags the exchange by 3 rounds
+constexpr int kTRing = kTLag + 1;        // red / prow / named-barrier ring depth
 constexpr int kTSlots = 3;               // DSMEM receive slots
 constexpr int kTV = kTRB * 4;            // row-dot values per round (RMAX = 4)
 
@@ -490,14 +490,16 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 qr[v][k] = (active && k < rr_res) ? qres_ptr[(col0 + v) * rr_res + k] : 0.f;
             }
         }
-        float zacc[4][4], x1[kTRB][4], x2[kTRB][4];   // x of rounds b-1 and b-2
+        float zacc[4][4];
 #pragma unroll
         for (int v = 0; v < 4; ++v)
 #pragma unroll
             for (int k = 0; k < 4; ++k) zacc[v][k] = 0.f;
         bool bad = false;
-        auto consume = [&](int bb, const float (&xp)[kTRB][4]) {
-            const int q = bb % kTRing;
+        // round bb's x values live in its stage slot (written over w); the slot is
+        // released to the producer only after this lagged Z update
+        auto consume = [&](int bb) {
+            const int q = bb % kTRing, s = bb % kTStages;
             ptx::mbar_wait(&sm.prowready[q], (bb / kTRing) & 1);
             const int64_t i0 = t.row0 + (int64_t)bb * kTRB;
             if (me == 0 && tid < kTV) {
@@ -505,13 +507,20 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 if (i0 + rr < t.row1 && k < r) praw_ptr[(i0 + rr) * r + k] = sm.prow[q][tid];
             }
 #pragma unroll
-            for (int rr = 0; rr < kTRB; ++rr)
+            for (int rr = 0; rr < kTRB; ++rr) {
+                const float4 xv = *reinterpret_cast<const float4 *>(&sm.w[s][rr][4 * tid]);
+                const float xx[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const float pv = (float)sm.prow[q][rr * 4 + k];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) zacc[v][k] = fmaf(xp[rr][v], pv, zacc[v][k]);
+                    for (int v = 0; v < 4; ++v) zacc[v][k] = fmaf(xx[v], pv, zacc[v][k]);
                 }
+            }
+            // order this thread's generic smem writes (x) before the next bulk copy into slot s
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_relaxed(&sm.empty[s]);   // slot s free for the producer
         };
 #pragma unroll 1
         for (int b = 0; b < nrounds; ++b) {
@@ -526,13 +535,10 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                     presr[rr][k] = (k < rr_res && rr < rows) ? __ldg(pres_ptr + (i0 + rr) * rr_res + k) : 0.f;
             if (chunk_cols > 0) ptx::mbar_wait(&sm.full[s], (b / kTStages) & 1);
             double acc[kTV];
-            float x[kTRB][4];
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) {
-                float pres[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) pres[k] = presr[rr][k];
                 double pk[4] = {0.0, 0.0, 0.0, 0.0};
+                float xx[4] = {0.f, 0.f, 0.f, 0.f};
                 if (active && rr < rows) {
                     const float4 gv = *reinterpret_cast<const float4 *>(&sm.g[s][rr][4 * tid]);
                     const float4 wv = *reinterpret_cast<const float4 *>(&sm.w[s][rr][4 * tid]);
@@ -541,39 +547,26 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                     for (int v = 0; v < 4; ++v) {
                         float dot = 0.f;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) dot = fmaf(pres[k], qr[v][k], dot);
+                        for (int k = 0; k < 4; ++k) dot = fmaf(presr[rr][k], qr[v][k], dot);
                         const float xv = gg[v] + (ww[v] - dot);
                         bad |= !isfinite(xv);
-                        x[rr][v] = xv;
+                        xx[v] = xv;
                         const double xd = (double)xv;
 #pragma unroll
                         for (int k = 0; k < 4; ++k) pk[k] = fma(xd, qw[v][k], pk[k]);
                     }
-                    ptx::st_global_v4(wptr + (i0 + rr) * n + col0, x[rr][0], x[rr][1], x[rr][2], x[rr][3]);
-                } else {
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) x[rr][v] = 0.f;
+                    ptx::st_global_v4(wptr + (i0 + rr) * n + col0, xx[0], xx[1], xx[2], xx[3]);
                 }
+                *reinterpret_cast<float4 *>(&sm.w[s][rr][4 * tid]) = make_float4(xx[0], xx[1], xx[2], xx[3]);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[rr * 4 + k] = pk[k];
             }
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_relaxed(&sm.empty[s]);   // stage s read by this warp
             const double part = warp_reduce_scatter<kTV>(acc, lane);
             if ((lane & 1) == 0) sm.red[q][warp][scatter_owner_index<kTV>(lane)] = part;
             ptx::named_bar_arrive(2 + q, kTCons + 32);   // hand red[q] to the exchange warp
-            if (b >= kTLag) consume(b - kTLag, x2);
-#pragma unroll
-            for (int rr = 0; rr < kTRB; ++rr)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    x2[rr][v] = x1[rr][v];
-                    x1[rr][v] = x[rr][v];
-                }
+            if (b >= kTLag) consume(b - kTLag);
         }
-        // drain: rounds nrounds-2 (in x2) and nrounds-1 (in x1)
-        if (nrounds >= 2) consume(nrounds - 2, x2);
-        if (nrounds >= 1) consume(nrounds - 1, x1);
+        for (int bb = max(0, nrounds - kTLag); bb < nrounds; ++bb) consume(bb);
         if (active) {
 #pragma unroll
             for (int v = 0; v < 4; ++v)

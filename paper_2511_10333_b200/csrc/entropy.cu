@@ -22,7 +22,7 @@ constexpr int kRedThreads = 256;
 // one or two matrices at a time, so their sectors stay in L2 and each matrix is
 // read from DRAM about once (a scattered gather over all layers at once thrashes
 // L2 and moves ~30x the algorithmic bytes).
-constexpr int kGaussBlocksPerDesc = 1184;
+constexpr int kGaussBlocksPerDesc = 1184;   // 8 x 148 SMs, persistent over layers
 
 // ---------------------------------------------------------------- Gaussian
 struct GaussDev {
@@ -41,9 +41,12 @@ __device__ __forceinline__ double load_sample(const GaussDev &d, int64_t i) {
 
 // partial[desc][block] = {sum(x-K), sum((x-K)^2)} with the shift K = first sample
 template <typename T>
-__global__ void __launch_bounds__(kRedThreads) k_gauss_partial(const GaussDev *descs, double2 *partial) {
-    const GaussDev d = descs[blockIdx.y];
+__global__ void __launch_bounds__(kRedThreads) k_gauss_partial(const GaussDev *descs, int ndesc, double2 *partial) {
     __shared__ double2 s_red[kRedThreads / 32];
+    // one persistent grid walks the layers in order (layer-major: the whole GPU
+    // works on one matrix at a time, which keeps a gather's sectors in L2)
+    for (int di = 0; di < ndesc; ++di) {
+    const GaussDev d = descs[di];
     double s1 = 0.0, s2 = 0.0;
     if (d.count > 0 && d.bitmap) {
         // stream the whole matrix, keep the plan's members: coalesced reads
@@ -107,7 +110,9 @@ __global__ void __launch_bounds__(kRedThreads) k_gauss_partial(const GaussDev *d
     if (threadIdx.x == 0) {
         double a = 0.0, b = 0.0;
         for (int w = 0; w < kRedThreads / 32; ++w) { a += s_red[w].x; b += s_red[w].y; }
-        partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = make_double2(a, b);
+        partial[(int64_t)di * gridDim.x + blockIdx.x] = make_double2(a, b);
+    }
+    __syncthreads();
     }
 }
 
@@ -504,11 +509,10 @@ extern "C" int edgc_entropy_gaussian(int src_dtype, const edgc_gauss_desc *descs
     }
     cudaStream_t st = (cudaStream_t)stream;
     EDGC_CUDA_TRY(cudaMemcpyAsync(d, h.data(), sizeof(GaussDev) * n, cudaMemcpyHostToDevice, st));
-    dim3 grid(kGaussBlocksPerDesc, n);
     if (src_dtype == 0)
-        k_gauss_partial<float><<<grid, kRedThreads, 0, st>>>(d, part);
+        k_gauss_partial<float><<<kGaussBlocksPerDesc, kRedThreads, 0, st>>>(d, n, part);
     else
-        k_gauss_partial<double><<<grid, kRedThreads, 0, st>>>(d, part);
+        k_gauss_partial<double><<<kGaussBlocksPerDesc, kRedThreads, 0, st>>>(d, n, part);
     EDGC_LAUNCH_CHECK();
     k_gauss_finish<<<(n + 127) / 128, 128, 0, st>>>(d, n, part, kGaussBlocksPerDesc, h_out, status_dev);
     EDGC_LAUNCH_CHECK();

@@ -186,8 +186,11 @@ def _dtype_code(t: torch.Tensor) -> int:
     return 0 if t.dtype == torch.float32 else 1
 
 
-def _gaussian_batch(items, dtype_code: int, device) -> list:
-    """items: (src, idx or None, count[, bitmap]) -> per-item entropies (floats; synchronises)."""
+def _gaussian_launch(items, dtype_code: int, device):
+    """Queue the batched Gaussian estimator; returns device (h, status) without synchronising.
+
+    items: (src, idx or None, count[, bitmap]).
+    """
     L = _lib.lib()
     n = len(items)
     rows = []
@@ -202,8 +205,14 @@ def _gaussian_batch(items, dtype_code: int, device) -> list:
     status = torch.empty(n, dtype=torch.int32, device=device)
     _lib.check(L.edgc_entropy_gaussian(dtype_code, descs, n, _lib.ptr(h), _lib.ptr(status), _lib.ptr(ws),
                                        ws.numel(), _lib.stream_ptr(device)), "edgc_entropy_gaussian")
+    return h, status
+
+
+def _gaussian_collect(h, status, plan_status=None) -> list:
     h_host = h.cpu().tolist()
     st_host = status.cpu().tolist()
+    if plan_status is not None and int(plan_status.max().item()) != 0:
+        raise RuntimeError("sample plan exhausted its pre-generated draws")
     for code in st_host:
         if code == _lib.EDGC_EINVAL:
             raise ValueError("need at least 2 samples")
@@ -211,6 +220,22 @@ def _gaussian_batch(items, dtype_code: int, device) -> list:
             raise DegenerateInputError("zero-variance sample has no differential entropy")
         _lib.raise_device_status(code, "entropy_gaussian_plugin")
     return h_host
+
+
+def _gaussian_batch(items, dtype_code: int, device) -> list:
+    """items: (src, idx or None, count[, bitmap]) -> per-item entropies (floats; synchronises)."""
+    return _gaussian_collect(*_gaussian_launch(items, dtype_code, device))
+
+
+class _DeferredMean:
+    """A sampled iteration's layer mean whose device entropies are read only when needed."""
+
+    def __init__(self, h, status, plan_status):
+        self.h, self.status, self.plan_status = h, status, plan_status
+
+    def value(self) -> float:
+        # np.mean over the per-layer Python floats, as entropy.py:177 does
+        return float(np.mean(_gaussian_collect(self.h, self.status, self.plan_status)))
 
 
 def entropy_gaussian_plugin(samples) -> float:
@@ -297,7 +322,8 @@ def _layer_specs(flats, iteration: int, config: SamplerConfig):
             for k, f in enumerate(flats)]
 
 
-def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=None, prefetched=None) -> list:
+def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=None, prefetched=None,
+                    deferred: bool = False):
     """Per-layer entropies of one sampled iteration, all layers batched on the device.
 
     Gaussian plug-in (the default): each matrix is streamed once against the
@@ -319,10 +345,10 @@ def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=N
         else:
             plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False)
         items = [(f, p, c) if p is None else (f, p, c, bm) for f, p, bm, (_, c, _) in zip(flats, plans, bms, specs)]
-        out = _gaussian_batch(items, 0, dev)
-        if int(status.max().item()) != 0:
-            raise RuntimeError("sample plan exhausted its pre-generated draws")
-        return out
+        h, hstat = _gaussian_launch(items, 0, dev)
+        if deferred:
+            return _DeferredMean(h, hstat, status)
+        return _gaussian_collect(h, hstat, status)
     plans = sample_plans(specs, dev)
     out = []
     L = _lib.lib()
@@ -410,9 +436,14 @@ class EntropyTracker:
         mats = list(matrices)
         if should_sample_iteration(iteration, self.config.alpha):
             pre = self._take_prefetch(iteration)
-            per_layer = layer_entropies(mats, iteration, self.config, self.estimator, prefetched=pre)
-            if per_layer:
-                self._pending.append(float(np.mean(per_layer)))
+            if self.estimator is entropy_gaussian_plugin and mats:
+                # read back lazily: the host needs the value only when the window closes
+                self._pending.append(layer_entropies(mats, iteration, self.config, self.estimator,
+                                                     prefetched=pre, deferred=True))
+            else:
+                per_layer = layer_entropies(mats, iteration, self.config, self.estimator, prefetched=pre)
+                if per_layer:
+                    self._pending.append(float(np.mean(per_layer)))
         if self.prefetch and mats:
             period = sampling_period(self.config.alpha)
             nxt = (iteration // period + 1) * period
@@ -428,6 +459,7 @@ class EntropyTracker:
         return out
 
     def _close(self) -> EntropyWindow:
+        self._pending = [v.value() if isinstance(v, _DeferredMean) else v for v in self._pending]
         rec = close_window(self._pending, window_index=self._current, window_size=self.window)
         self.windows.append(rec)
         self._pending = []
