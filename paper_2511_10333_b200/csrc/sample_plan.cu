@@ -72,10 +72,7 @@ struct PlanDev {
     int64_t n_draws;   // even
     int32_t *rv;       // [count] bounded values
     int32_t *next;     // [count]
-    int32_t *keys;     // [cap]
-    int32_t *heads;    // [cap]
-    int64_t cap;       // power of two
-    int32_t log2cap;
+    int32_t *head;     // [n_elems] latest step targeting each position (-1: none)
     int32_t tail;      // 1 = tail shuffle, 0 = Floyd
     int64_t draw_chunk0;  // first P1 chunk index of this plan
     int64_t step_block0;  // first P3/P4 block index of this plan
@@ -281,43 +278,21 @@ __global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *sta
     if (tid == 0) status[blockIdx.x] = (s_err || s < count) ? EDGC_EDRAWS : EDGC_OK;
 }
 
-__device__ __forceinline__ uint32_t hash_slot(uint32_t key, uint32_t cap) {
-    // murmur3 finaliser, then multiply-shift range reduction onto [0, cap)
-    key ^= key >> 16; key *= 0x85ebca6bu; key ^= key >> 13; key *= 0xc2b2ae35u; key ^= key >> 16;
-    return (uint32_t)(((uint64_t)key * cap) >> 32);
-}
-
 __device__ __forceinline__ int find_plan_steps(const PlanDev *plans, int n, int64_t blk) {
     return find_plan(plans, n, blk, false);
 }
 
-// ---- P3: hash (key = bounded value) -> list of steps ----------------------
+// ---- P3: per-position lists of the steps whose bounded value is that position
+// (direct-mapped heads: one atomic exchange per step, no probing)
 __global__ void __launch_bounds__(kStepThreads) k_index(const PlanDev *plans, int p0, int p1, int64_t blk0) {
     const int p = p0 + find_plan_steps(plans + p0, p1 - p0, blk0 + blockIdx.x);
     const PlanDev &P = plans[p];
     const int64_t s = (int64_t)(blk0 + blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
     if (s >= P.count) return;
-    const int32_t key = P.rv[s];
-    const uint32_t cap = (uint32_t)P.cap;
-    uint32_t slot = hash_slot((uint32_t)key, cap);
-    while (true) {
-        const int32_t k = atomicCAS(P.keys + slot, -1, key);
-        if (k == -1 || k == key) break;
-        if (++slot == cap) slot = 0;
-    }
-    P.next[s] = atomicExch(P.heads + slot, (int32_t)s);
+    P.next[s] = atomicExch(P.head + P.rv[s], (int32_t)s);
 }
 
-__device__ __forceinline__ int32_t lookup_head(const PlanDev &P, int32_t key) {
-    const uint32_t cap = (uint32_t)P.cap;
-    uint32_t slot = hash_slot((uint32_t)key, cap);
-    while (true) {
-        const int32_t k = P.keys[slot];
-        if (k == key) return P.heads[slot];
-        if (k == -1) return -1;
-        if (++slot == cap) slot = 0;
-    }
-}
+__device__ __forceinline__ int32_t lookup_head(const PlanDev &P, int32_t key) { return P.head[key]; }
 
 // largest step < before in the list of `key` (or -1)
 __device__ __forceinline__ int32_t latest_before(const PlanDev &P, int32_t key, int32_t before) {
@@ -387,8 +362,7 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
     PlanDev *descs_dev = a.take<PlanDev>(n);
     (void)descs_dev;
     int64_t chunk = 0, blocks = 0;
-    // tables are contiguous so one memset clears them
-    std::vector<int64_t> caps(n);
+
     for (int i = 0; i < n; ++i) {
         const edgc_plan_desc &d = plans[i];
         EDGC_REQUIRE(d.n_elems >= 2 && d.n_elems < (int64_t(1) << 31), "plan %d: N=%lld outside [2, 2^31)", i,
@@ -413,10 +387,7 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
         chunk += ceil_div(nd / 2, kDrawsPerBlock);
         P.step_block0 = blocks;
         blocks += ceil_div(d.count, kStepThreads);
-        const int64_t cap = ((d.count * 4 / 3 + 256) + 255) & ~int64_t(255);   // load <= 0.75
-        P.cap = cap;
-        P.log2cap = 0;
-        caps[i] = cap;
+
     }
     // round the P1 chunk index up so blocks never straddle more than needed
     L.draw_chunks = chunk;
@@ -433,10 +404,8 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
     for (int i = 0; i < n; ++i) {
         PlanDev &P = L.dev[i];
         L.table_off[i] = a.off - t0;
-        P.keys = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
-        a.off += caps[i] * 4;
-        P.heads = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
-        a.off += caps[i] * 4;
+        P.head = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
+        a.off += align256(P.n_elems * 4);
     }
     L.table_off[n] = a.off - t0;
     L.table_bytes = a.off - t0;
