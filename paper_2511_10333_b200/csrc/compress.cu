@@ -453,14 +453,20 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 double a = 0.0;
 #pragma unroll
                 for (int w = 0; w < kTCons / 32; ++w) a += sm.red[q][w][lane];
-                const uint32_t dst = ptx::smem_addr(&sm.recv[slot][me][lane]);
-                for (uint32_t cc = 0; cc < C; ++cc) ptx::st_cluster_f64(ptx::mapa(dst, cc), a);
+                sm.recv[slot][me][lane] = a;            // my own contribution, in place
             }
             __syncwarp();
-            if (lane == 0) {
-                const uint32_t bar = ptx::smem_addr(&sm.xfull[slot]);
-                for (uint32_t cc = 0; cc < C; ++cc) ptx::mbar_arrive_remote(ptx::mapa(bar, cc));
+            if ((uint32_t)lane < C && (uint32_t)lane != me) {
+                // lane cc pushes the whole row-dot vector to peer cc, then release-arrives
+                // there: the C pushes and releases proceed in parallel
+                const uint32_t cc = (uint32_t)lane;
+                const uint32_t dst = ptx::mapa(ptx::smem_addr(&sm.recv[slot][me][0]), cc);
+#pragma unroll
+                for (int e = 0; e < kTV; e += 2)
+                    ptx::st_cluster_v2_f64(dst + 8u * e, sm.recv[slot][me][e], sm.recv[slot][me][e + 1]);
+                ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_addr(&sm.xfull[slot]), cc));
             }
+            if ((uint32_t)lane == me) ptx::mbar_arrive_cta(&sm.xfull[slot]);
             ptx::mbar_wait_cluster(&sm.xfull[slot], (b / kTSlots) & 1);
             if (lane < kTV) {
                 double a = 0.0;

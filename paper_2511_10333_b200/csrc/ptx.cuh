@@ -123,3 +123,11 @@ __device__ __forceinline__ void named_bar_arrive(int id, int threads) {
 }
 }  // namespace ptx
 }  // namespace edgc
+
+namespace edgc {
+namespace ptx {
+__device__ __forceinline__ void st_cluster_v2_f64(uint32_t addr, double a, double b) {
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
+}  // namespace ptx
+}  // namespace edgc
