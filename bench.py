@@ -242,15 +242,6 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
 
     def one_step(t, ev=None):
-        if tracker is not None:
-            sampled = t % period == 0
-            if ev is not None and sampled:
-                ev["ent0"].append(torch.cuda.Event(enable_timing=True))
-                ev["ent0"][-1].record(stream)
-            tracker.observe(t, eng.grads)   # non-sampled iterations only schedule the next plan
-            if ev is not None and sampled:
-                ev["ent1"].append(torch.cuda.Event(enable_timing=True))
-                ev["ent1"][-1].record(stream)
         marks = []
         if ev is not None:
             marks = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
@@ -272,6 +263,17 @@ def run_ours(args):
             marks[5].record(stream)
             ev["marks"].append(marks)
         eng.advance()
+        if tracker is not None:
+            # train_toy order (grad_source.py:416): the tracker sees worker 0's raw gradients
+            # after the step's compression; g is read-only in compress, so it is unchanged
+            sampled = t % period == 0
+            if ev is not None and sampled:
+                ev["ent0"].append(torch.cuda.Event(enable_timing=True))
+                ev["ent0"][-1].record(stream)
+            tracker.observe(t, eng.grads)   # non-sampled iterations only schedule the next plan
+            if ev is not None and sampled:
+                ev["ent1"].append(torch.cuda.Event(enable_timing=True))
+                ev["ent1"][-1].record(stream)
 
     for t in range(args.warmup):
         one_step(t)
@@ -344,9 +346,9 @@ def run_ours(args):
         s0.record(stream)
         for t in range(t0, t0 + ke):
             eng.grad_arena.copy_(host_g, non_blocking=True)
+            eng.step()
             if tracker is not None:
                 tracker.observe(t, eng.grads)
-            eng.step()
             host_out.copy_(eng.out_arena, non_blocking=True)
         s1.record(stream)
         barrier()

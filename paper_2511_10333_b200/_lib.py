@@ -16,7 +16,8 @@ import torch
 from .errors import DegenerateInputError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libedgc_b200.so")
+# EDGC_LIB_PATH selects an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("EDGC_LIB_PATH", os.path.join(HERE, "libedgc_b200.so"))
 
 EDGC_OK = 0
 EDGC_EINVAL = 1

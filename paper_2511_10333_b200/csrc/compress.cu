@@ -360,12 +360,15 @@ __global__ void __launch_bounds__(kZThreads, 2) k_pass1z(const MatDev *mats, con
 //                  the peer's mbarrier, waits for all peers, writes P_raw
 //                  rows to shared memory and signals the consumers.
 // All hand-offs are mbarriers; no block-wide barrier in the steady state.
+#ifndef EDGC_TLAG
+#define EDGC_TLAG 2
+#endif
 constexpr int kTCons = 256;
 constexpr int kTThreads = kTCons + 64;   // + producer warp + exchange warp
 constexpr int kTRB = 4;
-constexpr int kTStages = 6;              // 6 x 32 KB: lag + 1 held by consumers, the rest prefetched
+constexpr int kTStages = 5;              // 5 x 32 KB TMA ring (pure prefetch: x lives in its own ring)
 constexpr int kTCW = 4 * kTCons;
-constexpr int kTLag = 3;                 // consumer Z update lags the exchange by 3 rounds
+constexpr int kTLag = EDGC_TLAG;           // consumer Z update lags the exchange by this many rounds
 constexpr int kTRing = kTLag + 1;        // red / prow / named-barrier ring depth
 constexpr int kTSlots = 3;               // DSMEM receive slots
 constexpr int kTV = kTRB * 4;            // row-dot values per round (RMAX = 4)
@@ -373,6 +376,7 @@ constexpr int kTV = kTRB * 4;            // row-dot values per round (RMAX = 4)
 struct TSmem {
     float g[kTStages][kTRB][kTCW];
     float w[kTStages][kTRB][kTCW];
+    float xs[kTRing][kTRB][kTCW];        // x (new w) of the last kTRing rounds, for the lagged Z update
     double recv[kTSlots][8][kTV];
     double red[kTRing][kTCons / 32][kTV];
     double prow[kTRing][kTV];
@@ -502,10 +506,9 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
 #pragma unroll
             for (int k = 0; k < 4; ++k) zacc[v][k] = 0.f;
         bool bad = false;
-        // round bb's x values live in its stage slot (written over w); the slot is
-        // released to the producer only after this lagged Z update
+        // round bb's x values wait in xs[bb % kTRing] for this lagged Z update
         auto consume = [&](int bb) {
-            const int q = bb % kTRing, s = bb % kTStages;
+            const int q = bb % kTRing;
             ptx::mbar_wait(&sm.prowready[q], (bb / kTRing) & 1);
             const int64_t i0 = t.row0 + (int64_t)bb * kTRB;
             if (me == 0 && tid < kTV) {
@@ -514,7 +517,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             }
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) {
-                const float4 xv = *reinterpret_cast<const float4 *>(&sm.w[s][rr][4 * tid]);
+                const float4 xv = ptx::ld_shared_v4(&sm.xs[q][rr][4 * tid]);
                 const float xx[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -523,10 +526,6 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                     for (int v = 0; v < 4; ++v) zacc[v][k] = fmaf(xx[v], pv, zacc[v][k]);
                 }
             }
-            // order this thread's generic smem writes (x) before the next bulk copy into slot s
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_relaxed(&sm.empty[s]);   // slot s free for the producer
         };
 #pragma unroll 1
         for (int b = 0; b < nrounds; ++b) {
@@ -546,8 +545,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 double pk[4] = {0.0, 0.0, 0.0, 0.0};
                 float xx[4] = {0.f, 0.f, 0.f, 0.f};
                 if (active && rr < rows) {
-                    const float4 gv = *reinterpret_cast<const float4 *>(&sm.g[s][rr][4 * tid]);
-                    const float4 wv = *reinterpret_cast<const float4 *>(&sm.w[s][rr][4 * tid]);
+                    const float4 gv = ptx::ld_shared_v4(&sm.g[s][rr][4 * tid]);
+                    const float4 wv = ptx::ld_shared_v4(&sm.w[s][rr][4 * tid]);
                     const float gg[4] = {gv.x, gv.y, gv.z, gv.w}, ww[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
@@ -563,10 +562,12 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                     }
                     ptx::st_global_v4(wptr + (i0 + rr) * n + col0, xx[0], xx[1], xx[2], xx[3]);
                 }
-                *reinterpret_cast<float4 *>(&sm.w[s][rr][4 * tid]) = make_float4(xx[0], xx[1], xx[2], xx[3]);
+                ptx::st_shared_v4(&sm.xs[q][rr][4 * tid], xx[0], xx[1], xx[2], xx[3]);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[rr * 4 + k] = pk[k];
             }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_relaxed(&sm.empty[s]);   // stage s read: refill it
             const double part = warp_reduce_scatter<kTV>(acc, lane);
             if ((lane & 1) == 0) sm.red[q][warp][scatter_owner_index<kTV>(lane)] = part;
             ptx::named_bar_arrive(2 + q, kTCons + 32);   // hand red[q] to the exchange warp

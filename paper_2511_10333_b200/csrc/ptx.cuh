@@ -131,3 +131,19 @@ __device__ __forceinline__ void st_cluster_v2_f64(uint32_t addr, double a, doubl
 }
 }  // namespace ptx
 }  // namespace edgc
+
+namespace edgc {
+namespace ptx {
+__device__ __forceinline__ void st_shared_v4(void *p, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(smem_addr(p)), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ float4 ld_shared_v4(const void *p) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(smem_addr(p)));
+    return v;
+}
+}  // namespace ptx
+}  // namespace edgc

@@ -35,14 +35,21 @@ GAUSSIAN_ENTROPY_CONST = 0.5 * math.log(2.0 * math.pi * math.e)
 
 
 
+_WS_CAP = {}
+
+
 def _plan_ws_cap(device) -> int:
-    """Workspace cap of one edgc_sample_plan call: half the free HBM (>= 2 GiB).
+    """Workspace cap of one edgc_sample_plan call: half the HBM free at first use (>= 2 GiB).
 
     All plans of a batch walk concurrently (one CTA each), so fewer, larger
     batches are faster; bucket sets beyond the cap are planned in several calls.
+    Cached per device (cudaMemGetInfo must not run inside a timed step).
     """
-    free, _ = torch.cuda.mem_get_info(device)
-    return max(2 << 30, free // 2)
+    key = torch.device(device).index
+    if key not in _WS_CAP:
+        free, _ = torch.cuda.mem_get_info(device)
+        _WS_CAP[key] = max(2 << 30, free // 2)
+    return _WS_CAP[key]
 
 
 @dataclass(frozen=True)
@@ -444,7 +451,9 @@ class EntropyTracker:
                 per_layer = layer_entropies(mats, iteration, self.config, self.estimator, prefetched=pre)
                 if per_layer:
                     self._pending.append(float(np.mean(per_layer)))
-        if self.prefetch and mats:
+        if self.prefetch and mats and not should_sample_iteration(iteration, self.config.alpha):
+            # build the next sampled iteration's plans on the side stream; launched from a
+            # non-sampled iteration so the sampled one stays a single short device pass
             period = sampling_period(self.config.alpha)
             nxt = (iteration // period + 1) * period
             if nxt not in self._pf:
