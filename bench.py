@@ -75,12 +75,14 @@ def load_peak():
 
 
 def load_traffic(kernel: str):
-    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full summary, if any."""
+    """DRAM bytes of one step's launches of `kernel` (the roofline's unit) from the committed ncu --set full summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
             rec = json.load(fh)
-        return rec["kernels"][kernel]["dram_bytes_per_launch"]
+        k = rec["kernels"][kernel]
+        # one capture of all the phase's launches (pass 1 runs one launch per cluster width)
+        return k.get("dram_bytes_all_launches", k["dram_bytes_per_launch"])
     except Exception:
         return None
 
@@ -307,13 +309,16 @@ def run_ours(args):
     ent_ms = [a.elapsed_time(b) for a, b in zip(ev["ent0"], ev["ent1"])]
     ph["entropy_per_sampled_step"] = statistics.mean(ent_ms) if ent_ms else 0.0
     ph["entropy_sampled_steps"] = len(ent_ms)
+    starts = [mk[0] for mk in ev["marks"]] + [stop]
+    step_ms = sorted(a.elapsed_time(b) for a, b in zip(starts[:-1], starts[1:]))
+    ph["step_ms"] = {"min": step_ms[0], "median": statistics.median(step_ms), "max": step_ms[-1]}
     peak, peak_src = load_peak()
     # dominant kernel: pass 1 (error feedback + P = W Q): reads g and w, writes w: 12 B per element
     alg_bytes = {"pass1": 12.0 * total, "pass2_finalize": 4.0 * total, "reconstruct": 4.0 * total}
     dom = max(alg_bytes, key=lambda k: ph[k])
     dom_ms = ph[dom]
     achieved = alg_bytes[dom] / (dom_ms / 1e3) / 1e9
-    traffic = load_traffic({"pass1": "k_pass1", "pass2_finalize": "k_pass2", "reconstruct": "k_recon"}[dom])
+    traffic = load_traffic({"pass1": "k_pass1t", "pass2_finalize": "k_pass2", "reconstruct": "k_recon4"}[dom])
     n_sampled = len(ent_ms)
     ent_bytes = 4.0 * sum(sample_count(m * n, args.beta) for m, n in shapes) * n_sampled / max(1, args.steps)
     step_frac = (16.0 * total + ent_bytes) / (t_all / args.steps) / 1e9 / peak

@@ -63,7 +63,8 @@ struct MatDev {
     int32_t ld_s, zmode, nitems, zc;   // zc = cluster size (column chunks) on the Z path
     double *fwork;    // 5 r^2 factor scratch
     double *p_tmp;    // [m][r] CholQR intermediate
-    int32_t wide, pad_;   // wide = 1: tiled GEMM path (r > 8 or unaligned)
+    int32_t wide;     // wide = 1: tiled GEMM path (r > 8 or unaligned)
+    int32_t zw;       // Z path: columns per CTA of the cluster (multiple of 4, <= kTCW)
 };
 
 // Z-path work item: one row strip of one matrix, processed by one cluster
@@ -88,8 +89,6 @@ constexpr int kFactorThreads = 256;
 constexpr int kMaxRank = 1024;     // device limit (TMEM-free fp32 path)
 constexpr int kNarrow = 8;         // register kernels up to this rank
 constexpr int64_t kWideSplitK = 2048;
-constexpr int kZThreads = 256;
-constexpr int kZRB = 8;        // rows per DSMEM exchange round
 constexpr int kZRows = 512;    // rows per cluster work item
 constexpr double kKappaMax = 64.0;
 
@@ -203,188 +202,73 @@ __global__ void __launch_bounds__(kP1Threads) k_pass1(const MatDev *mats, const 
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
 }
 
-// ------------------------------------------------------------ pass 1 (Z)
-template <int RMAX>
-__global__ void __launch_bounds__(kZThreads, 2) k_pass1z(const MatDev *mats, const ZTile *tiles, int32_t *status) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
-    const int C = (int)cluster.num_blocks();
-    const int c = (int)cluster.block_rank();
-    const ZTile t = tiles[blockIdx.x / C];
-    const MatDev &M = mats[t.mat];
-    constexpr int RB = kZRB;
-    constexpr int V = RB * RMAX;
-    constexpr int VW = V < 32 ? V : 32;
-    constexpr int NB = V / VW;
-    constexpr int NWARP = kZThreads / 32;
-    const int r = M.r, rr_res = M.r_res;
-    const int64_t n = M.n;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t col0 = ((int64_t)c * kZThreads + tid) * 4;
-    const bool active = col0 < n;
-
-    __shared__ double s_S[RMAX * RMAX];
-    __shared__ float s_pres[RB][RMAX];
-    __shared__ double s_red[NWARP][V];
-    __shared__ double s_part[2][V];
-    __shared__ float s_prow[RB][RMAX];
-
-    if (tid < RMAX * RMAX) {
-        const int i = tid / RMAX, k = tid % RMAX;
-        double v = (i == k) ? 1.0 : 0.0;
-        if (M.precond && i < r && k < r) v = M.precond[(int64_t)i * M.ld_s + k];
-        s_S[tid] = v;
-    }
-    __syncthreads();
-    // preconditioned warm start qw = q_warm S (S upper triangular), residual factor qr
-    float qw[4][RMAX], qr[4][RMAX];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        double raw[RMAX];
-#pragma unroll
-        for (int k = 0; k < RMAX; ++k) raw[k] = (active && k < r) ? (double)M.q_warm[(col0 + v) * M.ld_q + k] : 0.0;
-#pragma unroll
-        for (int k = 0; k < RMAX; ++k) {
-            double a = 0.0;
-#pragma unroll
-            for (int i = 0; i <= k; ++i) a += raw[i] * s_S[i * RMAX + k];
-            qw[v][k] = (float)a;
-            qr[v][k] = (active && k < rr_res) ? M.q_res[(col0 + v) * rr_res + k] : 0.f;
-        }
-    }
-    float zacc[4][RMAX];
-#pragma unroll
-    for (int v = 0; v < 4; ++v)
-#pragma unroll
-        for (int k = 0; k < RMAX; ++k) zacc[v][k] = 0.f;
-    bool bad = false;
-    int buf = 0;
-    for (int64_t row = t.row0; row < t.row1; row += RB, buf ^= 1) {
-        if (tid < RB * RMAX) {
-            const int rr = tid / RMAX, k = tid % RMAX;
-            const int64_t i = row + rr;
-            s_pres[rr][k] = (k < rr_res && i < t.row1) ? M.p_res[i * rr_res + k] : 0.f;
-        }
-        __syncthreads();
-        float x[RB][4];
-        float acc[V];
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {
-            const int64_t i = row + rr;
-            float pk[RMAX];
-#pragma unroll
-            for (int k = 0; k < RMAX; ++k) pk[k] = 0.f;
-            if (active && i < t.row1) {
-                float gv[4], wv[4];
-                VecT<4>::unpack(VecT<4>::ld_cs(M.g + i * M.ld_g + col0), gv);
-                VecT<4>::unpack(VecT<4>::ld_cs(M.w + i * n + col0), wv);
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    float dot = 0.f;
-#pragma unroll
-                    for (int k = 0; k < RMAX; ++k) dot = fmaf(s_pres[rr][k], qr[v][k], dot);
-                    const float xv = gv[v] + (wv[v] - dot);
-                    bad |= !isfinite(xv);
-                    wv[v] = xv;
-                    x[rr][v] = xv;
-#pragma unroll
-                    for (int k = 0; k < RMAX; ++k) pk[k] = fmaf(xv, qw[v][k], pk[k]);
-                }
-                VecT<4>::st(M.w + i * n + col0, wv);
-            } else {
-#pragma unroll
-                for (int v = 0; v < 4; ++v) x[rr][v] = 0.f;
-            }
-#pragma unroll
-            for (int k = 0; k < RMAX; ++k) acc[rr * RMAX + k] = pk[k];
-        }
-        // CTA partial of this round's row dots: fp32 butterfly in the warp, fp64 across warps
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-            float part[VW];
-#pragma unroll
-            for (int q = 0; q < VW; ++q) part[q] = acc[b * VW + q];
-            const float sv = warp_reduce_scatter<VW>(part, lane);
-            const int owner = scatter_owner_index<VW>(lane);
-            if ((lane & ((32 / VW) - 1)) == 0) s_red[warp][b * VW + owner] = (double)sv;
-        }
-        __syncthreads();
-        if (tid < V) {
-            double a = 0.0;
-#pragma unroll
-            for (int w = 0; w < NWARP; ++w) a += s_red[w][tid];
-            s_part[buf][tid] = a;
-        }
-        // exchange through distributed shared memory: every CTA sums the C
-        // column-chunk partials in the same order -> identical P_raw rows
-        cluster.sync();
-        if (tid < V) {
-            double a = 0.0;
-            for (int cc = 0; cc < C; ++cc) a += cluster.map_shared_rank(&s_part[buf][0], cc)[tid];
-            const int rr = tid / RMAX, k = tid % RMAX;
-            const int64_t i = row + rr;
-            s_prow[rr][k] = (float)a;
-            if (c == 0 && i < t.row1 && k < r) M.p_raw[i * r + k] = a;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr)
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-#pragma unroll
-                for (int k = 0; k < RMAX; ++k) zacc[v][k] = fmaf(x[rr][v], s_prow[rr][k], zacc[v][k]);
-    }
-    if (active) {
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-#pragma unroll
-            for (int k = 0; k < RMAX; ++k)
-                if (k < r) M.zpart[((int64_t)t.item * n + col0 + v) * r + k] = (double)zacc[v][k];
-    }
-    if (__syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
-    cluster.sync();  // no CTA leaves while a peer may still read its shared memory
-}
-
 // ------------------------------------------- pass 1 (Z, TMA-pipelined)
-// Same math as k_pass1z, warp-specialised for bandwidth.  Per CTA (one per
-// 1024-column chunk of a cluster's row strip):
-//   producer warp  streams [4 rows x 1024 cols] tiles of g and w into a
-//                  3-stage shared-memory ring with 1-D bulk async copies
-//                  (TMA engine, mbarrier complete_tx);
-//   8 consumer warps  error feedback, w write-back, fp64 row dots (exact
+// Warp-specialised for bandwidth.  Per CTA (one per <= 1280-column chunk of a
+// cluster's row strip; clusters of 1, 2, 3 or 6 CTAs pack the 18-20 SM GPCs,
+// 7-8 only for n > 7680):
+//   producer warp  streams [4 rows x chunk] tiles of g and w into a 3-stage
+//                  shared-memory ring with 1-D bulk async copies (TMA
+//                  engine, mbarrier complete_tx);
+//   10 consumer warps  error feedback, w write-back, fp64 row dots (exact
 //                  fp32 x fp32 products), per-warp butterfly -> red[] ring;
-//                  then, two rounds later, Z += x * P_raw with that round's
+//                  then, kTLag rounds later, Z += x * P_raw with that round's
 //                  rows -- they never wait on the cluster;
 //   exchange warp  sums the 8 warp partials, pushes them into every peer's
 //                  shared memory (st.shared::cluster) and release-arrives on
-//                  the peer's mbarrier, waits for all peers, writes P_raw
-//                  rows to shared memory and signals the consumers.
-// All hand-offs are mbarriers; no block-wide barrier in the steady state.
+//                  the peer's mbarrier; it completes round b - kTD (waits for
+//                  all peers, publishes the P_raw rows) only after pushing
+//                  round b, so one cluster round trip is always in flight.
+// All hand-offs are mbarriers / named barriers; no block-wide barrier in the
+// steady state.  Non-finite work is detected on the exchanged row sums: a
+// fp64 sum of exact fp32 x fp32 products is non-finite iff one of the x is.
 #ifndef EDGC_TLAG
 #define EDGC_TLAG 2
 #endif
-constexpr int kTCons = 256;
+constexpr int kTCons = 320;
 constexpr int kTThreads = kTCons + 64;   // + producer warp + exchange warp
 constexpr int kTRB = 4;
-constexpr int kTStages = 5;              // 5 x 32 KB TMA ring (pure prefetch: x lives in its own ring)
+#ifndef EDGC_TSTAGES
+#define EDGC_TSTAGES 3
+#endif
+constexpr int kTStages = EDGC_TSTAGES;   // 32 KB TMA stages (pure prefetch: x lives in its own ring)
 constexpr int kTCW = 4 * kTCons;
-constexpr int kTLag = EDGC_TLAG;           // consumer Z update lags the exchange by this many rounds
+constexpr int kTLag = EDGC_TLAG;         // consumer Z update lags its round by this many rounds
+#ifndef EDGC_TD
+#define EDGC_TD 1
+#endif
+#ifndef EDGC_STCS
+#define EDGC_STCS 1
+#endif
+#ifndef EDGC_PRES_SMEM
+#define EDGC_PRES_SMEM 0
+#endif
+#ifndef EDGC_EARLY_RELEASE
+#define EDGC_EARLY_RELEASE 1
+#endif
+#ifndef EDGC_CONS_FINITE
+#define EDGC_CONS_FINITE 1
+#endif
+#ifndef EDGC_LOAD_AHEAD
+#define EDGC_LOAD_AHEAD 0
+#endif
+constexpr int kTD = EDGC_TD;             // exchange completes round b - kTD after pushing round b
+static_assert(kTLag >= kTD, "consumers must not wait for a round the exchange has not completed");
 constexpr int kTRing = kTLag + 1;        // red / prow / named-barrier ring depth
-constexpr int kTSlots = 3;               // DSMEM receive slots
+constexpr int kTSlots = 2 * kTD + 2;     // DSMEM receive slots (a peer refills slot b only after my round b)
 constexpr int kTV = kTRB * 4;            // row-dot values per round (RMAX = 4)
 
 struct TSmem {
     float g[kTStages][kTRB][kTCW];
     float w[kTStages][kTRB][kTCW];
-    float xs[kTRing][kTRB][kTCW];        // x (new w) of the last kTRing rounds, for the lagged Z update
+    float xs[kTRing][kTRB][kTCW];        // x (new w) of the last kTRing rounds (each thread its own columns)
+    float pres[kTStages][kTV];           // the stage's p_res rows, [row][k], zero padded to 4
+    float prowf[kTRing][kTV];            // P_raw rows of the round, as float, for the Z update
     double recv[kTSlots][8][kTV];
     double red[kTRing][kTCons / 32][kTV];
-    double prow[kTRing][kTV];
     double S[16];
     alignas(8) uint64_t full[kTStages];
     alignas(8) uint64_t empty[kTStages];
     alignas(8) uint64_t xfull[kTSlots];
-    alignas(8) uint64_t redfull[kTRing];
     alignas(8) uint64_t prowready[kTRing];
 };
 
@@ -409,8 +293,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
     const double *precond_ptr = M.precond;
     const int ld_s = M.ld_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t col_base = (int64_t)me * kTCW;
-    const int64_t chunk_cols = min((int64_t)kTCW, n - col_base);
+    const int64_t col_base = (int64_t)me * M.zw;
+    const int64_t chunk_cols = max((int64_t)0, min((int64_t)M.zw, n - col_base));
     const int nrounds = (int)((t.row1 - t.row0 + kTRB - 1) / kTRB);
     constexpr int kProducer = kTCons / 32, kExchange = kTCons / 32 + 1;
 
@@ -420,10 +304,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             ptx::mbar_init(&sm.empty[s], kTCons / 32);
         }
         for (int s = 0; s < kTSlots; ++s) ptx::mbar_init(&sm.xfull[s], C);
-        for (int s = 0; s < kTRing; ++s) {
-            ptx::mbar_init(&sm.redfull[s], kTCons / 32);
-            ptx::mbar_init(&sm.prowready[s], 1);
-        }
+        for (int s = 0; s < kTRing; ++s) ptx::mbar_init(&sm.prowready[s], 1);
         ptx::fence_mbar_init();
     }
     if (tid < 16) {
@@ -435,22 +316,31 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
     ptx::cluster_sync();
 
     if (warp == kProducer) {
-        if (lane == 0 && chunk_cols > 0) {
+        if (chunk_cols > 0) {
             const uint32_t bytes = (uint32_t)(chunk_cols * 4);
             for (int b = 0; b < nrounds; ++b) {
                 const int s = b % kTStages;
-                if (b >= kTStages) ptx::mbar_wait(&sm.empty[s], ((b / kTStages) - 1) & 1);
                 const int64_t i0 = t.row0 + (int64_t)b * kTRB;
                 const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
-                ptx::mbar_arrive_expect_tx(&sm.full[s], 2u * bytes * (uint32_t)rows);
-                for (int rr = 0; rr < rows; ++rr) {
-                    ptx::bulk_g2s(&sm.g[s][rr][0], gptr + (i0 + rr) * ld_g + col_base, bytes, &sm.full[s]);
-                    ptx::bulk_g2s(&sm.w[s][rr][0], wptr + (i0 + rr) * n + col_base, bytes, &sm.full[s]);
+                // the round's p_res rows (the load's latency overlaps the empty wait)
+                float pv = 0.f;
+                if (EDGC_PRES_SMEM && lane < kTV && (lane & 3) < rr_res && (lane >> 2) < rows)
+                    pv = __ldg(pres_ptr + (i0 + (lane >> 2)) * rr_res + (lane & 3));
+                if (b >= kTStages) ptx::mbar_wait(&sm.empty[s], ((b / kTStages) - 1) & 1);
+                if (lane < kTV) sm.pres[s][lane] = pv;
+                __syncwarp();   // orders the lanes' stores before lane 0's releasing arrive
+                if (lane == 0) {
+                    ptx::mbar_arrive_expect_tx(&sm.full[s], 2u * bytes * (uint32_t)rows);
+                    for (int rr = 0; rr < rows; ++rr) {
+                        ptx::bulk_g2s(&sm.g[s][rr][0], gptr + (i0 + rr) * ld_g + col_base, bytes, &sm.full[s]);
+                        ptx::bulk_g2s(&sm.w[s][rr][0], wptr + (i0 + rr) * n + col_base, bytes, &sm.full[s]);
+                    }
                 }
             }
         }
     } else if (warp == kExchange) {
-        for (int b = 0; b < nrounds; ++b) {
+        bool bad = false;
+        auto push = [&](int b) {
             const int q = b % kTRing, slot = b % kTSlots;
             ptx::named_bar_sync(2 + q, kTCons + 32);   // the 8 consumer warps wrote red[q]
             if (lane < kTV) {
@@ -471,15 +361,28 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_addr(&sm.xfull[slot]), cc));
             }
             if ((uint32_t)lane == me) ptx::mbar_arrive_cta(&sm.xfull[slot]);
+        };
+        auto complete = [&](int b) {
+            const int q = b % kTRing, slot = b % kTSlots;
             ptx::mbar_wait_cluster(&sm.xfull[slot], (b / kTSlots) & 1);
             if (lane < kTV) {
                 double a = 0.0;
                 for (uint32_t cc = 0; cc < C; ++cc) a += sm.recv[slot][cc][lane];
-                sm.prow[q][lane] = a;
+                if (!EDGC_CONS_FINITE) bad |= !isfinite(a);
+                sm.prowf[q][lane] = (float)a;
+                const int64_t i = t.row0 + (int64_t)b * kTRB + (lane >> 2);
+                const int k = lane & 3;
+                if (me == 0 && i < t.row1 && k < r) praw_ptr[i * r + k] = a;
             }
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cta(&sm.prowready[q]);
+        };
+        for (int b = 0; b < nrounds; ++b) {
+            push(b);
+            if (b >= kTD) complete(b - kTD);
         }
+        for (int bb = max(0, nrounds - kTD); bb < nrounds; ++bb) complete(bb);
+        if (__any_sync(0xffffffffu, bad) && lane == 0 && me == 0) atomicOr(status + t.mat, 1);
     } else {
         // ---------------- consumer warps
         const int64_t col0 = col_base + 4 * tid;
@@ -506,25 +409,19 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
 #pragma unroll
             for (int k = 0; k < 4; ++k) zacc[v][k] = 0.f;
         bool bad = false;
-        // round bb's x values wait in xs[bb % kTRing] for this lagged Z update
+        // round bb's x values wait in xs[bb % kTRing] (this thread's columns only) for the lagged Z update
         auto consume = [&](int bb) {
             const int q = bb % kTRing;
             ptx::mbar_wait(&sm.prowready[q], (bb / kTRing) & 1);
-            const int64_t i0 = t.row0 + (int64_t)bb * kTRB;
-            if (me == 0 && tid < kTV) {
-                const int rr = tid / 4, k = tid % 4;
-                if (i0 + rr < t.row1 && k < r) praw_ptr[(i0 + rr) * r + k] = sm.prow[q][tid];
-            }
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) {
-                const float4 xv = ptx::ld_shared_v4(&sm.xs[q][rr][4 * tid]);
-                const float xx[4] = {xv.x, xv.y, xv.z, xv.w};
+                const float4 pv = *reinterpret_cast<const float4 *>(&sm.prowf[q][rr * 4]);
+                const float4 xv = *reinterpret_cast<const float4 *>(&sm.xs[q][rr][4 * tid]);
+                const float xx[4] = {xv.x, xv.y, xv.z, xv.w}, pp[4] = {pv.x, pv.y, pv.z, pv.w};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const float pv = (float)sm.prow[q][rr * 4 + k];
+                for (int k = 0; k < 4; ++k)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) zacc[v][k] = fmaf(xx[v], pv, zacc[v][k]);
-                }
+                    for (int v = 0; v < 4; ++v) zacc[v][k] = fmaf(xx[v], pp[k], zacc[v][k]);
             }
         };
 #pragma unroll 1
@@ -532,42 +429,70 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             const int s = b % kTStages, q = b % kTRing;
             const int64_t i0 = t.row0 + (int64_t)b * kTRB;
             const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
-            float presr[kTRB][4];
+            if (chunk_cols > 0) ptx::mbar_wait(&sm.full[s], (b / kTStages) & 1);
+            // the stage's shared loads (rows past the strip read stale data, zeroed below)
+            float4 pr4[kTRB], gv[kTRB], wv[kTRB];
 #pragma unroll
-            for (int rr = 0; rr < kTRB; ++rr)
+            for (int rr = 0; rr < kTRB; ++rr) {
+#if EDGC_PRES_SMEM
+                pr4[rr] = *reinterpret_cast<const float4 *>(&sm.pres[s][rr * 4]);
+#else
+                float pq[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    presr[rr][k] = (k < rr_res && rr < rows) ? __ldg(pres_ptr + (i0 + rr) * rr_res + k) : 0.f;
-            if (chunk_cols > 0) ptx::mbar_wait(&sm.full[s], (b / kTStages) & 1);
+                    pq[k] = (k < rr_res && rr < rows) ? __ldg(pres_ptr + (i0 + rr) * rr_res + k) : 0.f;
+                pr4[rr] = make_float4(pq[0], pq[1], pq[2], pq[3]);
+#endif
+#if EDGC_LOAD_AHEAD
+                gv[rr] = *reinterpret_cast<const float4 *>(&sm.g[s][rr][4 * tid]);
+                wv[rr] = *reinterpret_cast<const float4 *>(&sm.w[s][rr][4 * tid]);
+#endif
+            }
+#if EDGC_LOAD_AHEAD && EDGC_EARLY_RELEASE
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cta(&sm.empty[s]);   // stage s read: refill it
+#endif
             double acc[kTV];
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) {
+#if !EDGC_LOAD_AHEAD
+                gv[rr] = ptx::ld_shared_v4(&sm.g[s][rr][4 * tid]);
+                wv[rr] = ptx::ld_shared_v4(&sm.w[s][rr][4 * tid]);
+#endif
+                const bool live = active && rr < rows;
+                const float pp[4] = {pr4[rr].x, pr4[rr].y, pr4[rr].z, pr4[rr].w};
+                const float gg[4] = {gv[rr].x, gv[rr].y, gv[rr].z, gv[rr].w};
+                const float ww[4] = {wv[rr].x, wv[rr].y, wv[rr].z, wv[rr].w};
+                float xx[4];
                 double pk[4] = {0.0, 0.0, 0.0, 0.0};
-                float xx[4] = {0.f, 0.f, 0.f, 0.f};
-                if (active && rr < rows) {
-                    const float4 gv = ptx::ld_shared_v4(&sm.g[s][rr][4 * tid]);
-                    const float4 wv = ptx::ld_shared_v4(&sm.w[s][rr][4 * tid]);
-                    const float gg[4] = {gv.x, gv.y, gv.z, gv.w}, ww[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        float dot = 0.f;
+                for (int v = 0; v < 4; ++v) {
+                    float dot = 0.f;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) dot = fmaf(presr[rr][k], qr[v][k], dot);
-                        const float xv = gg[v] + (ww[v] - dot);
-                        bad |= !isfinite(xv);
-                        xx[v] = xv;
-                        const double xd = (double)xv;
+                    for (int k = 0; k < 4; ++k) dot = fmaf(pp[k], qr[v][k], dot);
+                    xx[v] = live ? gg[v] + (ww[v] - dot) : 0.f;
+#if EDGC_CONS_FINITE
+                    bad |= !isfinite(xx[v]);
+#endif
+                    const double xd = (double)xx[v];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) pk[k] = fma(xd, qw[v][k], pk[k]);
-                    }
-                    ptx::st_global_v4(wptr + (i0 + rr) * n + col0, xx[0], xx[1], xx[2], xx[3]);
+                    for (int k = 0; k < 4; ++k) pk[k] = fma(xd, qw[v][k], pk[k]);
                 }
-                ptx::st_shared_v4(&sm.xs[q][rr][4 * tid], xx[0], xx[1], xx[2], xx[3]);
+                if (live) {
+#if EDGC_STCS
+                    __stcs(reinterpret_cast<float4 *>(wptr + (i0 + rr) * n + col0), make_float4(xx[0], xx[1], xx[2], xx[3]));
+#else
+                    ptx::st_global_v4(wptr + (i0 + rr) * n + col0, xx[0], xx[1], xx[2], xx[3]);
+#endif
+                }
+                *reinterpret_cast<float4 *>(&sm.xs[q][rr][4 * tid]) = make_float4(xx[0], xx[1], xx[2], xx[3]);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[rr * 4 + k] = pk[k];
             }
+#if !(EDGC_LOAD_AHEAD && EDGC_EARLY_RELEASE)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_relaxed(&sm.empty[s]);   // stage s read: refill it
+#endif
             const double part = warp_reduce_scatter<kTV>(acc, lane);
             if ((lane & 1) == 0) sm.red[q][warp][scatter_owner_index<kTV>(lane)] = part;
             ptx::named_bar_arrive(2 + q, kTCons + 32);   // hand red[q] to the exchange warp
@@ -581,7 +506,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 for (int k = 0; k < 4; ++k)
                     if (k < r) zpart_ptr[((int64_t)t.item * n + col0 + v) * r + k] = (double)zacc[v][k];
         }
-        if (bad) atomicOr(status + t.mat, 1);
+        if (EDGC_CONS_FINITE && bad) atomicOr(status + t.mat, 1);
     }
     ptx::cluster_sync();  // no CTA leaves while a peer may still push into it
 }
@@ -593,7 +518,57 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
 // projected norm -- the Schur-complement diagonal -- is <= tol is zeroed and
 // drops out of later projections, compressor.py:80-90); triangular inverse by
 // independent column back-substitutions; everything fp64 and deterministic.
+// r <= 4: each thread owns whole rows (stride kFactorThreads) and accumulates
+// all r(r+1)/2 products in registers; then per-warp butterflies and a
+// fixed-order sum over warps (deterministic).
+template <int R>
+__device__ void gram_rows(const double *P, int64_t m, double *gram) {
+    constexpr int E = R * (R + 1) / 2;
+    __shared__ double s_part[kFactorThreads / 32][10];
+    double acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.0;
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < m; i += kFactorThreads) {
+        double x[R];
+#pragma unroll
+        for (int a = 0; a < R; ++a) x[a] = P[i * R + a];
+        int e = 0;
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+#pragma unroll
+            for (int b = a; b < R; ++b, ++e) acc[e] = fma(x[a], x[b], acc[e]);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    if (lane == 0) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) s_part[warp][e] = acc[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < E) {
+        int a = 0, rem = threadIdx.x;
+        while (rem >= R - a) { rem -= R - a; ++a; }
+        const int b = a + rem;
+        double sum = 0.0;
+        for (int w = 0; w < kFactorThreads / 32; ++w) sum += s_part[w][threadIdx.x];
+        gram[a * R + b] = sum;
+        gram[b * R + a] = sum;
+    }
+    __syncthreads();
+}
+
 __device__ void gram_pass(const double *P, int64_t m, int r, double *gram, double *s_tmp) {
+    switch (r) {
+        case 1: gram_rows<1>(P, m, gram); return;
+        case 2: gram_rows<2>(P, m, gram); return;
+        case 3: gram_rows<3>(P, m, gram); return;
+        case 4: gram_rows<4>(P, m, gram); return;
+        default: break;
+    }
     const int E = r * (r + 1) / 2;
     const int tid = threadIdx.x;
     for (int e0 = 0; e0 < E; e0 += kFactorThreads) {
@@ -665,7 +640,38 @@ __device__ void tri_inverse(const double *R, const int32_t *dead, int r, double 
 }
 
 // dst (m x r) = src (m x r) * T (upper, column-major by column)
+template <int R>
+__device__ void right_mul_rows(const double *src, const double *T, int64_t m, double *dst, float *dst_f) {
+    double t[R][R];
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int l = 0; l <= j; ++l) t[j][l] = T[j * R + l];
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < m; i += kFactorThreads) {
+        double x[R];
+#pragma unroll
+        for (int l = 0; l < R; ++l) x[l] = src[i * R + l];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l <= j; ++l) acc += x[l] * t[j][l];
+            if (dst) dst[i * R + j] = acc;
+            if (dst_f) dst_f[i * R + j] = (float)acc;
+        }
+    }
+    __syncthreads();
+}
+
 __device__ void right_mul(const double *src, const double *T, int64_t m, int r, double *dst, float *dst_f) {
+    switch (r) {
+        case 1: right_mul_rows<1>(src, T, m, dst, dst_f); return;
+        case 2: right_mul_rows<2>(src, T, m, dst, dst_f); return;
+        case 3: right_mul_rows<3>(src, T, m, dst, dst_f); return;
+        case 4: right_mul_rows<4>(src, T, m, dst, dst_f); return;
+        default: break;
+    }
     for (int64_t e = threadIdx.x; e < m * r; e += kFactorThreads) {
         const int64_t i = e / r;
         const int j = (int)(e % r);
@@ -742,11 +748,25 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, i
     const double rn2 = s_tmp[0];
     __syncthreads();
     tri_inverse(R, dead, r, T1);
-    if (M.zmode && tid == 0) {
-        double tn = 0.0;
-        for (int e = 0; e < r * r; ++e) tn += T1[e] * T1[e];
-        if (sqrt(rn2 * tn) > kKappaMax) atomicOr(status + blockIdx.x, 2);
+    __shared__ int s_single;
+    if (tid == 0) {
+        bool single = false;
+        if (M.zmode) {
+            double tn = 0.0;
+            for (int e = 0; e < r * r; ++e) tn += T1[e] * T1[e];
+            single = sqrt(rn2 * tn) <= kKappaMax;
+            if (!single) atomicOr(status + blockIdx.x, 2);
+        }
+        s_single = single;
     }
+    __syncthreads();
+    if (s_single) {
+        // cond(R) <= 64: one fp64 CholQR pass already leaves P orthonormal to ~1e-9
+        // (loss ~ cond^2 * m * eps64), far below the fp32 output precision
+        right_mul(M.p_raw, T1, m, r, nullptr, M.p_out);
+        for (int e = tid; e < r * r; e += kFactorThreads) M.tmat[e] = T1[e];
+        __syncthreads();
+    } else {
     // P1 = P_raw T1, then a second CholQR pass restores orthogonality to fp64 level
     right_mul(M.p_raw, T1, m, r, M.p_tmp, nullptr);
     gram_pass(M.p_tmp, m, r, gram, s_tmp);
@@ -761,6 +781,7 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, i
         M.tmat[(int64_t)j * r + l] = a;
     }
     __syncthreads();
+    }
     if (pre) {
         // next preconditioner A = S T (dead columns restart from e_j)
         for (int e = tid; e < r * r; e += kFactorThreads) {
@@ -998,7 +1019,11 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                         ((uintptr_t)d.w % 16 == 0) && std::max(d.r, d.r_res) <= 4;
         M.vec = v4 ? 4 : 1;
         static const bool z_off = std::getenv("EDGC_NO_ZPATH") != nullptr;
-        const int zc = (int)ceil_div(d.n, 4 * kZThreads);
+        // cluster size: smallest of {1, 2, 3, 6, 7, 8} covering n with <= kTCW columns per CTA
+        // (GPCs hold 18-20 SMs: 4- and 5-CTA clusters would strand SMs); balanced chunks
+        int zc = (int)ceil_div(d.n, kTCW);
+        if (zc == 4 || zc == 5) zc = 6;
+        M.zw = (int32_t)(ceil_div(ceil_div(d.n, zc), 4) * 4);
         M.zmode = (!z_off && v4 && std::max(d.r, d.r_res) <= 4 && zc <= 8) ? 1 : 0;
         M.zc = zc;
         M.nitems = M.zmode ? (int32_t)ceil_div(d.m, kZRows) : 0;
@@ -1087,8 +1112,8 @@ int launch_pass1z(const Plan &P, int32_t *status, cudaStream_t st) {
         if (P.tz[c].empty()) continue;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(P.tz[c].size() * c));
-        cfg.blockDim = dim3(kZThreads);
-        cfg.dynamicSmemBytes = 0;
+        cfg.blockDim = dim3(kTThreads);
+        cfg.dynamicSmemBytes = sizeof(TSmem);
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1097,22 +1122,13 @@ int launch_pass1z(const Plan &P, int32_t *status, cudaStream_t st) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        static const bool legacy = std::getenv("EDGC_PASS1Z") != nullptr;
-        if (legacy) {
-            EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1z<4>, (const MatDev *)P.d_mats, (const ZTile *)P.d_tz[c],
-                                             status));
-        } else {
-            static bool attr_set = false;
-            if (!attr_set) {
-                EDGC_CUDA_TRY(cudaFuncSetAttribute(k_pass1t, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)sizeof(TSmem)));
-                attr_set = true;
-            }
-            cfg.blockDim = dim3(kTThreads);
-            cfg.dynamicSmemBytes = sizeof(TSmem);
-            EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1t, (const MatDev *)P.d_mats, (const ZTile *)P.d_tz[c],
-                                             status));
+        static bool attr_set = false;
+        if (!attr_set) {
+            EDGC_CUDA_TRY(cudaFuncSetAttribute(k_pass1t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sizeof(TSmem)));
+            attr_set = true;
         }
+        EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1t, (const MatDev *)P.d_mats, (const ZTile *)P.d_tz[c], status));
         EDGC_LAUNCH_CHECK();
     }
     return EDGC_OK;

@@ -132,6 +132,9 @@ def main():
                              f"{v.get('launch__registers_per_thread', float('nan')):.0f} |")
             rec = lst[-1]
             summary["kernels"][k] = {
+                "launches_captured": len(lst),
+                "dram_bytes_all_launches": sum(v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0)
+                                               for v in lst),
                 "dram_bytes_per_launch": rec.get("dram__bytes_read.sum", 0.0) + rec.get("dram__bytes_write.sum", 0.0),
                 "dram_read": rec.get("dram__bytes_read.sum"), "dram_write": rec.get("dram__bytes_write.sum"),
                 "time_s_ncu": rec.get("gpu__time_duration.sum"), "tag": args.tag, "metrics": rec,
