@@ -62,6 +62,9 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--entropy", choices=["prefetch", "inline", "off"], default="prefetch",
+                    help="diagnostics: entropy plans built ahead on a side stream (default), inline, or no tracker")
+    ap.add_argument("--hi-prio", action="store_true", help="diagnostics: run the step on a high-priority stream")
     ap.add_argument("--cpu-steps", type=int, default=6, help="EF steps in the bounded CPU sample")
     return ap.parse_args()
 
@@ -202,7 +205,9 @@ def config_dict(args, shapes):
                         f"elements ({4 * total / 1e9:.2f} GB) per GPU",
             "rank": args.rank, "alpha": args.alpha, "beta": args.beta, "estimator": "gaussian_plugin",
             "l2": "inputs 9.2 GB/GPU >> 126 MB L2 (no flush needed)" if args.model == "2.5B" and args.layers is None
-            else "inputs larger than L2", "parallelism": f"dp{args.gpus}"}
+            else "inputs larger than L2", "parallelism": f"dp{args.gpus}",
+            "entropy_plans": {"prefetch": "side stream, built during the preceding iterations",
+                              "inline": "built inside the sampled iteration", "off": "tracker disabled"}[args.entropy]}
 
 
 # ------------------------------------------------------------------ GPU side
@@ -234,7 +239,12 @@ def run_ours(args):
         b = min(total, a + chunk)
         eng.grad_arena[a:b].normal_(0.0, 1e-2, generator=gen)
     cfg = SamplerConfig(alpha=args.alpha, beta=args.beta, rng_seed=args.seed)
-    tracker = EntropyTracker(cfg, window=max(100, args.steps + args.warmup + 10)) if me == 0 else None
+    tracker = None
+    if me == 0 and args.entropy != "off":
+        tracker = EntropyTracker(cfg, window=max(100, args.steps + args.warmup + 10),
+                                 prefetch=args.entropy == "prefetch")
+    if args.hi_prio:
+        torch.cuda.set_stream(torch.cuda.Stream(dev, priority=-1))
     period = max(1, round(1.0 / args.alpha))
     stream = torch.cuda.current_stream(dev)
 

@@ -64,10 +64,14 @@ typedef struct {
     uint64_t state_hi, state_lo, inc_hi, inc_lo;
     int64_t n_elems;   /* N = m * n                       */
     int64_t count;     /* ceil(beta * N); 1 <= count < N  */
-    int32_t *idx;      /* device out [count], NumPy order */
+    int32_t *idx;      /* device out [count], NumPy order ([1] with EDGC_PLAN_BITMAP_ONLY) */
     uint32_t *bitmap;  /* optional device out [ceil(N/32)] membership bits
-                          (caller zeroes; bit e set iff e is sampled) or NULL */
+                          (bit e set iff e is sampled; the caller zeroes it) or NULL */
+    int64_t flags;     /* EDGC_PLAN_* */
 } edgc_plan_desc;
+/* Only the membership bitmap (required) and idx[0] (the first sample in NumPy
+ * order, the Gaussian estimator's shift) are produced: the set, not the order. */
+#define EDGC_PLAN_BITMAP_ONLY 1
 
 int64_t edgc_sample_plan_workspace_bytes(const edgc_plan_desc *plans, int n_plans);
 /* status_dev: device int32[n_plans]; nonzero = EDGC_EDRAWS for that plan. */

@@ -29,6 +29,7 @@ EDGC_ECAPACITY = 7
 EDGC_EDRAWS = 8
 
 PHASE_PASS1, PHASE_FACTOR, PHASE_PASS2, PHASE_FINALIZE, PHASE_ALL = 1, 2, 4, 8, 15
+PLAN_BITMAP_ONLY = 1
 
 c_i32, c_i64, c_u64, c_f32, c_f64, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float,
                                            ctypes.c_double, ctypes.c_void_p)
@@ -36,7 +37,8 @@ c_i32, c_i64, c_u64, c_f32, c_f64, c_vp = (ctypes.c_int32, ctypes.c_int64, ctype
 
 class PlanDesc(ctypes.Structure):
     _fields_ = [("state_hi", c_u64), ("state_lo", c_u64), ("inc_hi", c_u64), ("inc_lo", c_u64),
-                ("n_elems", c_i64), ("count", c_i64), ("idx", c_vp), ("bitmap", c_vp)]
+                ("n_elems", c_i64), ("count", c_i64), ("idx", c_vp), ("bitmap", c_vp),
+                ("flags", c_i64)]
 
 
 class GaussDesc(ctypes.Structure):

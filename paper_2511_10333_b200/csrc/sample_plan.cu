@@ -21,6 +21,7 @@
 //               draw or an earlier collided step's j.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -76,6 +77,18 @@ struct PlanDev {
     int32_t tail;      // 1 = tail shuffle, 0 = Floyd
     int64_t draw_chunk0;  // first P1 chunk index of this plan
     int64_t step_block0;  // first P3/P4 block index of this plan
+    // bucketed resolve (tail-shuffle plans; see k_bucket_sort)
+    int32_t *lst_s, *lst_j;   // [count] each chunk's steps sorted by bucket, and their bounded values
+    int32_t *segoff;          // [nch][nb + 1] per chunk: start of each bucket's segment in the chunk
+    int32_t *pred;            // chain list: latest earlier step that wrote the step's target
+    int32_t *wtail;           // [count] latest step before N-1-p that wrote tail position p >= N-count
+    int32_t *nchain;          // chain list length
+    int32_t nb, nch;          // buckets, sort chunks
+    int32_t bucketed;         // 1: bucket path, 0: global head-table path
+    int32_t full_idx;         // 0: EDGC_PLAN_BITMAP_ONLY (only idx[0] is written)
+    int64_t chunk0;           // first sort CTA of this plan
+    int64_t bucket0;          // first bucket-resolve CTA of this plan
+    int64_t oblock0;          // first chain-pass CTA of this plan
 };
 
 constexpr int kDrawsPerThread = 64;  // 64-bit outputs per P1 thread
@@ -288,7 +301,7 @@ __global__ void __launch_bounds__(kStepThreads) k_index(const PlanDev *plans, in
     const int p = p0 + find_plan_steps(plans + p0, p1 - p0, blk0 + blockIdx.x);
     const PlanDev &P = plans[p];
     const int64_t s = (int64_t)(blk0 + blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
-    if (s >= P.count) return;
+    if (P.bucketed || s >= P.count) return;
     P.next[s] = atomicExch(P.head + P.rv[s], (int32_t)s);
 }
 
@@ -307,7 +320,7 @@ __global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, 
     const int p = p0 + find_plan_steps(plans + p0, p1 - p0, blk0 + blockIdx.x);
     const PlanDev &P = plans[p];
     const int64_t s64 = (int64_t)(blk0 + blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
-    if (s64 >= P.count) return;
+    if (P.bucketed || s64 >= P.count) return;
     const int32_t s = (int32_t)s64;
     const int64_t N = P.n_elems, count = P.count;
     if (P.tail) {
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, 
                 t = t2;
             }
         }
-        P.idx[count - 1 - s] = (int32_t)val;
+        if (P.full_idx || s == count - 1) P.idx[count - 1 - s] = (int32_t)val;
         if (P.bitmap) atomicOr(P.bitmap + (val >> 5), 1u << (val & 31));
     } else {
         const int64_t base = N - count;
@@ -342,7 +355,336 @@ __global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, 
             cur = prev;
         }
         const int32_t outv = collide ? (int32_t)(base + s) : P.rv[s];
-        P.idx[s] = outv;
+        if (P.full_idx || s == 0) P.idx[s] = outv;
+        if (P.bitmap) atomicOr(P.bitmap + (outv >> 5), 1u << (outv & 31));
+    }
+}
+
+
+// ---- P3/P4, bucketed (tail-shuffle plans, N <= 2^25) -------------------------
+// The tail-shuffle resolve needs per-position list queries: pred(s) = the
+// latest earlier step whose bounded value equals rv[s], and for each tail
+// position p the latest step before N-1-p that targeted p.  Instead of a
+// global N-entry head table (random L2/DRAM atomics, a memset per plan):
+//   sort     each 32K-step chunk orders its steps by 8K-position bucket in
+//            shared memory and writes the block back contiguously (full
+//            sectors), with the per-bucket segment offsets;
+//   resolve  one CTA per bucket gathers the bucket's segment from every chunk
+//            into shared memory, builds the position lists there (int16
+//            links) and answers all of the bucket's queries.  A step whose
+//            target no earlier step wrote outputs the target itself -- a
+//            position of the bucket -- so its membership bit is set in the
+//            bucket's shared bitmap, which is then stored whole (no global
+//            atomics, no pre-zeroed bitmap); the ~12% of steps whose target
+//            was already written go to a chain list;
+//   chain    value at j_s before step s = the value an earlier step t moved
+//            there = the value at i_t = N-1-t before step t, recursively
+//            through the tail-position answers.
+// Every answer is a maximum, so no stage needs a stable order.
+constexpr int kBBits = 13;
+constexpr int kBSize = 1 << kBBits;          // positions per bucket
+constexpr int kBWords = kBSize / 32;
+constexpr int kBMaxBuckets = 4096;           // N <= 2^25 on the bucket path
+constexpr int kBChunk = 32768;               // steps per sort CTA
+constexpr int kBSortThreads = 1024;
+constexpr int kBSortPer = kBChunk / kBSortThreads;
+constexpr int kBResThreads = 512;
+constexpr int kBCap = 4096;                  // entries per resolve pass (several passes if a bucket holds more)
+constexpr int kBMaxChunks = (1 << 25) / kBChunk;
+constexpr int kOutPerThread = 8;
+constexpr int kOutPerBlock = kOutPerThread * kStepThreads;
+
+struct BSortSmem {
+    int32_t hist[kBMaxBuckets + 1];
+    int32_t warp_tmp[33];
+    uint16_t st_s[kBChunk];
+    int32_t st_j[kBChunk];
+};
+
+constexpr int kBSub = 64;                    // position sub-ranges for sizing multi-pass resolves
+constexpr int kBStage = 1024;                // chain-list entries staged per CTA
+struct BResSmem {
+    int32_t head[kBSize];              // list heads; then the tail-position answers
+    uint32_t bits[kBWords];
+    int32_t ls[kBCap];                 // step of entry e
+    int16_t nx[kBCap];                 // list link
+    int16_t lp[kBCap];                 // position (in the bucket) of entry e; single pass: first the chunk of entry e
+    union {
+        struct {
+            int32_t segoff[kBMaxChunks + 1];   // entry prefix per sort chunk (+ total)
+            int32_t segstart[kBMaxChunks];     // global start of the bucket's segment in each chunk
+        } g;
+        struct {
+            int32_t cs[kBStage], ct[kBStage];  // staged chain entries (step, pred), after the gather
+        } c;
+    } u;
+    int32_t sub[kBSub + 1];            // entries per sub-range, then pass boundaries
+    int32_t warp_tmp[33];
+    int32_t fill, err, npass, nchain, chain_base;
+};
+
+// CTA -> plan: the host table gives the plan holding CTA (64 g) for every group
+// g of 64 CTAs; a short forward scan skips the plans that start inside the
+// group (zero-width ranges of the other path included).
+constexpr int kLutShift = 6;
+struct PlanLut {
+    const int32_t *sort, *bucket, *chain;
+};
+
+__device__ __forceinline__ int64_t plan_off(const PlanDev &P, int which) {
+    return which == 0 ? P.chunk0 : which == 1 ? P.bucket0 : P.oblock0;
+}
+
+__device__ __forceinline__ int find_plan_by(const PlanDev *plans, int n, const int32_t *lut, int64_t blk,
+                                            int which) {
+    int p = lut[blk >> kLutShift];
+    while (p + 1 < n && plan_off(plans[p + 1], which) <= blk) ++p;
+    return p;
+}
+
+// in-place exclusive scan of a[0..n) in shared memory by the whole block; returns the total
+__device__ int32_t block_exclusive_scan(int32_t *a, int n, int32_t *warp_tmp) {
+    const int T = blockDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = (n + T - 1) / T;
+    const int i0 = min(n, threadIdx.x * per), i1 = min(n, i0 + per);
+    int32_t sum = 0;
+    for (int i = i0; i < i1; ++i) sum += a[i];
+    int32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) warp_tmp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = T / 32;
+        int32_t v = lane < nw ? warp_tmp[lane] : 0, x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane < nw) warp_tmp[lane] = x - v;
+        if (lane == 31) warp_tmp[32] = x;   // the total
+    }
+    __syncthreads();
+    int32_t run = warp_tmp[warp] + inc - sum;
+    const int32_t total = warp_tmp[32];
+    for (int i = i0; i < i1; ++i) {
+        const int32_t v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    __syncthreads();
+    return total;
+}
+
+__global__ void __launch_bounds__(kBSortThreads) k_bucket_sort(const PlanDev *plans, int n_plans, PlanLut lut) {
+    extern __shared__ __align__(16) unsigned char bsm_raw[];
+    BSortSmem &sm = *reinterpret_cast<BSortSmem *>(bsm_raw);
+    const PlanDev &P = plans[find_plan_by(plans, n_plans, lut.sort, blockIdx.x, 0)];
+    const int c = (int)(blockIdx.x - P.chunk0);
+    const int nb = P.nb;
+    const int64_t c0 = (int64_t)c * kBChunk;
+    const int len = (int)min((int64_t)kBChunk, P.count - c0);
+    for (int b = threadIdx.x; b <= nb; b += kBSortThreads) sm.hist[b] = 0;
+    __syncthreads();
+    int32_t j[kBSortPer];
+#pragma unroll
+    for (int k = 0; k < kBSortPer; ++k) {
+        const int i = threadIdx.x + k * kBSortThreads;
+        j[k] = i < len ? P.rv[c0 + i] : -1;
+        if (j[k] >= 0) atomicAdd(&sm.hist[j[k] >> kBBits], 1);
+    }
+    __syncthreads();
+    block_exclusive_scan(sm.hist, nb + 1, sm.warp_tmp);
+    int32_t *seg = P.segoff + (int64_t)c * (nb + 1);
+    for (int b = threadIdx.x; b <= nb; b += kBSortThreads) seg[b] = sm.hist[b];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBSortPer; ++k) {
+        if (j[k] < 0) continue;
+        const int slot = atomicAdd(&sm.hist[j[k] >> kBBits], 1);
+        sm.st_s[slot] = (uint16_t)(threadIdx.x + k * kBSortThreads);
+        sm.st_j[slot] = j[k];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += kBSortThreads) {
+        P.lst_s[c0 + i] = (int32_t)(c0 + sm.st_s[i]);
+        P.lst_j[c0 + i] = sm.st_j[i];
+    }
+}
+
+__global__ void __launch_bounds__(kBResThreads, 3) k_bucket_resolve(const PlanDev *plans, int n_plans,
+                                                                    PlanLut lut, int32_t *status) {
+    extern __shared__ __align__(16) unsigned char brm_raw[];
+    BResSmem &sm = *reinterpret_cast<BResSmem *>(brm_raw);
+    const int pi = find_plan_by(plans, n_plans, lut.bucket, blockIdx.x, 1);
+    const PlanDev &P = plans[pi];
+    const int b = (int)(blockIdx.x - P.bucket0);
+    const int nb = P.nb, nch = P.nch;
+    const int64_t N = P.n_elems, count = P.count, z0 = N - count;
+    const int64_t pbase = (int64_t)b << kBBits;
+    const int64_t lim0 = N - 1 - pbase;   // position pbase + l is the i of step lim0 - l
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int32_t *segoff = sm.u.g.segoff, *segstart = sm.u.g.segstart;
+    for (int c = tid; c < nch; c += kBResThreads) {
+        const int32_t *row = P.segoff + (int64_t)c * (nb + 1);
+        const int32_t r0 = row[b];
+        segstart[c] = c * kBChunk + r0;
+        segoff[c] = row[b + 1] - r0;
+    }
+    for (int i = tid; i < kBWords; i += kBResThreads) sm.bits[i] = 0u;
+    for (int i = tid; i <= kBSub; i += kBResThreads) sm.sub[i] = 0;
+    if (tid == 0) { sm.err = 0; sm.npass = 1; sm.nchain = 0; }
+    __syncthreads();
+    const int32_t n = block_exclusive_scan(segoff, nch, sm.warp_tmp);
+    if (tid == 0) segoff[nch] = n;
+    // entry k of the bucket lives in chunk c (last segoff <= k), at segstart[c] + k - segoff[c]
+    auto chunk_of = [&](int32_t k) -> int {
+        int lo = 0, hi = nch - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (segoff[mid] <= k) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    };
+    const bool multi = n > kBCap;
+    __syncthreads();
+    if (multi) {
+        // size the passes from a 64-bin position histogram (a 128-position bin holds at most
+        // ~21 entries per position, far below kBCap), greedily filling each pass to kBCap
+        for (int32_t k = tid; k < n; k += kBResThreads) {
+            const int c = chunk_of(k);
+            atomicAdd(&sm.sub[(P.lst_j[segstart[c] + k - segoff[c]] & (kBSize - 1)) / (kBSize / kBSub)], 1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int np = 0, acc = 0;
+            int bounds[kBSub + 1];
+            bounds[0] = 0;
+            for (int i = 0; i < kBSub; ++i) {
+                if (acc + sm.sub[i] > kBCap && acc > 0) { bounds[++np] = i; acc = 0; }
+                acc += sm.sub[i];
+            }
+            bounds[++np] = kBSub;
+            for (int i = 0; i <= np; ++i) sm.sub[i] = bounds[i] * (kBSize / kBSub);
+            sm.npass = np;
+        }
+    } else {
+        // single pass: expand the segments into a per-entry chunk table (lp doubles as it)
+        for (int c = warp; c < nch; c += kBResThreads / 32)
+            for (int32_t k = segoff[c] + lane; k < segoff[c + 1]; k += 32) sm.lp[k] = (int16_t)c;
+        if (tid == 0) { sm.sub[0] = 0; sm.sub[1] = kBSize; }
+    }
+    __syncthreads();
+    const int npass = sm.npass;
+    for (int ps = 0; ps < npass; ++ps) {
+        const int plo = sm.sub[ps], phi = sm.sub[ps + 1];
+        for (int i = plo + tid; i < phi; i += kBResThreads) sm.head[i] = -1;
+        if (tid == 0) sm.fill = 0;
+        __syncthreads();
+        for (int32_t k = tid; k < n; k += kBResThreads) {
+            const int c = multi ? chunk_of(k) : sm.lp[k];
+            const int32_t g = segstart[c] + (k - segoff[c]);
+            const int32_t jj = P.lst_j[g], ss = P.lst_s[g];
+            const int l = jj & (kBSize - 1);
+            const bool mine = l >= plo && l < phi;
+            int e = k;
+            if (multi) {
+                const unsigned act = __activemask();
+                const unsigned want = __ballot_sync(act, mine);
+                const int leader = __ffs(act) - 1;
+                int base = 0;
+                if (lane == leader) base = atomicAdd(&sm.fill, __popc(want));
+                base = __shfl_sync(act, base, leader);
+                e = base + __popc(want & ((1u << lane) - 1u));
+            }
+            if (!mine) continue;
+            if (e >= kBCap) { sm.err = 1; continue; }
+            sm.ls[e] = ss;
+            sm.lp[e] = (int16_t)l;
+            sm.nx[e] = (int16_t)atomicExch(&sm.head[l], e);
+        }
+        __syncthreads();
+        const int fill = multi ? min(sm.fill, kBCap) : n;
+        for (int e = tid; e < fill; e += kBResThreads) {
+            const int32_t s = sm.ls[e];
+            const int l = sm.lp[e];
+            int32_t best = -1;
+            for (int x = sm.head[l]; x >= 0; x = sm.nx[x]) {
+                const int32_t t = sm.ls[x];
+                if (t < s && t > best) best = t;
+            }
+            if (best < 0) {
+                // nothing wrote the target before step s: the step outputs it
+                atomicOr(&sm.bits[l >> 5], 1u << (l & 31));
+                if (P.full_idx || s == count - 1) P.idx[count - 1 - s] = (int32_t)(pbase + l);
+            } else {
+                // chain-list entry: staged in shared memory (the segment tables are dead in a single pass)
+                const int i = multi ? kBStage : atomicAdd(&sm.nchain, 1);
+                if (i < kBStage) {
+                    sm.u.c.cs[i] = s;
+                    sm.u.c.ct[i] = best;
+                } else {
+                    const int32_t slot = atomicAdd(P.nchain, 1);
+                    P.rv[slot] = s;      // rv is free once the sort has read it
+                    P.pred[slot] = best;
+                }
+            }
+        }
+        __syncthreads();
+        if (!multi) {
+            const int staged = min(sm.nchain, kBStage);
+            if (tid == 0) sm.chain_base = staged ? atomicAdd(P.nchain, staged) : 0;
+            __syncthreads();
+            for (int i = tid; i < staged; i += kBResThreads) {
+                P.rv[sm.chain_base + i] = sm.u.c.cs[i];
+                P.pred[sm.chain_base + i] = sm.u.c.ct[i];
+            }
+        }
+        // tail positions of this range: the latest step before the position's own step that wrote it
+        // (the head array is reused for the answers)
+        const int64_t q0 = max(pbase + plo, z0), q1 = min(pbase + phi, N);
+        if (q0 < q1) {
+            for (int i = plo + tid; i < phi; i += kBResThreads) sm.head[i] = -1;
+            __syncthreads();
+            for (int e = tid; e < fill; e += kBResThreads) {
+                const int l = sm.lp[e];
+                const int32_t s = sm.ls[e];
+                if (pbase + l >= z0 && s < lim0 - l) atomicMax(&sm.head[l], s);
+            }
+            __syncthreads();
+            for (int64_t pos = q0 + tid; pos < q1; pos += kBResThreads) P.wtail[pos - z0] = sm.head[pos - pbase];
+        }
+        __syncthreads();
+    }
+    if (P.bitmap) {
+        const int64_t w0 = (int64_t)b * kBWords;
+        const int nw = (int)min((int64_t)kBWords, (N + 31) / 32 - w0);
+        for (int i = tid; i < nw; i += kBResThreads) P.bitmap[w0 + i] = sm.bits[i];
+    }
+    if (tid == 0 && sm.err) atomicOr(status + pi, EDGC_ECAPACITY);
+}
+
+__global__ void __launch_bounds__(kStepThreads) k_bucket_chain(const PlanDev *plans, int n_plans, PlanLut lut) {
+    const PlanDev &P = plans[find_plan_by(plans, n_plans, lut.chain, blockIdx.x, 2)];
+    const int64_t N = P.n_elems, count = P.count, z0 = N - count;
+    const int64_t e_base = (int64_t)(blockIdx.x - P.oblock0) * kOutPerBlock + threadIdx.x;
+    const int64_t nch = *P.nchain;
+    for (int k = 0; k < kOutPerThread; ++k) {
+        const int64_t e = e_base + (int64_t)k * kStepThreads;
+        if (e >= nch) break;
+        const int32_t s = P.rv[e];
+        int32_t t = P.pred[e], outv = 0;
+        while (true) {
+            const int32_t pos = (int32_t)(N - 1 - t);
+            const int32_t t2 = P.wtail[pos - z0];
+            if (t2 < 0) { outv = pos; break; }
+            t = t2;
+        }
+        if (P.full_idx || s == count - 1) P.idx[count - 1 - s] = outv;
         if (P.bitmap) atomicOr(P.bitmap + (outv >> 5), 1u << (outv & 31));
     }
 }
@@ -351,9 +693,15 @@ struct PlanLayout {
     std::vector<PlanDev> dev;
     int64_t ws_bytes = 0;
     int64_t draw_chunks = 0, step_blocks = 0;
+    int64_t bchunks = 0, buckets = 0, oblocks = 0;   // bucket path (plans with bucketed = 1)
+    int32_t *nchains = nullptr;                       // all bucket plans' chain counters (zeroed per call)
+    std::vector<int32_t> lut_host;                    // [sort | bucket | chain] CTA-group -> plan tables
+    int64_t lut_n[3] = {0, 0, 0};
+    int32_t *lut_dev = nullptr;
+    int n_bucketed = 0;
     int64_t table_bytes = 0;
     char *table_base = nullptr;
-    std::vector<int64_t> table_off;   // per plan, relative to table_base (plan tables are contiguous)
+    std::vector<int64_t> table_off;   // head-table plans, relative to table_base (contiguous)
 };
 
 int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes, PlanLayout &L) {
@@ -362,7 +710,7 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
     PlanDev *descs_dev = a.take<PlanDev>(n);
     (void)descs_dev;
     int64_t chunk = 0, blocks = 0;
-
+    static const bool no_bucket = std::getenv("EDGC_PLAN_HEADTABLE") != nullptr;
     for (int i = 0; i < n; ++i) {
         const edgc_plan_desc &d = plans[i];
         EDGC_REQUIRE(d.n_elems >= 2 && d.n_elems < (int64_t(1) << 31), "plan %d: N=%lld outside [2, 2^31)", i,
@@ -370,13 +718,16 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
         EDGC_REQUIRE(d.count >= 1 && d.count < d.n_elems, "plan %d: count=%lld must be in [1, N)", i,
                      (long long)d.count);
         PlanDev &P = L.dev[i];
+        P = PlanDev{};
         P.state = (((u128)d.state_hi) << 64) | d.state_lo;
         P.inc = (((u128)d.inc_hi) << 64) | d.inc_lo;
         P.n_elems = d.n_elems;
         P.count = d.count;
         P.idx = d.idx;
         P.bitmap = d.bitmap;
+        P.full_idx = (d.flags & EDGC_PLAN_BITMAP_ONLY) ? 0 : 1;
         P.tail = (d.n_elems > 10000 && d.count > d.n_elems / 20) ? 1 : 0;
+        P.bucketed = (!no_bucket && P.tail && ceil_div(d.n_elems, kBSize) <= kBMaxBuckets) ? 1 : 0;
         // expected rejections ~ count * N / 2^33 (threshold ~ uniform below rng+1)
         const double lam = (double)d.count * (double)d.n_elems / 4294967296.0;
         int64_t slack = (int64_t)(2.0 * lam + 16.0 * std::sqrt(lam + 1.0)) + 4096;
@@ -387,23 +738,62 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
         chunk += ceil_div(nd / 2, kDrawsPerBlock);
         P.step_block0 = blocks;
         blocks += ceil_div(d.count, kStepThreads);
-
     }
-    // round the P1 chunk index up so blocks never straddle more than needed
     L.draw_chunks = chunk;
     L.step_blocks = blocks;
     for (int i = 0; i < n; ++i) {
         PlanDev &P = L.dev[i];
         P.draws = a.take<uint32_t>(P.n_draws);
         P.rv = a.take<int32_t>(P.count);
-        P.next = a.take<int32_t>(P.count);
+        if (!P.bucketed) {
+            // zero-width ranges at the running offsets keep the CTA -> plan searches monotone
+            P.chunk0 = L.bchunks;
+            P.bucket0 = L.buckets;
+            P.oblock0 = L.oblocks;
+            P.next = a.take<int32_t>(P.count);
+            continue;
+        }
+        P.nb = (int32_t)ceil_div(P.n_elems, kBSize);
+        P.nch = (int32_t)ceil_div(P.count, kBChunk);
+        P.lst_s = a.take<int32_t>(P.count);
+        P.lst_j = a.take<int32_t>(P.count);
+        P.segoff = a.take<int32_t>((int64_t)P.nch * (P.nb + 1));
+        P.pred = a.take<int32_t>(P.count);
+        P.wtail = a.take<int32_t>(P.count);
+        P.chunk0 = L.bchunks;
+        L.bchunks += P.nch;
+        P.bucket0 = L.buckets;
+        L.buckets += P.nb;
+        P.oblock0 = L.oblocks;
+        L.oblocks += ceil_div(P.count, kOutPerBlock);
+        ++L.n_bucketed;
+    }
+    // CTA-group -> plan tables (largest plan whose range starts at or before the group's first CTA)
+    const int64_t tot[3] = {L.bchunks, L.buckets, L.oblocks};
+    L.lut_host.clear();
+    for (int w = 0; w < 3; ++w) {
+        L.lut_n[w] = (tot[w] >> kLutShift) + 1;
+        int p = 0;
+        for (int64_t g = 0; g < L.lut_n[w]; ++g) {
+            const int64_t blk = g << kLutShift;
+            auto off = [&](int q) { return w == 0 ? L.dev[q].chunk0 : w == 1 ? L.dev[q].bucket0 : L.dev[q].oblock0; };
+            while (p + 1 < n && off(p + 1) <= blk) ++p;
+            L.lut_host.push_back(p);
+        }
     }
     a.off = align256(a.off);
+    L.lut_dev = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
+    a.off += align256(4 * (int64_t)L.lut_host.size());
+    L.nchains = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
+    for (int i = 0; i < n; ++i)
+        if (L.dev[i].bucketed) L.dev[i].nchain = L.nchains + i;
+    a.off += align256(4 * (int64_t)n);
     const int64_t t0 = a.off;
     L.table_off.assign(n + 1, 0);
     for (int i = 0; i < n; ++i) {
         PlanDev &P = L.dev[i];
         L.table_off[i] = a.off - t0;
+        if (P.bucketed) continue;
         P.head = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
         a.off += align256(P.n_elems * 4);
     }
@@ -444,6 +834,9 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
                                 int64_t ws_bytes, void *stream) {
     if (n_plans == 0) return EDGC_OK;
     EDGC_REQUIRE(n_plans > 0 && plans && status_dev, "edgc_sample_plan: bad arguments");
+    for (int i = 0; i < n_plans; ++i)
+        EDGC_REQUIRE(plans[i].idx && (!(plans[i].flags & EDGC_PLAN_BITMAP_ONLY) || plans[i].bitmap),
+                     "plan %d: idx is required, and a bitmap with EDGC_PLAN_BITMAP_ONLY", i);
     PlanLayout L;
     int rc = layout_plans(plans, n_plans, ws, ws_bytes, L);
     if (rc != EDGC_OK) return rc;
@@ -462,14 +855,38 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
     }
     k_walk<<<n_plans, kWT, kRing * sizeof(uint32_t), st>>>(d_plans, status_dev);
     EDGC_LAUNCH_CHECK();
-    // index + resolve plan groups whose hash tables, links and bounded values
-    // fit in L2 together, so the random table traffic stays on chip
+    if (L.n_bucketed) {
+        // bucket path (tail-shuffle plans); plans are ordered, so each kernel's CTA range covers
+        // only the bucketed plans' chunks / buckets / chain blocks
+        static bool battr = false;
+        if (!battr) {
+            EDGC_CUDA_TRY(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sizeof(BSortSmem)));
+            EDGC_CUDA_TRY(cudaFuncSetAttribute(k_bucket_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sizeof(BResSmem)));
+            battr = true;
+        }
+        EDGC_CUDA_TRY(cudaMemsetAsync(L.nchains, 0, 4 * (size_t)n_plans, st));
+        EDGC_CUDA_TRY(cudaMemcpyAsync(L.lut_dev, L.lut_host.data(), 4 * L.lut_host.size(), cudaMemcpyHostToDevice,
+                                      st));
+        const PlanLut lut{L.lut_dev, L.lut_dev + L.lut_n[0], L.lut_dev + L.lut_n[0] + L.lut_n[1]};
+        k_bucket_sort<<<(unsigned)L.bchunks, kBSortThreads, sizeof(BSortSmem), st>>>(d_plans, n_plans, lut);
+        EDGC_LAUNCH_CHECK();
+        k_bucket_resolve<<<(unsigned)L.buckets, kBResThreads, sizeof(BResSmem), st>>>(d_plans, n_plans, lut,
+                                                                                      status_dev);
+        EDGC_LAUNCH_CHECK();
+        k_bucket_chain<<<(unsigned)L.oblocks, kStepThreads, 0, st>>>(d_plans, n_plans, lut);
+        EDGC_LAUNCH_CHECK();
+    }
+    // head-table path (Floyd plans, N > 2^25, or EDGC_PLAN_HEADTABLE): index + resolve groups of
+    // consecutive such plans whose tables, links and bounded values fit in L2 together
     const int64_t kGroupBytes = 48ll << 20;
     int p0 = 0;
     while (p0 < n_plans) {
+        if (L.dev[p0].bucketed) { ++p0; continue; }
         int p1 = p0 + 1;
         int64_t bytes = (L.table_off[p0 + 1] - L.table_off[p0]) + 8 * L.dev[p0].count;
-        while (p1 < n_plans) {
+        while (p1 < n_plans && !L.dev[p1].bucketed) {
             const int64_t more = (L.table_off[p1 + 1] - L.table_off[p1]) + 8 * L.dev[p1].count;
             if (bytes + more > kGroupBytes) break;
             bytes += more;

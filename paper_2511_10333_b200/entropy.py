@@ -93,7 +93,8 @@ def sample_count(n_elems: int, beta: float) -> int:
     return min(n_elems, math.ceil(beta * n_elems))
 
 
-def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, workspace=None, check: bool = True):
+def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, workspace=None, check: bool = True,
+                 indices: bool = True):
     """Device index plans for many (n_elems, count, seed) at once.
 
     Returns a list of int32 CUDA tensors (None where count == n_elems, i.e. the
@@ -102,8 +103,12 @@ def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, work
     bit e set iff element e is sampled.  ``stream`` / ``workspace`` let the
     tracker build the next sampled iteration's plans on a side stream;
     ``check=False`` skips the synchronising status check (the caller checks
-    ``status`` later).
+    ``status`` later).  ``indices=False`` (with ``bitmaps``) builds only the
+    membership sets: each returned index tensor then holds just the first
+    sample (the Gaussian estimator's shift).
     """
+    if not indices and not bitmaps:
+        raise ValueError("indices=False needs bitmaps=True")
     L = _lib.lib()
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     st = torch.cuda.current_stream(dev) if stream is None else stream
@@ -117,15 +122,29 @@ def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, work
                 continue
             if n_elems >= 2**31:
                 raise ValueError(f"sampling over {n_elems} >= 2^31 elements is outside the device plan's range")
-            out[i] = torch.empty(count, dtype=torch.int32, device=dev)
-            if bitmaps:
-                bms[i] = torch.zeros((n_elems + 31) // 32, dtype=torch.int32, device=dev)
             todo.append(i)
+        # one index buffer and one (zeroed) bitmap buffer for all plans: two allocations and one
+        # fill instead of one per plan; slices start on 256-byte boundaries
+        pad = lambda x: (x + 63) // 64 * 64
+        n_out = (lambda c: c) if indices else (lambda c: 1)
+        o_all = torch.empty(max(1, sum(pad(n_out(specs[i][1])) for i in todo)), dtype=torch.int32, device=dev)
+        b_all = (torch.zeros(max(1, sum(pad((specs[i][0] + 31) // 32) for i in todo)), dtype=torch.int32, device=dev)
+                 if bitmaps else None)
+        oo = bo = 0
+        for i in todo:
+            n_elems, count, _ = specs[i]
+            out[i] = o_all[oo:oo + n_out(count)]
+            oo += pad(n_out(count))
+            if bitmaps:
+                words = (n_elems + 31) // 32
+                bms[i] = b_all[bo:bo + words]
+                bo += pad(words)
         cap_bytes = _plan_ws_cap(dev)
         descs, sizes = {}, {}
         for i in todo:
             n_elems, count, seed = specs[i]
-            descs[i] = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]), _lib.ptr(bms[i]))
+            descs[i] = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]), _lib.ptr(bms[i]),
+                                     0 if indices else _lib.PLAN_BITMAP_ONLY)
             sizes[i] = L.edgc_sample_plan_workspace_bytes((_lib.PlanDesc * 1)(descs[i]), 1) + 4096
         status_all = torch.zeros(max(1, len(todo)), dtype=torch.int32, device=dev)
         k = 0
@@ -143,11 +162,20 @@ def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, work
             status = status_all[k - len(batch):k]
             _lib.check(L.edgc_sample_plan(arr, len(batch), _lib.ptr(status), _lib.ptr(ws), ws.numel(),
                                           st.cuda_stream), "edgc_sample_plan")
-    if check and todo and int(status_all.max().item()) != 0:
-        raise RuntimeError("sample plan exhausted its pre-generated draws")
+    if check and todo:
+        _raise_plan_status(status_all)
     if bitmaps:
         return out, bms, status_all
     return out
+
+
+def _raise_plan_status(status) -> None:
+    code = int(status.max().item())
+    if code == 0:
+        return
+    if code & _lib.EDGC_EDRAWS:
+        raise RuntimeError("sample plan exhausted its pre-generated draws")
+    raise RuntimeError(f"sample plan failed on the device (status {code})")
 
 
 def sample_indices(n_elems: int, beta: float, seed: int, device=None) -> torch.Tensor:
@@ -218,8 +246,8 @@ def _gaussian_launch(items, dtype_code: int, device):
 def _gaussian_collect(h, status, plan_status=None) -> list:
     h_host = h.cpu().tolist()
     st_host = status.cpu().tolist()
-    if plan_status is not None and int(plan_status.max().item()) != 0:
-        raise RuntimeError("sample plan exhausted its pre-generated draws")
+    if plan_status is not None:
+        _raise_plan_status(plan_status)
     for code in st_host:
         if code == _lib.EDGC_EINVAL:
             raise ValueError("need at least 2 samples")
@@ -350,7 +378,7 @@ def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=N
         if prefetched is not None and prefetched[0] == specs:
             _, plans, bms, status = prefetched
         else:
-            plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False)
+            plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False, indices=False)
         items = [(f, p, c) if p is None else (f, p, c, bm) for f, p, bm, (_, c, _) in zip(flats, plans, bms, specs)]
         h, hstat = _gaussian_launch(items, 0, dev)
         if deferred:
@@ -415,7 +443,7 @@ class EntropyTracker:
         if any(c < 2 for _, c, _ in specs):
             return
         plans, bms, status = sample_plans(specs, dev, bitmaps=True, stream=self._pf_stream,
-                                          workspace=self._pf_ws, check=False)
+                                          workspace=self._pf_ws, check=False, indices=False)
         ev = torch.cuda.Event()
         ev.record(self._pf_stream)
         self._pf[iteration] = (specs, plans, bms, status, ev)

@@ -76,3 +76,28 @@ def test_native_library_is_loaded():
     import paper_2511_10333_b200._lib as L
     L.lib()
     assert L._lib is not None and torch.cuda.is_available()
+
+
+@pytest.mark.parametrize("indices", [True, False])
+def test_membership_bitmaps_match_oracle_sets(indices):
+    """Membership bitmaps (full plans and EDGC_PLAN_BITMAP_ONLY plans) equal the oracle's
+    sampled sets; bitmap-only plans still return the first sample (the Gaussian shift).
+    Includes a matrix spanning many 16K-position buckets and Floyd / tail branches."""
+    from paper_2511_10333_b200.entropy import sample_count, sample_plans
+    specs = [(n, sample_count(n, b), s) for n, b, s in [
+        (14_745_600, 0.25, 3), (3_686_400, 0.25, 11), (1_000_000, 0.05, 2), (20_000, 0.999, 5),
+        (9_999, 0.5, 1), (65_537, 0.051, 4), (100, 0.3, 9)]]
+    plans, bms, status = sample_plans(specs, bitmaps=True, indices=indices)
+    assert int(status.max()) == 0
+    for (n, c, seed), p, bm in zip(specs, plans, bms):
+        ref = oracle.choice_indices(seed, n, c)
+        words = to_np(bm).astype(np.uint32)
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:n]
+        want = np.zeros(n, dtype=np.uint8)
+        want[ref] = 1
+        assert np.array_equal(bits, want), (n, c, seed)
+        got = to_np(p).astype(np.int64)
+        if indices:
+            assert np.array_equal(got, ref)
+        else:
+            assert got.size == 1 and got[0] == ref[0]

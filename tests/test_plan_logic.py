@@ -23,7 +23,8 @@ def lemire(x, rng):
     return left >= thr, val
 
 
-def emulate(seed, n_elems, count, window=64):
+def walk(seed, n_elems, count, window=64):
+    """k_walk: bounded value of every step (speculative shifts, first-rejection windows)."""
     tail = n_elems > 10000 and count > n_elems // 20
     draws = oracle.pcg64_u32(seed, count + 4096 + 2 * count).astype(np.int64)
     step_rng = (lambda s: n_elems - 1 - s) if tail else (lambda s: n_elems - count + s)
@@ -54,6 +55,11 @@ def emulate(seed, n_elems, count, window=64):
             rv[s + lane] = vals[sh][lane]
         s += length
         u += length + len(events)
+    return rv, tail
+
+
+def emulate(seed, n_elems, count, window=64):
+    rv, tail = walk(seed, n_elems, count, window)
     lists = {}                            # k_index (hash lists)
     for st in range(count):
         lists.setdefault(rv[st], []).append(st)
@@ -102,3 +108,67 @@ def test_plan_algorithm_matches_numpy(n_elems, beta, seed, window):
         pytest.skip("copy branch")
     ref = np.random.default_rng(seed).choice(n_elems, size=count, replace=False, shuffle=False)
     assert np.array_equal(emulate(seed, n_elems, count, window), ref)
+
+
+def resolve_buckets(rv, n_elems, count, tail, bbits, order_seed=0):
+    """k_bucket_hist / k_bucket_scan / k_bucket_resolve / k_bucket_out with 2^bbits-position
+    buckets; the scatter order inside a bucket is deliberately shuffled (the device's is
+    arbitrary)."""
+    nb = -(-n_elems // (1 << bbits))
+    buckets = [[] for _ in range(nb)]
+    order = np.random.default_rng(order_seed).permutation(count)
+    for st in order:                      # histogram + scatter (any order)
+        buckets[rv[st] >> bbits].append(st)
+    pred = [-1] * count
+    z0 = n_elems - count
+    wtail = [-1] * count
+    for b, steps in enumerate(buckets):   # one CTA per bucket
+        head = {}
+        for st in steps:
+            head.setdefault(rv[st], []).append(st)
+        for st in steps:
+            c = [t for t in head[rv[st]] if t < st]
+            pred[st] = max(c) if c else -1
+        if tail:
+            for pos in range(max(b << bbits, z0), min((b + 1) << bbits, n_elems)):
+                lim = n_elems - 1 - pos
+                c = [t for t in head.get(pos, []) if t < lim]
+                wtail[pos - z0] = max(c) if c else -1
+    out = [0] * count                     # k_bucket_out
+    base = n_elems - count
+    for st in range(count):
+        if tail:
+            t, val = pred[st], rv[st]
+            while t >= 0:
+                pos = n_elems - 1 - t
+                t2 = wtail[pos - z0]
+                if t2 < 0:
+                    val = pos
+                    break
+                t = t2
+            out[count - 1 - st] = val
+        else:
+            cur, collide = st, False
+            while True:
+                if pred[cur] >= 0:
+                    collide = True
+                    break
+                v = rv[cur]
+                if v < base or v - base >= cur:
+                    break
+                cur = v - base
+            out[st] = base + st if collide else rv[st]
+    return np.asarray(out, dtype=np.int64)
+
+
+@pytest.mark.parametrize("bbits", [3, 14])
+@pytest.mark.parametrize("n_elems,beta,seed", [
+    (100, 0.5, 3), (101, 0.9, 1), (4096, 0.25, 1), (10000, 0.5, 4), (10001, 0.06, 4), (12000, 0.25, 5),
+    (20000, 0.05, 9), (20000, 0.0501, 11), (40000, 0.999, 2), (7, 0.3, 5), (2, 0.5, 0), (300, 0.99, 8)])
+def test_bucketed_resolve_matches_numpy(n_elems, beta, seed, bbits):
+    count = min(n_elems, math.ceil(beta * n_elems))
+    if count == n_elems:
+        pytest.skip("copy branch")
+    ref = np.random.default_rng(seed).choice(n_elems, size=count, replace=False, shuffle=False)
+    rv, tail = walk(seed, n_elems, count)
+    assert np.array_equal(resolve_buckets(rv, n_elems, count, tail, bbits, order_seed=seed), ref)
