@@ -112,7 +112,7 @@ __device__ __forceinline__ int find_plan(const PlanDev *plans, int n, int64_t bl
 // produces outputs t, t+256, t+512, ... of that range (one jump-ahead, then a
 // 256-step affine LCG map per output), so every warp store is coalesced.
 __global__ void __launch_bounds__(kP1Threads) k_draws(const PlanDev *plans, int n_plans) {
-    const PlanDev &P = plans[find_plan(plans, n_plans, blockIdx.x, true)];
+    const PlanDev P = plans[find_plan(plans, n_plans, blockIdx.x, true)];
     const int64_t o_base = (int64_t)(blockIdx.x - P.draw_chunk0) * kDrawsPerBlock;
     const int64_t n64 = P.n_draws / 2;
     if (o_base >= n64) return;
@@ -141,154 +141,239 @@ __device__ __forceinline__ bool lemire_accept(uint32_t x, uint32_t rng, uint32_t
     return left >= thr;
 }
 
+// 2^32 mod excl (NumPy's Lemire threshold (2^32 - excl) % excl), excl >= 1.  For
+// excl >= 2^16 the quotient is < 2^16, so a float reciprocal estimate is within
+// +-2 of it and two exact corrections finish; smaller excl take the division.
+__device__ __forceinline__ uint32_t lemire_threshold(uint32_t excl) {
+    if (excl < 65536u) return (0u - excl) % excl;
+    const uint32_t q = (uint32_t)(4294967296.0f * __frcp_rn((float)excl));
+    int64_t r = (int64_t)4294967296ll - (int64_t)q * (int64_t)excl;
+    r += (r < 0) ? (int64_t)excl : 0;
+    r += (r < 0) ? (int64_t)excl : 0;
+    r -= (r >= (int64_t)excl) ? (int64_t)excl : 0;
+    r -= (r >= (int64_t)excl) ? (int64_t)excl : 0;
+    return (uint32_t)r;
+}
+
 __device__ __forceinline__ uint32_t step_rng(const PlanDev &P, int64_t s) {
     // tail: i = N-1-s (bounded(0..i)); Floyd: j = N-count+s (bounded(0..j))
     return P.tail ? (uint32_t)(P.n_elems - 1 - s) : (uint32_t)(P.n_elems - P.count + s);
 }
 
 // ---- P2: assign draws to steps --------------------------------------------
-// One CTA per plan walks windows of kWT steps.  Lane l tests its step against
-// the draws at shifts 0..kWK-1 (draw u+l+j): a Lemire rejection at lane f and
-// shift d moves every later step one draw further, so the window resolves by
-// scanning rejection events in lane order (warp 0, ballots) and accepting each
-// lane at shift #events at lanes <= l.  Up to kWK-1 rejections fit in one
-// window; rarer bursts end the window early.  The draw window lives in shared
-// memory and the next one is prefetched while the current one resolves.
-constexpr int kWT = 256;                  // threads per walk CTA
-constexpr int kWQ = 4;                    // consecutive steps per thread
+// A group of kWT threads walks one plan in windows of kWW steps.  Thread t
+// tests its kWQ consecutive steps against the draws at shifts 0..kWK-1 (draw
+// u + step + j): a Lemire rejection at step f and shift d moves every later
+// step one draw further, so the window resolves by scanning rejection events
+// in step order (one warp, ballots) and accepting each step at shift #events
+// at or before it.  Up to kWK-1 rejections fit in one window (~3.5 expected at
+// GPT-2 sizes); rarer bursts end the window early.  Draws stream into a
+// shared ring with bulk async copies.  kWG plans share a CTA (one group each,
+// named barriers), so the walk holds few SMs while it prefetches.
+constexpr int kWT = 256;                  // threads per plan group
+constexpr int kWQ = 8;                    // consecutive steps per thread
 constexpr int kWW = kWT * kWQ;            // steps per window
-constexpr int kWK = 4;                    // speculative shifts
+#ifndef EDGC_WALK_K
+#define EDGC_WALK_K 4
+#endif
+constexpr int kWK = EDGC_WALK_K;          // speculative shifts
+static_assert(kWK <= 8, "the shift switch in k_walk covers 8 shifts");
+constexpr int kWG = 4;                    // plan groups per CTA
+constexpr int kWWords = kWW / 32;         // mask words per shift
 constexpr int kRingBlk = 1024;            // draws per ring block (4 KB bulk copy)
 constexpr int kRingN = 8;                 // blocks in flight
 constexpr int kRing = kRingBlk * kRingN;  // ring size (draws), power of two
+static_assert(kWWords == 64, "event scan assumes two mask words per lane");
 
-__global__ void __launch_bounds__(kWT) k_walk(const PlanDev *plans, int32_t *status) {
-    const PlanDev &P = plans[blockIdx.x];
-    extern __shared__ __align__(128) uint32_t s_ring[];   // kRing draws (dynamic: 32 KB)
-    __shared__ uint32_t s_mask[kWK][kWW / 32];
-    __shared__ int s_ev[kWK];
-    __shared__ int s_ne, s_len, s_err;
-    __shared__ __align__(8) uint64_t s_full[kRingN];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+struct WalkGroup {
+    uint32_t ring[kRing];
+    uint32_t mask[kWK][kWWords];
+    int ev[kWK];
+    int ne, len, err;
+    alignas(8) uint64_t full[kRingN];
+};
+
+__device__ __forceinline__ void group_sync(int g) { ptx::named_bar_sync(1 + g, kWT); }
+
+__global__ void __launch_bounds__(kWT * kWG, 1) k_walk(const PlanDev *plans, int n_plans, int32_t *status) {
+    extern __shared__ __align__(128) unsigned char walk_raw[];
+    const int g = threadIdx.x / kWT;
+    const int pid = blockIdx.x * kWG + g;
+    if (pid >= n_plans) return;   // the whole group leaves; groups synchronise only among themselves
+    WalkGroup &W = reinterpret_cast<WalkGroup *>(walk_raw)[g];
+    const PlanDev P = plans[pid];
+    const int tid = threadIdx.x % kWT, lane = tid & 31, warp = tid >> 5;
     const int64_t count = P.count, nd = P.n_draws;
     const int64_t nblocks = (nd + kRingBlk - 1) / kRingBlk;
     const uint32_t tail = (uint32_t)P.tail;
     const uint32_t rng_hi = tail ? (uint32_t)(P.n_elems - 1) : (uint32_t)(P.n_elems - P.count);
     int32_t *rv = P.rv;
     const uint32_t *draws = P.draws;
-    int64_t next_blk = 0;   // first block not yet requested (thread 0)
+    int64_t next_blk = 0;   // first block not yet requested (thread 0 of the group)
     auto request = [&](int64_t upto) {
         while (next_blk < upto && next_blk < nblocks) {
             const int slot = (int)(next_blk % kRingN);
             const int64_t first = next_blk * kRingBlk;
             const uint32_t bytes = (uint32_t)(min((int64_t)kRingBlk, nd - first) * 4);
-            ptx::mbar_arrive_expect_tx(&s_full[slot], bytes);
-            ptx::bulk_g2s(&s_ring[slot * kRingBlk], draws + first, bytes, &s_full[slot]);
+            ptx::mbar_arrive_expect_tx(&W.full[slot], bytes);
+            ptx::bulk_g2s(&W.ring[slot * kRingBlk], draws + first, bytes, &W.full[slot]);
             ++next_blk;
         }
     };
     if (tid == 0) {
-        for (int i = 0; i < kRingN; ++i) ptx::mbar_init(&s_full[i], 1);
+        for (int i = 0; i < kRingN; ++i) ptx::mbar_init(&W.full[i], 1);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        s_err = 0;
+        W.err = 0;
+        request(kRingN);
     }
-    __syncthreads();
-    if (tid == 0) request(kRingN);
+    group_sync(g);
     int64_t s = 0, u = 0;
     while (s < count) {
         const int64_t b0 = u / kRingBlk;
-        for (int64_t bb = b0; bb <= b0 + 1 && bb < nblocks; ++bb)
-            ptx::mbar_wait(&s_full[bb % kRingN], (uint32_t)((bb / kRingN) & 1));
-        // this thread's steps s + 4 tid + q use draws u + 4 tid + q + j
+        for (int64_t bb = b0; bb <= b0 + 2 && bb < nblocks; ++bb)
+            ptx::mbar_wait(&W.full[bb % kRingN], (uint32_t)((bb / kRingN) & 1));
+        // this thread's steps s + kWQ tid + q use draws u + kWQ tid + q + j
         const int nvalid = (int)min((int64_t)kWW, count - s);
-        const uint32_t ubase = (uint32_t)(u & (kRing - 1)) + 4u * tid;
-        const int64_t dleft = nd - u - 4 * tid;   // draws generated from this thread's first one on
+        const uint32_t ubase = (uint32_t)(u & (kRing - 1)) + (uint32_t)(kWQ * tid);
+        const int64_t dleft = nd - u - kWQ * tid;   // draws generated from this thread's first one on
+        const bool near_end = dleft < kWQ + kWK;
         uint32_t d[kWQ + kWK - 1];
 #pragma unroll
-        for (int e = 0; e < kWQ + kWK - 1; ++e) d[e] = s_ring[(ubase + e) & (kRing - 1)];
-        uint32_t val[kWQ][kWK];
-        uint32_t nib[kWK] = {0u, 0u, 0u, 0u};
+        for (int e = 0; e < kWQ + kWK - 1; ++e) d[e] = W.ring[(ubase + e) & (kRing - 1)];
+        // speculative pass: rejection bits only (the bounded values are recomputed below for
+        // the one shift each step ends up at)
+        uint32_t byt[kWK];
+#pragma unroll
+        for (int j = 0; j < kWK; ++j) byt[j] = 0u;
 #pragma unroll
         for (int q = 0; q < kWQ; ++q) {
-            const int step = 4 * tid + q;
+            const int step = kWQ * tid + q;
             // rng of step s + step: tail i = N-1-(s+step); Floyd j = N-count+(s+step)
             const uint32_t off = (uint32_t)s + (uint32_t)step;
             const uint32_t rng = tail ? rng_hi - off : rng_hi + off;
             const uint32_t excl = rng + 1u;
+            uint32_t left[kWK];
+            bool cand = false;
 #pragma unroll
             for (int j = 0; j < kWK; ++j) {
-                const uint64_t m = (uint64_t)d[q + j] * excl;
-                val[q][j] = (uint32_t)(m >> 32);
-                bool rej = false;
-                const uint32_t left = (uint32_t)m;
-                if (left < excl) rej = left < (0xFFFFFFFFu - rng) % excl;
-                if ((int64_t)(q + j) >= dleft) rej = true;   // past the generated stream
-                if (step < nvalid && rej) nib[j] |= 1u << q;
+                left[j] = d[q + j] * excl;   // low half of the 64-bit product
+                cand |= left[j] < excl;      // necessary for a rejection (p ~ excl / 2^32)
+            }
+            if (cand) {
+                const uint32_t thr = lemire_threshold(excl);   // the step's, shared by every shift
+#pragma unroll
+                for (int j = 0; j < kWK; ++j) byt[j] |= (uint32_t)(left[j] < thr) << q;
+            }
+            if (near_end) {
+#pragma unroll
+                for (int j = 0; j < kWK; ++j)
+                    if ((int64_t)(q + j) >= dleft) byt[j] |= 1u << q;   // past the generated stream
             }
         }
-        // assemble per-shift 32-bit words: word (8 warp + lane/8) holds steps 32 w .. 32 w + 31
+        {
+            const int valid = min(kWQ, max(0, nvalid - kWQ * tid));   // steps of this thread inside the window
+            const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+#pragma unroll
+            for (int j = 0; j < kWK; ++j) byt[j] &= vm;
+        }
+        // per-shift 32-bit words: word (8 warp + lane/4) holds steps 32 w .. 32 w + 31
 #pragma unroll
         for (int j = 0; j < kWK; ++j) {
-            uint32_t wv = nib[j] << (4 * (lane & 7));
+            uint32_t wv = byt[j] << (8 * (lane & 3));
             wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
             wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
-            wv |= __shfl_xor_sync(0xffffffffu, wv, 4);
-            if ((lane & 7) == 0) s_mask[j][warp * 4 + (lane >> 3)] = wv;
+            if ((lane & 3) == 0) W.mask[j][warp * 8 + (lane >> 2)] = wv;
         }
-        __syncthreads();
+        group_sync(g);
         if (warp == 0) {
             int cur = 0, dd = 0, ne = 0, len = nvalid;
             while (true) {
-                uint32_t bits = s_mask[dd][lane];
-                const int lo = lane * 32;
-                if (lo + 32 <= cur) bits = 0u;
-                else if (lo < cur) bits &= ~((1u << (cur - lo)) - 1u);
-                const unsigned any = __ballot_sync(0xffffffffu, bits != 0u);
-                if (!any) break;
-                const int wi = __ffs(any) - 1;
-                const uint32_t wbits = __shfl_sync(0xffffffffu, bits, wi);
-                const int f = wi * 32 + __ffs(wbits) - 1;
-                if (lane == 0) s_ev[ne] = f;
+                uint32_t lo_bits = W.mask[dd][lane], hi_bits = W.mask[dd][lane + 32];
+                const int lo0 = lane * 32, hi0 = (lane + 32) * 32;
+                if (lo0 + 32 <= cur) lo_bits = 0u;
+                else if (lo0 < cur) lo_bits &= ~((1u << (cur - lo0)) - 1u);
+                if (hi0 + 32 <= cur) hi_bits = 0u;
+                else if (hi0 < cur) hi_bits &= ~((1u << (cur - hi0)) - 1u);
+                const unsigned any_lo = __ballot_sync(0xffffffffu, lo_bits != 0u);
+                const unsigned any_hi = __ballot_sync(0xffffffffu, hi_bits != 0u);
+                if (!any_lo && !any_hi) break;
+                int f;
+                if (any_lo) {
+                    const int wi = __ffs(any_lo) - 1;
+                    f = wi * 32 + __ffs(__shfl_sync(0xffffffffu, lo_bits, wi)) - 1;
+                } else {
+                    const int wi = __ffs(any_hi) - 1;
+                    f = (wi + 32) * 32 + __ffs(__shfl_sync(0xffffffffu, hi_bits, wi)) - 1;
+                }
+                if (lane == 0) W.ev[ne] = f;
                 ++ne;
                 ++dd;
                 if (dd == kWK) { len = f; break; }
                 cur = f;
             }
-            if (lane == 0) { s_ne = ne; s_len = len; }
+            if (lane == 0) { W.ne = ne; W.len = len; }
         }
-        __syncthreads();
-        const int ne = s_ne, len = s_len;
+        group_sync(g);
+        const int ne = W.ne, len = W.len;
         int ev[kWK];
 #pragma unroll
-        for (int e = 0; e < kWK; ++e) ev[e] = (e < ne) ? s_ev[e] : 0x7fffffff;
+        for (int e = 0; e < kWK; ++e) ev[e] = (e < ne) ? W.ev[e] : 0x7fffffff;
         uint32_t out[kWQ];
+        {
+            const int first = kWQ * tid, last = first + kWQ - 1;
+            int sh0 = 0;
 #pragma unroll
-        for (int q = 0; q < kWQ; ++q) {
-            const int step = 4 * tid + q;
-            int sh = 0;
+            for (int e = 0; e < kWK; ++e) sh0 += (ev[e] <= first);
+            const bool split = sh0 < kWK && ev[sh0 < kWK ? sh0 : 0] <= last;   // an event inside my steps
+            uint32_t x[kWQ];
+            if (!split) {
+                // one shift for all of this thread's steps
+                switch (sh0) {
+#define EDGC_PICK(SH) case SH: _Pragma("unroll") for (int q = 0; q < kWQ; ++q) x[q] = d[q + (SH < kWK ? SH : 0)]; break;
+                    EDGC_PICK(0) EDGC_PICK(1) EDGC_PICK(2) EDGC_PICK(3)
+                    EDGC_PICK(4) EDGC_PICK(5) EDGC_PICK(6) EDGC_PICK(7)
+#undef EDGC_PICK
+                    default:
 #pragma unroll
-            for (int e = 0; e < kWK; ++e) sh += (ev[e] <= step);
-            uint32_t v = val[q][0];
+                        for (int q = 0; q < kWQ; ++q) x[q] = d[q];   // shift kWK: steps past the window end
+                }
+            } else {
 #pragma unroll
-            for (int j = 1; j < kWK; ++j) v = (sh == j) ? val[q][j] : v;
-            out[q] = v;
+                for (int q = 0; q < kWQ; ++q) {
+                    int sh = 0;
+#pragma unroll
+                    for (int e = 0; e < kWK; ++e) sh += (ev[e] <= first + q);
+                    uint32_t v = d[q];
+#pragma unroll
+                    for (int j = 1; j < kWK; ++j) v = (sh == j) ? d[q + j] : v;
+                    x[q] = v;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kWQ; ++q) {
+                const uint32_t off = (uint32_t)s + (uint32_t)(first + q);
+                const uint32_t excl = (tail ? rng_hi - off : rng_hi + off) + 1u;
+                out[q] = __umulhi(x[q], excl);
+            }
         }
-        const int first = 4 * tid;
+        const int first = kWQ * tid;
         if (first + kWQ <= len && ((s & 3) == 0)) {
-            *reinterpret_cast<int4 *>(rv + s + first) = make_int4(out[0], out[1], out[2], out[3]);
+            int4 *dst = reinterpret_cast<int4 *>(rv + s + first);
+            dst[0] = make_int4(out[0], out[1], out[2], out[3]);
+            dst[1] = make_int4(out[4], out[5], out[6], out[7]);
         } else {
 #pragma unroll
             for (int q = 0; q < kWQ; ++q)
                 if (first + q < len) rv[s + first + q] = (int32_t)out[q];
         }
-        if (tid == 0 && u + len + ne > nd) s_err = 1;
+        if (tid == 0 && u + len + ne > nd) W.err = 1;
         s += len;
         u += len + ne;
-        __syncthreads();   // every read of ring blocks below u / kRingBlk is done
+        group_sync(g);   // every read of ring blocks below u / kRingBlk is done
         if (tid == 0) request(u / kRingBlk + kRingN);
-        if (s_err || (len == 0 && ne == 0)) break;
+        if (W.err || (len == 0 && ne == 0)) break;
     }
-    if (tid == 0) status[blockIdx.x] = (s_err || s < count) ? EDGC_EDRAWS : EDGC_OK;
+    if (tid == 0) status[pid] = (W.err || s < count) ? EDGC_EDRAWS : EDGC_OK;
 }
 
 __device__ __forceinline__ int find_plan_steps(const PlanDev *plans, int n, int64_t blk) {
@@ -299,7 +384,7 @@ __device__ __forceinline__ int find_plan_steps(const PlanDev *plans, int n, int6
 // (direct-mapped heads: one atomic exchange per step, no probing)
 __global__ void __launch_bounds__(kStepThreads) k_index(const PlanDev *plans, int p0, int p1, int64_t blk0) {
     const int p = p0 + find_plan_steps(plans + p0, p1 - p0, blk0 + blockIdx.x);
-    const PlanDev &P = plans[p];
+    const PlanDev P = plans[p];
     const int64_t s = (int64_t)(blk0 + blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
     if (P.bucketed || s >= P.count) return;
     P.next[s] = atomicExch(P.head + P.rv[s], (int32_t)s);
@@ -318,7 +403,7 @@ __device__ __forceinline__ int32_t latest_before(const PlanDev &P, int32_t key, 
 // ---- P4: resolve chains / collisions ---------------------------------------
 __global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, int p0, int p1, int64_t blk0) {
     const int p = p0 + find_plan_steps(plans + p0, p1 - p0, blk0 + blockIdx.x);
-    const PlanDev &P = plans[p];
+    const PlanDev P = plans[p];
     const int64_t s64 = (int64_t)(blk0 + blockIdx.x - P.step_block0) * kStepThreads + threadIdx.x;
     if (P.bucketed || s64 >= P.count) return;
     const int32_t s = (int32_t)s64;
@@ -381,15 +466,15 @@ __global__ void __launch_bounds__(kStepThreads) k_resolve(const PlanDev *plans, 
 //            there = the value at i_t = N-1-t before step t, recursively
 //            through the tail-position answers.
 // Every answer is a maximum, so no stage needs a stable order.
-constexpr int kBBits = 13;
+constexpr int kBBits = 14;
 constexpr int kBSize = 1 << kBBits;          // positions per bucket
 constexpr int kBWords = kBSize / 32;
-constexpr int kBMaxBuckets = 4096;           // N <= 2^25 on the bucket path
+constexpr int kBMaxBuckets = 2048;           // N <= 2^25 on the bucket path
 constexpr int kBChunk = 32768;               // steps per sort CTA
 constexpr int kBSortThreads = 1024;
 constexpr int kBSortPer = kBChunk / kBSortThreads;
 constexpr int kBResThreads = 512;
-constexpr int kBCap = 4096;                  // entries per resolve pass (several passes if a bucket holds more)
+constexpr int kBCap = 8192;                  // entries per resolve pass (several passes if a bucket holds more)
 constexpr int kBMaxChunks = (1 << 25) / kBChunk;
 constexpr int kOutPerThread = 8;
 constexpr int kOutPerBlock = kOutPerThread * kStepThreads;
@@ -404,11 +489,11 @@ struct BSortSmem {
 constexpr int kBSub = 64;                    // position sub-ranges for sizing multi-pass resolves
 constexpr int kBStage = 1024;                // chain-list entries staged per CTA
 struct BResSmem {
-    int32_t head[kBSize];              // list heads; then the tail-position answers
+    uint32_t head2[kBSize / 2];        // list heads, two int16 per word (0xFFFF: empty)
     uint32_t bits[kBWords];
     int32_t ls[kBCap];                 // step of entry e
     int16_t nx[kBCap];                 // list link
-    int16_t lp[kBCap];                 // position (in the bucket) of entry e; single pass: first the chunk of entry e
+    uint16_t lp[kBCap];                // position (in the bucket) of entry e; single pass: first the chunk of entry e
     union {
         struct {
             int32_t segoff[kBMaxChunks + 1];   // entry prefix per sort chunk (+ total)
@@ -422,6 +507,22 @@ struct BResSmem {
     int32_t warp_tmp[33];
     int32_t fill, err, npass, nchain, chain_base;
 };
+
+__device__ __forceinline__ int head_get(const BResSmem &sm, int l) {
+    return (int)(int16_t)(sm.head2[l >> 1] >> ((l & 1) * 16));
+}
+
+// push entry e on position l's list; returns the previous head (-1: empty)
+__device__ __forceinline__ int head_push(BResSmem &sm, int l, int e) {
+    uint32_t *w = &sm.head2[l >> 1];
+    const int sh = (l & 1) * 16;
+    uint32_t old = *w, assumed;
+    do {
+        assumed = old;
+        old = atomicCAS(w, assumed, (assumed & ~(0xFFFFu << sh)) | ((uint32_t)(uint16_t)e << sh));
+    } while (old != assumed);
+    return (int)(int16_t)(old >> sh);
+}
 
 // CTA -> plan: the host table gives the plan holding CTA (64 g) for every group
 // g of 64 CTAs; a short forward scan skips the plans that start inside the
@@ -483,7 +584,7 @@ __device__ int32_t block_exclusive_scan(int32_t *a, int n, int32_t *warp_tmp) {
 __global__ void __launch_bounds__(kBSortThreads) k_bucket_sort(const PlanDev *plans, int n_plans, PlanLut lut) {
     extern __shared__ __align__(16) unsigned char bsm_raw[];
     BSortSmem &sm = *reinterpret_cast<BSortSmem *>(bsm_raw);
-    const PlanDev &P = plans[find_plan_by(plans, n_plans, lut.sort, blockIdx.x, 0)];
+    const PlanDev P = plans[find_plan_by(plans, n_plans, lut.sort, blockIdx.x, 0)];
     const int c = (int)(blockIdx.x - P.chunk0);
     const int nb = P.nb;
     const int64_t c0 = (int64_t)c * kBChunk;
@@ -491,12 +592,15 @@ __global__ void __launch_bounds__(kBSortThreads) k_bucket_sort(const PlanDev *pl
     for (int b = threadIdx.x; b <= nb; b += kBSortThreads) sm.hist[b] = 0;
     __syncthreads();
     int32_t j[kBSortPer];
+    // all of the thread's loads in flight before the first shared-memory atomic
 #pragma unroll
     for (int k = 0; k < kBSortPer; ++k) {
         const int i = threadIdx.x + k * kBSortThreads;
-        j[k] = i < len ? P.rv[c0 + i] : -1;
-        if (j[k] >= 0) atomicAdd(&sm.hist[j[k] >> kBBits], 1);
+        j[k] = i < len ? __ldcs(P.rv + c0 + i) : -1;
     }
+#pragma unroll
+    for (int k = 0; k < kBSortPer; ++k)
+        if (j[k] >= 0) atomicAdd(&sm.hist[j[k] >> kBBits], 1);
     __syncthreads();
     block_exclusive_scan(sm.hist, nb + 1, sm.warp_tmp);
     int32_t *seg = P.segoff + (int64_t)c * (nb + 1);
@@ -516,12 +620,12 @@ __global__ void __launch_bounds__(kBSortThreads) k_bucket_sort(const PlanDev *pl
     }
 }
 
-__global__ void __launch_bounds__(kBResThreads, 3) k_bucket_resolve(const PlanDev *plans, int n_plans,
+__global__ void __launch_bounds__(kBResThreads, 2) k_bucket_resolve(const PlanDev *plans, int n_plans,
                                                                     PlanLut lut, int32_t *status) {
     extern __shared__ __align__(16) unsigned char brm_raw[];
     BResSmem &sm = *reinterpret_cast<BResSmem *>(brm_raw);
     const int pi = find_plan_by(plans, n_plans, lut.bucket, blockIdx.x, 1);
-    const PlanDev &P = plans[pi];
+    const PlanDev P = plans[pi];
     const int b = (int)(blockIdx.x - P.bucket0);
     const int nb = P.nb, nch = P.nch;
     const int64_t N = P.n_elems, count = P.count, z0 = N - count;
@@ -536,6 +640,7 @@ __global__ void __launch_bounds__(kBResThreads, 3) k_bucket_resolve(const PlanDe
         segoff[c] = row[b + 1] - r0;
     }
     for (int i = tid; i < kBWords; i += kBResThreads) sm.bits[i] = 0u;
+    for (int i = tid; i < kBSize / 2; i += kBResThreads) sm.head2[i] = 0xFFFFFFFFu;
     for (int i = tid; i <= kBSub; i += kBResThreads) sm.sub[i] = 0;
     if (tid == 0) { sm.err = 0; sm.npass = 1; sm.nchain = 0; }
     __syncthreads();
@@ -575,14 +680,16 @@ __global__ void __launch_bounds__(kBResThreads, 3) k_bucket_resolve(const PlanDe
     } else {
         // single pass: expand the segments into a per-entry chunk table (lp doubles as it)
         for (int c = warp; c < nch; c += kBResThreads / 32)
-            for (int32_t k = segoff[c] + lane; k < segoff[c + 1]; k += 32) sm.lp[k] = (int16_t)c;
+            for (int32_t k = segoff[c] + lane; k < segoff[c + 1]; k += 32) sm.lp[k] = (uint16_t)c;
         if (tid == 0) { sm.sub[0] = 0; sm.sub[1] = kBSize; }
     }
     __syncthreads();
     const int npass = sm.npass;
     for (int ps = 0; ps < npass; ++ps) {
         const int plo = sm.sub[ps], phi = sm.sub[ps + 1];
-        for (int i = plo + tid; i < phi; i += kBResThreads) sm.head[i] = -1;
+        if (ps > 0) {   // pass 0's heads were cleared with the rest of the state
+            for (int i = plo / 2 + tid; i < phi / 2; i += kBResThreads) sm.head2[i] = 0xFFFFFFFFu;
+        }
         if (tid == 0) sm.fill = 0;
         __syncthreads();
         for (int32_t k = tid; k < n; k += kBResThreads) {
@@ -604,8 +711,8 @@ __global__ void __launch_bounds__(kBResThreads, 3) k_bucket_resolve(const PlanDe
             if (!mine) continue;
             if (e >= kBCap) { sm.err = 1; continue; }
             sm.ls[e] = ss;
-            sm.lp[e] = (int16_t)l;
-            sm.nx[e] = (int16_t)atomicExch(&sm.head[l], e);
+            sm.lp[e] = (uint16_t)l;
+            sm.nx[e] = (int16_t)head_push(sm, l, e);
         }
         __syncthreads();
         const int fill = multi ? min(sm.fill, kBCap) : n;
@@ -613,7 +720,7 @@ __global__ void __launch_bounds__(kBResThreads, 3) k_bucket_resolve(const PlanDe
             const int32_t s = sm.ls[e];
             const int l = sm.lp[e];
             int32_t best = -1;
-            for (int x = sm.head[l]; x >= 0; x = sm.nx[x]) {
+            for (int x = head_get(sm, l); x >= 0; x = sm.nx[x]) {
                 const int32_t t = sm.ls[x];
                 if (t < s && t > best) best = t;
             }
@@ -623,7 +730,14 @@ __global__ void __launch_bounds__(kBResThreads, 3) k_bucket_resolve(const PlanDe
                 if (P.full_idx || s == count - 1) P.idx[count - 1 - s] = (int32_t)(pbase + l);
             } else {
                 // chain-list entry: staged in shared memory (the segment tables are dead in a single pass)
-                const int i = multi ? kBStage : atomicAdd(&sm.nchain, 1);
+                int i = kBStage;
+                if (!multi) {
+                    const unsigned mask = __activemask();
+                    const int leader = __ffs(mask) - 1;
+                    int base = 0;
+                    if (lane == leader) base = atomicAdd(&sm.nchain, __popc(mask));
+                    i = __shfl_sync(mask, base, leader) + __popc(mask & ((1u << lane) - 1u));
+                }
                 if (i < kBStage) {
                     sm.u.c.cs[i] = s;
                     sm.u.c.ct[i] = best;
@@ -645,18 +759,16 @@ __global__ void __launch_bounds__(kBResThreads, 3) k_bucket_resolve(const PlanDe
             }
         }
         // tail positions of this range: the latest step before the position's own step that wrote it
-        // (the head array is reused for the answers)
         const int64_t q0 = max(pbase + plo, z0), q1 = min(pbase + phi, N);
-        if (q0 < q1) {
-            for (int i = plo + tid; i < phi; i += kBResThreads) sm.head[i] = -1;
-            __syncthreads();
-            for (int e = tid; e < fill; e += kBResThreads) {
-                const int l = sm.lp[e];
-                const int32_t s = sm.ls[e];
-                if (pbase + l >= z0 && s < lim0 - l) atomicMax(&sm.head[l], s);
+        for (int64_t pos = q0 + tid; pos < q1; pos += kBResThreads) {
+            const int l = (int)(pos - pbase);
+            const int32_t lim = (int32_t)(lim0 - l);
+            int32_t best = -1;
+            for (int x = head_get(sm, l); x >= 0; x = sm.nx[x]) {
+                const int32_t t = sm.ls[x];
+                if (t < lim && t > best) best = t;
             }
-            __syncthreads();
-            for (int64_t pos = q0 + tid; pos < q1; pos += kBResThreads) P.wtail[pos - z0] = sm.head[pos - pbase];
+            P.wtail[pos - z0] = best;
         }
         __syncthreads();
     }
@@ -669,7 +781,7 @@ __global__ void __launch_bounds__(kBResThreads, 3) k_bucket_resolve(const PlanDe
 }
 
 __global__ void __launch_bounds__(kStepThreads) k_bucket_chain(const PlanDev *plans, int n_plans, PlanLut lut) {
-    const PlanDev &P = plans[find_plan_by(plans, n_plans, lut.chain, blockIdx.x, 2)];
+    const PlanDev P = plans[find_plan_by(plans, n_plans, lut.chain, blockIdx.x, 2)];
     const int64_t N = P.n_elems, count = P.count, z0 = N - count;
     const int64_t e_base = (int64_t)(blockIdx.x - P.oblock0) * kOutPerBlock + threadIdx.x;
     const int64_t nch = *P.nchain;
@@ -850,10 +962,11 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
     static bool walk_attr = false;
     if (!walk_attr) {
         EDGC_CUDA_TRY(cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(kRing * sizeof(uint32_t))));
+                                           (int)(kWG * sizeof(WalkGroup))));
         walk_attr = true;
     }
-    k_walk<<<n_plans, kWT, kRing * sizeof(uint32_t), st>>>(d_plans, status_dev);
+    k_walk<<<(unsigned)ceil_div(n_plans, kWG), kWT * kWG, kWG * sizeof(WalkGroup), st>>>(d_plans, n_plans,
+                                                                                       status_dev);
     EDGC_LAUNCH_CHECK();
     if (L.n_bucketed) {
         // bucket path (tail-shuffle plans); plans are ordered, so each kernel's CTA range covers

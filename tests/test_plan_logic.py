@@ -23,14 +23,13 @@ def lemire(x, rng):
     return left >= thr, val
 
 
-def walk(seed, n_elems, count, window=64):
+def walk(seed, n_elems, count, window=64, K=8):
     """k_walk: bounded value of every step (speculative shifts, first-rejection windows)."""
     tail = n_elems > 10000 and count > n_elems // 20
     draws = oracle.pcg64_u32(seed, count + 4096 + 2 * count).astype(np.int64)
     step_rng = (lambda s: n_elems - 1 - s) if tail else (lambda s: n_elems - count + s)
     rv = [0] * count
     s = u = 0
-    K = 4
     while s < count:                      # k_walk (speculative shifts 0..K-1)
         nvalid = min(window, count - s)
         vals = [[0] * window for _ in range(K)]
@@ -58,8 +57,8 @@ def walk(seed, n_elems, count, window=64):
     return rv, tail
 
 
-def emulate(seed, n_elems, count, window=64):
-    rv, tail = walk(seed, n_elems, count, window)
+def emulate(seed, n_elems, count, window=64, K=8):
+    rv, tail = walk(seed, n_elems, count, window, K)
     lists = {}                            # k_index (hash lists)
     for st in range(count):
         lists.setdefault(rv[st], []).append(st)
@@ -98,16 +97,16 @@ def emulate(seed, n_elems, count, window=64):
     return np.asarray(out, dtype=np.int64)
 
 
-@pytest.mark.parametrize("window", [64, 7])
+@pytest.mark.parametrize("window,K", [(64, 8), (7, 4), (2048, 8)])
 @pytest.mark.parametrize("n_elems,beta,seed", [
     (100, 0.5, 3), (101, 0.9, 1), (4096, 0.25, 1), (10000, 0.5, 4), (10001, 0.06, 4), (12000, 0.25, 5),
     (20000, 0.05, 9), (20000, 0.0501, 11), (40000, 0.999, 2), (7, 0.3, 5), (2, 0.5, 0), (300, 0.99, 8)])
-def test_plan_algorithm_matches_numpy(n_elems, beta, seed, window):
+def test_plan_algorithm_matches_numpy(n_elems, beta, seed, window, K):
     count = min(n_elems, math.ceil(beta * n_elems))
     if count == n_elems:
         pytest.skip("copy branch")
     ref = np.random.default_rng(seed).choice(n_elems, size=count, replace=False, shuffle=False)
-    assert np.array_equal(emulate(seed, n_elems, count, window), ref)
+    assert np.array_equal(emulate(seed, n_elems, count, window, K), ref)
 
 
 def resolve_buckets(rv, n_elems, count, tail, bbits, order_seed=0):
@@ -172,3 +171,25 @@ def test_bucketed_resolve_matches_numpy(n_elems, beta, seed, bbits):
     ref = np.random.default_rng(seed).choice(n_elems, size=count, replace=False, shuffle=False)
     rv, tail = walk(seed, n_elems, count)
     assert np.array_equal(resolve_buckets(rv, n_elems, count, tail, bbits, order_seed=seed), ref)
+
+
+def lemire_threshold(excl):
+    """csrc/sample_plan.cu:lemire_threshold, restated with float32 rounding."""
+    if excl < 65536:
+        return (2**32 - excl) % excl
+    q = int(np.float32(4294967296.0) * (np.float32(1.0) / np.float32(excl)))
+    r = 2**32 - q * excl
+    for _ in range(2):
+        r += excl if r < 0 else 0
+    for _ in range(2):
+        r -= excl if r >= excl else 0
+    return r
+
+
+def test_lemire_threshold_fast_path():
+    rng = np.random.default_rng(0)
+    xs = list(rng.integers(1, 2**31, size=20000)) + [1, 2, 3, 65535, 65536, 65537, 2**31 - 1, 2**30, 3 << 29]
+    xs += [int(x) for x in np.arange(65536, 65536 + 2000)]
+    for x in xs:
+        x = int(x)
+        assert lemire_threshold(x) == (2**32 - x) % x, x

@@ -2,8 +2,8 @@
 
     python tools/variants.py name:-DEDGC_TD=0,-DEDGC_STCS=0 name2:...
 
-Only compress.cu is recompiled with the extra defines; the other objects come
-from the in-tree build.  Select a variant at run time with EDGC_LIB_PATH.
+Every source is recompiled with the extra defines.  Select a variant at run
+time with EDGC_LIB_PATH.
 """
 
 import os
@@ -26,16 +26,22 @@ def main():
     for spec in sys.argv[1:]:
         name, _, defs = spec.partition(":")
         defs = [d for d in defs.split(",") if d]
-        obj = os.path.join(out, f"{name}_compress.o")
-        cmd = [_build.NVCC] + flags + defs + ["-c", os.path.join(_build.HERE, "csrc", "compress.cu"), "-o", obj]
-        procs.append((name, obj, subprocess.Popen(cmd)))
-    for name, obj, p in procs:
+        objs = []
+        for src in _build.sources():
+            obj = os.path.join(out, f"{name}_{os.path.basename(src).replace('.cu', '.o')}")
+            objs.append(obj)
+            procs.append((name, subprocess.Popen([_build.NVCC] + flags + defs + ["-c", src, "-o", obj])))
+        procs.append((name, objs))
+    pending = {}
+    for name, p in procs:
+        if isinstance(p, list):
+            pending[name] = p
+            continue
         if p.wait() != 0:
             raise SystemExit(f"variant {name} failed")
-        others = [os.path.join(objdir, f) for f in sorted(os.listdir(objdir)) if f.endswith(".o") and f != "compress.o"]
+    for name, objs in pending.items():
         lib = os.path.join(out, f"{name}.so")
-        subprocess.run([_build.NVCC] + _build.ARCH + ["-shared", "-o", lib, obj] + others + ["-cudart", "static"],
-                       check=True)
+        subprocess.run([_build.NVCC] + _build.ARCH + ["-shared", "-o", lib] + objs + ["-cudart", "static"], check=True)
         print(lib)
 
 
