@@ -227,6 +227,24 @@ __global__ void __launch_bounds__(kP1Threads) k_pass1(const MatDev *mats, const 
 constexpr int kTCons = 320;
 constexpr int kTThreads = kTCons + 64;   // + producer warp + exchange warp
 constexpr int kTRB = 4;
+#ifndef EDGC_P1_STASYNC
+#define EDGC_P1_STASYNC 1   // peer pushes by st.async + complete_tx (0: st.shared::cluster + release arrive)
+#endif
+#ifndef EDGC_P1_MEMONLY
+#define EDGC_P1_MEMONLY 0   // diagnostics: stream g, w -> w only (no row dots, exchange or Z)
+#endif
+#ifndef EDGC_P1_NOEXCH
+#define EDGC_P1_NOEXCH 0    // diagnostics: row dots + warp reductions, no cluster exchange / Z
+#endif
+#ifndef EDGC_P1_NOZ
+#define EDGC_P1_NOZ 0       // diagnostics: full exchange, Z update skipped
+#endif
+#ifndef EDGC_PROD_SLEEP
+#define EDGC_PROD_SLEEP 64
+#endif
+#ifndef EDGC_CONS_SLEEP
+#define EDGC_CONS_SLEEP 0
+#endif
 #ifndef EDGC_TSTAGES
 #define EDGC_TSTAGES 3
 #endif
@@ -239,17 +257,8 @@ constexpr int kTLag = EDGC_TLAG;         // consumer Z update lags its round by 
 #ifndef EDGC_STCS
 #define EDGC_STCS 1
 #endif
-#ifndef EDGC_PRES_SMEM
-#define EDGC_PRES_SMEM 0
-#endif
-#ifndef EDGC_EARLY_RELEASE
-#define EDGC_EARLY_RELEASE 1
-#endif
 #ifndef EDGC_CONS_FINITE
-#define EDGC_CONS_FINITE 1
-#endif
-#ifndef EDGC_LOAD_AHEAD
-#define EDGC_LOAD_AHEAD 0
+#define EDGC_CONS_FINITE 0
 #endif
 constexpr int kTD = EDGC_TD;             // exchange completes round b - kTD after pushing round b
 static_assert(kTLag >= kTD, "consumers must not wait for a round the exchange has not completed");
@@ -261,7 +270,6 @@ struct TSmem {
     float g[kTStages][kTRB][kTCW];
     float w[kTStages][kTRB][kTCW];
     float xs[kTRing][kTRB][kTCW];        // x (new w) of the last kTRing rounds (each thread its own columns)
-    float pres[kTStages][kTV];           // the stage's p_res rows, [row][k], zero padded to 4
     float prowf[kTRing][kTV];            // P_raw rows of the round, as float, for the Z update
     double recv[kTSlots][8][kTV];
     double red[kTRing][kTCons / 32][kTV];
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             ptx::mbar_init(&sm.full[s], 1);
             ptx::mbar_init(&sm.empty[s], kTCons / 32);
         }
-        for (int s = 0; s < kTSlots; ++s) ptx::mbar_init(&sm.xfull[s], C);
+        for (int s = 0; s < kTSlots; ++s) ptx::mbar_init(&sm.xfull[s], EDGC_P1_STASYNC ? 1 : C);
         for (int s = 0; s < kTRing; ++s) ptx::mbar_init(&sm.prowready[s], 1);
         ptx::fence_mbar_init();
     }
@@ -316,29 +324,26 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
     ptx::cluster_sync();
 
     if (warp == kProducer) {
-        if (chunk_cols > 0) {
+        if (lane == 0 && chunk_cols > 0) {
             const uint32_t bytes = (uint32_t)(chunk_cols * 4);
             for (int b = 0; b < nrounds; ++b) {
                 const int s = b % kTStages;
                 const int64_t i0 = t.row0 + (int64_t)b * kTRB;
                 const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
-                // the round's p_res rows (the load's latency overlaps the empty wait)
-                float pv = 0.f;
-                if (EDGC_PRES_SMEM && lane < kTV && (lane & 3) < rr_res && (lane >> 2) < rows)
-                    pv = __ldg(pres_ptr + (i0 + (lane >> 2)) * rr_res + (lane & 3));
-                if (b >= kTStages) ptx::mbar_wait(&sm.empty[s], ((b / kTStages) - 1) & 1);
-                if (lane < kTV) sm.pres[s][lane] = pv;
-                __syncwarp();   // orders the lanes' stores before lane 0's releasing arrive
-                if (lane == 0) {
-                    ptx::mbar_arrive_expect_tx(&sm.full[s], 2u * bytes * (uint32_t)rows);
-                    for (int rr = 0; rr < rows; ++rr) {
-                        ptx::bulk_g2s(&sm.g[s][rr][0], gptr + (i0 + rr) * ld_g + col_base, bytes, &sm.full[s]);
-                        ptx::bulk_g2s(&sm.w[s][rr][0], wptr + (i0 + rr) * n + col_base, bytes, &sm.full[s]);
-                    }
+                if (b >= kTStages) ptx::mbar_wait_sleep<EDGC_PROD_SLEEP>(&sm.empty[s], ((b / kTStages) - 1) & 1);
+                ptx::mbar_arrive_expect_tx(&sm.full[s], 2u * bytes * (uint32_t)rows);
+                for (int rr = 0; rr < rows; ++rr) {
+                    ptx::bulk_g2s(&sm.g[s][rr][0], gptr + (i0 + rr) * ld_g + col_base, bytes, &sm.full[s]);
+                    ptx::bulk_g2s(&sm.w[s][rr][0], wptr + (i0 + rr) * n + col_base, bytes, &sm.full[s]);
                 }
             }
         }
     } else if (warp == kExchange) {
+        if (EDGC_P1_MEMONLY) goto done;
+        if (EDGC_P1_NOEXCH) {
+            for (int b = 0; b < nrounds; ++b) ptx::named_bar_sync(2 + b % kTRing, kTCons + 32);
+            goto done;
+        }
         bool bad = false;
         auto push = [&](int b) {
             const int q = b % kTRing, slot = b % kTSlots;
@@ -350,6 +355,20 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 sm.recv[slot][me][lane] = a;            // my own contribution, in place
             }
             __syncwarp();
+#if EDGC_P1_STASYNC
+            // my barrier expects the C-1 peers' vectors as transaction bytes; my own arrive
+            // (release) publishes my own slot; the peers' st.async complete the transaction
+            if (lane == 0) ptx::mbar_arrive_expect_tx(&sm.xfull[slot], (C - 1u) * kTV * 8u);
+            if ((uint32_t)lane < C && (uint32_t)lane != me) {
+                // lane cc streams the whole row-dot vector into peer cc's slot for me
+                const uint32_t cc = (uint32_t)lane;
+                const uint32_t dst = ptx::mapa(ptx::smem_addr(&sm.recv[slot][me][0]), cc);
+                const uint32_t bar = ptx::mapa(ptx::smem_addr(&sm.xfull[slot]), cc);
+#pragma unroll
+                for (int e = 0; e < kTV; e += 2)
+                    ptx::st_async_v2_f64(dst + 8u * e, sm.recv[slot][me][e], sm.recv[slot][me][e + 1], bar);
+            }
+#else
             if ((uint32_t)lane < C && (uint32_t)lane != me) {
                 // lane cc pushes the whole row-dot vector to peer cc, then release-arrives
                 // there: the C pushes and releases proceed in parallel
@@ -361,6 +380,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_addr(&sm.xfull[slot]), cc));
             }
             if ((uint32_t)lane == me) ptx::mbar_arrive_cta(&sm.xfull[slot]);
+#endif
         };
         auto complete = [&](int b) {
             const int q = b % kTRing, slot = b % kTSlots;
@@ -385,13 +405,20 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
         if (__any_sync(0xffffffffu, bad) && lane == 0 && me == 0) atomicOr(status + t.mat, 1);
     } else {
         // ---------------- consumer warps
+        // Lane-permuted partials: lane L computes output (row, k) = slot i ^ f(L) into slot i,
+        // f(L) = bits (16, 8, 4, 2) of L.  Partner lanes at every butterfly level then hold their
+        // halves in opposite order, so the fp64 reduce-scatter is shuffle + add only (no selects):
+        // rows are processed in order rr ^ f/4 and the q_warm columns are pre-permuted by f%4.
+        const int f = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) |
+                      ((lane >> 1) & 1);
+        const int fr = f >> 2, fk = f & 3;
         const int64_t col0 = col_base + 4 * tid;
         const bool active = 4 * tid < chunk_cols;
         double qw[4][4];
         float qr[4][4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-            double raw[4];
+            double raw[4], nat[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) raw[k] = (active && k < r) ? (double)qwarm_ptr[(col0 + v) * ld_q + k] : 0.0;
 #pragma unroll
@@ -399,9 +426,12 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 double a = 0.0;
 #pragma unroll
                 for (int i = 0; i <= k; ++i) a += raw[i] * sm.S[i * 4 + k];
-                qw[v][k] = a;
+                nat[k] = a;
                 qr[v][k] = (active && k < rr_res) ? qres_ptr[(col0 + v) * rr_res + k] : 0.f;
             }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                qw[v][k] = fk == 0 ? nat[k] : fk == 1 ? nat[k ^ 1] : fk == 2 ? nat[k ^ 2] : nat[k ^ 3];
         }
         float zacc[4][4];
 #pragma unroll
@@ -412,7 +442,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
         // round bb's x values wait in xs[bb % kTRing] (this thread's columns only) for the lagged Z update
         auto consume = [&](int bb) {
             const int q = bb % kTRing;
-            ptx::mbar_wait(&sm.prowready[q], (bb / kTRing) & 1);
+            ptx::mbar_wait_sleep<EDGC_CONS_SLEEP>(&sm.prowready[q], (bb / kTRing) & 1);
+            if (EDGC_P1_NOZ) return;
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) {
                 const float4 pv = *reinterpret_cast<const float4 *>(&sm.prowf[q][rr * 4]);
@@ -424,45 +455,47 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                     for (int v = 0; v < 4; ++v) zacc[v][k] = fmaf(xx[v], pp[k], zacc[v][k]);
             }
         };
+        // p_res rows of a round in this lane's row order, one round ahead (broadcast loads)
+        const bool pres_v4 = rr_res == 4 && ((uintptr_t)pres_ptr & 15) == 0;
+        auto load_pres = [&](int bb, float4 (&pr)[kTRB]) {
+            const int64_t r0 = t.row0 + (int64_t)bb * kTRB;
+            const int nrow = (int)min((int64_t)kTRB, t.row1 - r0);   // <= 0 past the strip
+            if (pres_v4) {
+                const float4 *base = reinterpret_cast<const float4 *>(pres_ptr) + r0;
+#pragma unroll
+                for (int rr = 0; rr < kTRB; ++rr)
+                    pr[rr] = (rr ^ fr) < nrow ? __ldg(base + (rr ^ fr)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+#pragma unroll
+                for (int rr = 0; rr < kTRB; ++rr) {
+                    float pq[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        pq[k] = ((rr ^ fr) < nrow && k < rr_res) ? __ldg(pres_ptr + (r0 + (rr ^ fr)) * rr_res + k) : 0.f;
+                    pr[rr] = make_float4(pq[0], pq[1], pq[2], pq[3]);
+                }
+            }
+        };
+        float4 pcur[kTRB];
+        load_pres(0, pcur);
 #pragma unroll 1
         for (int b = 0; b < nrounds; ++b) {
             const int s = b % kTStages, q = b % kTRing;
             const int64_t i0 = t.row0 + (int64_t)b * kTRB;
             const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
-            if (chunk_cols > 0) ptx::mbar_wait(&sm.full[s], (b / kTStages) & 1);
-            // the stage's shared loads (rows past the strip read stale data, zeroed below)
-            float4 pr4[kTRB], gv[kTRB], wv[kTRB];
-#pragma unroll
-            for (int rr = 0; rr < kTRB; ++rr) {
-#if EDGC_PRES_SMEM
-                pr4[rr] = *reinterpret_cast<const float4 *>(&sm.pres[s][rr * 4]);
-#else
-                float pq[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    pq[k] = (k < rr_res && rr < rows) ? __ldg(pres_ptr + (i0 + rr) * rr_res + k) : 0.f;
-                pr4[rr] = make_float4(pq[0], pq[1], pq[2], pq[3]);
-#endif
-#if EDGC_LOAD_AHEAD
-                gv[rr] = *reinterpret_cast<const float4 *>(&sm.g[s][rr][4 * tid]);
-                wv[rr] = *reinterpret_cast<const float4 *>(&sm.w[s][rr][4 * tid]);
-#endif
-            }
-#if EDGC_LOAD_AHEAD && EDGC_EARLY_RELEASE
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cta(&sm.empty[s]);   // stage s read: refill it
-#endif
+            float4 pnext[kTRB];
+            load_pres(b + 1, pnext);
+            if (chunk_cols > 0) ptx::mbar_wait_sleep<EDGC_CONS_SLEEP>(&sm.full[s], (b / kTStages) & 1);
             double acc[kTV];
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) {
-#if !EDGC_LOAD_AHEAD
-                gv[rr] = ptx::ld_shared_v4(&sm.g[s][rr][4 * tid]);
-                wv[rr] = ptx::ld_shared_v4(&sm.w[s][rr][4 * tid]);
-#endif
-                const bool live = active && rr < rows;
-                const float pp[4] = {pr4[rr].x, pr4[rr].y, pr4[rr].z, pr4[rr].w};
-                const float gg[4] = {gv[rr].x, gv[rr].y, gv[rr].z, gv[rr].w};
-                const float ww[4] = {wv[rr].x, wv[rr].y, wv[rr].z, wv[rr].w};
+                const int lr = rr ^ fr;   // the logical row of this slot
+                const float4 gv = *reinterpret_cast<const float4 *>(&sm.g[s][lr][4 * tid]);
+                const float4 wv = *reinterpret_cast<const float4 *>(&sm.w[s][lr][4 * tid]);
+                const bool live = active && lr < rows;
+                const float pp[4] = {pcur[rr].x, pcur[rr].y, pcur[rr].z, pcur[rr].w};
+                const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
+                const float ww[4] = {wv.x, wv.y, wv.z, wv.w};
                 float xx[4];
                 double pk[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -480,24 +513,31 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 }
                 if (live) {
 #if EDGC_STCS
-                    __stcs(reinterpret_cast<float4 *>(wptr + (i0 + rr) * n + col0), make_float4(xx[0], xx[1], xx[2], xx[3]));
+                    __stcs(reinterpret_cast<float4 *>(wptr + (i0 + lr) * n + col0), make_float4(xx[0], xx[1], xx[2], xx[3]));
 #else
-                    ptx::st_global_v4(wptr + (i0 + rr) * n + col0, xx[0], xx[1], xx[2], xx[3]);
+                    ptx::st_global_v4(wptr + (i0 + lr) * n + col0, xx[0], xx[1], xx[2], xx[3]);
 #endif
                 }
-                *reinterpret_cast<float4 *>(&sm.xs[q][rr][4 * tid]) = make_float4(xx[0], xx[1], xx[2], xx[3]);
+                *reinterpret_cast<float4 *>(&sm.xs[q][lr][4 * tid]) = make_float4(xx[0], xx[1], xx[2], xx[3]);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[rr * 4 + k] = pk[k];
             }
-#if !(EDGC_LOAD_AHEAD && EDGC_EARLY_RELEASE)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_relaxed(&sm.empty[s]);   // stage s read: refill it
-#endif
-            const double part = warp_reduce_scatter<kTV>(acc, lane);
-            if ((lane & 1) == 0) sm.red[q][warp][scatter_owner_index<kTV>(lane)] = part;
+            if (EDGC_P1_MEMONLY) continue;
+            // select-free reduce-scatter (offsets 16, 8, 4, 2 halve the slots; 1 finishes)
+#pragma unroll
+            for (int h = kTV / 2; h >= 1; h >>= 1)
+#pragma unroll
+                for (int i = 0; i < h; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i + h], 2 * h);
+            acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+            if ((lane & 1) == 0) sm.red[q][warp][f] = acc[0];
             ptx::named_bar_arrive(2 + q, kTCons + 32);   // hand red[q] to the exchange warp
-            if (b >= kTLag) consume(b - kTLag);
+            if (!EDGC_P1_NOEXCH && b >= kTLag) consume(b - kTLag);
+#pragma unroll
+            for (int rr = 0; rr < kTRB; ++rr) pcur[rr] = pnext[rr];
         }
+        if (EDGC_P1_MEMONLY || EDGC_P1_NOEXCH) goto done;
         for (int bb = max(0, nrounds - kTLag); bb < nrounds; ++bb) consume(bb);
         if (active) {
 #pragma unroll
@@ -508,6 +548,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
         }
         if (EDGC_CONS_FINITE && bad) atomicOr(status + t.mat, 1);
     }
+done:
     ptx::cluster_sync();  // no CTA leaves while a peer may still push into it
 }
 

@@ -45,7 +45,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  : "memory");
 }
 
+#ifndef EDGC_WAIT_HINT_NS
+#define EDGC_WAIT_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#if EDGC_WAIT_HINT_NS > 0
+    // suspend (up to the hint) instead of re-issuing the test: spinning waiters steal issue slots
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity), "n"(EDGC_WAIT_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -53,6 +66,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
         "r"(parity)
         : "memory");
+#endif
+}
+
+// 16 bytes into a peer CTA's shared memory, counted as complete_tx bytes on the
+// peer's mbarrier (no fence: the mbarrier completion orders the data)
+__device__ __forceinline__ void st_async_v2_f64(uint32_t remote_addr, double a, double b, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),
+                 "d"(a), "d"(b), "r"(remote_bar)
+                 : "memory");
+}
+
+// wait with a __nanosleep backoff between probes (ns == 0: plain spin)
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+template <int NS>
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    if (NS == 0) {
+        mbar_wait(bar, parity);
+        return;
+    }
+    while (!mbar_try(bar, parity)) __nanosleep(NS);
 }
 
 // wait with acquire at cluster scope: pairs with remote release-arrives
