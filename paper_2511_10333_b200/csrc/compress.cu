@@ -347,12 +347,16 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
         bool bad = false;
         auto push = [&](int b) {
             const int q = b % kTRing, slot = b % kTSlots;
-            ptx::named_bar_sync(2 + q, kTCons + 32);   // the 8 consumer warps wrote red[q]
-            if (lane < kTV) {
+            ptx::named_bar_sync(2 + q, kTCons + 32);   // the consumer warps wrote red[q]
+            {
+                // all 32 lanes: lane l sums half of the warps' partials of value l % 16, fixed order
+                constexpr int kHalf = kTCons / 64;
+                const int v = lane & (kTV - 1), w0 = (lane >> 4) * kHalf;
                 double a = 0.0;
 #pragma unroll
-                for (int w = 0; w < kTCons / 32; ++w) a += sm.red[q][w][lane];
-                sm.recv[slot][me][lane] = a;            // my own contribution, in place
+                for (int w = 0; w < kHalf; ++w) a += sm.red[q][w0 + w][v];
+                a += __shfl_xor_sync(0xffffffffu, a, 16);
+                if (lane < kTV) sm.recv[slot][me][lane] = a;            // my own contribution, in place
             }
             __syncwarp();
 #if EDGC_P1_STASYNC
