@@ -222,13 +222,16 @@ __global__ void __launch_bounds__(kP1Threads) k_pass1(const MatDev *mats, const 
 // steady state.  Non-finite work is detected on the exchanged row sums: a
 // fp64 sum of exact fp32 x fp32 products is non-finite iff one of the x is.
 #ifndef EDGC_TLAG
-#define EDGC_TLAG 2
+#define EDGC_TLAG 3
 #endif
 constexpr int kTCons = 320;
 constexpr int kTThreads = kTCons + 64;   // + producer warp + exchange warp
 constexpr int kTRB = 4;
 #ifndef EDGC_P1_STASYNC
 #define EDGC_P1_STASYNC 1   // peer pushes by st.async + complete_tx (0: st.shared::cluster + release arrive)
+#endif
+#ifndef EDGC_P1_EARLYZ
+#define EDGC_P1_EARLYZ 1    // 1: the lagged Z update runs right after the stage wait (interleaves with the round)
 #endif
 #ifndef EDGC_P1_MEMONLY
 #define EDGC_P1_MEMONLY 0   // diagnostics: stream g, w -> w only (no row dots, exchange or Z)
@@ -490,6 +493,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             float4 pnext[kTRB];
             load_pres(b + 1, pnext);
             if (chunk_cols > 0) ptx::mbar_wait_sleep<EDGC_CONS_SLEEP>(&sm.full[s], (b / kTStages) & 1);
+            if (EDGC_P1_EARLYZ && !EDGC_P1_NOEXCH && b >= kTLag) consume(b - kTLag);
             double acc[kTV];
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) {
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
             if ((lane & 1) == 0) sm.red[q][warp][f] = acc[0];
             ptx::named_bar_arrive(2 + q, kTCons + 32);   // hand red[q] to the exchange warp
-            if (!EDGC_P1_NOEXCH && b >= kTLag) consume(b - kTLag);
+            if (!EDGC_P1_EARLYZ && !EDGC_P1_NOEXCH && b >= kTLag) consume(b - kTLag);
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) pcur[rr] = pnext[rr];
         }

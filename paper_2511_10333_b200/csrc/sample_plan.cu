@@ -111,9 +111,9 @@ __device__ __forceinline__ int find_plan(const PlanDev *plans, int n, int64_t bl
 // Block b of a plan owns 64-bit outputs [b*64*256, (b+1)*64*256); thread t
 // produces outputs t, t+256, t+512, ... of that range (one jump-ahead, then a
 // 256-step affine LCG map per output), so every warp store is coalesced.
-__global__ void __launch_bounds__(kP1Threads) k_draws(const PlanDev *plans, int n_plans) {
-    const PlanDev P = plans[find_plan(plans, n_plans, blockIdx.x, true)];
-    const int64_t o_base = (int64_t)(blockIdx.x - P.draw_chunk0) * kDrawsPerBlock;
+__device__ __forceinline__ void k_draws_body(const PlanDev *plans, int n_plans, int64_t vb) {
+    const PlanDev P = plans[find_plan(plans, n_plans, vb, true)];
+    const int64_t o_base = (int64_t)(vb - P.draw_chunk0) * kDrawsPerBlock;
     const int64_t n64 = P.n_draws / 2;
     if (o_base >= n64) return;
     u128 s = pcg_jump(P.state, P.inc, (uint64_t)(o_base + threadIdx.x));
@@ -127,6 +127,14 @@ __global__ void __launch_bounds__(kP1Threads) k_draws(const PlanDev *plans, int 
         const uint64_t v = pcg_output(s * m1 + P.inc);   // output o = XSL-RR(state after o+1 steps)
         out[o] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
         s = a_t * s + c_t;
+    }
+}
+
+__global__ void __launch_bounds__(kP1Threads) k_draws(const PlanDev *plans, int n_plans, int64_t nvb) {
+    // grid-stride over the virtual CTAs: the launch may be capped to a share of the SMs
+    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+        k_draws_body(plans, n_plans, vb);
+        __syncthreads();
     }
 }
 
@@ -581,11 +589,11 @@ __device__ int32_t block_exclusive_scan(int32_t *a, int n, int32_t *warp_tmp) {
     return total;
 }
 
-__global__ void __launch_bounds__(kBSortThreads) k_bucket_sort(const PlanDev *plans, int n_plans, PlanLut lut) {
+__device__ __forceinline__ void k_bucket_sort_body(const PlanDev *plans, int n_plans, PlanLut lut, int64_t vb) {
     extern __shared__ __align__(16) unsigned char bsm_raw[];
     BSortSmem &sm = *reinterpret_cast<BSortSmem *>(bsm_raw);
-    const PlanDev P = plans[find_plan_by(plans, n_plans, lut.sort, blockIdx.x, 0)];
-    const int c = (int)(blockIdx.x - P.chunk0);
+    const PlanDev P = plans[find_plan_by(plans, n_plans, lut.sort, vb, 0)];
+    const int c = (int)(vb - P.chunk0);
     const int nb = P.nb;
     const int64_t c0 = (int64_t)c * kBChunk;
     const int len = (int)min((int64_t)kBChunk, P.count - c0);
@@ -620,13 +628,21 @@ __global__ void __launch_bounds__(kBSortThreads) k_bucket_sort(const PlanDev *pl
     }
 }
 
-__global__ void __launch_bounds__(kBResThreads, 2) k_bucket_resolve(const PlanDev *plans, int n_plans,
-                                                                    PlanLut lut, int32_t *status) {
+__global__ void __launch_bounds__(kBSortThreads) k_bucket_sort(const PlanDev *plans, int n_plans, PlanLut lut, int64_t nvb) {
+    // grid-stride over the virtual CTAs: the launch may be capped to a share of the SMs
+    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+        k_bucket_sort_body(plans, n_plans, lut, vb);
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void k_bucket_resolve_body(const PlanDev *plans, int n_plans,
+                                                                    PlanLut lut, int32_t *status, int64_t vb) {
     extern __shared__ __align__(16) unsigned char brm_raw[];
     BResSmem &sm = *reinterpret_cast<BResSmem *>(brm_raw);
-    const int pi = find_plan_by(plans, n_plans, lut.bucket, blockIdx.x, 1);
+    const int pi = find_plan_by(plans, n_plans, lut.bucket, vb, 1);
     const PlanDev P = plans[pi];
-    const int b = (int)(blockIdx.x - P.bucket0);
+    const int b = (int)(vb - P.bucket0);
     const int nb = P.nb, nch = P.nch;
     const int64_t N = P.n_elems, count = P.count, z0 = N - count;
     const int64_t pbase = (int64_t)b << kBBits;
@@ -780,10 +796,19 @@ __global__ void __launch_bounds__(kBResThreads, 2) k_bucket_resolve(const PlanDe
     if (tid == 0 && sm.err) atomicOr(status + pi, EDGC_ECAPACITY);
 }
 
-__global__ void __launch_bounds__(kStepThreads) k_bucket_chain(const PlanDev *plans, int n_plans, PlanLut lut) {
-    const PlanDev P = plans[find_plan_by(plans, n_plans, lut.chain, blockIdx.x, 2)];
+__global__ void __launch_bounds__(kBResThreads, 2) k_bucket_resolve(const PlanDev *plans, int n_plans,
+                                                                    PlanLut lut, int32_t *status, int64_t nvb) {
+    // grid-stride over the virtual CTAs: the launch may be capped to a share of the SMs
+    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+        k_bucket_resolve_body(plans, n_plans, lut, status, vb);
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void k_bucket_chain_body(const PlanDev *plans, int n_plans, PlanLut lut, int64_t vb) {
+    const PlanDev P = plans[find_plan_by(plans, n_plans, lut.chain, vb, 2)];
     const int64_t N = P.n_elems, count = P.count, z0 = N - count;
-    const int64_t e_base = (int64_t)(blockIdx.x - P.oblock0) * kOutPerBlock + threadIdx.x;
+    const int64_t e_base = (int64_t)(vb - P.oblock0) * kOutPerBlock + threadIdx.x;
     const int64_t nch = *P.nchain;
     for (int k = 0; k < kOutPerThread; ++k) {
         const int64_t e = e_base + (int64_t)k * kStepThreads;
@@ -798,6 +823,14 @@ __global__ void __launch_bounds__(kStepThreads) k_bucket_chain(const PlanDev *pl
         }
         if (P.full_idx || s == count - 1) P.idx[count - 1 - s] = outv;
         if (P.bitmap) atomicOr(P.bitmap + (outv >> 5), 1u << (outv & 31));
+    }
+}
+
+__global__ void __launch_bounds__(kStepThreads) k_bucket_chain(const PlanDev *plans, int n_plans, PlanLut lut, int64_t nvb) {
+    // grid-stride over the virtual CTAs: the launch may be capped to a share of the SMs
+    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+        k_bucket_chain_body(plans, n_plans, lut, vb);
+        __syncthreads();
     }
 }
 
@@ -957,7 +990,18 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
     cudaStream_t st = (cudaStream_t)stream;
     PlanDev *d_plans = reinterpret_cast<PlanDev *>(ws);
     EDGC_CUDA_TRY(cudaMemcpyAsync(d_plans, L.dev.data(), sizeof(PlanDev) * n_plans, cudaMemcpyHostToDevice, st));
-    k_draws<<<(unsigned)L.draw_chunks, kP1Threads, 0, st>>>(d_plans, n_plans);
+    // side-stream friendly: the plan kernels run grid-stride on at most a third of the SMs
+    // (EDGC_PLAN_SMS overrides), so the training stream's small latency-bound kernels always
+    // find free SMs while the next sampled iteration's plans are built behind it
+    static const int plan_sms = [] {
+        const char *e = std::getenv("EDGC_PLAN_SMS");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? std::min(v, edgc::sm_count()) : std::max(1, edgc::sm_count() / 3);
+    }();
+    auto capped = [&](int64_t nvb, int per_sm) {
+        return (unsigned)std::max<int64_t>(1, std::min<int64_t>(nvb, (int64_t)plan_sms * per_sm));
+    };
+    k_draws<<<capped(L.draw_chunks, 8), kP1Threads, 0, st>>>(d_plans, n_plans, L.draw_chunks);
     EDGC_LAUNCH_CHECK();
     static bool walk_attr = false;
     if (!walk_attr) {
@@ -983,12 +1027,13 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
         EDGC_CUDA_TRY(cudaMemcpyAsync(L.lut_dev, L.lut_host.data(), 4 * L.lut_host.size(), cudaMemcpyHostToDevice,
                                       st));
         const PlanLut lut{L.lut_dev, L.lut_dev + L.lut_n[0], L.lut_dev + L.lut_n[0] + L.lut_n[1]};
-        k_bucket_sort<<<(unsigned)L.bchunks, kBSortThreads, sizeof(BSortSmem), st>>>(d_plans, n_plans, lut);
+        k_bucket_sort<<<capped(L.bchunks, 1), kBSortThreads, sizeof(BSortSmem), st>>>(d_plans, n_plans, lut,
+                                                                                      L.bchunks);
         EDGC_LAUNCH_CHECK();
-        k_bucket_resolve<<<(unsigned)L.buckets, kBResThreads, sizeof(BResSmem), st>>>(d_plans, n_plans, lut,
-                                                                                      status_dev);
+        k_bucket_resolve<<<capped(L.buckets, 2), kBResThreads, sizeof(BResSmem), st>>>(d_plans, n_plans, lut,
+                                                                                       status_dev, L.buckets);
         EDGC_LAUNCH_CHECK();
-        k_bucket_chain<<<(unsigned)L.oblocks, kStepThreads, 0, st>>>(d_plans, n_plans, lut);
+        k_bucket_chain<<<capped(L.oblocks, 8), kStepThreads, 0, st>>>(d_plans, n_plans, lut, L.oblocks);
         EDGC_LAUNCH_CHECK();
     }
     // head-table path (Floyd plans, N > 2^25, or EDGC_PLAN_HEADTABLE): index + resolve groups of
