@@ -65,6 +65,8 @@ struct MatDev {
     double *p_tmp;    // [m][r] CholQR intermediate
     int32_t wide;     // wide = 1: tiled GEMM path (r > 8 or unaligned)
     int32_t zw;       // Z path: columns per CTA of the cluster (multiple of 4, <= kTCW)
+    int32_t al4;      // g and w rows float4-aligned (n, ld_g multiples of 4, 16-byte bases)
+    int32_t pad3_;
 };
 
 // Z-path work item: one row strip of one matrix, processed by one cluster
@@ -928,12 +930,12 @@ __global__ void __launch_bounds__(kGThreads) k_gemm(const MatDev *mats, const Ge
     const int r = M.r, rres = M.r_res;
     const int64_t MM = OP == 0 ? m : (OP == 1 ? n : m);
     const int64_t NN = OP == 2 ? n : r;
-    __shared__ float As[kGK][kGT + 4];
-    __shared__ float Bs[kGK][kGT + 4];
-    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
     // P_raw and Q partials accumulate exact fp32 products in fp64: at high rank
     // P_raw can be ill-conditioned and its rounding is amplified by cond(R)
     typedef typename std::conditional<OP == 2, float, double>::type AccT;
+    __shared__ float As[kGK][kGT + 4];
+    __shared__ float Bs[kGK][kGT + 4];
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
     AccT acc[4][4] = {};
     for (int64_t k0 = t.k0; k0 < t.k1; k0 += kGK) {
         // A tile: kGT rows x kGK cols
@@ -974,6 +976,26 @@ __global__ void __launch_bounds__(kGThreads) k_gemm(const MatDev *mats, const Ge
         __syncthreads();
     }
     bool bad = false;
+    if (OP == 2 && M.al4) {
+        // error-feedback epilogue, float4 rows: each thread's 4 columns are adjacent (n % 4 == 0)
+        const int64_t gj = t.j0 + tx * 4;
+        if (gj < NN) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t gi = t.i0 + ty * 4 + u;
+                if (gi >= MM) continue;
+                const float4 g4 = __ldcs(reinterpret_cast<const float4 *>(M.g + gi * M.ld_g + gj));
+                float4 *wp = reinterpret_cast<float4 *>(M.w + gi * n + gj);
+                const float4 w4 = __ldcs(wp);
+                const float x0 = g4.x + (w4.x - (float)acc[u][0]), x1 = g4.y + (w4.y - (float)acc[u][1]);
+                const float x2 = g4.z + (w4.z - (float)acc[u][2]), x3 = g4.w + (w4.w - (float)acc[u][3]);
+                bad |= !(isfinite(x0) && isfinite(x1) && isfinite(x2) && isfinite(x3));
+                __stcs(wp, make_float4(x0, x1, x2, x3));
+            }
+        }
+        if (__syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
+        return;
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -1119,8 +1141,9 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.p_out = d.p_out; M.q_out = d.q_out;
         M.m = d.m; M.n = d.n; M.ld_g = d.ld_g; M.r = d.r; M.r_res = d.r_res; M.ld_q = d.ld_q;
         M.precond = d.precond; M.ld_s = d.ld_s;
-        const bool v4 = (d.n % 4 == 0) && (d.ld_g % 4 == 0) && ((uintptr_t)d.g % 16 == 0) &&
-                        ((uintptr_t)d.w % 16 == 0) && std::max(d.r, d.r_res) <= kNarrow;
+        M.al4 = (d.n % 4 == 0) && (d.ld_g % 4 == 0) && ((uintptr_t)d.g % 16 == 0) &&
+                        ((uintptr_t)d.w % 16 == 0);
+        const bool v4 = M.al4 && std::max(d.r, d.r_res) <= kNarrow;
         M.vec = v4 ? 4 : 1;
         static const bool z_off = std::getenv("EDGC_NO_ZPATH") != nullptr;
         // cluster size: smallest of {1, 2, 3, 6, 7, 8} covering n with <= kTCW columns per CTA
@@ -1312,6 +1335,48 @@ __global__ void __launch_bounds__(kRThreads) k_recon(const ReconDev *descs, cons
                 if (i < t.row1) __stcs(D.out + i * D.ld_out + j, acc[rr] * D.scale);
             }
         }
+    }
+}
+
+// W*r > 8 with float4-aligned output: 64x64 output tiles, K = W*r staged through
+// shared memory 16 at a time, 4x4 fp32 outputs per thread (the same fma order over
+// (worker, k) as k_recon), float4 streaming stores.
+__global__ void __launch_bounds__(kGThreads) k_recon_tiled(const ReconDev *descs, const RTile *tiles) {
+    const RTile t = tiles[blockIdx.x];
+    const ReconDev D = descs[t.d];
+    const int r = D.r, K = D.r * D.n_ranks;
+    __shared__ float As[kGK][kGT + 4];
+    __shared__ float Bs[kGK][kGT + 4];
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < K; k0 += kGK) {
+        for (int e = tid; e < kGT * kGK; e += kGThreads) {
+            const int kk = e % kGK, ii = e / kGK, wk = k0 + kk;
+            const int64_t i = t.row0 + ii, j = t.col0 + ii;
+            As[kk][ii] = (i < t.row1 && wk < K) ? __ldg(D.p + (int64_t)(wk / r) * D.p_stride + i * r + wk % r) : 0.f;
+            Bs[kk][ii] = (j < t.col1 && wk < K) ? __ldg(D.q + (int64_t)(wk / r) * D.q_stride + j * r + wk % r) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kGK; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { a[u] = As[kk][ty * 4 + u]; b[u] = Bs[kk][tx * 4 + u]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+    const int64_t j = t.col0 + tx * 4;
+    if (j >= t.col1) return;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t i = t.row0 + ty * 4 + u;
+        if (i >= t.row1) continue;
+        __stcs(reinterpret_cast<float4 *>(D.out + i * D.ld_out + j),
+               make_float4(acc[u][0] * D.scale, acc[u][1] * D.scale, acc[u][2] * D.scale, acc[u][3] * D.scale));
     }
 }
 
@@ -1516,12 +1581,14 @@ struct RPlan {
     std::vector<RTile> tiles, tiles4;
     int64_t bytes = 0;
     ReconDev *dd = nullptr;
-    RTile *dt = nullptr, *dt4 = nullptr;
+    RTile *dt = nullptr, *dt4 = nullptr, *dtT = nullptr;
+    std::vector<RTile> tilesT;        // k_recon_tiled (W*r > 8, float4-aligned output)
 };
 int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
     Arena a(ws, INT64_MAX);
     P.tiles.clear();
     P.tiles4.clear();
+    P.tilesT.clear();
     P.d.resize(n);
     P.dd = a.take<ReconDev>(n);
     for (int k = 0; k < n; ++k) {
@@ -1535,6 +1602,10 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
             for (int64_t c0 = 0; c0 < s.n; c0 += kV4Cols)
                 for (int64_t r0 = 0; r0 < s.m; r0 += kV4TileRows)
                     P.tiles4.push_back(RTile{k, c0, std::min(s.n, c0 + kV4Cols), r0, std::min(s.m, r0 + kV4TileRows)});
+        } else if (s.n % 4 == 0 && s.ld_out % 4 == 0 && ((uintptr_t)s.out % 16 == 0)) {
+            for (int64_t r0 = 0; r0 < s.m; r0 += kGT)
+                for (int64_t c0 = 0; c0 < s.n; c0 += kGT)
+                    P.tilesT.push_back(RTile{k, c0, std::min(s.n, c0 + kGT), r0, std::min(s.m, r0 + kGT)});
         } else {
             for (int64_t c0 = 0; c0 < s.n; c0 += kRThreads)
                 for (int64_t r0 = 0; r0 < s.m; r0 += kRTileRows)
@@ -1543,6 +1614,7 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
     }
     P.dt = a.take<RTile>(P.tiles.size());
     P.dt4 = a.take<RTile>(P.tiles4.size());
+    P.dtT = a.take<RTile>(P.tilesT.size());
     P.bytes = a.off;
     return EDGC_OK;
 }
@@ -1585,6 +1657,9 @@ extern "C" int edgc_recon_plan_bind(edgc_recon_plan *h, void *ws, int64_t ws_byt
     if (!P.tiles4.empty())
         EDGC_CUDA_TRY(
             cudaMemcpyAsync(P.dt4, P.tiles4.data(), sizeof(RTile) * P.tiles4.size(), cudaMemcpyHostToDevice, st));
+    if (!P.tilesT.empty())
+        EDGC_CUDA_TRY(
+            cudaMemcpyAsync(P.dtT, P.tilesT.data(), sizeof(RTile) * P.tilesT.size(), cudaMemcpyHostToDevice, st));
     EDGC_CUDA_TRY(cudaStreamSynchronize(st));
     return EDGC_OK;
 }
@@ -1604,6 +1679,10 @@ extern "C" int edgc_recon_plan_run(edgc_recon_plan *h, void *stream) {
         else if (h->wr <= 8) k_recon<8><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
         else if (h->wr <= 16) k_recon<16><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
         else k_recon<32><<<grid, kRThreads, 0, st>>>(h->P.dd, h->P.dt);
+        EDGC_LAUNCH_CHECK();
+    }
+    if (!h->P.tilesT.empty()) {
+        k_recon_tiled<<<(unsigned)h->P.tilesT.size(), kGThreads, 0, st>>>(h->P.dd, h->P.dtT);
         EDGC_LAUNCH_CHECK();
     }
     return EDGC_OK;
