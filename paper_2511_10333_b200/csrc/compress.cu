@@ -1015,6 +1015,68 @@ __global__ void __launch_bounds__(kGThreads) k_gemm(const MatDev *mats, const Ge
     if (OP == 2 && __syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
 }
 
+// Skinny fp64-accumulating GEMMs of the wide path with the output tile matched
+// to the rank: OP 0 P_raw partial = W[:, K-chunk] q_warm[K-chunk, :], OP 1 Q
+// partial = W[K-chunk, :]^T P[K-chunk, :].  BM x BN outputs per CTA (BM * BN =
+// 4096, 4x4 per thread); A staged as fp32, the small B tile pre-converted to fp64.
+template <int OP, int BM, int BN>
+__global__ void __launch_bounds__(kGThreads) k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
+    constexpr int TX = BN / 4;
+    static_assert((BM / 4) * TX == kGThreads, "4x4 outputs per thread");
+    const GemmTile t = tiles[blockIdx.x];
+    const MatDev &M = mats[t.mat];
+    if (OP == 1) {
+        const int st = status[t.mat];
+        if ((st & 1) || (M.zmode && !(st & 2))) return;
+    }
+    const int64_t n = M.n, m = M.m;
+    const int r = M.r;
+    const int64_t MM = OP == 0 ? m : n;
+    const float *__restrict__ w = M.w;
+    const float *__restrict__ bsrc = OP == 0 ? M.q_warm : M.p_out;
+    const int64_t ldb = OP == 0 ? M.ld_q : r;
+    __shared__ float As[kGK][BM + 4];
+    __shared__ double Bs[kGK][BN + 2];
+    const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+    double acc[4][4] = {};
+    for (int64_t k0 = t.k0; k0 < t.k1; k0 += kGK) {
+        for (int e = tid; e < BM * kGK; e += kGThreads) {
+            int ii, kk;
+            if (OP == 1) { ii = e % BM; kk = e / BM; } else { kk = e % kGK; ii = e / kGK; }
+            const int64_t gi = t.i0 + ii, gk = k0 + kk;
+            float v = 0.f;
+            if (gi < MM && gk < t.k1) v = OP == 0 ? w[gi * n + gk] : w[gk * n + gi];
+            As[kk][ii] = v;
+        }
+        for (int e = tid; e < BN * kGK; e += kGThreads) {
+            const int jj = e % BN, kk = e / BN;
+            const int64_t gj = t.j0 + jj, gk = k0 + kk;
+            Bs[kk][jj] = (gj < r && gk < t.k1) ? (double)bsrc[gk * ldb + gj] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kGK; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { a[u] = (double)As[kk][ty * 4 + u]; b[u] = Bs[kk][tx * 4 + u]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t gi = t.i0 + ty * 4 + u, gj = t.j0 + tx * 4 + v;
+            if (gi >= MM || gj >= r) continue;
+            if (OP == 0) M.p_part[((int64_t)t.split * m + gi) * r + gj] = acc[u][v];
+            else M.q_part[((int64_t)t.split * n + gi) * r + gj] = acc[u][v];
+        }
+}
+
 // ------------------------------------------------------------------ pass 2
 // Q partial over this tile's rows: thread owns VEC columns x RMAX ranks;
 // fp32 FMA over 32-row groups, fp64 across groups.
@@ -1111,12 +1173,14 @@ struct Plan {
     std::vector<MatDev> mats;
     std::vector<Tile> t1v4, t1v1, t2v4, t2v1;
     std::vector<ZTile> tz[9];          // Z-path items grouped by cluster size 1..8
-    std::vector<GemmTile> gw, gp, gq;  // wide path: EF update, P_raw, Q tiles
+    std::vector<GemmTile> gw, gp, gq;  // wide path: EF update, P_raw and Q tiles for r > 32
+    std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles for r <= 16 (256x16) and <= 32 (128x32)
     int64_t bytes = 0;
     MatDev *d_mats = nullptr;
     Tile *d_t1v4 = nullptr, *d_t1v1 = nullptr, *d_t2v4 = nullptr, *d_t2v1 = nullptr;
     ZTile *d_tz[9] = {};
     GemmTile *d_gw = nullptr, *d_gp = nullptr, *d_gq = nullptr;
+    GemmTile *d_sp[3] = {}, *d_sq[3] = {};
     int rmax4 = 0, rmax1 = 0;
 };
 
@@ -1165,15 +1229,19 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         if (M.wide) {
             for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
                 for (int64_t j0 = 0; j0 < d.n; j0 += kGT) P.gw.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
+            // skinny GEMM tile shape matched to the rank (r > 32: the 64x64 k_gemm tiles)
+            const int cfg = d.r <= 16 ? 0 : (d.r <= 32 ? 1 : 2);
+            const int BM = cfg == 0 ? 256 : (cfg == 1 ? 128 : kGT), BN = cfg == 0 ? 16 : (cfg == 1 ? 32 : kGT);
+            std::vector<GemmTile> &tp = cfg == 2 ? P.gp : P.sp[cfg], &tq = cfg == 2 ? P.gq : P.sq[cfg];
             for (int32_t c = 0; c < M.nchunk1; ++c)
-                for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
-                    for (int64_t j0 = 0; j0 < d.r; j0 += kGT)
-                        P.gp.push_back(GemmTile{k, c, i0, j0, c * kWideSplitK, std::min(d.n, (c + 1) * kWideSplitK)});
+                for (int64_t i0 = 0; i0 < d.m; i0 += BM)
+                    for (int64_t j0 = 0; j0 < d.r; j0 += BN)
+                        tp.push_back(GemmTile{k, c, i0, j0, c * kWideSplitK, std::min(d.n, (c + 1) * kWideSplitK)});
             for (int32_t b = 0; b < M.nblk2; ++b)
-                for (int64_t i0 = 0; i0 < d.n; i0 += kGT)
-                    for (int64_t j0 = 0; j0 < d.r; j0 += kGT)
-                        P.gq.push_back(GemmTile{k, b, i0, j0, (int64_t)b * kP2Rows,
-                                                std::min(d.m, (int64_t)(b + 1) * kP2Rows)});
+                for (int64_t i0 = 0; i0 < d.n; i0 += BM)
+                    for (int64_t j0 = 0; j0 < d.r; j0 += BN)
+                        tq.push_back(GemmTile{k, b, i0, j0, (int64_t)b * kP2Rows,
+                                              std::min(d.m, (int64_t)(b + 1) * kP2Rows)});
             continue;
         }
         (v4 ? P.rmax4 : P.rmax1) = std::max(v4 ? P.rmax4 : P.rmax1, std::max(d.r, d.r_res));
@@ -1206,6 +1274,10 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     P.d_t2v4 = a.take<Tile>(P.t2v4.size());
     P.d_t2v1 = a.take<Tile>(P.t2v1.size());
     for (int c = 1; c <= 8; ++c) P.d_tz[c] = a.take<ZTile>(P.tz[c].size());
+    for (int c = 0; c < 3; ++c) {
+        P.d_sp[c] = a.take<GemmTile>(P.sp[c].size());
+        P.d_sq[c] = a.take<GemmTile>(P.sq[c].size());
+    }
     P.d_gw = a.take<GemmTile>(P.gw.size());
     P.d_gp = a.take<GemmTile>(P.gp.size());
     P.d_gq = a.take<GemmTile>(P.gq.size());
@@ -1518,6 +1590,10 @@ extern "C" int edgc_compress_plan_bind(edgc_compress_plan *h, void *ws, int64_t 
     EDGC_CUDA_TRY(upg(P.d_gw, P.gw));
     EDGC_CUDA_TRY(upg(P.d_gp, P.gp));
     EDGC_CUDA_TRY(upg(P.d_gq, P.gq));
+    for (int c = 0; c < 3; ++c) {
+        EDGC_CUDA_TRY(upg(P.d_sp[c], P.sp[c]));
+        EDGC_CUDA_TRY(upg(P.d_sq[c], P.sq[c]));
+    }
     // the host staging vectors stay alive in the plan; make the upload complete
     // before the caller could destroy or rebind it
     EDGC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1537,6 +1613,14 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if ((rc = launch_pass1(P, false, status_dev, st))) return rc;
         if ((rc = launch_pass1z(P, status_dev, st))) return rc;
         if ((rc = launch_gemm<2>(P, P.gw, P.d_gw, status_dev, st))) return rc;
+        if (!P.sp[0].empty()) {
+            k_skinny<0, 256, 16><<<(unsigned)P.sp[0].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sp[0], status_dev);
+            EDGC_LAUNCH_CHECK();
+        }
+        if (!P.sp[1].empty()) {
+            k_skinny<0, 128, 32><<<(unsigned)P.sp[1].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sp[1], status_dev);
+            EDGC_LAUNCH_CHECK();
+        }
         if ((rc = launch_gemm<0>(P, P.gp, P.d_gp, status_dev, st))) return rc;
     }
     if (phases & EDGC_PHASE_FACTOR) {
@@ -1546,6 +1630,14 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
     if (phases & EDGC_PHASE_PASS2) {
         if ((rc = launch_pass2(P, true, status_dev, st))) return rc;
         if ((rc = launch_pass2(P, false, status_dev, st))) return rc;
+        if (!P.sq[0].empty()) {
+            k_skinny<1, 256, 16><<<(unsigned)P.sq[0].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sq[0], status_dev);
+            EDGC_LAUNCH_CHECK();
+        }
+        if (!P.sq[1].empty()) {
+            k_skinny<1, 128, 32><<<(unsigned)P.sq[1].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sq[1], status_dev);
+            EDGC_LAUNCH_CHECK();
+        }
         if ((rc = launch_gemm<1>(P, P.gq, P.d_gq, status_dev, st))) return rc;
     }
     if (phases & EDGC_PHASE_FINALIZE) {
