@@ -1452,53 +1452,78 @@ __global__ void __launch_bounds__(kGThreads) k_recon_tiled(const ReconDev *descs
     }
 }
 
-// float4 variant for W*r <= 8 (the DP-average hot case): each thread owns 4
+// float4 variant for W*r <= 32 (the DP-average hot case, r = 4 up to W = 8): each thread owns 4
 // adjacent columns and kV4Rows rows per pass, with Q (4 x W*r) in registers and
 // P rows broadcast from shared memory; 512-byte coalesced streaming stores.
 constexpr int kV4Threads = 128;
 constexpr int kV4Cols = 4 * kV4Threads;
 constexpr int kV4Rows = 8;
-constexpr int kV4TileRows = 64;
+constexpr int kV4TileRows = 256;   // rows per tile: amortises the per-thread Q loads
 
-template <int WR>
-__global__ void __launch_bounds__(kV4Threads) k_recon4(const ReconDev *descs, const RTile *tiles) {
+// VC adjacent columns per thread (4, or 2 when W*r = 32 to keep Q in registers);
+// kV4Cols = 512 columns per tile either way.
+template <int WR, int VC>
+__global__ void __launch_bounds__(kV4Cols / VC) k_recon4(const ReconDev *descs, const RTile *tiles) {
+    constexpr int NT = kV4Cols / VC;
     const RTile t = tiles[blockIdx.x];
     const ReconDev D = descs[t.d];
     const int r = D.r, wr = D.r * D.n_ranks;
-    const int64_t j0 = t.col0 + 4 * threadIdx.x;
+    const int64_t j0 = t.col0 + VC * threadIdx.x;
     const bool active = j0 < t.col1;
-    __shared__ float s_p[kV4TileRows][WR];
-    for (int e = threadIdx.x; e < kV4TileRows * WR; e += kV4Threads) {
-        const int rr = e / WR, c = e % WR;
+    // P tile transposed ([k][row]): one 16-byte shared read gives 4 rows of one k
+    __shared__ __align__(16) float s_pT[WR][kV4TileRows];
+    // thread = (row, rank): its r consecutive P values; (worker, k) indexed incrementally (no div/mod)
+    for (int e = threadIdx.x; e < kV4TileRows * D.n_ranks; e += NT) {
+        const int rr = e % kV4TileRows, w = e / kV4TileRows;
         const int64_t i = t.row0 + rr;
-        s_p[rr][c] = (i < t.row1 && c < wr) ? D.p[(int64_t)(c / r) * D.p_stride + i * r + (c % r)] : 0.f;
+        const float *src = D.p + (int64_t)w * D.p_stride + i * r;
+        for (int k = 0; k < r; ++k) s_pT[w * r + k][rr] = i < t.row1 ? src[k] : 0.f;
     }
-    float q[4][WR];
+    for (int e = threadIdx.x; e < kV4TileRows * (WR - wr); e += NT)   // zero padding columns
+        s_pT[wr + e / kV4TileRows][e % kV4TileRows] = 0.f;
+    float q[VC][WR];
 #pragma unroll
-    for (int v = 0; v < 4; ++v)
+    for (int v = 0; v < VC; ++v) {
+        const float *qp = D.q + (j0 + v) * r;
+        int k = 0;
+        int64_t wo = 0;
 #pragma unroll
-        for (int c = 0; c < WR; ++c)
-            q[v][c] = (active && c < wr) ? __ldg(D.q + (int64_t)(c / r) * D.q_stride + (j0 + v) * r + (c % r)) : 0.f;
+        for (int c = 0; c < WR; ++c) {
+            q[v][c] = (active && c < wr) ? __ldg(qp + wo + k) : 0.f;
+            if (++k == r) { k = 0; wo += D.q_stride; }
+        }
+    }
     __syncthreads();
     if (!active) return;
     for (int64_t row = t.row0; row < t.row1; row += kV4Rows) {
-        float acc[kV4Rows][4];
+        const int lr = (int)(row - t.row0);
+        float acc[kV4Rows][VC];
 #pragma unroll
-        for (int rr = 0; rr < kV4Rows; ++rr) {
+        for (int rr = 0; rr < kV4Rows; ++rr)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                float a = 0.f;
+            for (int v = 0; v < VC; ++v) acc[rr][v] = 0.f;
+        // per output the fma order over (worker, k) is c ascending
 #pragma unroll
-                for (int c = 0; c < WR; ++c) a = fmaf(s_p[row - t.row0 + rr][c], q[v][c], a);
-                acc[rr][v] = a * D.scale;
-            }
+        for (int c = 0; c < WR; ++c) {
+            const float4 pa = *reinterpret_cast<const float4 *>(&s_pT[c][lr]);
+            const float4 pb = *reinterpret_cast<const float4 *>(&s_pT[c][lr + 4]);
+            const float pr[kV4Rows] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+#pragma unroll
+            for (int rr = 0; rr < kV4Rows; ++rr)
+#pragma unroll
+                for (int v = 0; v < VC; ++v) acc[rr][v] = fmaf(pr[rr], q[v][c], acc[rr][v]);
         }
 #pragma unroll
         for (int rr = 0; rr < kV4Rows; ++rr) {
             const int64_t i = row + rr;
-            if (i < t.row1)
+            if (i >= t.row1) continue;
+            if (VC == 4)
                 __stcs(reinterpret_cast<float4 *>(D.out + i * D.ld_out + j0),
-                       make_float4(acc[rr][0], acc[rr][1], acc[rr][2], acc[rr][3]));
+                       make_float4(acc[rr][0] * D.scale, acc[rr][VC > 1 ? 1 : 0] * D.scale,
+                                   acc[rr][VC > 2 ? 2 : 0] * D.scale, acc[rr][VC > 3 ? 3 : 0] * D.scale));
+            else
+                __stcs(reinterpret_cast<float2 *>(D.out + i * D.ld_out + j0),
+                       make_float2(acc[rr][0] * D.scale, acc[rr][VC > 1 ? 1 : 0] * D.scale));
         }
     }
 }
@@ -1689,7 +1714,7 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
                      "recon desc %d: bad arguments", k);
         P.d[k] = ReconDev{s.p, s.q, s.out, s.m, s.n, s.ld_out, s.p_rank_stride, s.q_rank_stride, s.r, s.n_ranks,
                           s.scale};
-        const bool v4 = s.r * s.n_ranks <= 8 && s.n % 4 == 0 && s.ld_out % 4 == 0 && ((uintptr_t)s.out % 16 == 0);
+        const bool v4 = s.r * s.n_ranks <= 32 && s.n % 4 == 0 && s.ld_out % 4 == 0 && ((uintptr_t)s.out % 16 == 0);
         if (v4) {
             for (int64_t c0 = 0; c0 < s.n; c0 += kV4Cols)
                 for (int64_t r0 = 0; r0 < s.m; r0 += kV4TileRows)
@@ -1726,7 +1751,7 @@ extern "C" int edgc_recon_plan_create(const edgc_recon_desc *descs, int n, edgc_
     if (rc != EDGC_OK) { delete h; return rc; }
     for (int k = 0; k < n; ++k) {
         const int wr = descs[k].r * descs[k].n_ranks;
-        if (wr <= 8) h->wr4 = std::max(h->wr4, wr);
+        if (wr <= 32) h->wr4 = std::max(h->wr4, wr);
         h->wr = std::max(h->wr, wr);
     }
     *out = h;
@@ -1761,8 +1786,10 @@ extern "C" int edgc_recon_plan_run(edgc_recon_plan *h, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (!h->P.tiles4.empty()) {
         const unsigned g4 = (unsigned)h->P.tiles4.size();
-        if (h->wr4 <= 4) k_recon4<4><<<g4, kV4Threads, 0, st>>>(h->P.dd, h->P.dt4);
-        else k_recon4<8><<<g4, kV4Threads, 0, st>>>(h->P.dd, h->P.dt4);
+        if (h->wr4 <= 4) k_recon4<4, 4><<<g4, kV4Cols / 4, 0, st>>>(h->P.dd, h->P.dt4);
+        else if (h->wr4 <= 8) k_recon4<8, 4><<<g4, kV4Cols / 4, 0, st>>>(h->P.dd, h->P.dt4);
+        else if (h->wr4 <= 16) k_recon4<16, 4><<<g4, kV4Cols / 4, 0, st>>>(h->P.dd, h->P.dt4);
+        else k_recon4<32, 2><<<g4, kV4Cols / 2, 0, st>>>(h->P.dd, h->P.dt4);
         EDGC_LAUNCH_CHECK();
     }
     if (!h->P.tiles.empty()) {

@@ -1,4 +1,7 @@
-"""GPU, >= 2 devices: the NCCL factor exchange against the sequential reference (tools/dp_check.py)."""
+"""GPU, >= 2 devices: the NCCL factor exchange against the sequential reference (tools/dp_check.py).
+
+W = 2 exercises the W*r <= 8 reconstruction, W = 4 the W*r = 16 one.
+"""
 
 import os
 import subprocess
@@ -12,10 +15,12 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_two_gpu_exchange_matches_reference():
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tools", "dp_check.py")]
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_exchange_matches_reference(world):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={29533 + world}", os.path.join(ROOT, "tools", "dp_check.py")]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
     assert '"ok": true' in res.stdout
