@@ -65,6 +65,8 @@ def parse_args():
     ap.add_argument("--entropy", choices=["prefetch", "inline", "off"], default="prefetch",
                     help="diagnostics: entropy plans built ahead on a side stream (default), inline, or no tracker")
     ap.add_argument("--hi-prio", action="store_true", help="diagnostics: run the step on a high-priority stream")
+    ap.add_argument("--no-fuse-entropy", dest="fuse_entropy", action="store_false",
+                    help="diagnostics: separate Gaussian pass instead of gathering the statistics in pass 1")
     ap.add_argument("--cpu-steps", type=int, default=6, help="EF steps in the bounded CPU sample")
     return ap.parse_args()
 
@@ -206,6 +208,7 @@ def config_dict(args, shapes):
             "rank": args.rank, "alpha": args.alpha, "beta": args.beta, "estimator": "gaussian_plugin",
             "l2": "inputs 9.2 GB/GPU >> 126 MB L2 (no flush needed)" if args.model == "2.5B" and args.layers is None
             else "inputs larger than L2", "parallelism": f"dp{args.gpus}",
+            "entropy_stats": "gathered in pass 1" if getattr(args, "fuse_entropy", True) else "separate Gaussian pass",
             "entropy_plans": {"prefetch": "side stream, built during the preceding iterations",
                               "inline": "built inside the sampled iteration", "off": "tracker disabled"}[args.entropy]}
 
@@ -255,6 +258,8 @@ def run_ours(args):
 
     def one_step(t, ev=None):
         marks = []
+        # sampled iteration: pass 1 also gathers the Gaussian statistics of the sampled elements
+        fused = tracker.fused_request(t, eng, eng.grads) if tracker is not None and args.fuse_entropy else None
         if ev is not None:
             marks = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
             marks[0].record(stream)
@@ -282,7 +287,7 @@ def run_ours(args):
             if ev is not None and sampled:
                 ev["ent0"].append(torch.cuda.Event(enable_timing=True))
                 ev["ent0"][-1].record(stream)
-            tracker.observe(t, eng.grads)   # non-sampled iterations only schedule the next plan
+            tracker.observe(t, eng.grads, fused=fused)   # non-sampled iterations only schedule the next plan
             if ev is not None and sampled:
                 ev["ent1"].append(torch.cuda.Event(enable_timing=True))
                 ev["ent1"][-1].record(stream)

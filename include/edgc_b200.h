@@ -173,6 +173,29 @@ int edgc_compress_plan_run(edgc_compress_plan *plan, double col_tol, int32_t *st
                            void *stream);
 void edgc_compress_plan_destroy(edgc_compress_plan *plan);
 
+/* Fused sampled-iteration statistics (EntropyTracker.observe, entropy.py:168-177,
+ * with the Gaussian plug-in on worker 0's raw gradients): pass 1 already streams
+ * every raw gradient element, so on a sampled iteration it can also accumulate
+ * the fp64 shifted sums {sum (x-K), sum (x-K)^2} of the elements whose
+ * membership bit is set (K = the first sample, as edgc_entropy_gaussian).
+ * sample_slots: partial slots per matrix, 0 when some matrix of the plan is
+ * off the Z path (the caller then uses edgc_entropy_gaussian).
+ * set_sampling arms the NEXT run that includes EDGC_PHASE_PASS1: descs[k] for
+ * every matrix of the plan (bitmap NULL = not sampled), partials_dev =
+ * double[n][slots][2], zeroed by the caller (a matrix writes only the slots
+ * of its own CTAs).  edgc_entropy_gaussian_partials
+ * reduces the slots in fixed order into h_out / status_dev as
+ * edgc_entropy_gaussian does (counts_dev: int64[n] sample counts). */
+typedef struct {
+    const uint32_t *bitmap;   /* device membership bits [ceil(m*n/32)] (row-major flat index)  */
+    const int32_t *first;     /* device: flat index of the first sample (the shift's element) */
+} edgc_sample_desc;
+int64_t edgc_compress_plan_sample_slots(const edgc_compress_plan *plan);
+int edgc_compress_plan_set_sampling(edgc_compress_plan *plan, const edgc_sample_desc *descs, int n,
+                                    double *partials_dev, void *stream);
+int edgc_entropy_gaussian_partials(const double *partials_dev, int64_t slots, const int64_t *counts_dev, int n,
+                                   double *h_out, int32_t *status_dev, void *stream);
+
 int64_t edgc_compress_workspace_bytes(const edgc_compress_desc *descs, int n);
 /* col_tol: relative dead-column tolerance (reference: 1e-12 at fp64,
  * compressor.py:23; see DESIGN.md for the fp32 value).

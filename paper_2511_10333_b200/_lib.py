@@ -45,6 +45,10 @@ class GaussDesc(ctypes.Structure):
     _fields_ = [("src", c_vp), ("idx", c_vp), ("count", c_i64), ("bitmap", c_vp), ("n_elems", c_i64)]
 
 
+class SampleDesc(ctypes.Structure):
+    _fields_ = [("bitmap", c_vp), ("first", c_vp)]
+
+
 class CompressDesc(ctypes.Structure):
     _fields_ = [("g", c_vp), ("w", c_vp), ("p_res", c_vp), ("q_res", c_vp), ("q_warm", c_vp), ("basis", c_vp),
                 ("p_out", c_vp), ("q_out", c_vp), ("precond", c_vp), ("m", c_i64), ("n", c_i64), ("ld_g", c_i64),
@@ -74,6 +78,9 @@ SIGNATURES = {
     "edgc_compress_plan_workspace_bytes": (c_i64, [c_vp]),
     "edgc_compress_plan_bind": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "edgc_compress_plan_run": (c_i32, [c_vp, c_f64, c_vp, c_i32, c_vp]),
+    "edgc_compress_plan_sample_slots": (c_i64, [c_vp]),
+    "edgc_compress_plan_set_sampling": (c_i32, [c_vp, ctypes.POINTER(SampleDesc), c_i32, c_vp, c_vp]),
+    "edgc_entropy_gaussian_partials": (c_i32, [c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "edgc_compress_plan_destroy": (None, [c_vp]),
     "edgc_compress_workspace_bytes": (c_i64, [ctypes.POINTER(CompressDesc), c_i32]),
     "edgc_compress": (c_i32, [ctypes.POINTER(CompressDesc), c_i32, c_f64, c_vp, c_vp, c_i64, c_vp]),

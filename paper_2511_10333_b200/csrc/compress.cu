@@ -69,6 +69,13 @@ struct MatDev {
     int32_t pad3_;
 };
 
+// fused sampled-iteration statistics of one matrix (edgc_compress_plan_set_sampling)
+struct SampDev {
+    const uint32_t *bitmap;   // membership bits, NULL = not sampled
+    const int32_t *first;     // flat index of the first sample (shift)
+    double *part;             // [slots][2] shifted sums of this matrix
+};
+
 // Z-path work item: one row strip of one matrix, processed by one cluster
 struct ZTile {
     int32_t mat, item;
@@ -285,7 +292,9 @@ struct TSmem {
     alignas(8) uint64_t prowready[kTRing];
 };
 
-__global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, const ZTile *tiles, int32_t *status) {
+template <bool SAMPLE>
+__global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, const ZTile *tiles, int32_t *status,
+                                                         const SampDev *samp) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TSmem &sm = *reinterpret_cast<TSmem *>(smem_raw);
     const uint32_t C = ptx::cluster_nctarank();
@@ -448,6 +457,16 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
 #pragma unroll
             for (int k = 0; k < 4; ++k) zacc[v][k] = 0.f;
         bool bad = false;
+        // sampled iteration: shifted sums of the raw gradient over the membership bits
+        double gs1 = 0.0, gs2 = 0.0, gK = 0.0;
+        const uint32_t *sbits = nullptr;
+        if (SAMPLE) {
+            sbits = samp[t.mat].bitmap;
+            if (sbits) {
+                const int64_t f = __ldg(samp[t.mat].first);
+                gK = (double)__ldg(gptr + (f / n) * ld_g + f % n);
+            }
+        }
         // round bb's x values wait in xs[bb % kTRing] (this thread's columns only) for the lagged Z update
         auto consume = [&](int bb) {
             const int q = bb % kTRing;
@@ -496,6 +515,15 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             load_pres(b + 1, pnext);
             if (chunk_cols > 0) ptx::mbar_wait_sleep<EDGC_CONS_SLEEP>(&sm.full[s], (b / kTStages) & 1);
             if (EDGC_P1_EARLYZ && !EDGC_P1_NOEXCH && b >= kTLag) consume(b - kTLag);
+            uint32_t sw[kTRB];
+            if (SAMPLE && sbits) {
+#pragma unroll
+                for (int rr = 0; rr < kTRB; ++rr) {
+                    const int lr = rr ^ fr;
+                    const int64_t e = (i0 + lr) * n + col0;   // 4-aligned: the 4 bits share a word
+                    sw[rr] = (active && lr < rows) ? (__ldg(sbits + (e >> 5)) >> (e & 31)) & 0xFu : 0u;
+                }
+            }
             double acc[kTV];
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) {
@@ -506,6 +534,15 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                 const float pp[4] = {pcur[rr].x, pcur[rr].y, pcur[rr].z, pcur[rr].w};
                 const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
                 const float ww[4] = {wv.x, wv.y, wv.z, wv.w};
+                if (SAMPLE && sbits) {
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        if ((sw[rr] >> v) & 1u) {
+                            const double d = (double)gg[v] - gK;
+                            gs1 += d;
+                            gs2 = fma(d, d, gs2);
+                        }
+                }
                 float xx[4];
                 double pk[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -557,6 +594,21 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
                     if (k < r) zpart_ptr[((int64_t)t.item * n + col0 + v) * r + k] = (double)zacc[v][k];
         }
         if (EDGC_CONS_FINITE && bad) atomicOr(status + t.mat, 1);
+        if (SAMPLE && sbits) {
+            // this CTA's slot: fixed-order sum over the consumer warps
+            __shared__ double s_gs[kTCons / 32][2];
+            gs1 = warp_sum(gs1);
+            gs2 = warp_sum(gs2);
+            if (lane == 0) { s_gs[warp][0] = gs1; s_gs[warp][1] = gs2; }
+            ptx::named_bar_sync(7, kTCons);
+            if (tid == 0) {
+                double a = 0.0, c = 0.0;
+                for (int w = 0; w < kTCons / 32; ++w) { a += s_gs[w][0]; c += s_gs[w][1]; }
+                double *dst = samp[t.mat].part + 2 * ((int64_t)t.item * C + me);
+                dst[0] = a;
+                dst[1] = c;
+            }
+        }
     }
 done:
     ptx::cluster_sync();  // no CTA leaves while a peer may still push into it
@@ -1182,6 +1234,10 @@ struct Plan {
     GemmTile *d_gw = nullptr, *d_gp = nullptr, *d_gq = nullptr;
     GemmTile *d_sp[3] = {}, *d_sq[3] = {};
     int rmax4 = 0, rmax1 = 0;
+    SampDev *d_samp = nullptr;          // fused sampling descriptors (workspace)
+    std::vector<SampDev> samp_host;
+    bool sample_armed = false;
+    int64_t sample_slots = 0;           // partial slots per matrix (0: some matrix off the Z path)
 };
 
 int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes, Plan &P) {
@@ -1269,6 +1325,16 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.fwork = a.take<double>(5 * (int64_t)M.r * M.r);
         M.p_tmp = a.take<double>(M.m * M.r);
     }
+    P.d_samp = a.take<SampDev>(n);
+    P.sample_slots = 0;
+    {
+        bool all_z = true;
+        for (int k = 0; k < n; ++k) {
+            all_z = all_z && P.mats[k].zmode;
+            if (P.mats[k].zmode) P.sample_slots = std::max<int64_t>(P.sample_slots, (int64_t)P.mats[k].nitems * P.mats[k].zc);
+        }
+        if (!all_z) P.sample_slots = 0;
+    }
     P.d_t1v4 = a.take<Tile>(P.t1v4.size());
     P.d_t1v1 = a.take<Tile>(P.t1v1.size());
     P.d_t2v4 = a.take<Tile>(P.t2v4.size());
@@ -1307,7 +1373,7 @@ int launch_gemm(const Plan &P, const std::vector<GemmTile> &h, const GemmTile *d
     return EDGC_OK;
 }
 
-int launch_pass1z(const Plan &P, int32_t *status, cudaStream_t st) {
+int launch_pass1z(const Plan &P, int32_t *status, bool sample, cudaStream_t st) {
     for (int c = 1; c <= 8; ++c) {
         if (P.tz[c].empty()) continue;
         cudaLaunchConfig_t cfg = {};
@@ -1324,11 +1390,18 @@ int launch_pass1z(const Plan &P, int32_t *status, cudaStream_t st) {
         cfg.numAttrs = 1;
         static bool attr_set = false;
         if (!attr_set) {
-            EDGC_CUDA_TRY(cudaFuncSetAttribute(k_pass1t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            EDGC_CUDA_TRY(cudaFuncSetAttribute(k_pass1t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sizeof(TSmem)));
+            EDGC_CUDA_TRY(cudaFuncSetAttribute(k_pass1t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)sizeof(TSmem)));
             attr_set = true;
         }
-        EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1t, (const MatDev *)P.d_mats, (const ZTile *)P.d_tz[c], status));
+        if (sample)
+            EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1t<true>, (const MatDev *)P.d_mats,
+                                             (const ZTile *)P.d_tz[c], status, (const SampDev *)P.d_samp));
+        else
+            EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1t<false>, (const MatDev *)P.d_mats,
+                                             (const ZTile *)P.d_tz[c], status, (const SampDev *)P.d_samp));
         EDGC_LAUNCH_CHECK();
     }
     return EDGC_OK;
@@ -1636,7 +1709,8 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         EDGC_CUDA_TRY(cudaMemsetAsync(status_dev, 0, sizeof(int32_t) * n, st));
         if ((rc = launch_pass1(P, true, status_dev, st))) return rc;
         if ((rc = launch_pass1(P, false, status_dev, st))) return rc;
-        if ((rc = launch_pass1z(P, status_dev, st))) return rc;
+        if ((rc = launch_pass1z(P, status_dev, P.sample_armed, st))) return rc;
+        h->P.sample_armed = false;   // set_sampling arms exactly one pass 1
         if ((rc = launch_gemm<2>(P, P.gw, P.d_gw, status_dev, st))) return rc;
         if (!P.sp[0].empty()) {
             k_skinny<0, 256, 16><<<(unsigned)P.sp[0].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sp[0], status_dev);
@@ -1669,6 +1743,26 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         k_finalize<<<dim3(16, n), 256, 0, st>>>(P.d_mats, status_dev);
         EDGC_LAUNCH_CHECK();
     }
+    return EDGC_OK;
+}
+
+extern "C" int64_t edgc_compress_plan_sample_slots(const edgc_compress_plan *h) {
+    return (h && h->P.d_mats) ? h->P.sample_slots : -1;
+}
+
+extern "C" int edgc_compress_plan_set_sampling(edgc_compress_plan *h, const edgc_sample_desc *descs, int n,
+                                               double *partials_dev, void *stream) {
+    EDGC_REQUIRE(h && h->P.d_mats && descs && partials_dev, "edgc_compress_plan_set_sampling: bad arguments");
+    Plan &P = h->P;
+    EDGC_REQUIRE(n == (int)h->descs.size(), "edgc_compress_plan_set_sampling: %d descriptors for a %d-matrix plan", n,
+                 (int)h->descs.size());
+    EDGC_REQUIRE(P.sample_slots > 0, "edgc_compress_plan_set_sampling: a matrix of this plan is off the Z path");
+    P.samp_host.resize(n);
+    for (int k = 0; k < n; ++k)
+        P.samp_host[k] = SampDev{descs[k].bitmap, descs[k].first, partials_dev + 2 * P.sample_slots * (int64_t)k};
+    EDGC_CUDA_TRY(cudaMemcpyAsync(P.d_samp, P.samp_host.data(), sizeof(SampDev) * n, cudaMemcpyHostToDevice,
+                                  (cudaStream_t)stream));
+    P.sample_armed = true;
     return EDGC_OK;
 }
 

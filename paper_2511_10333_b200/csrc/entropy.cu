@@ -170,6 +170,24 @@ __global__ void k_gauss_finish(const GaussDev *descs, int n, const double2 *part
     h_out[i] = log(sigma) + kGaussConst;
 }
 
+// fused partials (edgc_compress_plan_set_sampling): slots summed in fixed order
+__global__ void k_gauss_finish_slots(const double *part, int64_t slots, const int64_t *counts, int n, double *h_out,
+                                     int32_t *status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t cnt = counts[i];
+    if (cnt < 2) { status[i] = EDGC_EINVAL; h_out[i] = NAN; return; }
+    double s1 = 0.0, s2 = 0.0;
+    for (int64_t b = 0; b < slots; ++b) { s1 += part[(i * slots + b) * 2]; s2 += part[(i * slots + b) * 2 + 1]; }
+    const double nn = (double)cnt;
+    double var = (s2 - s1 * (s1 / nn)) / (nn - 1.0);
+    if (var < 0.0) var = 0.0;
+    const double sigma = sqrt(var);
+    if (sigma == 0.0) { status[i] = EDGC_EDEGENERATE; h_out[i] = NAN; return; }
+    status[i] = EDGC_OK;
+    h_out[i] = log(sigma) + kGaussConst;
+}
+
 // --------------------------------------------------------------- histogram
 template <typename T> struct KeyOf;
 template <> struct KeyOf<float> {
@@ -575,4 +593,15 @@ extern "C" int edgc_entropy_histogram(int dtype, const void *samples, int64_t co
                                     (long long *)counts_dev, edges_dev, result_dev, status_dev, ws, st);
     return run_histogram<double>((const double *)samples, count, inv_cbrt_n, fixed_bins, bins_cap,
                                  (long long *)counts_dev, edges_dev, result_dev, status_dev, ws, st);
+}
+
+extern "C" int edgc_entropy_gaussian_partials(const double *partials_dev, int64_t slots, const int64_t *counts_dev,
+                                              int n, double *h_out, int32_t *status_dev, void *stream) {
+    EDGC_REQUIRE(n >= 0 && slots >= 1 && (n == 0 || (partials_dev && counts_dev && h_out && status_dev)),
+                 "edgc_entropy_gaussian_partials: bad arguments");
+    if (n == 0) return EDGC_OK;
+    k_gauss_finish_slots<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(partials_dev, slots, counts_dev, n, h_out,
+                                                                           status_dev);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
 }

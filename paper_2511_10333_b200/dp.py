@@ -79,7 +79,11 @@ class EdgcDataParallel:
             for dst, src in zip(eng.grads, grads):
                 if dst.data_ptr() != src.data_ptr():
                     dst.copy_(src, non_blocking=True)
+        fused = None
         if self.ctl.phase == PHASE_ACTIVE:
+            if self.tracker is not None:
+                # sampled iteration: pass 1 also gathers the sample's Gaussian statistics
+                fused = self.tracker.fused_request(t, eng, eng.grads)
             outs = eng.step()
             self.bytes_per_step.append(float(self.world * eng.wire_bytes()))
         else:
@@ -88,7 +92,7 @@ class EdgcDataParallel:
         decision = None
         closed = None
         if self.tracker is not None:
-            closed = self.tracker.observe(t, eng.grads)
+            closed = self.tracker.observe(t, eng.grads, fused=fused)
             if closed is not None:
                 decision = self._window_update(closed)
         if self.world > 1:

@@ -107,6 +107,15 @@ class _Plan:
         self.h = h
         self.descs = arr
 
+    def sample_slots(self) -> int:
+        """Fused-sampling partial slots per matrix (0: the plan cannot fuse the Gaussian statistics)."""
+        return int(self.L.edgc_compress_plan_sample_slots(self.h)) if self.kind == "compress" else 0
+
+    def set_sampling(self, descs, partials, stream):
+        arr = (_lib.SampleDesc * len(descs))(*descs)
+        _lib.check(self.L.edgc_compress_plan_set_sampling(self.h, arr, len(descs), _lib.ptr(partials), stream),
+                   "compress plan sampling")
+
     def run(self, stream, *, col_tol=None, status=None, phases=_lib.PHASE_ALL):
         if self.kind == "compress":
             _lib.check(self.L.edgc_compress_plan_run(self.h, col_tol, _lib.ptr(status), phases, stream),
@@ -260,6 +269,18 @@ class BucketEngine:
         """
         stream = _lib.stream_ptr(self.device)
         self._compress_plan().run(stream, col_tol=self.col_tol, status=self.status, phases=phases)
+
+    def sample_slots(self) -> int:
+        """Partial slots per matrix when the next pass 1 can also gather the sampled-iteration
+        Gaussian statistics (every matrix on the Z path), else 0."""
+        return self._compress_plan().sample_slots()
+
+    def set_sampling(self, bitmaps, firsts, partials):
+        """Arm the next pass 1 to accumulate, per matrix k, the fp64 shifted sums of the raw
+        gradient over bitmaps[k] (shift = element firsts[k][0]) into partials[k] (float64,
+        [n, slots, 2]); see edgc_compress_plan_set_sampling."""
+        descs = [_lib.SampleDesc(_lib.ptr(b), _lib.ptr(f)) for b, f in zip(bitmaps, firsts)]
+        self._compress_plan().set_sampling(descs, partials, _lib.stream_ptr(self.device))
 
     def exchange(self):
         """Phase 2: all-gather the packed factors of every rank (NCCL); no-op at W = 1."""

@@ -460,7 +460,37 @@ class EntropyTracker:
                 t.record_stream(cur)
         return specs, plans, bms, status
 
-    def observe(self, iteration: int, matrices) -> EntropyWindow | None:
+    def fused_request(self, iteration: int, engine, matrices):
+        """On a sampled iteration (Gaussian estimator), arm `engine`'s next pass 1 to gather the
+        sample statistics while it streams the raw gradients -- `matrices` must be the engine's
+        gradient tensors.  Returns a handle for ``observe(iteration, matrices, fused=handle)``,
+        or None when the step cannot fuse (then observe computes the entropies itself)."""
+        if not should_sample_iteration(iteration, self.config.alpha) or self.estimator is not entropy_gaussian_plugin:
+            return None
+        slots = engine.sample_slots()
+        mats = list(matrices)
+        if slots <= 0 or not mats:
+            return None
+        flats = [as_device_matrix(m).reshape(-1) for m in mats]
+        specs = _layer_specs(flats, iteration, self.config)
+        if any(c < 2 or c == n for n, c, _ in specs):
+            return None                      # beta = 1 copies have no membership bitmap
+        dev = flats[0].device
+        pre = self._take_prefetch(iteration)
+        if pre is not None and pre[0] == specs:
+            _, plans, bms, status = pre
+        else:
+            plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False, indices=False)
+        # slots beyond a matrix's own CTA count stay zero
+        partials = torch.zeros((len(specs), slots, 2), dtype=torch.float64, device=dev)
+        engine.set_sampling(bms, plans, partials)
+        key = tuple(c for _, c, _ in specs)
+        if getattr(self, "_counts_key", None) != key:
+            self._counts = torch.tensor(key, dtype=torch.int64, device=dev)
+            self._counts_key = key
+        return (iteration, partials, slots, self._counts, status, (plans, bms))
+
+    def observe(self, iteration: int, matrices, fused=None) -> EntropyWindow | None:
         closed = None
         win = iteration // self.window
         if win < self._current:
@@ -469,7 +499,18 @@ class EntropyTracker:
             closed = self._close()
             self._current = win
         mats = list(matrices)
-        if should_sample_iteration(iteration, self.config.alpha):
+        if should_sample_iteration(iteration, self.config.alpha) and fused is not None and fused[0] == iteration:
+            # pass 1 gathered the shifted sums; finish them into per-layer entropies (read lazily)
+            _, partials, slots, counts, status, _keep = fused
+            n = partials.shape[0]
+            h = torch.empty(n, dtype=torch.float64, device=partials.device)
+            hstat = torch.empty(n, dtype=torch.int32, device=partials.device)
+            _lib.check(_lib.lib().edgc_entropy_gaussian_partials(_lib.ptr(partials), slots, _lib.ptr(counts), n,
+                                                                 _lib.ptr(h), _lib.ptr(hstat),
+                                                                 _lib.stream_ptr(partials.device)),
+                       "edgc_entropy_gaussian_partials")
+            self._pending.append(_DeferredMean(h, hstat, status))
+        elif should_sample_iteration(iteration, self.config.alpha):
             pre = self._take_prefetch(iteration)
             if self.estimator is entropy_gaussian_plugin and mats:
                 # read back lazily: the host needs the value only when the window closes
