@@ -1373,14 +1373,55 @@ int launch_gemm(const Plan &P, const std::vector<GemmTile> &h, const GemmTile *d
     return EDGC_OK;
 }
 
+// Per-device side streams for the concurrent cluster-width launches (fork/join by
+// events: graph-capturable).
+struct ForkJoin {
+    cudaStream_t side[8] = {};
+    cudaEvent_t fork = nullptr, join[8] = {};
+};
+static int fork_join(ForkJoin *&out) {
+    static ForkJoin fj[16];
+    static bool ready[16] = {};
+    int dev = 0;
+    EDGC_CUDA_TRY(cudaGetDevice(&dev));
+    EDGC_REQUIRE(dev >= 0 && dev < 16, "device %d", dev);
+    if (!ready[dev]) {
+        for (int i = 0; i < 8; ++i) {
+            EDGC_CUDA_TRY(cudaStreamCreateWithFlags(&fj[dev].side[i], cudaStreamNonBlocking));
+            EDGC_CUDA_TRY(cudaEventCreateWithFlags(&fj[dev].join[i], cudaEventDisableTiming));
+        }
+        EDGC_CUDA_TRY(cudaEventCreateWithFlags(&fj[dev].fork, cudaEventDisableTiming));
+        ready[dev] = true;
+    }
+    out = &fj[dev];
+    return EDGC_OK;
+}
+
 int launch_pass1z(const Plan &P, int32_t *status, bool sample, cudaStream_t st) {
-    for (int c = 1; c <= 8; ++c) {
+    // one launch per cluster width; with several widths they run concurrently on forked
+    // streams, so each launch's partial last wave is filled by the other's clusters
+    int widths = 0;
+    for (int c = 1; c <= 8; ++c) widths += !P.tz[c].empty();
+    ForkJoin *fj = nullptr;
+    static const bool serial = std::getenv("EDGC_PASS1_SERIAL") != nullptr;
+    if (widths > 1 && !serial) {
+        int rc = fork_join(fj);
+        if (rc != EDGC_OK) return rc;
+        EDGC_CUDA_TRY(cudaEventRecord(fj->fork, st));
+    }
+    int used = 0;
+    for (int c = 8; c >= 1; --c) {   // widest clusters first
         if (P.tz[c].empty()) continue;
+        cudaStream_t ls = st;
+        if (fj && used > 0) {
+            ls = fj->side[used];
+            EDGC_CUDA_TRY(cudaStreamWaitEvent(ls, fj->fork, 0));
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(P.tz[c].size() * c));
         cfg.blockDim = dim3(kTThreads);
         cfg.dynamicSmemBytes = sizeof(TSmem);
-        cfg.stream = st;
+        cfg.stream = ls;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = c;
@@ -1403,6 +1444,11 @@ int launch_pass1z(const Plan &P, int32_t *status, bool sample, cudaStream_t st) 
             EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1t<false>, (const MatDev *)P.d_mats,
                                              (const ZTile *)P.d_tz[c], status, (const SampDev *)P.d_samp));
         EDGC_LAUNCH_CHECK();
+        if (fj && used > 0) {
+            EDGC_CUDA_TRY(cudaEventRecord(fj->join[used], ls));
+            EDGC_CUDA_TRY(cudaStreamWaitEvent(st, fj->join[used], 0));
+        }
+        ++used;
     }
     return EDGC_OK;
 }
@@ -1531,13 +1577,16 @@ __global__ void __launch_bounds__(kGThreads) k_recon_tiled(const ReconDev *descs
 constexpr int kV4Threads = 128;
 constexpr int kV4Cols = 4 * kV4Threads;
 constexpr int kV4Rows = 8;
-constexpr int kV4TileRows = 256;   // rows per tile: amortises the per-thread Q loads
+constexpr int kV4TileRowsMax = 256;
+// rows per tile: 64 while Q (W*r <= 8 per column) is cheap to load, 256 above to amortise it
+__host__ __device__ constexpr int v4_tile_rows(int wr) { return wr <= 8 ? 64 : 256; }
 
 // VC adjacent columns per thread (4, or 2 when W*r = 32 to keep Q in registers);
 // kV4Cols = 512 columns per tile either way.
 template <int WR, int VC>
 __global__ void __launch_bounds__(kV4Cols / VC) k_recon4(const ReconDev *descs, const RTile *tiles) {
     constexpr int NT = kV4Cols / VC;
+    constexpr int kV4TileRows = v4_tile_rows(WR);
     const RTile t = tiles[blockIdx.x];
     const ReconDev D = descs[t.d];
     const int r = D.r, wr = D.r * D.n_ranks;
@@ -1810,9 +1859,10 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
                           s.scale};
         const bool v4 = s.r * s.n_ranks <= 32 && s.n % 4 == 0 && s.ld_out % 4 == 0 && ((uintptr_t)s.out % 16 == 0);
         if (v4) {
+            const int64_t tr = v4_tile_rows(s.r * s.n_ranks <= 4 ? 4 : s.r * s.n_ranks <= 8 ? 8 : 16);
             for (int64_t c0 = 0; c0 < s.n; c0 += kV4Cols)
-                for (int64_t r0 = 0; r0 < s.m; r0 += kV4TileRows)
-                    P.tiles4.push_back(RTile{k, c0, std::min(s.n, c0 + kV4Cols), r0, std::min(s.m, r0 + kV4TileRows)});
+                for (int64_t r0 = 0; r0 < s.m; r0 += tr)
+                    P.tiles4.push_back(RTile{k, c0, std::min(s.n, c0 + kV4Cols), r0, std::min(s.m, r0 + tr)});
         } else if (s.n % 4 == 0 && s.ld_out % 4 == 0 && ((uintptr_t)s.out % 16 == 0)) {
             for (int64_t r0 = 0; r0 < s.m; r0 += kGT)
                 for (int64_t c0 = 0; c0 < s.n; c0 += kGT)

@@ -990,13 +990,13 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
     cudaStream_t st = (cudaStream_t)stream;
     PlanDev *d_plans = reinterpret_cast<PlanDev *>(ws);
     EDGC_CUDA_TRY(cudaMemcpyAsync(d_plans, L.dev.data(), sizeof(PlanDev) * n_plans, cudaMemcpyHostToDevice, st));
-    // side-stream friendly: the plan kernels run grid-stride on at most a third of the SMs
-    // (EDGC_PLAN_SMS overrides), so the training stream's small latency-bound kernels always
-    // find free SMs while the next sampled iteration's plans are built behind it
+    // the plan kernels run grid-stride over their virtual CTAs; EDGC_PLAN_SMS caps them to a
+    // share of the SMs (measured: capping spreads the interference over more steps and costs
+    // more than it saves, so the default is the whole GPU)
     static const int plan_sms = [] {
         const char *e = std::getenv("EDGC_PLAN_SMS");
         const int v = e ? std::atoi(e) : 0;
-        return v > 0 ? std::min(v, edgc::sm_count()) : std::max(1, edgc::sm_count() / 3);
+        return v > 0 ? std::min(v, edgc::sm_count()) : edgc::sm_count();
     }();
     auto capped = [&](int64_t nvb, int per_sm) {
         return (unsigned)std::max<int64_t>(1, std::min<int64_t>(nvb, (int64_t)plan_sms * per_sm));
