@@ -8,6 +8,7 @@ Device work runs in libedgc_b200.so (hand-written sm_100a CUDA, ctypes C-ABI);
 there is no CPU fallback.
 """
 
+from .calibrate import calibrate_gpu, fit_comm_model, measure_compressor_gpu, write_comm_model
 from .compressor import (CompressorState, LowRankFactors, compress, compressed_element_count, decompress,
                          set_rank)
 from .controller import (CommModel, RankBounds, RankControllerState, RankDecision, adjust_rank_window,
