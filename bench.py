@@ -65,6 +65,8 @@ def parse_args():
     ap.add_argument("--entropy", choices=["prefetch", "inline", "off"], default="prefetch",
                     help="diagnostics: entropy plans built ahead on a side stream (default), inline, or no tracker")
     ap.add_argument("--hi-prio", action="store_true", help="diagnostics: run the step on a high-priority stream")
+    ap.add_argument("--alias-output", action="store_true",
+                    help="averaged gradients overwrite the raw ones (default for the 12.1B set, to fit in HBM)")
     ap.add_argument("--no-fuse-entropy", dest="fuse_entropy", action="store_false",
                     help="diagnostics: separate Gaussian pass instead of gathering the statistics in pass 1")
     ap.add_argument("--cpu-steps", type=int, default=6, help="EF steps in the bounded CPU sample")
@@ -234,7 +236,8 @@ def run_ours(args):
     L = _lib.lib()
     shapes = gpt2_shapes(args.model, args.layers)
     total = sum(m * n for m, n in shapes)
-    eng = BucketEngine(shapes, rank=args.rank, seed=args.seed, world_size=world, rank_id=me)
+    alias = args.alias_output or args.model == "12.1B"
+    eng = BucketEngine(shapes, rank=args.rank, seed=args.seed, world_size=world, rank_id=me, alias_output=alias)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + me)
     chunk = 1 << 28
@@ -261,7 +264,7 @@ def run_ours(args):
         # sampled iteration: pass 1 also gathers the Gaussian statistics of the sampled elements
         fused = tracker.fused_request(t, eng, eng.grads) if tracker is not None and args.fuse_entropy else None
         if ev is not None:
-            marks = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            marks = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
             marks[0].record(stream)
         eng.compress(_lib.PHASE_PASS1)
         if ev is not None:
@@ -272,25 +275,22 @@ def run_ours(args):
         eng.compress(_lib.PHASE_PASS2 | _lib.PHASE_FINALIZE)
         if ev is not None:
             marks[3].record(stream)
-        eng.exchange()
+        if tracker is not None:
+            # train_toy order (grad_source.py:416): the tracker sees worker 0's raw gradients after
+            # the step's compression -- before the reconstruction, which may overwrite them
+            tracker.observe(t, eng.grads, fused=fused)   # non-sampled iterations only schedule the next plan
         if ev is not None:
             marks[4].record(stream)
-        eng.reconstruct()
+            if t % period == 0:
+                ev["ent"].append((marks[3], marks[4]))
+        eng.exchange()
         if ev is not None:
             marks[5].record(stream)
+        eng.reconstruct()
+        if ev is not None:
+            marks[6].record(stream)
             ev["marks"].append(marks)
         eng.advance()
-        if tracker is not None:
-            # train_toy order (grad_source.py:416): the tracker sees worker 0's raw gradients
-            # after the step's compression; g is read-only in compress, so it is unchanged
-            sampled = t % period == 0
-            if ev is not None and sampled:
-                ev["ent0"].append(torch.cuda.Event(enable_timing=True))
-                ev["ent0"][-1].record(stream)
-            tracker.observe(t, eng.grads, fused=fused)   # non-sampled iterations only schedule the next plan
-            if ev is not None and sampled:
-                ev["ent1"].append(torch.cuda.Event(enable_timing=True))
-                ev["ent1"][-1].record(stream)
 
     for t in range(args.warmup):
         one_step(t)
@@ -298,7 +298,7 @@ def run_ours(args):
     barrier()
     clocks = ClockSampler(local) if me == 0 else None
     launches0 = L.edgc_launch_count()
-    ev = {"ent0": [], "ent1": [], "marks": []}
+    ev = {"ent": [], "marks": []}
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     start.record(stream)
@@ -316,12 +316,12 @@ def run_ours(args):
     t_all = float(t_max.item())
     value = world * 4.0 * total * args.steps / t_all / 1e9
     # per-phase device times (ms, mean over timed steps)
-    names = ["pass1", "factor", "pass2_finalize", "exchange", "reconstruct"]
+    names = ["pass1", "factor", "pass2_finalize", "entropy", "exchange", "reconstruct"]
     ph = {n: 0.0 for n in names}
     for mk in ev["marks"]:
         for i, n in enumerate(names):
             ph[n] += mk[i].elapsed_time(mk[i + 1]) / len(ev["marks"])
-    ent_ms = [a.elapsed_time(b) for a, b in zip(ev["ent0"], ev["ent1"])]
+    ent_ms = [a.elapsed_time(b) for a, b in ev["ent"]]
     ph["entropy_per_sampled_step"] = statistics.mean(ent_ms) if ent_ms else 0.0
     ph["entropy_sampled_steps"] = len(ent_ms)
     starts = [mk[0] for mk in ev["marks"]] + [stop]
@@ -389,9 +389,13 @@ def run_ours(args):
                     dev_in.copy_(host_g, non_blocking=True)
                 in_ready = ev()
                 in_ready.record(h2d_s)
-            eng.step()
+            fused = tracker.fused_request(t, eng, eng.grads) if tracker is not None and args.fuse_entropy else None
+            eng.compress()
             if tracker is not None:
-                tracker.observe(t, eng.grads)
+                tracker.observe(t, eng.grads, fused=fused)
+            eng.exchange()
+            eng.reconstruct()
+            eng.advance()
             if out_free is not None:
                 stream.wait_event(out_free)
             dev_out.copy_(eng.out_arena)

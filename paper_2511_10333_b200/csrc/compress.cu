@@ -679,7 +679,8 @@ __device__ void gram_pass(const double *P, int64_t m, int r, double *gram, doubl
     const int tid = threadIdx.x;
     const int nbk = (r + 3) / 4, nblocks = nbk * (nbk + 1) / 2;
     const int ng = max(1, kFactorThreads / nblocks);      // row groups
-    const int g = tid / nblocks < ng ? tid / nblocks : -1;
+    const int per = kFactorThreads / ng;                   // block slots per row group (>= nblocks or all)
+    const int g = tid / per < ng ? tid / per : -1;
     for (int blk0 = 0; blk0 < nblocks; blk0 += kFactorThreads / ng) {
         const int slots = min(nblocks - blk0, kFactorThreads / ng);
         const int blk = blk0 + tid % (kFactorThreads / ng);
@@ -1281,7 +1282,10 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         const int64_t threads1 = kP1Threads;
         M.wide = std::max(d.r, d.r_res) > kNarrow ? 1 : 0;
         M.nchunk1 = M.wide ? (int32_t)ceil_div(d.n, kWideSplitK) : (int32_t)ceil_div(slots, threads1);
-        M.nblk2 = (int32_t)ceil_div(d.m, kP2Rows);
+        // Q partials: 256-row K blocks, or 2048 for the wide path above r = 32 (the fp64
+        // partials [nblk2][n][r] would otherwise take ~1 GB per GPT2-12.1B layer at r = 256)
+        const int64_t k2 = (M.wide && d.r > 32) ? kWideSplitK : kP2Rows;
+        M.nblk2 = (int32_t)ceil_div(d.m, k2);
         if (M.wide) {
             for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
                 for (int64_t j0 = 0; j0 < d.n; j0 += kGT) P.gw.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
@@ -1296,8 +1300,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
             for (int32_t b = 0; b < M.nblk2; ++b)
                 for (int64_t i0 = 0; i0 < d.n; i0 += BM)
                     for (int64_t j0 = 0; j0 < d.r; j0 += BN)
-                        tq.push_back(GemmTile{k, b, i0, j0, (int64_t)b * kP2Rows,
-                                              std::min(d.m, (int64_t)(b + 1) * kP2Rows)});
+                        tq.push_back(GemmTile{k, b, i0, j0, (int64_t)b * k2, std::min(d.m, (int64_t)(b + 1) * k2)});
             continue;
         }
         (v4 ? P.rmax4 : P.rmax1) = std::max(v4 ? P.rmax4 : P.rmax1, std::max(d.r, d.r_res));

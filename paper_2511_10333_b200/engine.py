@@ -136,7 +136,8 @@ class BucketEngine:
     """One DP rank's bucket set: compress + exchange + averaged reconstruction."""
 
     def __init__(self, shapes, rank: int, seed: int = 0, *, world_size: int = 1, rank_id: int = 0, group=None,
-                 rank_cap: int | None = None, col_tol: float = DEVICE_COLUMN_TOL, device=None):
+                 rank_cap: int | None = None, col_tol: float = DEVICE_COLUMN_TOL, device=None,
+                 alias_output: bool = False):
         self.L = _lib.lib()
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.shapes = [(int(m), int(n)) for m, n in shapes]
@@ -154,7 +155,10 @@ class BucketEngine:
         self.total_elems = total
         self.grad_arena = torch.zeros(total, dtype=torch.float32, device=dev)
         self.w_arena = torch.zeros(total, dtype=torch.float32, device=dev)
-        self.out_arena = torch.zeros(total, dtype=torch.float32, device=dev)
+        # alias_output: the averaged reconstruction overwrites the gradients (one 4 B/elem arena less,
+        # e.g. GPT2-12.1B: 46.9 GB); the raw gradients are then valid only until reconstruct()
+        self.alias_output = bool(alias_output)
+        self.out_arena = self.grad_arena if self.alias_output else torch.zeros(total, dtype=torch.float32, device=dev)
         self.grads = [self.grad_arena[a:b].view(m, n) for (a, b), (m, n) in zip(self._spans(), self.shapes)]
         self.outs = [self.out_arena[a:b].view(m, n) for (a, b), (m, n) in zip(self._spans(), self.shapes)]
         self.ws_views = [self.w_arena[a:b].view(m, n) for (a, b), (m, n) in zip(self._spans(), self.shapes)]

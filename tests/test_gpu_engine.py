@@ -20,7 +20,7 @@ def _shapes():
     return [(256, 768), (256, 256), (256, 1024), (1024, 256), (48, 36), (7, 9)]
 
 
-@pytest.mark.parametrize("rank", [1, 4, 8, 16, 32])
+@pytest.mark.parametrize("rank", [1, 4, 8, 16, 32, 64])
 def test_engine_matches_oracle_dp_step_chained(rank):
     from paper_2511_10333_b200.engine import BucketEngine
     shapes = _shapes()
