@@ -1281,10 +1281,13 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         const int64_t slots = d.n / M.vec;
         const int64_t threads1 = kP1Threads;
         M.wide = std::max(d.r, d.r_res) > kNarrow ? 1 : 0;
-        M.nchunk1 = M.wide ? (int32_t)ceil_div(d.n, kWideSplitK) : (int32_t)ceil_div(slots, threads1);
+        // wide path K split of P_raw = w q_warm: 2048 columns up to r = 32; above, one K block
+        // (the fp64 partials [nchunk1][m][r] scale with r while the tile count already suffices)
+        const int64_t k1 = d.r > 32 ? d.n : kWideSplitK;
+        M.nchunk1 = M.wide ? (int32_t)ceil_div(d.n, k1) : (int32_t)ceil_div(slots, threads1);
         // Q partials: 256-row K blocks, or 2048 for the wide path above r = 32 (the fp64
         // partials [nblk2][n][r] would otherwise take ~1 GB per GPT2-12.1B layer at r = 256)
-        const int64_t k2 = (M.wide && d.r > 32) ? kWideSplitK : kP2Rows;
+        const int64_t k2 = (M.wide && d.r > 32) ? d.m : kP2Rows;
         M.nblk2 = (int32_t)ceil_div(d.m, k2);
         if (M.wide) {
             for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
@@ -1296,7 +1299,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
             for (int32_t c = 0; c < M.nchunk1; ++c)
                 for (int64_t i0 = 0; i0 < d.m; i0 += BM)
                     for (int64_t j0 = 0; j0 < d.r; j0 += BN)
-                        tp.push_back(GemmTile{k, c, i0, j0, c * kWideSplitK, std::min(d.n, (c + 1) * kWideSplitK)});
+                        tp.push_back(GemmTile{k, c, i0, j0, c * k1, std::min(d.n, (c + 1) * k1)});
             for (int32_t b = 0; b < M.nblk2; ++b)
                 for (int64_t i0 = 0; i0 < d.n; i0 += BM)
                     for (int64_t j0 = 0; j0 < d.r; j0 += BN)
@@ -1321,7 +1324,8 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         MatDev &M = P.mats[k];
         M.p_part = a.take<double>(M.zmode ? 0 : (int64_t)M.nchunk1 * M.m * M.r);
         M.zpart = a.take<double>((int64_t)M.nitems * M.n * M.r);
-        M.p_raw = a.take<double>(M.m * M.r);
+        // a single P_raw partial is P_raw itself (the factor's chunk sum copies it in place)
+        M.p_raw = (!M.zmode && M.nchunk1 == 1) ? M.p_part : a.take<double>(M.m * M.r);
         M.q_part = a.take<double>((int64_t)M.nblk2 * M.n * M.r);
         M.tmat = a.take<double>((int64_t)M.r * M.r);
         M.dead = a.take<int32_t>(M.r);

@@ -243,6 +243,10 @@ class BucketEngine:
                                            _lib.ptr(self.precond[k]), m, n, g.stride(0), r, r_res, self.cap,
                                            self.cap))
         plan = _Plan("compress", descs, self.device)
+        if res is not None:
+            # the residual-free first-step plan is never used again: release its workspace
+            for k in [k for k in self._plans if k[0] == "c" and k[3] is None]:
+                del self._plans[k]
         self._plans[key] = plan
         return plan
 

@@ -39,7 +39,8 @@ _WS_CAP = {}
 
 
 def _plan_ws_cap(device) -> int:
-    """Workspace cap of one edgc_sample_plan call: half the HBM free at first use (>= 2 GiB).
+    """Workspace cap of one edgc_sample_plan call: a quarter of the HBM free at first use, at most
+    16 GiB (>= 2 GiB).
 
     All plans of a batch walk concurrently (one CTA each), so fewer, larger
     batches are faster; bucket sets beyond the cap are planned in several calls.
@@ -48,7 +49,9 @@ def _plan_ws_cap(device) -> int:
     key = torch.device(device).index
     if key not in _WS_CAP:
         free, _ = torch.cuda.mem_get_info(device)
-        _WS_CAP[key] = max(2 << 30, free // 2)
+        # the workspace pool keeps its high-water mark: 16 GiB holds the whole GPT2-2.5B set's
+        # plans (one batch) and leaves the rest of HBM to the compressor at 12.1B scale
+        _WS_CAP[key] = max(2 << 30, min(free // 4, 16 << 30))
     return _WS_CAP[key]
 
 
@@ -358,7 +361,7 @@ def _layer_specs(flats, iteration: int, config: SamplerConfig):
 
 
 def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=None, prefetched=None,
-                    deferred: bool = False):
+                    deferred: bool = False, workspace=None):
     """Per-layer entropies of one sampled iteration, all layers batched on the device.
 
     Gaussian plug-in (the default): each matrix is streamed once against the
@@ -378,7 +381,8 @@ def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=N
         if prefetched is not None and prefetched[0] == specs:
             _, plans, bms, status = prefetched
         else:
-            plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False, indices=False)
+            plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False, indices=False,
+                                              workspace=workspace)
         items = [(f, p, c) if p is None else (f, p, c, bm) for f, p, bm, (_, c, _) in zip(flats, plans, bms, specs)]
         h, hstat = _gaussian_launch(items, 0, dev)
         if deferred:
@@ -442,6 +446,10 @@ class EntropyTracker:
         specs = _layer_specs(flats, iteration, self.config)
         if any(c < 2 for _, c, _ in specs):
             return
+        # the workspace is shared with the inline (main-stream) builds: order after them
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(dev))
+        self._pf_stream.wait_event(ready)
         plans, bms, status = sample_plans(specs, dev, bitmaps=True, stream=self._pf_stream,
                                           workspace=self._pf_ws, check=False, indices=False)
         ev = torch.cuda.Event()
@@ -480,7 +488,8 @@ class EntropyTracker:
         if pre is not None and pre[0] == specs:
             _, plans, bms, status = pre
         else:
-            plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False, indices=False)
+            plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False, indices=False,
+                                              workspace=self._pf_ws)
         # slots beyond a matrix's own CTA count stay zero
         partials = torch.zeros((len(specs), slots, 2), dtype=torch.float64, device=dev)
         engine.set_sampling(bms, plans, partials)
@@ -515,7 +524,7 @@ class EntropyTracker:
             if self.estimator is entropy_gaussian_plugin and mats:
                 # read back lazily: the host needs the value only when the window closes
                 self._pending.append(layer_entropies(mats, iteration, self.config, self.estimator,
-                                                     prefetched=pre, deferred=True))
+                                                     prefetched=pre, deferred=True, workspace=self._pf_ws))
             else:
                 per_layer = layer_entropies(mats, iteration, self.config, self.estimator, prefetched=pre)
                 if per_layer:
