@@ -36,6 +36,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "tc_gemm.cuh"
 
 namespace edgc {
 namespace {
@@ -66,7 +67,7 @@ struct MatDev {
     int32_t wide;     // wide = 1: tiled GEMM path (r > 8 or unaligned)
     int32_t zw;       // Z path: columns per CTA of the cluster (multiple of 4, <= kTCW)
     int32_t al4;      // g and w rows float4-aligned (n, ld_g multiples of 4, 16-byte bases)
-    int32_t pad3_;
+    int32_t tc;       // wide path on the tensor cores (P_raw and Q with one K split each)
 };
 
 // fused sampled-iteration statistics of one matrix (edgc_compress_plan_set_sampling)
@@ -1130,6 +1131,152 @@ __global__ void __launch_bounds__(kGThreads) k_skinny(const MatDev *mats, const 
         }
 }
 
+// ------------------------------------------------- wide path on tcgen05
+// Above kTcMinRank the wide-path contractions run on the tensor cores
+// (tc_gemm.cuh: 3xTF32 operands, fp32 accumulation in 128-K chunks folded
+// round-to-nearest; ~1e-6 relative error against an exact product):
+//   TcPraw  P_raw = w q_warm      (M = m, N = r, K = n; one fp64 partial)
+//   TcQ     Q = w^T P             (M = n, N = r, K = m; one fp64 partial)
+//   TcEF    w <- g + (w - p_res q_res^T)   (M = m, N = n, K = r_res)
+// The fp64 partial layouts are the CUDA-core path's with a single K split, so
+// the factorisation and finalize kernels are shared.
+// number of epilogue items u (rows row0 + 4u) inside the problem, rem = rows left from row0
+__device__ __forceinline__ int tc_rows4(int64_t rem) { return rem <= 0 ? 0 : rem >= 29 ? 8 : (int)((rem + 3) / 4); }
+
+struct TcPraw {
+    static constexpr bool kAMN = false, kBMN = true;
+    using Tile = GemmTile;
+    const MatDev *mats;
+    const GemmTile *tiles;
+    int ntiles;
+    __device__ Tile tile(int i) const { return tiles[i]; }
+    __device__ int64_t tile_k(const Tile &t) const { return t.k1 - t.k0; }
+    __device__ void views(const Tile &t, tc::View &a, tc::View &b) const {
+        const MatDev &M = mats[t.mat];
+        a = tc::View{M.w + t.i0 * M.n + t.k0, M.n, M.m - t.i0, t.k1 - t.k0, 0, 0};
+        b = tc::View{M.q_warm + t.k0 * M.ld_q + t.j0, M.ld_q, M.r - t.j0, t.k1 - t.k0, 0, 0};
+    }
+    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8]) const {
+        const MatDev &M = mats[t.mat];
+        const int nc = M.r - (int)t.j0 - col;
+        if (nc <= 0) return;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t gi = t.i0 + row0 + 4 * u;
+            if (gi >= M.m) break;
+            double *dst = M.p_part + ((int64_t)t.split * M.m + gi) * M.r + t.j0 + col;
+            dst[0] = v[u].x;
+            if (nc > 1) dst[1] = v[u].y;
+            if (nc > 2) dst[2] = v[u].z;
+            if (nc > 3) dst[3] = v[u].w;
+        }
+    }
+};
+
+struct TcQ {
+    static constexpr bool kAMN = true, kBMN = true;
+    using Tile = GemmTile;
+    const MatDev *mats;
+    const GemmTile *tiles;
+    const int32_t *status;
+    int ntiles;
+    __device__ Tile tile(int i) const { return tiles[i]; }
+    __device__ int64_t tile_k(const Tile &t) const {
+        const int st = status[t.mat];
+        if ((st & 1) || (mats[t.mat].zmode && !(st & 2))) return 0;   // diverged / Z path done
+        return t.k1 - t.k0;
+    }
+    __device__ void views(const Tile &t, tc::View &a, tc::View &b) const {
+        const MatDev &M = mats[t.mat];
+        a = tc::View{M.w + t.k0 * M.n + t.i0, M.n, M.n - t.i0, t.k1 - t.k0, 0, 0};
+        b = tc::View{M.p_out + t.k0 * M.r + t.j0, M.r, M.r - t.j0, t.k1 - t.k0, 0, 0};
+    }
+    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8]) const {
+        const MatDev &M = mats[t.mat];
+        const int nc = M.r - (int)t.j0 - col;
+        if (nc <= 0) return;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t gi = t.i0 + row0 + 4 * u;
+            if (gi >= M.n) break;
+            double *dst = M.q_part + ((int64_t)t.split * M.n + gi) * M.r + t.j0 + col;
+            dst[0] = v[u].x;
+            if (nc > 1) dst[1] = v[u].y;
+            if (nc > 2) dst[2] = v[u].z;
+            if (nc > 3) dst[3] = v[u].w;
+        }
+    }
+};
+
+struct TcEF {
+    static constexpr bool kAMN = false, kBMN = false;
+    using Tile = GemmTile;
+    const MatDev *mats;
+    const GemmTile *tiles;
+    int32_t *status;
+    int ntiles;
+    __device__ Tile tile(int i) const { return tiles[i]; }
+    __device__ int64_t tile_k(const Tile &t) const { return t.k1 - t.k0; }
+    __device__ void views(const Tile &t, tc::View &a, tc::View &b) const {
+        const MatDev &M = mats[t.mat];
+        const int rr = M.r_res;
+        a = tc::View{M.p_res + t.i0 * rr, rr, M.m - t.i0, rr, 0, 0};
+        b = tc::View{M.q_res + t.j0 * rr, rr, M.n - t.j0, rr, 0, 0};
+    }
+    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8]) const {
+        const MatDev &M = mats[t.mat];
+        const int64_t j = t.j0 + col;
+        if (j >= M.n) return;
+        const int nu = tc_rows4(M.m - t.i0 - row0);   // rows row0 + 4u < m
+        bool bad = false;
+        if (M.al4) {
+            // all loads first (16 in flight), then the stores
+            float4 g4[8], w4[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u < nu) {
+                    const int64_t gi = t.i0 + row0 + 4 * u;
+                    g4[u] = __ldcs(reinterpret_cast<const float4 *>(M.g + gi * M.ld_g + j));
+                    w4[u] = __ldcs(reinterpret_cast<const float4 *>(M.w + gi * M.n + j));
+                }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u < nu) {
+                    const int64_t gi = t.i0 + row0 + 4 * u;
+                    const float x0 = g4[u].x + (w4[u].x - v[u].x), x1 = g4[u].y + (w4[u].y - v[u].y);
+                    const float x2 = g4[u].z + (w4[u].z - v[u].z), x3 = g4[u].w + (w4[u].w - v[u].w);
+                    bad |= !(isfinite(x0) && isfinite(x1) && isfinite(x2) && isfinite(x3));
+                    __stcs(reinterpret_cast<float4 *>(M.w + gi * M.n + j), make_float4(x0, x1, x2, x3));
+                }
+        } else {
+            const int nc = M.n - j < 4 ? (int)(M.n - j) : 4;
+            for (int u = 0; u < nu; ++u) {
+                const int64_t gi = t.i0 + row0 + 4 * u;
+                const float *g = M.g + gi * M.ld_g + j;
+                float *w = M.w + gi * M.n + j;
+                const float a[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                for (int c = 0; c < nc; ++c) {
+                    const float x = g[c] + (w[c] - a[c]);
+                    bad |= !isfinite(x);
+                    w[c] = x;
+                }
+            }
+        }
+        if (bad) atomicOr(status + t.mat, 1);
+    }
+};
+
+// EDGC_TC_MIN_RANK (default 16): wide-path ranks above it use the tensor cores;
+// EDGC_NO_TC disables them (A/B runs)
+int tc_min_rank() {
+    static const int v = [] {
+        if (std::getenv("EDGC_NO_TC")) return 1 << 30;
+        const char *e = std::getenv("EDGC_TC_MIN_RANK");
+        return e ? std::atoi(e) : 16;
+    }();
+    return v;
+}
+
 // ------------------------------------------------------------------ pass 2
 // Q partial over this tile's rows: thread owns VEC columns x RMAX ranks;
 // fp32 FMA over 32-row groups, fp64 across groups.
@@ -1228,12 +1375,14 @@ struct Plan {
     std::vector<ZTile> tz[9];          // Z-path items grouped by cluster size 1..8
     std::vector<GemmTile> gw, gp, gq;  // wide path: EF update, P_raw and Q tiles for r > 32
     std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles for r <= 16 (256x16) and <= 32 (128x32)
+    std::vector<GemmTile> tce, tcp[2], tcq[2];   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
     int64_t bytes = 0;
     MatDev *d_mats = nullptr;
     Tile *d_t1v4 = nullptr, *d_t1v1 = nullptr, *d_t2v4 = nullptr, *d_t2v1 = nullptr;
     ZTile *d_tz[9] = {};
     GemmTile *d_gw = nullptr, *d_gp = nullptr, *d_gq = nullptr;
     GemmTile *d_sp[3] = {}, *d_sq[3] = {};
+    GemmTile *d_tce = nullptr, *d_tcp[2] = {}, *d_tcq[2] = {};
     int rmax4 = 0, rmax1 = 0;
     SampDev *d_samp = nullptr;          // fused sampling descriptors (workspace)
     std::vector<SampDev> samp_host;
@@ -1281,17 +1430,32 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         const int64_t slots = d.n / M.vec;
         const int64_t threads1 = kP1Threads;
         M.wide = std::max(d.r, d.r_res) > kNarrow ? 1 : 0;
+        M.tc = (M.wide && d.r > tc_min_rank()) ? 1 : 0;
         // wide path K split of P_raw = w q_warm: 2048 columns up to r = 32; above, one K block
         // (the fp64 partials [nchunk1][m][r] scale with r while the tile count already suffices)
-        const int64_t k1 = d.r > 32 ? d.n : kWideSplitK;
+        const int64_t k1 = (M.tc || d.r > 32) ? d.n : kWideSplitK;
         M.nchunk1 = M.wide ? (int32_t)ceil_div(d.n, k1) : (int32_t)ceil_div(slots, threads1);
         // Q partials: 256-row K blocks, or 2048 for the wide path above r = 32 (the fp64
         // partials [nblk2][n][r] would otherwise take ~1 GB per GPT2-12.1B layer at r = 256)
-        const int64_t k2 = (M.wide && d.r > 32) ? d.m : kP2Rows;
+        const int64_t k2 = (M.wide && (M.tc || d.r > 32)) ? d.m : kP2Rows;
         M.nblk2 = (int32_t)ceil_div(d.m, k2);
         if (M.wide) {
-            for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
-                for (int64_t j0 = 0; j0 < d.n; j0 += kGT) P.gw.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
+            if (d.r_res > tc_min_rank()) {
+                for (int64_t i0 = 0; i0 < d.m; i0 += tc::kBM)
+                    for (int64_t j0 = 0; j0 < d.n; j0 += 128) P.tce.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
+            } else {
+                for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
+                    for (int64_t j0 = 0; j0 < d.n; j0 += kGT) P.gw.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
+            }
+            if (M.tc) {
+                // rank blocks of one row block adjacent: co-resident CTAs share the w rows in L2
+                const int bn = d.r <= 64 ? 64 : 128, c = d.r <= 64 ? 0 : 1;
+                for (int64_t i0 = 0; i0 < d.m; i0 += tc::kBM)
+                    for (int64_t j0 = 0; j0 < d.r; j0 += bn) P.tcp[c].push_back(GemmTile{k, 0, i0, j0, 0, d.n});
+                for (int64_t i0 = 0; i0 < d.n; i0 += tc::kBM)
+                    for (int64_t j0 = 0; j0 < d.r; j0 += bn) P.tcq[c].push_back(GemmTile{k, 0, i0, j0, 0, d.m});
+                continue;
+            }
             // skinny GEMM tile shape matched to the rank (r > 32: the 64x64 k_gemm tiles)
             const int cfg = d.r <= 16 ? 0 : (d.r <= 32 ? 1 : 2);
             const int BM = cfg == 0 ? 256 : (cfg == 1 ? 128 : kGT), BN = cfg == 0 ? 16 : (cfg == 1 ? 32 : kGT);
@@ -1350,6 +1514,11 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     for (int c = 0; c < 3; ++c) {
         P.d_sp[c] = a.take<GemmTile>(P.sp[c].size());
         P.d_sq[c] = a.take<GemmTile>(P.sq[c].size());
+    }
+    P.d_tce = a.take<GemmTile>(P.tce.size());
+    for (int c = 0; c < 2; ++c) {
+        P.d_tcp[c] = a.take<GemmTile>(P.tcp[c].size());
+        P.d_tcq[c] = a.take<GemmTile>(P.tcq[c].size());
     }
     P.d_gw = a.take<GemmTile>(P.gw.size());
     P.d_gp = a.take<GemmTile>(P.gp.size());
@@ -1689,6 +1858,43 @@ __global__ void k_check_finite(const T *x, int64_t count, int32_t *flag) {
 
 int elementwise_blocks(int64_t count) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(count, 256), sm_count() * 8)); }
 
+// out = scale * P_all Q_all^T on the tensor cores (M = m, N = n, K = W r; the
+// per-rank factor blocks are the K index's rank blocks)
+struct TcRecon {
+    static constexpr bool kAMN = false, kBMN = false;
+    using Tile = RTile;
+    const ReconDev *descs;
+    const RTile *tiles;
+    int ntiles;
+    __device__ Tile tile(int i) const { return tiles[i]; }
+    __device__ int64_t tile_k(const Tile &t) const { return (int64_t)descs[t.d].r * descs[t.d].n_ranks; }
+    __device__ void views(const Tile &t, tc::View &a, tc::View &b) const {
+        const ReconDev &D = descs[t.d];
+        const int64_t K = (int64_t)D.r * D.n_ranks, kb = D.n_ranks > 1 ? D.r : 0;
+        a = tc::View{D.p + t.row0 * D.r, D.r, D.m - t.row0, K, kb, D.p_stride};
+        b = tc::View{D.q + t.col0 * D.r, D.r, D.n - t.col0, K, kb, D.q_stride};
+    }
+    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8]) const {
+        const ReconDev &D = descs[t.d];
+        const int64_t j = t.col0 + col;
+        if (j >= D.n) return;
+        const int nu = tc_rows4(D.m - t.row0 - row0);
+        const float sc = D.scale;
+        const bool vec = j + 4 <= D.n && D.ld_out % 4 == 0 && ((uintptr_t)D.out % 16) == 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (u >= nu) break;
+            float *o = D.out + (t.row0 + row0 + 4 * u) * D.ld_out + j;
+            if (vec) {
+                __stcs(reinterpret_cast<float4 *>(o), make_float4(v[u].x * sc, v[u].y * sc, v[u].z * sc, v[u].w * sc));
+            } else {
+                const float a[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                for (int c = 0; c < 4 && j + c < D.n; ++c) o[c] = a[c] * sc;
+            }
+        }
+    }
+};
+
 }  // namespace
 }  // namespace edgc
 
@@ -1742,6 +1948,11 @@ extern "C" int edgc_compress_plan_bind(edgc_compress_plan *h, void *ws, int64_t 
                          : cudaMemcpyAsync(d, v.data(), sizeof(GemmTile) * v.size(), cudaMemcpyHostToDevice, st);
     };
     EDGC_CUDA_TRY(upg(P.d_gw, P.gw));
+    EDGC_CUDA_TRY(upg(P.d_tce, P.tce));
+    for (int c = 0; c < 2; ++c) {
+        EDGC_CUDA_TRY(upg(P.d_tcp[c], P.tcp[c]));
+        EDGC_CUDA_TRY(upg(P.d_tcq[c], P.tcq[c]));
+    }
     EDGC_CUDA_TRY(upg(P.d_gp, P.gp));
     EDGC_CUDA_TRY(upg(P.d_gq, P.gq));
     for (int c = 0; c < 3; ++c) {
@@ -1768,6 +1979,12 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if ((rc = launch_pass1z(P, status_dev, P.sample_armed, st))) return rc;
         h->P.sample_armed = false;   // set_sampling arms exactly one pass 1
         if ((rc = launch_gemm<2>(P, P.gw, P.d_gw, status_dev, st))) return rc;
+        if (!P.tce.empty())
+            EDGC_CUDA_TRY((tc::launch<128, 4>(TcEF{P.d_mats, P.d_tce, status_dev, (int)P.tce.size()}, sm_count(), st)));
+        if (!P.tcp[0].empty())
+            EDGC_CUDA_TRY((tc::launch<64, 4>(TcPraw{P.d_mats, P.d_tcp[0], (int)P.tcp[0].size()}, sm_count(), st)));
+        if (!P.tcp[1].empty())
+            EDGC_CUDA_TRY((tc::launch<128, 4>(TcPraw{P.d_mats, P.d_tcp[1], (int)P.tcp[1].size()}, sm_count(), st)));
         if (!P.sp[0].empty()) {
             k_skinny<0, 256, 16><<<(unsigned)P.sp[0].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sp[0], status_dev);
             EDGC_LAUNCH_CHECK();
@@ -1794,6 +2011,10 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
             EDGC_LAUNCH_CHECK();
         }
         if ((rc = launch_gemm<1>(P, P.gq, P.d_gq, status_dev, st))) return rc;
+        if (!P.tcq[0].empty())
+            EDGC_CUDA_TRY((tc::launch<64, 4>(TcQ{P.d_mats, P.d_tcq[0], status_dev, (int)P.tcq[0].size()}, sm_count(), st)));
+        if (!P.tcq[1].empty())
+            EDGC_CUDA_TRY((tc::launch<128, 4>(TcQ{P.d_mats, P.d_tcq[1], status_dev, (int)P.tcq[1].size()}, sm_count(), st)));
     }
     if (phases & EDGC_PHASE_FINALIZE) {
         k_finalize<<<dim3(16, n), 256, 0, st>>>(P.d_mats, status_dev);
@@ -1848,14 +2069,16 @@ struct RPlan {
     std::vector<RTile> tiles, tiles4;
     int64_t bytes = 0;
     ReconDev *dd = nullptr;
-    RTile *dt = nullptr, *dt4 = nullptr, *dtT = nullptr;
+    RTile *dt = nullptr, *dt4 = nullptr, *dtT = nullptr, *dtc = nullptr;
     std::vector<RTile> tilesT;        // k_recon_tiled (W*r > 8, float4-aligned output)
+    std::vector<RTile> tilesC;        // TcRecon (W*r above the tensor-core threshold)
 };
 int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
     Arena a(ws, INT64_MAX);
     P.tiles.clear();
     P.tiles4.clear();
     P.tilesT.clear();
+    P.tilesC.clear();
     P.d.resize(n);
     P.dd = a.take<ReconDev>(n);
     for (int k = 0; k < n; ++k) {
@@ -1865,7 +2088,15 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
         P.d[k] = ReconDev{s.p, s.q, s.out, s.m, s.n, s.ld_out, s.p_rank_stride, s.q_rank_stride, s.r, s.n_ranks,
                           s.scale};
         const bool v4 = s.r * s.n_ranks <= 32 && s.n % 4 == 0 && s.ld_out % 4 == 0 && ((uintptr_t)s.out % 16 == 0);
-        if (v4) {
+        // tensor cores above the wide-path threshold; rank blocks must not straddle a
+        // 32-wide K block (single rank, or r % 32 == 0)
+        const bool tcr = s.r * s.n_ranks > std::max(32, tc_min_rank()) && s.r % 4 == 0 &&
+                         (s.n_ranks == 1 || s.r % 32 == 0);
+        if (tcr) {
+            for (int64_t r0 = 0; r0 < s.m; r0 += tc::kBM)
+                for (int64_t c0 = 0; c0 < s.n; c0 += 128)
+                    P.tilesC.push_back(RTile{k, c0, std::min(s.n, c0 + 128), r0, std::min(s.m, r0 + tc::kBM)});
+        } else if (v4) {
             const int64_t tr = v4_tile_rows(s.r * s.n_ranks <= 4 ? 4 : s.r * s.n_ranks <= 8 ? 8 : 16);
             for (int64_t c0 = 0; c0 < s.n; c0 += kV4Cols)
                 for (int64_t r0 = 0; r0 < s.m; r0 += tr)
@@ -1883,6 +2114,7 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
     P.dt = a.take<RTile>(P.tiles.size());
     P.dt4 = a.take<RTile>(P.tiles4.size());
     P.dtT = a.take<RTile>(P.tilesT.size());
+    P.dtc = a.take<RTile>(P.tilesC.size());
     P.bytes = a.off;
     return EDGC_OK;
 }
@@ -1928,6 +2160,9 @@ extern "C" int edgc_recon_plan_bind(edgc_recon_plan *h, void *ws, int64_t ws_byt
     if (!P.tilesT.empty())
         EDGC_CUDA_TRY(
             cudaMemcpyAsync(P.dtT, P.tilesT.data(), sizeof(RTile) * P.tilesT.size(), cudaMemcpyHostToDevice, st));
+    if (!P.tilesC.empty())
+        EDGC_CUDA_TRY(
+            cudaMemcpyAsync(P.dtc, P.tilesC.data(), sizeof(RTile) * P.tilesC.size(), cudaMemcpyHostToDevice, st));
     EDGC_CUDA_TRY(cudaStreamSynchronize(st));
     return EDGC_OK;
 }
@@ -1955,6 +2190,8 @@ extern "C" int edgc_recon_plan_run(edgc_recon_plan *h, void *stream) {
         k_recon_tiled<<<(unsigned)h->P.tilesT.size(), kGThreads, 0, st>>>(h->P.dd, h->P.dtT);
         EDGC_LAUNCH_CHECK();
     }
+    if (!h->P.tilesC.empty())
+        EDGC_CUDA_TRY((tc::launch<128, 4>(TcRecon{h->P.dd, h->P.dtc, (int)h->P.tilesC.size()}, sm_count(), st)));
     return EDGC_OK;
 }
 
