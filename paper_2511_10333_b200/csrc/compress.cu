@@ -68,6 +68,11 @@ struct MatDev {
     int32_t zw;       // Z path: columns per CTA of the cluster (multiple of 4, <= kTCW)
     int32_t al4;      // g and w rows float4-aligned (n, ld_g multiples of 4, 16-byte bases)
     int32_t tc;       // wide path on the tensor cores (P_raw and Q with one K split each)
+    int32_t fx;       // factorisation by the multi-CTA kernels (wide ranks): k_factor skips it
+    int32_t gks;      // rows per Gram K split (fx)
+    int32_t gsplit;   // Gram K splits (fx)
+    double *gpart;    // [gsplit][r][r] Gram partials (fx; aliases q_part when it fits)
+    int32_t *fmode;   // fx: 1 = single CholQR, 2 = CholQR2 (set by k_fx_chol1)
 };
 
 // fused sampled-iteration statistics of one matrix (edgc_compress_plan_set_sampling)
@@ -849,7 +854,7 @@ __device__ void right_mul(const double *src, const double *T, int64_t m, int r, 
 
 __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, int32_t *status, double col_tol) {
     const MatDev &M = mats[blockIdx.x];
-    if (status[blockIdx.x] & 1) return;
+    if ((status[blockIdx.x] & 1) || M.fx) return;
     const int r = M.r;
     const int64_t m = M.m;
     const int tid = threadIdx.x;
@@ -858,8 +863,8 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, i
     __shared__ double s_tol;
     int32_t *dead = M.dead;
     const bool pre = M.zmode && M.precond;
-    if (!M.zmode) {
-        // P_raw = sum over column chunks, fixed order
+    if (!M.zmode && M.p_raw != M.p_part) {
+        // P_raw = sum over column chunks, fixed order (a single chunk is P_raw itself)
         for (int64_t e = tid; e < m * r; e += kFactorThreads) {
             double acc = 0.0;
             for (int c = 0; c < M.nchunk1; ++c) acc += M.p_part[(int64_t)c * m * r + e];
@@ -955,6 +960,193 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, i
             M.precond[(int64_t)i * M.ld_s + j] = a;
         }
     }
+}
+
+// ------------------------------------------- multi-CTA factorisation (r >= 32)
+// At wide ranks the O(m r^2) parts of CholQR(2) -- the Gram matrices and the
+// right multiplications by the triangular transforms -- dominate, and one CTA
+// per matrix leaves most SMs idle.  They run here as tiled fp64 GEMMs over many
+// CTAs (64x64 output tiles, 4x4 per thread, fixed-order K-split reduction);
+// the r x r work (Cholesky with dead-column detection, triangular inverse,
+// conditioning) stays one CTA per matrix and reuses k_factor's routines.
+//   k_fx_gram(pass)   Gram partials of P_raw (pass 1) or P_raw T1 (pass 2)
+//   k_fx_chol1        gram -> R, T1 = R^-1, kappa -> fmode (1: single, 2: CholQR2)
+//   k_fx_rmul(pass)   pass 1: P = P_raw T1 (fp32 p_out) or p_tmp = P_raw T1 (fp64)
+//                     pass 2: P = p_tmp T2
+//   k_fx_chol2        fmode 2: second Cholesky -> T2, tmat = T1 T2
+struct FxTile {
+    int32_t mat, split;
+    int32_t i0, j0;        // Gram: output block origins; rmul: column block j0, row block in r0
+    int64_t r0, r1;        // Gram: K (row) range; rmul: output row range
+};
+
+constexpr int kFxT = 64, kFxK = 16, kFxThreads = 256;
+
+__device__ __forceinline__ bool fx_active(const MatDev &M, const int32_t *status, int mat, int pass) {
+    if (status[mat] & 1) return false;
+    return pass == 1 || *M.fmode == 2;
+}
+
+// gpart[split][i][j] = sum_{k in split} X[k][i] X[k][j] for the upper tile (i0 <= j0)
+__global__ void __launch_bounds__(kFxThreads) k_fx_gram(const MatDev *mats, const FxTile *tiles, const int32_t *status,
+                                                        int pass) {
+    const FxTile t = tiles[blockIdx.x];
+    const MatDev &M = mats[t.mat];
+    if (!fx_active(M, status, t.mat, pass)) return;
+    const int r = M.r;
+    const double *X = pass == 1 ? M.p_raw : M.p_tmp;
+    __shared__ double As[kFxK][kFxT + 1], Bs[kFxK][kFxT + 1];
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    double acc[4][4] = {};
+    for (int64_t k0 = t.r0; k0 < t.r1; k0 += kFxK) {
+        for (int e = tid; e < kFxK * kFxT; e += kFxThreads) {
+            const int kk = e / kFxT, c = e % kFxT;
+            const int64_t k = k0 + kk;
+            const bool kin = k < t.r1;
+            As[kk][c] = (kin && t.i0 + c < r) ? X[k * r + t.i0 + c] : 0.0;
+            Bs[kk][c] = (kin && t.j0 + c < r) ? X[k * r + t.j0 + c] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kFxK; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { a[u] = As[kk][ty * 4 + u]; b[u] = Bs[kk][tx * 4 + u]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+    double *G = M.gpart + (int64_t)t.split * r * r;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int i = t.i0 + ty * 4 + u, j = t.j0 + tx * 4 + v;
+            if (i < r && j < r) G[i * r + j] = acc[u][v];
+        }
+}
+
+// gram (upper, mirrored) = fixed-order sum of the split partials
+__device__ void fx_gram_sum(const MatDev &M, double *gram) {
+    const int r = M.r;
+    for (int e = threadIdx.x; e < r * r; e += kFactorThreads) {
+        const int i = e / r, j = e % r;
+        if (j < i) continue;
+        // the tile holding (i, j) is upper by block: (i/64 <= j/64); entries below the
+        // diagonal inside a diagonal block are computed too, use the upper one
+        double a = 0.0;
+        for (int c = 0; c < M.gsplit; ++c) a += M.gpart[(int64_t)c * r * r + e];
+        gram[i * r + j] = a;
+        gram[j * r + i] = a;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kFactorThreads) k_fx_chol1(const MatDev *mats, int32_t *status, double col_tol) {
+    const MatDev &M = mats[blockIdx.x];
+    if (!M.fx || (status[blockIdx.x] & 1)) return;
+    const int r = M.r, tid = threadIdx.x;
+    double *gram = M.fwork, *R = gram + r * r, *T1 = R + r * r;
+    __shared__ double s_tmp[kFactorThreads / 32];
+    __shared__ double s_tol;
+    int32_t *dead = M.dead;
+    for (int j = tid; j < r; j += kFactorThreads) dead[j] = 0;
+    fx_gram_sum(M, gram);
+    if (tid == 0) {
+        double fro2 = 0.0;   // ||P_raw||_F^2 (compressor.py:79)
+        for (int j = 0; j < r; ++j) fro2 += gram[j * r + j];
+        s_tol = col_tol * sqrt(fro2);
+    }
+    __syncthreads();
+    chol_dead(gram, r, s_tol, nullptr, dead, R, true);
+    auto block_sumsq = [&](const double *X) -> double {
+        double a = 0.0;
+        for (int e = tid; e < r * r; e += kFactorThreads) a += X[e] * X[e];
+        a = warp_sum(a);
+        if ((tid & 31) == 0) s_tmp[tid >> 5] = a;
+        __syncthreads();
+        double tot = 0.0;
+        for (int w = 0; w < kFactorThreads / 32; ++w) tot += s_tmp[w];
+        __syncthreads();
+        return tot;
+    };
+    const double rn2 = block_sumsq(R);
+    tri_inverse(R, dead, r, T1);
+    const double tn2 = block_sumsq(T1);
+    const bool single = sqrt(rn2 * tn2) <= 1000.0;   // as k_factor (non-Z)
+    if (single)
+        for (int e = tid; e < r * r; e += kFactorThreads) M.tmat[e] = T1[e];
+    if (tid == 0) *M.fmode = single ? 1 : 2;
+}
+
+__global__ void __launch_bounds__(kFactorThreads) k_fx_chol2(const MatDev *mats, const int32_t *status) {
+    const MatDev &M = mats[blockIdx.x];
+    if (!M.fx || (status[blockIdx.x] & 1) || *M.fmode != 2) return;
+    const int r = M.r, tid = threadIdx.x;
+    double *gram = M.fwork, *R = gram + r * r, *T1 = R + r * r, *T2 = T1 + r * r;
+    fx_gram_sum(M, gram);
+    chol_dead(gram, r, 0.0, nullptr, M.dead, R, false);
+    tri_inverse(R, M.dead, r, T2);
+    // T = T1 T2 (P = P_raw T)
+    for (int e = tid; e < r * r; e += kFactorThreads) {
+        const int j = e / r, l = e % r;
+        double a = 0.0;
+        for (int i = l; i <= j; ++i) a += T1[(int64_t)i * r + l] * T2[(int64_t)j * r + i];
+        M.tmat[(int64_t)j * r + l] = a;
+    }
+}
+
+// Y[i][j] = sum_{l <= j} X[i][l] T(l, j), T column j at T[j*r + l] (upper triangular)
+__global__ void __launch_bounds__(kFxThreads) k_fx_rmul(const MatDev *mats, const FxTile *tiles, const int32_t *status,
+                                                        int pass) {
+    const FxTile t = tiles[blockIdx.x];
+    const MatDev &M = mats[t.mat];
+    if (!fx_active(M, status, t.mat, pass)) return;
+    const int r = M.r;
+    const bool single = *M.fmode == 1;
+    const double *X = pass == 1 ? M.p_raw : M.p_tmp;
+    const double *T = M.fwork + (int64_t)(pass == 1 ? 2 : 3) * r * r;   // T1 or T2
+    __shared__ double As[kFxK][kFxT + 1], Bs[kFxK][kFxT + 1];
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    double acc[4][4] = {};
+    const int kend = min(r, t.j0 + kFxT);   // T upper: l <= j < j0 + 64
+    for (int k0 = 0; k0 < kend; k0 += kFxK) {
+        for (int e = tid; e < kFxK * kFxT; e += kFxThreads) {
+            // A: rows r0.. x K (coalesced along K); B: K x columns j0..
+            const int c = e / kFxK, kk = e % kFxK;
+            const int k = k0 + kk;
+            const int64_t i = t.r0 + c;
+            As[kk][c] = (i < t.r1 && k < kend) ? X[i * r + k] : 0.0;
+            const int j = t.j0 + c;
+            Bs[kk][c] = (j < r && k <= j) ? T[(int64_t)j * r + k] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kFxK; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { a[u] = As[kk][ty * 4 + u]; b[u] = Bs[kk][tx * 4 + u]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t i = t.r0 + ty * 4 + u;
+            const int j = t.j0 + tx * 4 + v;
+            if (i >= t.r1 || j >= r) continue;
+            const double y = acc[u][v];
+            if (pass == 1 && !single) M.p_tmp[i * r + j] = y;
+            else M.p_out[i * r + j] = (float)y;
+        }
 }
 
 // --------------------------------------------------------- wide-rank path
@@ -1375,7 +1567,8 @@ struct Plan {
     std::vector<ZTile> tz[9];          // Z-path items grouped by cluster size 1..8
     std::vector<GemmTile> gw, gp, gq;  // wide path: EF update, P_raw and Q tiles for r > 32
     std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles for r <= 16 (256x16) and <= 32 (128x32)
-    std::vector<GemmTile> tce, tcp[2], tcq[2];   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
+    std::vector<GemmTile> tce, tcp[2], tcq[2];
+    std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
     int64_t bytes = 0;
     MatDev *d_mats = nullptr;
     Tile *d_t1v4 = nullptr, *d_t1v1 = nullptr, *d_t2v4 = nullptr, *d_t2v1 = nullptr;
@@ -1383,6 +1576,7 @@ struct Plan {
     GemmTile *d_gw = nullptr, *d_gp = nullptr, *d_gq = nullptr;
     GemmTile *d_sp[3] = {}, *d_sq[3] = {};
     GemmTile *d_tce = nullptr, *d_tcp[2] = {}, *d_tcq[2] = {};
+    FxTile *d_fxg = nullptr, *d_fxr = nullptr;
     int rmax4 = 0, rmax1 = 0;
     SampDev *d_samp = nullptr;          // fused sampling descriptors (workspace)
     std::vector<SampDev> samp_host;
@@ -1431,6 +1625,23 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         const int64_t threads1 = kP1Threads;
         M.wide = std::max(d.r, d.r_res) > kNarrow ? 1 : 0;
         M.tc = (M.wide && d.r > tc_min_rank()) ? 1 : 0;
+        static const bool fx_off = std::getenv("EDGC_NO_FX") != nullptr;
+        M.fx = (M.wide && d.r >= 32 && (M.tc || d.r > 32) && !fx_off) ? 1 : 0;   // single P_raw chunk
+        if (M.fx) {
+            // Gram K splits: >= 512 rows, and few enough that [gsplit][r][r] fits in q_part when possible
+            const int64_t want = std::max<int64_t>(512, ceil_div((int64_t)d.m * d.r, d.n));
+            M.gks = (int32_t)(ceil_div(want, 16) * 16);
+            M.gsplit = (int32_t)ceil_div(d.m, (int64_t)M.gks);
+            const int nbt = (int)ceil_div(d.r, kFxT);
+            for (int32_t c = 0; c < M.gsplit; ++c)
+                for (int bi = 0; bi < nbt; ++bi)
+                    for (int bj = bi; bj < nbt; ++bj)
+                        P.fxg.push_back(FxTile{k, c, bi * kFxT, bj * kFxT, (int64_t)c * M.gks,
+                                               std::min<int64_t>(d.m, (int64_t)(c + 1) * M.gks)});
+            for (int64_t i0 = 0; i0 < d.m; i0 += kFxT)
+                for (int bj = 0; bj < nbt; ++bj)
+                    P.fxr.push_back(FxTile{k, 0, 0, bj * kFxT, i0, std::min<int64_t>(d.m, i0 + kFxT)});
+        }
         // wide path K split of P_raw = w q_warm: 2048 columns up to r = 32; above, one K block
         // (the fp64 partials [nchunk1][m][r] scale with r while the tile count already suffices)
         const int64_t k1 = (M.tc || d.r > 32) ? d.n : kWideSplitK;
@@ -1495,6 +1706,9 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.dead = a.take<int32_t>(M.r);
         M.fwork = a.take<double>(5 * (int64_t)M.r * M.r);
         M.p_tmp = a.take<double>(M.m * M.r);
+        M.fmode = a.take<int32_t>(M.fx ? 1 : 0);
+        const int64_t gp = M.fx ? (int64_t)M.gsplit * M.r * M.r : 0;
+        M.gpart = gp <= (int64_t)M.nblk2 * M.n * M.r ? M.q_part : a.take<double>(gp);
     }
     P.d_samp = a.take<SampDev>(n);
     P.sample_slots = 0;
@@ -1520,6 +1734,8 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         P.d_tcp[c] = a.take<GemmTile>(P.tcp[c].size());
         P.d_tcq[c] = a.take<GemmTile>(P.tcq[c].size());
     }
+    P.d_fxg = a.take<FxTile>(P.fxg.size());
+    P.d_fxr = a.take<FxTile>(P.fxr.size());
     P.d_gw = a.take<GemmTile>(P.gw.size());
     P.d_gp = a.take<GemmTile>(P.gp.size());
     P.d_gq = a.take<GemmTile>(P.gq.size());
@@ -1949,6 +2165,10 @@ extern "C" int edgc_compress_plan_bind(edgc_compress_plan *h, void *ws, int64_t 
     };
     EDGC_CUDA_TRY(upg(P.d_gw, P.gw));
     EDGC_CUDA_TRY(upg(P.d_tce, P.tce));
+    if (!P.fxg.empty())
+        EDGC_CUDA_TRY(cudaMemcpyAsync(P.d_fxg, P.fxg.data(), sizeof(FxTile) * P.fxg.size(), cudaMemcpyHostToDevice, st));
+    if (!P.fxr.empty())
+        EDGC_CUDA_TRY(cudaMemcpyAsync(P.d_fxr, P.fxr.data(), sizeof(FxTile) * P.fxr.size(), cudaMemcpyHostToDevice, st));
     for (int c = 0; c < 2; ++c) {
         EDGC_CUDA_TRY(upg(P.d_tcp[c], P.tcp[c]));
         EDGC_CUDA_TRY(upg(P.d_tcq[c], P.tcq[c]));
@@ -1998,6 +2218,16 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
     if (phases & EDGC_PHASE_FACTOR) {
         k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
         EDGC_LAUNCH_CHECK();
+        if (!P.fxg.empty()) {
+            const unsigned ng = (unsigned)P.fxg.size(), nr = (unsigned)P.fxr.size();
+            k_fx_gram<<<ng, kFxThreads, 0, st>>>(P.d_mats, P.d_fxg, status_dev, 1);
+            k_fx_chol1<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
+            k_fx_rmul<<<nr, kFxThreads, 0, st>>>(P.d_mats, P.d_fxr, status_dev, 1);
+            k_fx_gram<<<ng, kFxThreads, 0, st>>>(P.d_mats, P.d_fxg, status_dev, 2);
+            k_fx_chol2<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev);
+            k_fx_rmul<<<nr, kFxThreads, 0, st>>>(P.d_mats, P.d_fxr, status_dev, 2);
+            EDGC_LAUNCH_CHECK();
+        }
     }
     if (phases & EDGC_PHASE_PASS2) {
         if ((rc = launch_pass2(P, true, status_dev, st))) return rc;
