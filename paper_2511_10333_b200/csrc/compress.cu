@@ -1337,6 +1337,7 @@ __device__ __forceinline__ int tc_rows4(int64_t rem) { return rem <= 0 ? 0 : rem
 
 struct TcPraw {
     static constexpr bool kAMN = false, kBMN = true;
+    static constexpr int kPF = 0;
     using Tile = GemmTile;
     const MatDev *mats;
     const GemmTile *tiles;
@@ -1348,7 +1349,8 @@ struct TcPraw {
         a = tc::View{M.w + t.i0 * M.n + t.k0, M.n, M.m - t.i0, t.k1 - t.k0, 0, 0};
         b = tc::View{M.q_warm + t.k0 * M.ld_q + t.j0, M.ld_q, M.r - t.j0, t.k1 - t.k0, 0, 0};
     }
-    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8]) const {
+    __device__ void prefetch(const Tile &, int, int, uint8_t *) const {}
+    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8], const uint8_t *) const {
         const MatDev &M = mats[t.mat];
         const int nc = M.r - (int)t.j0 - col;
         if (nc <= 0) return;
@@ -1367,6 +1369,7 @@ struct TcPraw {
 
 struct TcQ {
     static constexpr bool kAMN = true, kBMN = true;
+    static constexpr int kPF = 0;
     using Tile = GemmTile;
     const MatDev *mats;
     const GemmTile *tiles;
@@ -1383,7 +1386,8 @@ struct TcQ {
         a = tc::View{M.w + t.k0 * M.n + t.i0, M.n, M.n - t.i0, t.k1 - t.k0, 0, 0};
         b = tc::View{M.p_out + t.k0 * M.r + t.j0, M.r, M.r - t.j0, t.k1 - t.k0, 0, 0};
     }
-    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8]) const {
+    __device__ void prefetch(const Tile &, int, int, uint8_t *) const {}
+    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8], const uint8_t *) const {
         const MatDev &M = mats[t.mat];
         const int nc = M.r - (int)t.j0 - col;
         if (nc <= 0) return;
@@ -1402,6 +1406,7 @@ struct TcQ {
 
 struct TcEF {
     static constexpr bool kAMN = false, kBMN = false;
+    static constexpr int kPF = 16;   // g and w of the slice, one slice ahead
     using Tile = GemmTile;
     const MatDev *mats;
     const GemmTile *tiles;
@@ -1415,28 +1420,34 @@ struct TcEF {
         a = tc::View{M.p_res + t.i0 * rr, rr, M.m - t.i0, rr, 0, 0};
         b = tc::View{M.q_res + t.j0 * rr, rr, M.n - t.j0, rr, 0, 0};
     }
-    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8]) const {
+    __device__ void prefetch(const Tile &t, int row0, int col, uint8_t *dst) const {
+        const MatDev &M = mats[t.mat];
+        const int64_t j = t.j0 + col;
+        if (!M.al4 || j >= M.n) return;
+        const int nu = tc_rows4(M.m - t.i0 - row0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (u < nu) {
+                const int64_t gi = t.i0 + row0 + 4 * u;
+                tc::cp_async16(dst + u * 2048, M.g + gi * M.ld_g + j);
+                tc::cp_async16(dst + (8 + u) * 2048, M.w + gi * M.n + j);
+            }
+    }
+    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8], const uint8_t *pf) const {
         const MatDev &M = mats[t.mat];
         const int64_t j = t.j0 + col;
         if (j >= M.n) return;
         const int nu = tc_rows4(M.m - t.i0 - row0);   // rows row0 + 4u < m
         bool bad = false;
         if (M.al4) {
-            // all loads first (16 in flight), then the stores
-            float4 g4[8], w4[8];
+            // g and w arrived through the prefetch slots
 #pragma unroll
             for (int u = 0; u < 8; ++u)
                 if (u < nu) {
                     const int64_t gi = t.i0 + row0 + 4 * u;
-                    g4[u] = __ldcs(reinterpret_cast<const float4 *>(M.g + gi * M.ld_g + j));
-                    w4[u] = __ldcs(reinterpret_cast<const float4 *>(M.w + gi * M.n + j));
-                }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (u < nu) {
-                    const int64_t gi = t.i0 + row0 + 4 * u;
-                    const float x0 = g4[u].x + (w4[u].x - v[u].x), x1 = g4[u].y + (w4[u].y - v[u].y);
-                    const float x2 = g4[u].z + (w4[u].z - v[u].z), x3 = g4[u].w + (w4[u].w - v[u].w);
+                    const float4 g4 = ptx::ld_shared_v4(pf + u * 2048), w4 = ptx::ld_shared_v4(pf + (8 + u) * 2048);
+                    const float x0 = g4.x + (w4.x - v[u].x), x1 = g4.y + (w4.y - v[u].y);
+                    const float x2 = g4.z + (w4.z - v[u].z), x3 = g4.w + (w4.w - v[u].w);
                     bad |= !(isfinite(x0) && isfinite(x1) && isfinite(x2) && isfinite(x3));
                     __stcs(reinterpret_cast<float4 *>(M.w + gi * M.n + j), make_float4(x0, x1, x2, x3));
                 }
@@ -2078,6 +2089,7 @@ int elementwise_blocks(int64_t count) { return (int)std::max<int64_t>(1, std::mi
 // per-rank factor blocks are the K index's rank blocks)
 struct TcRecon {
     static constexpr bool kAMN = false, kBMN = false;
+    static constexpr int kPF = 0;
     using Tile = RTile;
     const ReconDev *descs;
     const RTile *tiles;
@@ -2090,7 +2102,8 @@ struct TcRecon {
         a = tc::View{D.p + t.row0 * D.r, D.r, D.m - t.row0, K, kb, D.p_stride};
         b = tc::View{D.q + t.col0 * D.r, D.r, D.n - t.col0, K, kb, D.q_stride};
     }
-    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8]) const {
+    __device__ void prefetch(const Tile &, int, int, uint8_t *) const {}
+    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8], const uint8_t *) const {
         const ReconDev &D = descs[t.d];
         const int64_t j = t.col0 + col;
         if (j >= D.n) return;

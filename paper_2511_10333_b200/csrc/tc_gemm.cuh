@@ -34,11 +34,16 @@
 //   static constexpr bool kAMN, kBMN;   // operand majority in global memory
 //   int64_t tile_k(const Tile&) -> number of K elements (>= 1)
 //   void views(const Tile&, View &a, View &b) const   // operand windows at the tile origin
-//   void epilogue(const Tile&, int row0, int col, const float4 (&v)[8]) const
+//   void epilogue(const Tile&, int row0, int col, const float4 (&v)[8], const uint8_t *pf) const
 //     v[u] = tile rows row0 + 4u, columns col .. col+3 (8 lanes cover 128
 //     contiguous bytes of a row: the accumulator slice is transposed through
 //     shared memory so global accesses coalesce); rows / columns outside the
 //     problem are the Op's to skip
+//   static constexpr int kPF;   // > 0: the epilogue reads kPF float4 of global input per
+//     thread and slice; the Op's prefetch(t, row0, col, uint8_t *dst) issues them as
+//     cp.async into per-thread slots (slot u at dst + u * 2048) one slice ahead (the
+//     first slice of a tile before its accumulator is ready), and epilogue() gets
+//     the slots in pf
 #pragma once
 
 #include <stdint.h>
@@ -63,16 +68,17 @@ struct View {
     int64_t ld, rows, K, kblk, kstride;
 };
 
-template <int BN, int KCH>
+template <int BN, int KCH, int PF = 0>
 struct Cfg {
     static_assert(BN == 64 || BN == 128, "tile N");
     static constexpr int kAPlane = kBM * kBK * 4;          // bytes of one (hi or lo) plane
     static constexpr int kBPlane = BN * kBK * 4;
     static constexpr int kStageBytes = 2 * (kAPlane + kBPlane);
-    static constexpr int kStages = BN == 128 ? 3 : 4;
+    static constexpr int kStages = BN == 128 ? (PF > 0 ? 2 : 3) : 4;
+    static constexpr int kPFBytes = 2 * PF * kEpiWarps * 32 * 16;   // double-buffered prefetch slots
     static constexpr int kBarBytes = 8 * (2 * kStages + 4) + 16;
     static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;   // per-warp 32 x 32 transpose slices
-    static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kBarBytes + 1024;
+    static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kPFBytes + kBarBytes + 1024;
     // two chunk accumulators (+ the running sum when chunked), power of two >= 32
     static constexpr uint32_t kCols = (KCH > 0 ? 3 : 2) * BN;
     static constexpr uint32_t kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
@@ -129,6 +135,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float *v) {
         : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // hi = x with the 13 low mantissa bits cleared (exact TF32), lo = x - hi (exact in
@@ -263,11 +275,13 @@ __device__ __forceinline__ bool view_vec(const View &v) {
 // KCH = K blocks (of 32) per accumulation chunk; 0 = the whole tile in one chunk
 template <int BN, int KCH, class Op>
 __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
-    using C = Cfg<BN, KCH>;
+    constexpr int PF = Op::kPF;
+    using C = Cfg<BN, KCH, PF>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *epi_smem = smem + C::kStages * C::kStageBytes;
-    uint64_t *full = (uint64_t *)(epi_smem + C::kEpiBytes);
+    uint8_t *pf_smem = epi_smem + C::kEpiBytes;
+    uint64_t *full = (uint64_t *)(pf_smem + C::kPFBytes);
     uint64_t *empty = full + C::kStages;
     uint64_t *tfull = empty + C::kStages;
     uint64_t *tempty = tfull + 2;
@@ -365,18 +379,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
         uint8_t *xs = epi_smem + warp * 4096;   // this warp's 32 x 32 fp32 slice, 16-byte chunks swizzled
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
         const uint32_t run = tmem + lane_off + 2 * BN;   // running sum (chunked)
+        uint8_t *pf = pf_smem + threadIdx.x * 16;         // this thread's prefetch slots
+        constexpr int kPFBuf = PF * kEpiWarps * 32 * 16;
+        const int row0 = warp * 32 + lane / 8, lcol = (lane & 7) * 4;
         for (int ti = blockIdx.x; ti < op.ntiles; ti += gridDim.x) {
             const typename Op::Tile t = op.tile(ti);
             const int nkb = (int)((op.tile_k(t) + kBK - 1) / kBK);
             const int kch = KCH > 0 ? KCH : nkb;
             for (int c0 = 0; c0 < nkb; c0 += kch, ++cc) {
                 const int b = (int)(cc & 1);
+                const bool first = c0 == 0, last = c0 + kch >= nkb;
+                if (PF > 0 && last) {
+                    op.prefetch(t, row0, lcol, pf);
+                    cp_async_commit();
+                }
                 ptx::mbar_wait(tfull + b, (uint32_t)(cc >> 1) & 1);
                 fence_after();
                 const uint32_t acc = tmem + lane_off + b * BN;
-                const bool first = c0 == 0, last = c0 + kch >= nkb;
 #pragma unroll 1
                 for (int col = 0; col < BN; col += 32) {
+                    const bool more = col + 32 < BN;
+                    if (PF > 0 && last && more) {
+                        op.prefetch(t, row0, col + 32 + lcol, pf + (((col >> 5) + 1) & 1) * kPFBuf);
+                        cp_async_commit();
+                    }
                     float v[32];
                     tmem_ld16(acc + col, v);
                     tmem_ld16(acc + col + 16, v + 16);
@@ -404,7 +430,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
                             x[u] = ptx::ld_shared_v4(xs + r * 128 + (((lane & 7) ^ (r & 7)) << 4));
                         }
                         __syncwarp();
-                        op.epilogue(t, warp * 32 + lane / 8, col + (lane & 7) * 4, x);
+                        if (PF > 0) {
+                            if (more) cp_async_wait<1>();
+                            else cp_async_wait<0>();
+                        }
+                        op.epilogue(t, row0, col + lcol, x, pf + ((col >> 5) & 1) * kPFBuf);
                     } else {
                         tmem_st16(run + col, v);
                         tmem_st16(run + col + 16, v + 16);
@@ -428,16 +458,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
 // launch helper: persistent grid of min(tiles, SMs) CTAs
 template <int BN, int KCH, class Op>
 inline cudaError_t launch(const Op &op, int sms, cudaStream_t st) {
+    using C = Cfg<BN, KCH, Op::kPF>;
     if (op.ntiles <= 0) return cudaSuccess;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_tc<BN, KCH, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Cfg<BN, KCH>::kSmem);
+        cudaError_t e = cudaFuncSetAttribute(k_tc<BN, KCH, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const int grid = op.ntiles < sms ? op.ntiles : sms;
-    k_tc<BN, KCH, Op><<<grid, kThreads, Cfg<BN, KCH>::kSmem, st>>>(op);
+    k_tc<BN, KCH, Op><<<grid, kThreads, C::kSmem, st>>>(op);
     return cudaGetLastError();
 }
 

@@ -19,6 +19,7 @@ using namespace edgc;
 template <bool AMN, bool BMN, int BN>
 struct PlainOp {
     static constexpr bool kAMN = AMN, kBMN = BMN;
+    static constexpr int kPF = 0;
     struct Tile {
         int64_t i0, j0;
     };
@@ -32,7 +33,8 @@ struct PlainOp {
         a = AMN ? tc::View{A + t.i0, lda, M - t.i0, K, 0, 0} : tc::View{A + t.i0 * lda, lda, M - t.i0, K, 0, 0};
         b = BMN ? tc::View{B + t.j0, ldb, N - t.j0, K, 0, 0} : tc::View{B + t.j0 * ldb, ldb, N - t.j0, K, 0, 0};
     }
-    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8]) const {
+    __device__ void prefetch(const Tile &, int, int, uint8_t *) const {}
+    __device__ void epilogue(const Tile &t, int row0, int col, const float4 (&v)[8], const uint8_t *) const {
         const int64_t j = t.j0 + col;
         for (int u = 0; u < 8; ++u) {
             const int64_t i = t.i0 + row0 + 4 * u;
