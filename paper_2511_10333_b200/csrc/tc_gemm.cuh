@@ -233,11 +233,15 @@ __device__ __forceinline__ void load_plane(const View &v, bool vec, int64_t kbas
     if (fast) {
         const int64_t koff = kmap(v, kbase);
         const float *p = MN ? v.p + (koff + k0) * v.ld + r0 : v.p + (int64_t)r0 * v.ld + koff + k0;
-        const int64_t step = PL::kStep * v.ld;   // kStep rows (K-major) or K lines (MN-major)
+        // kStep rows (K-major) or K lines (MN-major), < 2^31 elements per plane.  Opaque per
+        // K block: otherwise the compiler hoists the kPer 64-bit row addresses out of the K
+        // loop and spills them (measured: LDL on the producer's critical path)
+        uint32_t step = (uint32_t)(PL::kStep * v.ld);
+        asm volatile("" : "+r"(step));
 #pragma unroll
         for (int u = 0; u < PL::kPer; ++u) {
             if (PL::kVec % kGroupThreads != 0 && tid + u * kGroupThreads >= PL::kVec) break;
-            x[u] = __ldg(reinterpret_cast<const float4 *>(p + u * step));
+            x[u] = __ldg(reinterpret_cast<const float4 *>(p + (uint32_t)u * step));
         }
     } else {
 #pragma unroll
@@ -321,12 +325,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
                 const int s = (int)(q % C::kStages);
                 const uint32_t use = (uint32_t)(q / C::kStages);
                 float4 va[Plane<Op::kAMN, kBM>::kPer], vb[Plane<Op::kBMN, BN>::kPer];
-                load_plane<Op::kAMN, kBM>(av, avec, (int64_t)kb * kBK, tid, va);
-                load_plane<Op::kBMN, BN>(bv, bvec, (int64_t)kb * kBK, tid, vb);
+                // tid is made opaque per K block so the per-slot global / shared offsets are
+                // recomputed (cheap integer ops) instead of hoisted out of the loop and spilled
+                int otid = tid;
+                asm volatile("" : "+r"(otid));
+                load_plane<Op::kAMN, kBM>(av, avec, (int64_t)kb * kBK, otid, va);
+                load_plane<Op::kBMN, BN>(bv, bvec, (int64_t)kb * kBK, otid, vb);
                 ptx::mbar_wait(empty + s, (use & 1) ^ 1);
                 uint8_t *st = smem + s * C::kStageBytes;
-                store_plane<Op::kAMN, kBM>(st, st + C::kAPlane, tid, va);
-                store_plane<Op::kBMN, BN>(st + 2 * C::kAPlane, st + 2 * C::kAPlane + C::kBPlane, tid, vb);
+                asm volatile("" : "+r"(otid));
+                store_plane<Op::kAMN, kBM>(st, st + C::kAPlane, otid, va);
+                store_plane<Op::kBMN, BN>(st + 2 * C::kAPlane, st + 2 * C::kAPlane + C::kBPlane, otid, vb);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(full + s);
