@@ -708,7 +708,36 @@ __device__ __forceinline__ void k_bucket_resolve_body(const PlanDev *plans, int 
         }
         if (tid == 0) sm.fill = 0;
         __syncthreads();
-        for (int32_t k = tid; k < n; k += kBResThreads) {
+        if (!multi) {
+            // single pass: every entry is this pass's.  The global loads of a batch of
+            // entries are issued together before their list pushes (a shared-memory CAS
+            // loop would otherwise serialise one global round trip per entry)
+            constexpr int kB = 8;
+            for (int32_t k0 = tid; k0 < n; k0 += kB * kBResThreads) {
+                int32_t jj[kB], ss[kB];
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                    const int32_t k = k0 + u * kBResThreads;
+                    if (k < n) {
+                        const int c = sm.lp[k];
+                        const int32_t g = segstart[c] + (k - segoff[c]);
+                        jj[u] = __ldcs(P.lst_j + g);
+                        ss[u] = __ldcs(P.lst_s + g);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                    const int32_t k = k0 + u * kBResThreads;
+                    if (k < n) {
+                        const int l = jj[u] & (kBSize - 1);
+                        sm.ls[k] = ss[u];
+                        sm.lp[k] = (uint16_t)l;   // entry k's chunk, read above by this same thread
+                        sm.nx[k] = (int16_t)head_push(sm, l, k);
+                    }
+                }
+            }
+        }
+        for (int32_t k = tid; multi && k < n; k += kBResThreads) {
             const int c = multi ? chunk_of(k) : sm.lp[k];
             const int32_t g = segstart[c] + (k - segoff[c]);
             const int32_t jj = P.lst_j[g], ss = P.lst_s[g];
