@@ -756,10 +756,12 @@ __device__ void chol_dead(double *A, int r, double tol, const double *scale, int
             const double piv = R[k * r + k];
             for (int j = k + 1 + tid; j < r; j += kFactorThreads) R[k * r + j] = A[k * r + j] / piv;
             __syncthreads();
-            const int rem = r - k - 1;
-            for (int e = tid; e < rem * rem; e += kFactorThreads) {
-                const int i = k + 1 + e / rem, j = k + 1 + e % rem;
-                if (j >= i) A[i * r + j] -= R[k * r + i] * R[k * r + j];
+            // trailing upper triangle, one warp per row i, lanes along j (coalesced, no div/mod)
+            const double *rk = R + k * r;
+            for (int i = k + 1 + tid / 32; i < r; i += kFactorThreads / 32) {
+                const double ri = rk[i];
+                double *Ai = A + i * r;
+                for (int j = i + tid % 32; j < r; j += 32) Ai[j] -= ri * rk[j];
             }
         }
         __syncthreads();
@@ -767,17 +769,27 @@ __device__ void chol_dead(double *A, int r, double tol, const double *scale, int
 }
 
 // T = R^{-1} over the live columns (dead rows/columns zero); T column j at T[j*r + i].
+// One warp per column (columns dealt round-robin, so the O(j^2) costs balance): the
+// back substitution is sequential in i, each step a lane-strided dot product of row i
+// of R with the column so far, summed by a fixed-order butterfly (deterministic).
 __device__ void tri_inverse(const double *R, const int32_t *dead, int r, double *T) {
-    for (int j = threadIdx.x; j < r; j += kFactorThreads) {
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    constexpr int kW = kFactorThreads / 32;
+    for (int j = warp; j < r; j += kW) {
         double *x = T + (int64_t)j * r;
-        for (int i = 0; i < r; ++i) x[i] = 0.0;
+        for (int i = lane; i < r; i += 32) x[i] = 0.0;
+        __syncwarp();
         if (dead[j]) continue;
-        x[j] = 1.0 / R[j * r + j];
+        if (lane == 0) x[j] = 1.0 / R[j * r + j];
+        __syncwarp();
         for (int i = j - 1; i >= 0; --i) {
             if (dead[i]) continue;
             double acc = 0.0;
-            for (int l = i + 1; l <= j; ++l) acc += R[i * r + l] * x[l];
-            x[i] = -acc / R[i * r + i];
+            for (int l = i + 1 + lane; l <= j; l += 32) acc += R[i * r + l] * x[l];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) x[i] = -acc / R[i * r + i];
+            __syncwarp();
         }
     }
     __syncthreads();
@@ -981,26 +993,39 @@ struct FxTile {
 };
 
 constexpr int kFxT = 64, kFxK = 16, kFxThreads = 256;
+constexpr int kFxBig = 128;   // tile edge of the fp64 factorisation GEMMs at r >= 128
 
 __device__ __forceinline__ bool fx_active(const MatDev &M, const int32_t *status, int mat, int pass) {
     if (status[mat] & 1) return false;
     return pass == 1 || *M.fmode == 2;
 }
 
+// fp64 register-blocked tile GEMMs of the multi-CTA factorisation: a TT x TT output tile
+// per CTA (TT = 64 below rank 128, 128 above), 256 threads as 16 x 16, each thread
+// RB x RB outputs at rows 2 ty + 32 u' + {0,1}, columns 2 tx + 32 v' + {0,1} (double2
+// shared loads, conflict-free across the 16 tx lanes).  Every output's K sum runs in
+// ascending k, so the result does not depend on TT.
+template <int TT>
+struct FxBlk {
+    static constexpr int RB = TT / 16, RP = RB / 2;
+};
+
 // gpart[split][i][j] = sum_{k in split} X[k][i] X[k][j] for the upper tile (i0 <= j0)
+template <int TT>
 __global__ void __launch_bounds__(kFxThreads) k_fx_gram(const MatDev *mats, const FxTile *tiles, const int32_t *status,
                                                         int pass) {
+    constexpr int RB = FxBlk<TT>::RB, RP = FxBlk<TT>::RP;
     const FxTile t = tiles[blockIdx.x];
     const MatDev &M = mats[t.mat];
     if (!fx_active(M, status, t.mat, pass)) return;
     const int r = M.r;
     const double *X = pass == 1 ? M.p_raw : M.p_tmp;
-    __shared__ double As[kFxK][kFxT + 1], Bs[kFxK][kFxT + 1];
+    __shared__ __align__(16) double As[kFxK][TT], Bs[kFxK][TT];
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-    double acc[4][4] = {};
+    double acc[RB][RB] = {};
     for (int64_t k0 = t.r0; k0 < t.r1; k0 += kFxK) {
-        for (int e = tid; e < kFxK * kFxT; e += kFxThreads) {
-            const int kk = e / kFxT, c = e % kFxT;
+        for (int e = tid; e < kFxK * TT; e += kFxThreads) {
+            const int kk = e / TT, c = e % TT;
             const int64_t k = k0 + kk;
             const bool kin = k < t.r1;
             As[kk][c] = (kin && t.i0 + c < r) ? X[k * r + t.i0 + c] : 0.0;
@@ -1009,22 +1034,27 @@ __global__ void __launch_bounds__(kFxThreads) k_fx_gram(const MatDev *mats, cons
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < kFxK; ++kk) {
-            double a[4], b[4];
+            double a[RB], b[RB];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) { a[u] = As[kk][ty * 4 + u]; b[u] = Bs[kk][tx * 4 + u]; }
+            for (int u = 0; u < RP; ++u) {
+                const double2 x = *reinterpret_cast<const double2 *>(&As[kk][2 * ty + 32 * u]);
+                const double2 y = *reinterpret_cast<const double2 *>(&Bs[kk][2 * tx + 32 * u]);
+                a[2 * u] = x.x; a[2 * u + 1] = x.y;
+                b[2 * u] = y.x; b[2 * u + 1] = y.y;
+            }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < RB; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+                for (int v = 0; v < RB; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
         }
         __syncthreads();
     }
     double *G = M.gpart + (int64_t)t.split * r * r;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < RB; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int i = t.i0 + ty * 4 + u, j = t.j0 + tx * 4 + v;
+        for (int v = 0; v < RB; ++v) {
+            const int i = t.i0 + 2 * ty + 32 * (u / 2) + (u & 1), j = t.j0 + 2 * tx + 32 * (v / 2) + (v & 1);
             if (i < r && j < r) G[i * r + j] = acc[u][v];
         }
 }
@@ -1100,8 +1130,10 @@ __global__ void __launch_bounds__(kFactorThreads) k_fx_chol2(const MatDev *mats,
 }
 
 // Y[i][j] = sum_{l <= j} X[i][l] T(l, j), T column j at T[j*r + l] (upper triangular)
+template <int TT>
 __global__ void __launch_bounds__(kFxThreads) k_fx_rmul(const MatDev *mats, const FxTile *tiles, const int32_t *status,
                                                         int pass) {
+    constexpr int RB = FxBlk<TT>::RB, RP = FxBlk<TT>::RP;
     const FxTile t = tiles[blockIdx.x];
     const MatDev &M = mats[t.mat];
     if (!fx_active(M, status, t.mat, pass)) return;
@@ -1109,12 +1141,12 @@ __global__ void __launch_bounds__(kFxThreads) k_fx_rmul(const MatDev *mats, cons
     const bool single = *M.fmode == 1;
     const double *X = pass == 1 ? M.p_raw : M.p_tmp;
     const double *T = M.fwork + (int64_t)(pass == 1 ? 2 : 3) * r * r;   // T1 or T2
-    __shared__ double As[kFxK][kFxT + 1], Bs[kFxK][kFxT + 1];
+    __shared__ __align__(16) double As[kFxK][TT], Bs[kFxK][TT];
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-    double acc[4][4] = {};
-    const int kend = min(r, t.j0 + kFxT);   // T upper: l <= j < j0 + 64
+    double acc[RB][RB] = {};
+    const int kend = min(r, t.j0 + TT);   // T upper: l <= j < j0 + TT
     for (int k0 = 0; k0 < kend; k0 += kFxK) {
-        for (int e = tid; e < kFxK * kFxT; e += kFxThreads) {
+        for (int e = tid; e < kFxK * TT; e += kFxThreads) {
             // A: rows r0.. x K (coalesced along K); B: K x columns j0..
             const int c = e / kFxK, kk = e % kFxK;
             const int k = k0 + kk;
@@ -1126,22 +1158,27 @@ __global__ void __launch_bounds__(kFxThreads) k_fx_rmul(const MatDev *mats, cons
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < kFxK; ++kk) {
-            double a[4], b[4];
+            double a[RB], b[RB];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) { a[u] = As[kk][ty * 4 + u]; b[u] = Bs[kk][tx * 4 + u]; }
+            for (int u = 0; u < RP; ++u) {
+                const double2 x = *reinterpret_cast<const double2 *>(&As[kk][2 * ty + 32 * u]);
+                const double2 y = *reinterpret_cast<const double2 *>(&Bs[kk][2 * tx + 32 * u]);
+                a[2 * u] = x.x; a[2 * u + 1] = x.y;
+                b[2 * u] = y.x; b[2 * u + 1] = y.y;
+            }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < RB; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+                for (int v = 0; v < RB; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < RB; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int64_t i = t.r0 + ty * 4 + u;
-            const int j = t.j0 + tx * 4 + v;
+        for (int v = 0; v < RB; ++v) {
+            const int64_t i = t.r0 + 2 * ty + 32 * (u / 2) + (u & 1);
+            const int j = t.j0 + 2 * tx + 32 * (v / 2) + (v & 1);
             if (i >= t.r1 || j >= r) continue;
             const double y = acc[u][v];
             if (pass == 1 && !single) M.p_tmp[i * r + j] = y;
@@ -1404,6 +1441,10 @@ struct TcQ {
     }
 };
 
+// TcEF tile width (measured: 64 columns with a 3-slice g / w prefetch ring is slower,
+// 13.6 vs 11.0 ms at r = 128)
+constexpr int kTcEFN = 128;
+
 struct TcEF {
     static constexpr bool kAMN = false, kBMN = false;
     static constexpr int kPF = 16;   // g and w of the slice, one slice ahead
@@ -1453,13 +1494,16 @@ struct TcEF {
                 }
         } else {
             const int nc = M.n - j < 4 ? (int)(M.n - j) : 4;
-            for (int u = 0; u < nu; ++u) {
+            // static u: a dynamic index into v[] would put the slice in local memory
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (u >= nu) break;
                 const int64_t gi = t.i0 + row0 + 4 * u;
                 const float *g = M.g + gi * M.ld_g + j;
                 float *w = M.w + gi * M.n + j;
-                const float a[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
                 for (int c = 0; c < nc; ++c) {
-                    const float x = g[c] + (w[c] - a[c]);
+                    const float a = c == 0 ? v[u].x : c == 1 ? v[u].y : c == 2 ? v[u].z : v[u].w;
+                    const float x = g[c] + (w[c] - a);
                     bad |= !isfinite(x);
                     w[c] = x;
                 }
@@ -1579,7 +1623,8 @@ struct Plan {
     std::vector<GemmTile> gw, gp, gq;  // wide path: EF update, P_raw and Q tiles for r > 32
     std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles for r <= 16 (256x16) and <= 32 (128x32)
     std::vector<GemmTile> tce, tcp[2], tcq[2];
-    std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
+    std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles
+    int64_t nfxg64 = 0, nfxr64 = 0;   // the first n are 64-edge tiles, the rest kFxBig-edge   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
     int64_t bytes = 0;
     MatDev *d_mats = nullptr;
     Tile *d_t1v4 = nullptr, *d_t1v1 = nullptr, *d_t2v4 = nullptr, *d_t2v1 = nullptr;
@@ -1599,6 +1644,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     Arena a(ws, ws_bytes);
     P.mats.resize(n);
     P.d_mats = a.take<MatDev>(n);
+    std::vector<FxTile> fxg_big, fxr_big;   // kFxBig-edge factorisation tiles, appended after the 64-edge ones
     for (int k = 0; k < n; ++k) {
         const edgc_compress_desc &d = descs[k];
         EDGC_REQUIRE(d.m >= 1 && d.n >= 1, "compress desc %d: dims must be positive", k);
@@ -1643,15 +1689,18 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
             const int64_t want = std::max<int64_t>(512, ceil_div((int64_t)d.m * d.r, d.n));
             M.gks = (int32_t)(ceil_div(want, 16) * 16);
             M.gsplit = (int32_t)ceil_div(d.m, (int64_t)M.gks);
-            const int nbt = (int)ceil_div(d.r, kFxT);
+            const int tt = d.r >= kFxBig ? kFxBig : kFxT;   // tile edge (see k_fx_gram)
+            auto &vg = tt == kFxBig ? fxg_big : P.fxg;
+            auto &vr = tt == kFxBig ? fxr_big : P.fxr;
+            const int nbt = (int)ceil_div(d.r, tt);
             for (int32_t c = 0; c < M.gsplit; ++c)
                 for (int bi = 0; bi < nbt; ++bi)
                     for (int bj = bi; bj < nbt; ++bj)
-                        P.fxg.push_back(FxTile{k, c, bi * kFxT, bj * kFxT, (int64_t)c * M.gks,
-                                               std::min<int64_t>(d.m, (int64_t)(c + 1) * M.gks)});
-            for (int64_t i0 = 0; i0 < d.m; i0 += kFxT)
+                        vg.push_back(FxTile{k, c, bi * tt, bj * tt, (int64_t)c * M.gks,
+                                            std::min<int64_t>(d.m, (int64_t)(c + 1) * M.gks)});
+            for (int64_t i0 = 0; i0 < d.m; i0 += tt)
                 for (int bj = 0; bj < nbt; ++bj)
-                    P.fxr.push_back(FxTile{k, 0, 0, bj * kFxT, i0, std::min<int64_t>(d.m, i0 + kFxT)});
+                    vr.push_back(FxTile{k, 0, 0, bj * tt, i0, std::min<int64_t>(d.m, i0 + tt)});
         }
         // wide path K split of P_raw = w q_warm: 2048 columns up to r = 32; above, one K block
         // (the fp64 partials [nchunk1][m][r] scale with r while the tile count already suffices)
@@ -1664,7 +1713,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         if (M.wide) {
             if (d.r_res > tc_min_rank()) {
                 for (int64_t i0 = 0; i0 < d.m; i0 += tc::kBM)
-                    for (int64_t j0 = 0; j0 < d.n; j0 += 128) P.tce.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
+                    for (int64_t j0 = 0; j0 < d.n; j0 += kTcEFN) P.tce.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
             } else {
                 for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
                     for (int64_t j0 = 0; j0 < d.n; j0 += kGT) P.gw.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
@@ -1706,6 +1755,10 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                 (v4 ? P.t2v4 : P.t2v1).push_back(t);
             }
     }
+    P.nfxg64 = (int64_t)P.fxg.size();
+    P.nfxr64 = (int64_t)P.fxr.size();
+    P.fxg.insert(P.fxg.end(), fxg_big.begin(), fxg_big.end());
+    P.fxr.insert(P.fxr.end(), fxr_big.begin(), fxr_big.end());
     for (int k = 0; k < n; ++k) {
         MatDev &M = P.mats[k];
         M.p_part = a.take<double>(M.zmode ? 0 : (int64_t)M.nchunk1 * M.m * M.r);
@@ -2213,7 +2266,7 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         h->P.sample_armed = false;   // set_sampling arms exactly one pass 1
         if ((rc = launch_gemm<2>(P, P.gw, P.d_gw, status_dev, st))) return rc;
         if (!P.tce.empty())
-            EDGC_CUDA_TRY((tc::launch<128, 4>(TcEF{P.d_mats, P.d_tce, status_dev, (int)P.tce.size()}, sm_count(), st)));
+            EDGC_CUDA_TRY((tc::launch<kTcEFN, 4>(TcEF{P.d_mats, P.d_tce, status_dev, (int)P.tce.size()}, sm_count(), st)));
         if (!P.tcp[0].empty())
             EDGC_CUDA_TRY((tc::launch<64, 4>(TcPraw{P.d_mats, P.d_tcp[0], (int)P.tcp[0].size()}, sm_count(), st)));
         if (!P.tcp[1].empty())
@@ -2232,13 +2285,22 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
         EDGC_LAUNCH_CHECK();
         if (!P.fxg.empty()) {
-            const unsigned ng = (unsigned)P.fxg.size(), nr = (unsigned)P.fxr.size();
-            k_fx_gram<<<ng, kFxThreads, 0, st>>>(P.d_mats, P.d_fxg, status_dev, 1);
+            const unsigned g64 = (unsigned)P.nfxg64, gbig = (unsigned)(P.fxg.size() - P.nfxg64);
+            const unsigned r64 = (unsigned)P.nfxr64, rbig = (unsigned)(P.fxr.size() - P.nfxr64);
+            auto gram = [&](int pass) {
+                if (g64) k_fx_gram<kFxT><<<g64, kFxThreads, 0, st>>>(P.d_mats, P.d_fxg, status_dev, pass);
+                if (gbig) k_fx_gram<kFxBig><<<gbig, kFxThreads, 0, st>>>(P.d_mats, P.d_fxg + g64, status_dev, pass);
+            };
+            auto rmul = [&](int pass) {
+                if (r64) k_fx_rmul<kFxT><<<r64, kFxThreads, 0, st>>>(P.d_mats, P.d_fxr, status_dev, pass);
+                if (rbig) k_fx_rmul<kFxBig><<<rbig, kFxThreads, 0, st>>>(P.d_mats, P.d_fxr + r64, status_dev, pass);
+            };
+            gram(1);
             k_fx_chol1<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
-            k_fx_rmul<<<nr, kFxThreads, 0, st>>>(P.d_mats, P.d_fxr, status_dev, 1);
-            k_fx_gram<<<ng, kFxThreads, 0, st>>>(P.d_mats, P.d_fxg, status_dev, 2);
+            rmul(1);
+            gram(2);
             k_fx_chol2<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev);
-            k_fx_rmul<<<nr, kFxThreads, 0, st>>>(P.d_mats, P.d_fxr, status_dev, 2);
+            rmul(2);
             EDGC_LAUNCH_CHECK();
         }
     }

@@ -1,0 +1,6 @@
+set -x
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for r in 32 64 128 256; do timeout 300 python tools/pass1_ab.py --rank $r --iters 3; done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_fx" --csv --log-file gpurun_out/launch_fx3.csv python tools/pass1_ab.py --rank 256 --iters 1 > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/launch_fx3.csv 8
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_fx_chol1 -s 1 -c 1 -o gpurun_out/chol1 -f python tools/pass1_ab.py --rank 256 --iters 1 > /dev/null 2>&1
