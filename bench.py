@@ -65,7 +65,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--entropy", choices=["prefetch", "inline", "off"], default="prefetch",
                     help="diagnostics: entropy plans built ahead on a side stream (default), inline, or no tracker")
-    ap.add_argument("--hi-prio", action="store_true", help="diagnostics: run the step on a high-priority stream")
+    ap.add_argument("--no-hi-prio", dest="hi_prio", action="store_false",
+                    help="run the step on the default stream instead of a high-priority one (the entropy "
+                         "tracker's plan kernels run on a low-priority side stream and yield SMs to the step)")
     ap.add_argument("--alias-output", action="store_true",
                     help="averaged gradients overwrite the raw ones (default for the 12.1B set, to fit in HBM)")
     ap.add_argument("--no-fuse-entropy", dest="fuse_entropy", action="store_false",
@@ -213,7 +215,9 @@ def config_dict(args, shapes):
             else "inputs larger than L2", "parallelism": f"dp{args.gpus}",
             "entropy_stats": "gathered in pass 1" if getattr(args, "fuse_entropy", True) else "separate Gaussian pass",
             "entropy_plans": {"prefetch": "side stream, built during the preceding iterations",
-                              "inline": "built inside the sampled iteration", "off": "tracker disabled"}[args.entropy]}
+                              "inline": "built inside the sampled iteration", "off": "tracker disabled"}[args.entropy],
+            "streams": "step on a high-priority stream, entropy plans on a low-priority side stream"
+            if getattr(args, "hi_prio", True) else "step on the default stream"}
 
 
 # ------------------------------------------------------------------ GPU side
