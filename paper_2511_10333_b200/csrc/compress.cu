@@ -741,9 +741,10 @@ __device__ void gram_pass(const double *P, int64_t m, int r, double *gram, doubl
 
 // A (r x r, destroyed) -> R (upper, row-major R[i*r+j]); dead[] updated when detect.
 // tol_k = tol * scale[k] (scale = NULL -> 1).
+template <int NT = kFactorThreads>
 __device__ void chol_dead(double *A, int r, double tol, const double *scale, int32_t *dead, double *R, bool detect) {
     const int tid = threadIdx.x;
-    for (int e = tid; e < r * r; e += kFactorThreads) R[e] = 0.0;
+    for (int e = tid; e < r * r; e += NT) R[e] = 0.0;
     __syncthreads();
     for (int k = 0; k < r; ++k) {
         if (tid == 0) {
@@ -754,14 +755,28 @@ __device__ void chol_dead(double *A, int r, double tol, const double *scale, int
         __syncthreads();
         if (!dead[k]) {
             const double piv = R[k * r + k];
-            for (int j = k + 1 + tid; j < r; j += kFactorThreads) R[k * r + j] = A[k * r + j] / piv;
+            for (int j = k + 1 + tid; j < r; j += NT) R[k * r + j] = A[k * r + j] / piv;
             __syncthreads();
             // trailing upper triangle, one warp per row i, lanes along j (coalesced, no div/mod)
             const double *rk = R + k * r;
-            for (int i = k + 1 + tid / 32; i < r; i += kFactorThreads / 32) {
+            for (int i = k + 1 + tid / 32; i < r; i += NT / 32) {
                 const double ri = rk[i];
                 double *Ai = A + i * r;
-                for (int j = i + tid % 32; j < r; j += 32) Ai[j] -= ri * rk[j];
+                int j = i + tid % 32;
+                // four elements per lane in flight (loads first: A and R share the workspace)
+                for (; j + 96 < r; j += 128) {
+                    double a0 = Ai[j], a1 = Ai[j + 32], a2 = Ai[j + 64], a3 = Ai[j + 96];
+                    const double b0 = rk[j], b1 = rk[j + 32], b2 = rk[j + 64], b3 = rk[j + 96];
+                    a0 -= ri * b0;
+                    a1 -= ri * b1;
+                    a2 -= ri * b2;
+                    a3 -= ri * b3;
+                    Ai[j] = a0;
+                    Ai[j + 32] = a1;
+                    Ai[j + 64] = a2;
+                    Ai[j + 96] = a3;
+                }
+                for (; j < r; j += 32) Ai[j] -= ri * rk[j];
             }
         }
         __syncthreads();
@@ -772,9 +787,10 @@ __device__ void chol_dead(double *A, int r, double tol, const double *scale, int
 // One warp per column (columns dealt round-robin, so the O(j^2) costs balance): the
 // back substitution is sequential in i, each step a lane-strided dot product of row i
 // of R with the column so far, summed by a fixed-order butterfly (deterministic).
+template <int NT = kFactorThreads>
 __device__ void tri_inverse(const double *R, const int32_t *dead, int r, double *T) {
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    constexpr int kW = kFactorThreads / 32;
+    constexpr int kW = NT / 32;
     for (int j = warp; j < r; j += kW) {
         double *x = T + (int64_t)j * r;
         for (int i = lane; i < r; i += 32) x[i] = 0.0;
@@ -1060,9 +1076,10 @@ __global__ void __launch_bounds__(kFxThreads) k_fx_gram(const MatDev *mats, cons
 }
 
 // gram (upper, mirrored) = fixed-order sum of the split partials
+template <int NT>
 __device__ void fx_gram_sum(const MatDev &M, double *gram) {
     const int r = M.r;
-    for (int e = threadIdx.x; e < r * r; e += kFactorThreads) {
+    for (int e = threadIdx.x; e < r * r; e += NT) {
         const int i = e / r, j = e % r;
         if (j < i) continue;
         // the tile holding (i, j) is upper by block: (i/64 <= j/64); entries below the
@@ -1075,53 +1092,56 @@ __device__ void fx_gram_sum(const MatDev &M, double *gram) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kFactorThreads) k_fx_chol1(const MatDev *mats, int32_t *status, double col_tol) {
+// the r x r work of the wide-rank factorisation: 16 warps per matrix (latency-bound chains)
+constexpr int kCholThreads = 512;
+
+__global__ void __launch_bounds__(kCholThreads) k_fx_chol1(const MatDev *mats, int32_t *status, double col_tol) {
     const MatDev &M = mats[blockIdx.x];
     if (!M.fx || (status[blockIdx.x] & 1)) return;
     const int r = M.r, tid = threadIdx.x;
     double *gram = M.fwork, *R = gram + r * r, *T1 = R + r * r;
-    __shared__ double s_tmp[kFactorThreads / 32];
+    __shared__ double s_tmp[kCholThreads / 32];
     __shared__ double s_tol;
     int32_t *dead = M.dead;
-    for (int j = tid; j < r; j += kFactorThreads) dead[j] = 0;
-    fx_gram_sum(M, gram);
+    for (int j = tid; j < r; j += kCholThreads) dead[j] = 0;
+    fx_gram_sum<kCholThreads>(M, gram);
     if (tid == 0) {
         double fro2 = 0.0;   // ||P_raw||_F^2 (compressor.py:79)
         for (int j = 0; j < r; ++j) fro2 += gram[j * r + j];
         s_tol = col_tol * sqrt(fro2);
     }
     __syncthreads();
-    chol_dead(gram, r, s_tol, nullptr, dead, R, true);
+    chol_dead<kCholThreads>(gram, r, s_tol, nullptr, dead, R, true);
     auto block_sumsq = [&](const double *X) -> double {
         double a = 0.0;
-        for (int e = tid; e < r * r; e += kFactorThreads) a += X[e] * X[e];
+        for (int e = tid; e < r * r; e += kCholThreads) a += X[e] * X[e];
         a = warp_sum(a);
         if ((tid & 31) == 0) s_tmp[tid >> 5] = a;
         __syncthreads();
         double tot = 0.0;
-        for (int w = 0; w < kFactorThreads / 32; ++w) tot += s_tmp[w];
+        for (int w = 0; w < kCholThreads / 32; ++w) tot += s_tmp[w];
         __syncthreads();
         return tot;
     };
     const double rn2 = block_sumsq(R);
-    tri_inverse(R, dead, r, T1);
+    tri_inverse<kCholThreads>(R, dead, r, T1);
     const double tn2 = block_sumsq(T1);
     const bool single = sqrt(rn2 * tn2) <= 1000.0;   // as k_factor (non-Z)
     if (single)
-        for (int e = tid; e < r * r; e += kFactorThreads) M.tmat[e] = T1[e];
+        for (int e = tid; e < r * r; e += kCholThreads) M.tmat[e] = T1[e];
     if (tid == 0) *M.fmode = single ? 1 : 2;
 }
 
-__global__ void __launch_bounds__(kFactorThreads) k_fx_chol2(const MatDev *mats, const int32_t *status) {
+__global__ void __launch_bounds__(kCholThreads) k_fx_chol2(const MatDev *mats, const int32_t *status) {
     const MatDev &M = mats[blockIdx.x];
     if (!M.fx || (status[blockIdx.x] & 1) || *M.fmode != 2) return;
     const int r = M.r, tid = threadIdx.x;
     double *gram = M.fwork, *R = gram + r * r, *T1 = R + r * r, *T2 = T1 + r * r;
-    fx_gram_sum(M, gram);
-    chol_dead(gram, r, 0.0, nullptr, M.dead, R, false);
-    tri_inverse(R, M.dead, r, T2);
+    fx_gram_sum<kCholThreads>(M, gram);
+    chol_dead<kCholThreads>(gram, r, 0.0, nullptr, M.dead, R, false);
+    tri_inverse<kCholThreads>(R, M.dead, r, T2);
     // T = T1 T2 (P = P_raw T)
-    for (int e = tid; e < r * r; e += kFactorThreads) {
+    for (int e = tid; e < r * r; e += kCholThreads) {
         const int j = e / r, l = e % r;
         double a = 0.0;
         for (int i = l; i <= j; ++i) a += T1[(int64_t)i * r + l] * T2[(int64_t)j * r + i];
@@ -2296,10 +2316,10 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
                 if (rbig) k_fx_rmul<kFxBig><<<rbig, kFxThreads, 0, st>>>(P.d_mats, P.d_fxr + r64, status_dev, pass);
             };
             gram(1);
-            k_fx_chol1<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
+            k_fx_chol1<<<n, kCholThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
             rmul(1);
             gram(2);
-            k_fx_chol2<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev);
+            k_fx_chol2<<<n, kCholThreads, 0, st>>>(P.d_mats, status_dev);
             rmul(2);
             EDGC_LAUNCH_CHECK();
         }
