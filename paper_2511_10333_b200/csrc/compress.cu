@@ -1461,6 +1461,9 @@ struct TcQ {
     }
 };
 
+#ifndef EDGC_EF_DIAG
+#define EDGC_EF_DIAG 0   // diagnostics (wrong results): 1 = no g / w loads, 2 = no w stores
+#endif
 // TcEF tile width (measured: 64 columns with a 3-slice g / w prefetch ring is slower,
 // 13.6 vs 11.0 ms at r = 128)
 constexpr int kTcEFN = 128;
@@ -1484,7 +1487,7 @@ struct TcEF {
     __device__ void prefetch(const Tile &t, int row0, int col, uint8_t *dst) const {
         const MatDev &M = mats[t.mat];
         const int64_t j = t.j0 + col;
-        if (!M.al4 || j >= M.n) return;
+        if (!M.al4 || j >= M.n || EDGC_EF_DIAG == 1) return;
         const int nu = tc_rows4(M.m - t.i0 - row0);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -1510,7 +1513,8 @@ struct TcEF {
                     const float x0 = g4.x + (w4.x - v[u].x), x1 = g4.y + (w4.y - v[u].y);
                     const float x2 = g4.z + (w4.z - v[u].z), x3 = g4.w + (w4.w - v[u].w);
                     bad |= !(isfinite(x0) && isfinite(x1) && isfinite(x2) && isfinite(x3));
-                    __stcs(reinterpret_cast<float4 *>(M.w + gi * M.n + j), make_float4(x0, x1, x2, x3));
+                    if (EDGC_EF_DIAG != 2)
+                        __stcs(reinterpret_cast<float4 *>(M.w + gi * M.n + j), make_float4(x0, x1, x2, x3));
                 }
         } else {
             const int nc = M.n - j < 4 ? (int)(M.n - j) : 4;

@@ -203,11 +203,15 @@ struct WalkGroup {
 
 __device__ __forceinline__ void group_sync(int g) { ptx::named_bar_sync(1 + g, kWT); }
 
-__global__ void __launch_bounds__(kWT * kWG, 1) k_walk(const PlanDev *plans, int n_plans, int32_t *status) {
+// order[]: the plans by decreasing step count, so a CTA's groups walk plans of similar
+// length and CTAs of short plans free their SMs early
+__global__ void __launch_bounds__(kWT * kWG, 1) k_walk(const PlanDev *plans, int n_plans, int32_t *status,
+                                                      const int32_t *order) {
     extern __shared__ __align__(128) unsigned char walk_raw[];
     const int g = threadIdx.x / kWT;
-    const int pid = blockIdx.x * kWG + g;
-    if (pid >= n_plans) return;   // the whole group leaves; groups synchronise only among themselves
+    const int slot = blockIdx.x * kWG + g;
+    if (slot >= n_plans) return;   // the whole group leaves; groups synchronise only among themselves
+    const int pid = order[slot];
     WalkGroup &W = reinterpret_cast<WalkGroup *>(walk_raw)[g];
     const PlanDev P = plans[pid];
     const int tid = threadIdx.x % kWT, lane = tid & 31, warp = tid >> 5;
@@ -872,6 +876,8 @@ struct PlanLayout {
     std::vector<int32_t> lut_host;                    // [sort | bucket | chain] CTA-group -> plan tables
     int64_t lut_n[3] = {0, 0, 0};
     int32_t *lut_dev = nullptr;
+    int32_t *walk_order = nullptr;            // k_walk: plans by decreasing step count
+    std::vector<int32_t> walk_order_host;
     int n_bucketed = 0;
     int64_t table_bytes = 0;
     char *table_base = nullptr;
@@ -962,6 +968,12 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
     for (int i = 0; i < n; ++i)
         if (L.dev[i].bucketed) L.dev[i].nchain = L.nchains + i;
     a.off += align256(4 * (int64_t)n);
+    L.walk_order = reinterpret_cast<int32_t *>(a.base ? a.base + a.off : nullptr);
+    a.off += align256(4 * (int64_t)n);
+    L.walk_order_host.resize(n);
+    for (int i = 0; i < n; ++i) L.walk_order_host[i] = i;
+    std::stable_sort(L.walk_order_host.begin(), L.walk_order_host.end(),
+                     [&](int x, int y) { return L.dev[x].count > L.dev[y].count; });
     const int64_t t0 = a.off;
     L.table_off.assign(n + 1, 0);
     for (int i = 0; i < n; ++i) {
@@ -1065,7 +1077,10 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = wc > 1 ? 1 : 0;
-        EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_walk, (const PlanDev *)d_plans, n_plans, status_dev));
+        EDGC_CUDA_TRY(cudaMemcpyAsync(L.walk_order, L.walk_order_host.data(), 4 * (size_t)n_plans,
+                                      cudaMemcpyHostToDevice, st));
+        EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_walk, (const PlanDev *)d_plans, n_plans, status_dev,
+                                         (const int32_t *)L.walk_order));
     }
     if (L.n_bucketed) {
         // bucket path (tail-shuffle plans); plans are ordered, so each kernel's CTA range covers
