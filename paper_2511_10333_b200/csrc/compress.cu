@@ -2063,8 +2063,11 @@ __host__ __device__ constexpr int v4_tile_rows(int wr) { return wr <= 8 ? 64 : 2
 
 // VC adjacent columns per thread (4, or 2 when W*r = 32 to keep Q in registers);
 // kV4Cols = 512 columns per tile either way.
+#ifndef EDGC_RECON32_MINB
+#define EDGC_RECON32_MINB 2   // CTAs per SM for W*r = 32 (2 caps registers at 128: Q partly spills)
+#endif
 template <int WR, int VC>
-__global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? 2 : 1) k_recon4(const ReconDev *descs, const RTile *tiles) {
+__global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1) k_recon4(const ReconDev *descs, const RTile *tiles) {
     constexpr int NT = kV4Cols / VC;
     constexpr int kV4TileRows = v4_tile_rows(WR);
     const RTile t = tiles[blockIdx.x];
