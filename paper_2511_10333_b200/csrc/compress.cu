@@ -2063,6 +2063,9 @@ __host__ __device__ constexpr int v4_tile_rows(int wr) { return wr <= 8 ? 64 : 2
 
 // VC adjacent columns per thread (4, or 2 when W*r = 32 to keep Q in registers);
 // kV4Cols = 512 columns per tile either way.
+#ifndef EDGC_RECON32_ROWS
+#define EDGC_RECON32_ROWS 8
+#endif
 #ifndef EDGC_RECON32_MINB
 #define EDGC_RECON32_MINB 2   // CTAs per SM for W*r = 32 (2 caps registers at 128: Q partly spills)
 #endif
@@ -2100,26 +2103,31 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
     }
     __syncthreads();
     if (!active) return;
-    for (int64_t row = t.row0; row < t.row1; row += kV4Rows) {
+    // rows per pass: 8, or EDGC_RECON32_ROWS for W*r = 32 (fewer live accumulators next to Q)
+    constexpr int RP = WR == 32 ? EDGC_RECON32_ROWS : kV4Rows;
+    for (int64_t row = t.row0; row < t.row1; row += RP) {
         const int lr = (int)(row - t.row0);
-        float acc[kV4Rows][VC];
+        float acc[RP][VC];
 #pragma unroll
-        for (int rr = 0; rr < kV4Rows; ++rr)
+        for (int rr = 0; rr < RP; ++rr)
 #pragma unroll
             for (int v = 0; v < VC; ++v) acc[rr][v] = 0.f;
         // per output the fma order over (worker, k) is c ascending
 #pragma unroll
         for (int c = 0; c < WR; ++c) {
-            const float4 pa = *reinterpret_cast<const float4 *>(&s_pT[c][lr]);
-            const float4 pb = *reinterpret_cast<const float4 *>(&s_pT[c][lr + 4]);
-            const float pr[kV4Rows] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+            float pr[RP];
 #pragma unroll
-            for (int rr = 0; rr < kV4Rows; ++rr)
+            for (int h = 0; h < RP; h += 4) {
+                const float4 pa = *reinterpret_cast<const float4 *>(&s_pT[c][lr + h]);
+                pr[h] = pa.x; pr[h + 1] = pa.y; pr[h + 2] = pa.z; pr[h + 3] = pa.w;
+            }
+#pragma unroll
+            for (int rr = 0; rr < RP; ++rr)
 #pragma unroll
                 for (int v = 0; v < VC; ++v) acc[rr][v] = fmaf(pr[rr], q[v][c], acc[rr][v]);
         }
 #pragma unroll
-        for (int rr = 0; rr < kV4Rows; ++rr) {
+        for (int rr = 0; rr < RP; ++rr) {
             const int64_t i = row + rr;
             if (i >= t.row1) continue;
             if (VC == 4)
