@@ -59,3 +59,34 @@ def test_fused_statistics_match_oracle_entropies():
     ref = [oracle.gaussian_entropy(oracle.subsample(g.astype(np.float64), 0.25, oracle.subsample_seed(0, 0, k)))
            for k, g in enumerate(gs)]
     assert abs(closed.mean_entropy - float(np.mean(ref))) <= 1e-11
+
+
+def test_prefetched_plans_on_priority_stream_match_inline():
+    """The bench's arrangement -- the step on a high-priority stream, the next sampled
+    iteration's plans prefetched as short CTAs on the tracker's low-priority side stream,
+    statistics gathered in pass 1 -- gives the same windows as a tracker that builds its
+    plans inline on the default stream (cross-stream ordering is by events only)."""
+    from paper_2511_10333_b200.engine import BucketEngine
+    from paper_2511_10333_b200.entropy import EntropyTracker, SamplerConfig
+    cfg = SamplerConfig(alpha=0.25, beta=0.25, rng_seed=7)
+    eng = BucketEngine(SHAPES, rank=4, seed=2)
+    pf_tr = EntropyTracker(cfg, window=8, prefetch=True)
+    inline_tr = EntropyTracker(cfg, window=8, prefetch=False)
+    hi = torch.cuda.Stream(priority=-1)
+    for t in range(16):
+        gs = [oracle.synth_matrix(11, t, k, 0, m, n, 1e-2 * math.exp(-t / 30)) for k, (m, n) in enumerate(SHAPES)]
+        with torch.cuda.stream(hi):
+            for dst, g in zip(eng.grads, gs):
+                dst.copy_(torch.from_numpy(g))
+            req = pf_tr.fused_request(t, eng, eng.grads)
+            eng.step(check=True)
+            pf_tr.observe(t, eng.grads, fused=req)
+        hi.synchronize()
+        inline_tr.observe(t, eng.grads)
+        torch.cuda.synchronize()
+    pf_tr.flush()
+    inline_tr.flush()
+    assert len(pf_tr.windows) == len(inline_tr.windows) == 2
+    for a, b in zip(pf_tr.windows, inline_tr.windows):
+        assert a.samples_used == b.samples_used
+        assert abs(a.mean_entropy - b.mean_entropy) <= 1e-12
