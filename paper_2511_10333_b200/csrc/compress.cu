@@ -2057,7 +2057,6 @@ __global__ void __launch_bounds__(kGThreads) k_recon_tiled(const ReconDev *descs
 constexpr int kV4Threads = 128;
 constexpr int kV4Cols = 4 * kV4Threads;
 constexpr int kV4Rows = 8;
-constexpr int kV4TileRowsMax = 256;
 // rows per tile: 64 while Q (W*r <= 8 per column) is cheap to load, 256 above to amortise it
 __host__ __device__ constexpr int v4_tile_rows(int wr) { return wr <= 8 ? 64 : 256; }
 

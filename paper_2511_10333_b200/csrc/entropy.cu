@@ -470,7 +470,6 @@ __global__ void k_hist_entropy_final(const double *partial, int nblk, const int3
 }
 
 constexpr int kMinMaxBlocks = 296;
-constexpr int kHistBlocks = 592;
 constexpr int kEntBlocks = 148;
 
 struct HistLayout {

@@ -91,11 +91,11 @@ __device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
 }
 template <int NS>
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
-    if (NS == 0) {
+    if constexpr (NS == 0) {
         mbar_wait(bar, parity);
-        return;
+    } else {
+        while (!mbar_try(bar, parity)) __nanosleep(NS);
     }
-    while (!mbar_try(bar, parity)) __nanosleep(NS);
 }
 
 // wait with acquire at cluster scope: pairs with remote release-arrives

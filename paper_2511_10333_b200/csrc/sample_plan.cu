@@ -94,7 +94,6 @@ struct PlanDev {
 constexpr int kDrawsPerThread = 64;  // 64-bit outputs per P1 thread
 constexpr int kP1Threads = 256;
 constexpr int64_t kDrawsPerBlock = (int64_t)kDrawsPerThread * kP1Threads;
-constexpr int kWalkThreads = 1024;
 constexpr int kStepThreads = 256;
 
 __device__ __forceinline__ int find_plan(const PlanDev *plans, int n, int64_t blk, bool by_draw) {
@@ -138,17 +137,6 @@ __global__ void __launch_bounds__(kP1Threads) k_draws(const PlanDev *plans, int 
     }
 }
 
-// Lemire 32-bit bounded draw check (NumPy bounded_lemire_uint32).
-__device__ __forceinline__ bool lemire_accept(uint32_t x, uint32_t rng, uint32_t &val) {
-    const uint32_t excl = rng + 1u;
-    const uint64_t m = (uint64_t)x * excl;
-    val = (uint32_t)(m >> 32);
-    const uint32_t left = (uint32_t)m;
-    if (left >= excl) return true;
-    const uint32_t thr = (0xFFFFFFFFu - rng) % excl;
-    return left >= thr;
-}
-
 // 2^32 mod excl (NumPy's Lemire threshold (2^32 - excl) % excl), excl >= 1.  For
 // excl >= 2^16 the quotient is < 2^16, so a float reciprocal estimate is within
 // +-2 of it and two exact corrections finish; smaller excl take the division.
@@ -161,11 +149,6 @@ __device__ __forceinline__ uint32_t lemire_threshold(uint32_t excl) {
     r -= (r >= (int64_t)excl) ? (int64_t)excl : 0;
     r -= (r >= (int64_t)excl) ? (int64_t)excl : 0;
     return (uint32_t)r;
-}
-
-__device__ __forceinline__ uint32_t step_rng(const PlanDev &P, int64_t s) {
-    // tail: i = N-1-s (bounded(0..i)); Floyd: j = N-count+s (bounded(0..j))
-    return P.tail ? (uint32_t)(P.n_elems - 1 - s) : (uint32_t)(P.n_elems - P.count + s);
 }
 
 // ---- P2: assign draws to steps --------------------------------------------
