@@ -115,15 +115,15 @@ __device__ __forceinline__ void k_draws_body(const PlanDev *plans, int n_plans, 
     const int64_t o_base = (int64_t)(vb - P.draw_chunk0) * kDrawsPerBlock;
     const int64_t n64 = P.n_draws / 2;
     if (o_base >= n64) return;
-    u128 s = pcg_jump(P.state, P.inc, (uint64_t)(o_base + threadIdx.x));
+    // s = state after o + 1 steps: output o = XSL-RR(s); one 128-bit multiply-add per output
+    u128 s = pcg_jump(P.state, P.inc, (uint64_t)(o_base + threadIdx.x) + 1u);
     u128 a_t, c_t;
     pcg_affine(P.inc, kP1Threads, a_t, c_t);
     uint2 *out = reinterpret_cast<uint2 *>(P.draws);
-    const u128 m1 = pcg_mult();
     for (int k = 0; k < kDrawsPerThread; ++k) {
         const int64_t o = o_base + threadIdx.x + (int64_t)k * kP1Threads;
         if (o >= n64) break;
-        const uint64_t v = pcg_output(s * m1 + P.inc);   // output o = XSL-RR(state after o+1 steps)
+        const uint64_t v = pcg_output(s);
         out[o] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
         s = a_t * s + c_t;
     }
