@@ -19,6 +19,7 @@ from .entropy import (EntropyTracker, EntropyWindow, SamplerConfig, close_window
 from .errors import (CalibrationError, CompressionInfeasibleError, ConfigError, DegenerateInputError,
                      DivergenceError, EdgcError, TraceFormatError)
 from .matrix_core import GradientMatrix, frobenius_norm, optimal_rank_r_error, pearson_correlation
+from .trace import analyze_trace, read_trace_header, replay_trace, write_trace
 from .rank_model import (GTable, MpSupport, build_g_table, estimate_g, g_table, invert_g, mp_cdf, mp_support,
                          rank_from_entropy, rank_from_sigma, sample_eigenvalues)
 

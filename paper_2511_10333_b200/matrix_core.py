@@ -75,6 +75,13 @@ class GradientMatrix:
             raise ValueError("gradient matrix contains non-finite entries")
         self.data = t
 
+    @classmethod
+    def trusted(cls, data: torch.Tensor, layer_id: int = 0, stage_id: int = 0, iteration: int = 0):
+        """Wrap a 2-D fp32 CUDA tensor whose finiteness the caller already checked (no sync)."""
+        obj = cls.__new__(cls)
+        obj.data, obj.layer_id, obj.stage_id, obj.iteration = data, layer_id, stage_id, iteration
+        return obj
+
     @property
     def m(self) -> int:
         return self.data.shape[0]

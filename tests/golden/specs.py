@@ -109,3 +109,23 @@ def rank_case_matrix(case, t: int) -> np.ndarray:
     m, n = case["shape"]
     z = np.random.default_rng([case["synth_seed"], 1, t, 0, 0]).standard_normal((m, n), dtype=np.float32)
     return z * np.float32(rank_case_sigma(case, t))
+
+
+# EDGT trace replay + analyze-trace (grad_source.py:44-131, cli.py:579-659).
+# Layers 0 and 1 share an element count (correlation pairs), layer 1 is
+# correlated with layer 0, every layer decays like SynthSchedule's "exp" kind.
+TRACE_SPEC = {"shapes": [(24, 40), (40, 24), (16, 16)], "iterations": 30, "seed": 7, "tau": 12.0,
+              "window": 10, "alpha": 0.1, "beta": 0.25, "correlation_iterations": 4}
+
+
+def trace_frames(spec=TRACE_SPEC):
+    rng = np.random.default_rng(spec["seed"])
+    frames = []
+    for t in range(spec["iterations"]):
+        s = np.float32(2.0 * math.exp(-t / spec["tau"]))
+        a = rng.standard_normal(spec["shapes"][0]).astype(np.float32) * s
+        noise = rng.standard_normal(spec["shapes"][1]).astype(np.float32) * s
+        b = (np.float32(0.6) * a.reshape(spec["shapes"][1]) + np.float32(0.8) * noise).astype(np.float32)
+        c = rng.standard_normal(spec["shapes"][2]).astype(np.float32) * s
+        frames.append([a, b, c])
+    return frames
