@@ -29,6 +29,7 @@ import os
 import queue
 import struct
 import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -49,6 +50,7 @@ _DIMS = struct.Struct("<II")
 _ELEMENT_WIDTH = 4
 _CHUNK_BYTES = 64 << 20
 _SLOTS = 3
+_READERS = 4
 
 
 def _host_array(mat) -> np.ndarray:
@@ -124,6 +126,15 @@ def _frame_bytes(shapes) -> int:
     return sum(m * n for m, n in shapes) * _ELEMENT_WIDTH
 
 
+def _pread_full(fd: int, view, offset: int) -> None:
+    got = 0
+    while got < len(view):
+        k = os.preadv(fd, [view[got:]], offset + got)
+        if not k:
+            raise TraceFormatError(f"trace ended early at byte {offset + got}")
+        got += k
+
+
 class _ChunkReader(threading.Thread):
     """Fills pinned host slots with consecutive file chunks; hands (slot, nbytes) over a queue."""
 
@@ -138,24 +149,27 @@ class _ChunkReader(threading.Thread):
 
     def run(self) -> None:
         try:
-            with open(self.path, "rb", buffering=0) as fh:
-                fh.seek(self.offset)
-                left, in_frame = self.frame * self.frames, self.frame
-                while left > 0 and not self.stop.is_set():
-                    sid = self.free.get()
-                    if sid is None:
-                        return
-                    want = min(in_frame, self.slots[sid].numel())  # chunks never straddle frames
-                    view = memoryview(self.slots[sid].numpy())[:want]
-                    got = 0
-                    while got < want:
-                        k = fh.readinto(view[got:])
-                        if not k:
-                            raise TraceFormatError(f"trace ended {left - got} bytes early")
-                        got += k
-                    left -= want
-                    in_frame = in_frame - want or self.frame
-                    self.ready.put((sid, want))
+            fd = os.open(self.path, os.O_RDONLY)
+            try:
+                with ThreadPoolExecutor(_READERS) as pool:
+                    pos, left, in_frame = self.offset, self.frame * self.frames, self.frame
+                    while left > 0 and not self.stop.is_set():
+                        sid = self.free.get()
+                        if sid is None:
+                            return
+                        want = min(in_frame, self.slots[sid].numel())  # chunks never straddle frames
+                        view = memoryview(self.slots[sid].numpy())
+                        # page-cache -> pinned memcpy split over _READERS threads (pread releases the GIL)
+                        step = -(-want // _READERS)
+                        parts = [(o, min(step, want - o)) for o in range(0, want, step)]
+                        for f in [pool.submit(_pread_full, fd, view[o:o + k], pos + o) for o, k in parts]:
+                            f.result()
+                        pos += want
+                        left -= want
+                        in_frame = in_frame - want or self.frame
+                        self.ready.put((sid, want))
+            finally:
+                os.close(fd)
         except BaseException as exc:  # handed to the consumer
             self.ready.put((None, exc))
 
