@@ -215,6 +215,9 @@ template <> struct KeyOf<double> {
     }
 };
 
+// independent element loads in flight per thread in the streaming histogram passes
+constexpr int kHistUnroll = 8;
+
 struct HistState {
     // order statistics: targets 0..3 = ranks lo25, lo25+1, lo75, lo75+1
     unsigned long long prefix[4];
@@ -251,8 +254,15 @@ __global__ void __launch_bounds__(kRedThreads) k_minmax(const T *x, int64_t n, d
 
 __global__ void k_hist_init(HistState *st, const double2 *mm, int nblk, int64_t n, int fixed, int32_t *status,
                             double *result) {
+    // one warp: strided partial min/max, then a shuffle reduction (fmin/fmax are exact)
     double lo = INFINITY, hi = -INFINITY;
-    for (int b = 0; b < nblk; ++b) { lo = fmin(lo, mm[b].x); hi = fmax(hi, mm[b].y); }
+    for (int b = threadIdx.x; b < nblk; b += 32) { lo = fmin(lo, mm[b].x); hi = fmax(hi, mm[b].y); }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (threadIdx.x != 0) return;
     st->minv = lo;
     st->maxv = hi;
     st->fixed = fixed;
@@ -283,12 +293,40 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
     K pre[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) pre[t] = (K)st->prefix[t];
-    for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kRedThreads) {
-        const K k = KeyOf<T>::key(x[i]);
-        const unsigned dig = (unsigned)((k >> shift) & 0xFF);
+    // Gaussian-like data puts most keys on a handful of digits (the first pass
+    // sees only sign + exponent bits) and the four targets usually share their
+    // prefix: aggregate per warp on (digit, target mask) so each distinct pair
+    // costs one shared atomic per target instead of one per element and target.
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * kRedThreads;
+    const int64_t n_iter = (n + stride - 1) / stride;
+    const int64_t base = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+    for (int64_t it0 = 0; it0 < n_iter; it0 += kHistUnroll) {
+        T v[kHistUnroll];  // kHistUnroll independent coalesced loads in flight per thread
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-            if (((k ^ pre[t]) & hi_mask) == 0) atomicAdd(&h[t][dig], 1u);
+        for (int u = 0; u < kHistUnroll; ++u) {
+            const int64_t i = (it0 + u) * stride + base;
+            v[u] = i < n ? __ldg(x + i) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) {
+        const int64_t i = (it0 + u) * stride + base;
+        unsigned tag = 0u;  // bits 0-7 digit, 8-11 matching targets; 0 = nothing to count
+        if (i < n) {
+            const K k = KeyOf<T>::key(v[u]);
+            unsigned m = 0u;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) m |= (((k ^ pre[t]) & hi_mask) == 0) ? (1u << t) : 0u;
+            if (m) tag = (unsigned)((k >> shift) & 0xFF) | (m << 8);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, tag);
+        if (tag && lane == __ffs(peers) - 1) {
+            const unsigned c = (unsigned)__popc(peers), dig = tag & 0xFFu;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (tag & (1u << (8 + t))) atomicAdd(&h[t][dig], c);
+        }
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 4 * 256; i += kRedThreads) {
@@ -298,18 +336,32 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
 }
 
 __global__ void k_radix_pick(HistState *st, unsigned int *ghist, int shift) {
-    const int t = threadIdx.x;
-    if (t < 4) {
-        long long r = st->rank[t];
-        long long cum = 0;
-        int d = 0;
-        for (; d < 256; ++d) {
-            const long long c = ghist[t * 256 + d];
-            if (r < cum + c) break;
-            cum += c;
+    // warp t < 4 picks target t's digit: each lane owns 8 consecutive digits,
+    // a warp scan of the lane sums finds the lane holding rank r, then 8 steps
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w < 4) {
+        const long long r = st->rank[w];
+        unsigned c[8];
+        long long local = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { c[j] = ghist[w * 256 + lane * 8 + j]; local += c[j]; }
+        long long incl = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
-        st->prefix[t] |= ((unsigned long long)d) << shift;
-        st->rank[t] = r - cum;
+        long long cum = incl - local;
+        if (cum <= r && r < incl) {
+            int d = lane * 8;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (r < cum + c[j]) { d = lane * 8 + j; break; }
+                cum += c[j];
+            }
+            st->prefix[w] |= ((unsigned long long)d) << shift;
+            st->rank[w] = r - cum;
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) ghist[i] = 0u;
@@ -389,24 +441,65 @@ __device__ __forceinline__ long long bin_of(const HistState &s, double v) {
 }
 
 template <typename T>
+__device__ __forceinline__ void k_hist_count_global_body(const T *x, int64_t n, const HistState &s, long long *counts,
+                                                         int64_t block, int64_t nblocks) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = nblocks * kRedThreads;
+    const int64_t n_iter = (n + stride - 1) / stride;
+    for (int64_t it0 = 0; it0 < n_iter; it0 += kHistUnroll) {
+        T v[kHistUnroll];
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) {
+            const int64_t i = (it0 + u) * stride + block * kRedThreads + threadIdx.x;
+            v[u] = i < n ? __ldg(x + i) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) {
+            const int64_t i = (it0 + u) * stride + block * kRedThreads + threadIdx.x;
+            const bool live = i < n;
+            const long long b = live ? bin_of<T>(s, (double)v[u]) : -1;
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            const int leader = __ffs(peers) - 1;
+            if (live && lane == leader)
+                atomicAdd(reinterpret_cast<unsigned long long *>(counts) + b, (unsigned long long)__popc(peers));
+        }
+    }
+}
+
+// bins in shared memory when the device-side bin count fits kSmemBins, else the
+// whole grid takes the global-atomic path (the decision needs nb, known only on
+// the device after k_hist_params)
+constexpr int kSmemBins = 16 * 1024;
+
+template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_hist_count_smem(const T *x, int64_t n, const HistState *st,
                                                                  const int32_t *status, long long *counts) {
     if (*status != EDGC_OK) return;
     extern __shared__ unsigned int sh[];
     const HistState s = *st;
+    if (s.nb > kSmemBins) {
+        k_hist_count_global_body<T>(x, n, s, counts, (int64_t)blockIdx.x, (int64_t)gridDim.x);
+        return;
+    }
     for (long long i = threadIdx.x; i < s.nb; i += kRedThreads) sh[i] = 0u;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * kRedThreads;
     const int64_t n_iter = (n + stride - 1) / stride;
-    for (int64_t it = 0; it < n_iter; ++it) {
-        const int64_t i = it * stride + (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
-        const bool live = i < n;
-        const int b = live ? (int)bin_of<T>(s, (double)x[i]) : -1;
-        // warp-aggregated: one shared atomic per distinct bin per warp
-        const unsigned peers = __match_any_sync(0xffffffffu, b);
-        const int leader = __ffs(peers) - 1;
-        if (live && lane == leader) atomicAdd(&sh[b], (unsigned)__popc(peers));
+    for (int64_t it0 = 0; it0 < n_iter; it0 += kHistUnroll) {
+        T v[kHistUnroll];
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) {
+            const int64_t i = (it0 + u) * stride + (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+            v[u] = i < n ? __ldg(x + i) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) {
+            const int64_t i = (it0 + u) * stride + (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+            const bool live = i < n;
+            // FD bins are narrow (~1% of sigma): a warp's values rarely share a
+            // bin, so direct shared atomics beat a match.any aggregation here
+            if (live) atomicAdd(&sh[(int)bin_of<T>(s, (double)v[u])], 1u);
+        }
     }
     __syncthreads();
     for (long long i = threadIdx.x; i < s.nb; i += kRedThreads) {
@@ -419,19 +512,7 @@ template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_hist_count_global(const T *x, int64_t n, const HistState *st,
                                                                    const int32_t *status, long long *counts) {
     if (*status != EDGC_OK) return;
-    const HistState s = *st;
-    const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * kRedThreads;
-    const int64_t n_iter = (n + stride - 1) / stride;
-    for (int64_t it = 0; it < n_iter; ++it) {
-        const int64_t i = it * stride + (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
-        const bool live = i < n;
-        const long long b = live ? bin_of<T>(s, (double)x[i]) : -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, b);
-        const int leader = __ffs(peers) - 1;
-        if (live && lane == leader)
-            atomicAdd(reinterpret_cast<unsigned long long *>(counts) + b, (unsigned long long)__popc(peers));
-    }
+    k_hist_count_global_body<T>(x, n, *st, counts, (int64_t)blockIdx.x, (int64_t)gridDim.x);
 }
 
 __global__ void __launch_bounds__(kRedThreads) k_hist_entropy_partial(const HistState *st, const int32_t *status,
@@ -499,7 +580,7 @@ int run_histogram(const T *x, int64_t n, double inv_cbrt_n, int64_t fixed_bins, 
     const int mmb = (int)std::max<int64_t>(1, std::min<int64_t>(kMinMaxBlocks, ceil_div(n, kRedThreads)));
     k_minmax<T><<<mmb, kRedThreads, 0, st>>>(x, n, L.mm);
     EDGC_LAUNCH_CHECK();
-    k_hist_init<<<1, 1, 0, st>>>(L.st, L.mm, mmb, n, fixed_bins > 0, status, result);
+    k_hist_init<<<1, 32, 0, st>>>(L.st, L.mm, mmb, n, fixed_bins > 0, status, result);
     EDGC_LAUNCH_CHECK();
     EDGC_CUDA_TRY(cudaMemsetAsync(L.ghist, 0, 4 * 256 * sizeof(unsigned int), st));
     const int kbits = KeyOf<T>::kBits;
@@ -517,13 +598,13 @@ int run_histogram(const T *x, int64_t n, double inv_cbrt_n, int64_t fixed_bins, 
     k_hist_edges<<<sms, 256, 0, st>>>(L.st, status, edges, status);
     EDGC_LAUNCH_CHECK();
     EDGC_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(long long) * cap, st));
-    // counts go to shared memory when they fit (<= 48K bins), else global atomics
-    const int64_t smem_bins = 48 * 1024;
-    const int cb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 2, ceil_div(n, kRedThreads)));
-    if (cap <= smem_bins) {
-        const size_t smem = sizeof(unsigned int) * (size_t)std::max<int64_t>(cap, 1);
+    // counts go to shared memory when the device-side bin count fits kSmemBins
+    // (the kernel decides), else global atomics
+    const int cb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 3, ceil_div(n, kRedThreads)));
+    if (cap <= kSmemBins || fixed_bins <= 0) {
+        const size_t smem = sizeof(unsigned int) * (size_t)std::min<int64_t>(std::max<int64_t>(cap, 1), kSmemBins);
         EDGC_CUDA_TRY(cudaFuncSetAttribute(k_hist_count_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(smem_bins * sizeof(unsigned int))));
+                                           (int)(kSmemBins * sizeof(unsigned int))));
         k_hist_count_smem<T><<<cb, kRedThreads, smem, st>>>(x, n, L.st, status, counts);
     } else {
         k_hist_count_global<T><<<cb * 4, kRedThreads, 0, st>>>(x, n, L.st, status, counts);
