@@ -189,6 +189,9 @@ __global__ void k_gauss_finish_slots(const double *part, int64_t slots, const in
 }
 
 // --------------------------------------------------------------- histogram
+// independent element loads in flight per thread in the streaming histogram passes
+constexpr int kHistUnroll = 8;
+
 template <typename T> struct KeyOf;
 template <> struct KeyOf<float> {
     typedef uint32_t K;
@@ -215,9 +218,6 @@ template <> struct KeyOf<double> {
     }
 };
 
-// independent element loads in flight per thread in the streaming histogram passes
-constexpr int kHistUnroll = 8;
-
 struct HistState {
     // order statistics: targets 0..3 = ranks lo25, lo25+1, lo75, lo75+1
     unsigned long long prefix[4];
@@ -231,10 +231,20 @@ struct HistState {
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_minmax(const T *x, int64_t n, double2 *partial) {
     double lo = INFINITY, hi = -INFINITY;
-    for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kRedThreads) {
-        const double v = (double)x[i];
-        lo = fmin(lo, v);
-        hi = fmax(hi, v);
+    const int64_t stride = (int64_t)gridDim.x * kRedThreads, base = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+    const int64_t n_iter = (n + stride - 1) / stride;
+    for (int64_t it0 = 0; it0 < n_iter; it0 += kHistUnroll) {
+        T v[kHistUnroll];  // independent loads in flight; out-of-range lanes repeat x[0] (min/max-neutral)
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) {
+            const int64_t i = (it0 + u) * stride + base;
+            v[u] = __ldg(x + (i < n ? i : 0));
+        }
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) {
+            lo = fmin(lo, (double)v[u]);
+            hi = fmax(hi, (double)v[u]);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -550,7 +560,7 @@ __global__ void k_hist_entropy_final(const double *partial, int nblk, const int3
     result[0] = -a;
 }
 
-constexpr int kMinMaxBlocks = 296;
+constexpr int kMinMaxBlocks = 592;
 constexpr int kEntBlocks = 148;
 
 struct HistLayout {
