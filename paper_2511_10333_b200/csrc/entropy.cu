@@ -191,6 +191,9 @@ __global__ void k_gauss_finish_slots(const double *part, int64_t slots, const in
 // --------------------------------------------------------------- histogram
 // independent element loads in flight per thread in the streaming histogram passes
 constexpr int kHistUnroll = 8;
+// radix-select digit width: 11 bits -> three passes for fp32 keys (6 for fp64)
+constexpr int kDigitBits = 11;
+constexpr int kDigits = 1 << kDigitBits;
 
 template <typename T> struct KeyOf;
 template <> struct KeyOf<float> {
@@ -293,13 +296,14 @@ __global__ void k_hist_init(HistState *st, const double2 *mm, int nblk, int64_t 
 // one radix-select digit pass (8-bit digits, most significant first)
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t n, const HistState *st, int shift,
-                                                           unsigned int *ghist /*[4][256]*/) {
+                                                           int width, unsigned int *ghist /*[4][kDigits]*/) {
     typedef typename KeyOf<T>::K K;
-    __shared__ unsigned int h[4][256];
-    for (int i = threadIdx.x; i < 4 * 256; i += kRedThreads) (&h[0][0])[i] = 0u;
+    __shared__ unsigned int h[4][kDigits];
+    for (int i = threadIdx.x; i < 4 * kDigits; i += kRedThreads) (&h[0][0])[i] = 0u;
     __syncthreads();
     const int kbits = KeyOf<T>::kBits;
-    const K hi_mask = (shift + 8 >= kbits) ? (K)0 : (K)(~(K)0) << (shift + 8);
+    const K hi_mask = (shift + width >= kbits) ? (K)0 : (K)(~(K)0) << (shift + width);
+    const unsigned dmask = (1u << width) - 1u;
     K pre[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) pre[t] = (K)st->prefix[t];
@@ -321,40 +325,44 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u) {
         const int64_t i = (it0 + u) * stride + base;
-        unsigned tag = 0u;  // bits 0-7 digit, 8-11 matching targets; 0 = nothing to count
+        unsigned tag = 0u;  // bits 0-10 digit, 12-15 matching targets; 0 = nothing to count
         if (i < n) {
             const K k = KeyOf<T>::key(v[u]);
             unsigned m = 0u;
 #pragma unroll
             for (int t = 0; t < 4; ++t) m |= (((k ^ pre[t]) & hi_mask) == 0) ? (1u << t) : 0u;
-            if (m) tag = (unsigned)((k >> shift) & 0xFF) | (m << 8);
+            if (m) tag = ((unsigned)(k >> shift) & dmask) | (m << 12);
         }
         const unsigned peers = __match_any_sync(0xffffffffu, tag);
         if (tag && lane == __ffs(peers) - 1) {
-            const unsigned c = (unsigned)__popc(peers), dig = tag & 0xFFu;
+            const unsigned c = (unsigned)__popc(peers), dig = tag & 0x7FFu;
 #pragma unroll
             for (int t = 0; t < 4; ++t)
-                if (tag & (1u << (8 + t))) atomicAdd(&h[t][dig], c);
+                if (tag & (1u << (12 + t))) atomicAdd(&h[t][dig], c);
         }
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 4 * 256; i += kRedThreads) {
+    for (int i = threadIdx.x; i < 4 * kDigits; i += kRedThreads) {
         const unsigned v = (&h[0][0])[i];
         if (v) atomicAdd(ghist + i, v);
     }
 }
 
 __global__ void k_radix_pick(HistState *st, unsigned int *ghist, int shift) {
-    // warp t < 4 picks target t's digit: each lane owns 8 consecutive digits,
-    // a warp scan of the lane sums finds the lane holding rank r, then 8 steps
+    // warp t < 4 picks target t's digit: each lane owns kDigits/32 consecutive
+    // digits, a warp scan of the lane sums finds the lane holding rank r
+    __shared__ unsigned sh[4 * kDigits];  // coalesced staging, then zero the global counts
+    for (int i = threadIdx.x; i < 4 * kDigits; i += blockDim.x) { sh[i] = ghist[i]; ghist[i] = 0u; }
+    __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (w < 4) {
         const long long r = st->rank[w];
-        unsigned c[8];
+        constexpr int kPer = kDigits / 32;
+        const unsigned *c = sh + w * kDigits + lane * kPer;
         long long local = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) { c[j] = ghist[w * 256 + lane * 8 + j]; local += c[j]; }
+#pragma unroll 16
+        for (int j = 0; j < kPer; ++j) local += c[j];
         long long incl = local;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -363,18 +371,15 @@ __global__ void k_radix_pick(HistState *st, unsigned int *ghist, int shift) {
         }
         long long cum = incl - local;
         if (cum <= r && r < incl) {
-            int d = lane * 8;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (r < cum + c[j]) { d = lane * 8 + j; break; }
+            int d = lane * kPer;
+            for (int j = 0; j < kPer; ++j) {
+                if (r < cum + c[j]) { d = lane * kPer + j; break; }
                 cum += c[j];
             }
             st->prefix[w] |= ((unsigned long long)d) << shift;
             st->rank[w] = r - cum;
         }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) ghist[i] = 0u;
 }
 
 __device__ __forceinline__ double np_lerp(double a, double b, double t) {
@@ -576,7 +581,7 @@ HistLayout hist_layout(void *ws) {
     HistLayout L;
     L.st = a.take<HistState>(1);
     L.mm = a.take<double2>(kMinMaxBlocks);
-    L.ghist = a.take<unsigned int>(4 * 256);
+    L.ghist = a.take<unsigned int>(4 * kDigits);
     L.ent = a.take<double>(kEntBlocks);
     L.bytes = a.off;
     return L;
@@ -592,12 +597,14 @@ int run_histogram(const T *x, int64_t n, double inv_cbrt_n, int64_t fixed_bins, 
     EDGC_LAUNCH_CHECK();
     k_hist_init<<<1, 32, 0, st>>>(L.st, L.mm, mmb, n, fixed_bins > 0, status, result);
     EDGC_LAUNCH_CHECK();
-    EDGC_CUDA_TRY(cudaMemsetAsync(L.ghist, 0, 4 * 256 * sizeof(unsigned int), st));
+    EDGC_CUDA_TRY(cudaMemsetAsync(L.ghist, 0, 4 * kDigits * sizeof(unsigned int), st));
     const int kbits = KeyOf<T>::kBits;
     const int hb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 4, ceil_div(n, kRedThreads)));
     if (fixed_bins <= 0) {
-        for (int shift = kbits - 8; shift >= 0; shift -= 8) {
-            k_radix_hist<T><<<hb, kRedThreads, 0, st>>>(x, n, L.st, shift, L.ghist);
+        // kDigitBits-wide digits, most significant first; the last one takes the rest
+        for (int hi = kbits; hi > 0; hi -= kDigitBits) {
+            const int width = std::min(kDigitBits, hi), shift = hi - width;
+            k_radix_hist<T><<<hb, kRedThreads, 0, st>>>(x, n, L.st, shift, width, L.ghist);
             EDGC_LAUNCH_CHECK();
             k_radix_pick<<<1, 256, 0, st>>>(L.st, L.ghist, shift);
             EDGC_LAUNCH_CHECK();
