@@ -265,15 +265,26 @@ __global__ void __launch_bounds__(kRedThreads) k_minmax(const T *x, int64_t n, d
     }
 }
 
-__global__ void k_hist_init(HistState *st, const double2 *mm, int nblk, int64_t n, int fixed, int32_t *status,
-                            double *result) {
-    // one warp: strided partial min/max, then a shuffle reduction (fmin/fmax are exact)
+// one warp: strided partial min/max, then a shuffle reduction (fmin/fmax are exact)
+__device__ __forceinline__ double2 warp_minmax(const double2 *mm, int nblk) {
     double lo = INFINITY, hi = -INFINITY;
-    for (int b = threadIdx.x; b < nblk; b += 32) { lo = fmin(lo, mm[b].x); hi = fmax(hi, mm[b].y); }
+    for (int b = threadIdx.x & 31; b < nblk; b += 32) { lo = fmin(lo, mm[b].x); hi = fmax(hi, mm[b].y); }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    return make_double2(lo, hi);
+}
+
+// mm == NULL: the min/max comes later, from the first radix pass (k_radix_pick)
+__global__ void k_hist_init(HistState *st, const double2 *mm, int nblk, int64_t n, int fixed, int32_t *status,
+                            double *result) {
+    double lo = 0.0, hi = 1.0;
+    if (mm) {
+        const double2 r = warp_minmax(mm, nblk);
+        lo = r.x;
+        hi = r.y;
     }
     if (threadIdx.x != 0) return;
     st->minv = lo;
@@ -294,15 +305,17 @@ __global__ void k_hist_init(HistState *st, const double2 *mm, int nblk, int64_t 
 }
 
 // one radix-select digit pass (8-bit digits, most significant first)
-template <typename T>
+template <typename T, bool kMinMax>
 __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t n, const HistState *st, int shift,
-                                                           int width, unsigned int *ghist /*[4][kDigits]*/) {
+                                                           int width, unsigned int *ghist /*[4][kDigits]*/,
+                                                           double2 *mm_out /* first pass: per-CTA min/max */) {
     typedef typename KeyOf<T>::K K;
     __shared__ unsigned int h[4][kDigits];
     for (int i = threadIdx.x; i < 4 * kDigits; i += kRedThreads) (&h[0][0])[i] = 0u;
     __syncthreads();
     const int kbits = KeyOf<T>::kBits;
     const K hi_mask = (shift + width >= kbits) ? (K)0 : (K)(~(K)0) << (shift + width);
+    double lo = INFINITY, hi = -INFINITY;  // min/max fused into the first pass (mm_out)
     const unsigned dmask = (1u << width) - 1u;
     K pre[4];
 #pragma unroll
@@ -325,6 +338,10 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u) {
         const int64_t i = (it0 + u) * stride + base;
+        if (kMinMax && i < n) {
+            lo = fmin(lo, (double)v[u]);
+            hi = fmax(hi, (double)v[u]);
+        }
         unsigned tag = 0u;  // bits 0-10 digit, 12-15 matching targets; 0 = nothing to count
         if (i < n) {
             const K k = KeyOf<T>::key(v[u]);
@@ -342,6 +359,22 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
         }
         }
     }
+    if constexpr (kMinMax) {
+        __shared__ double2 s_mm[kRedThreads / 32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) s_mm[threadIdx.x >> 5] = make_double2(lo, hi);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kRedThreads / 32; ++w) { lo = fmin(lo, s_mm[w].x); hi = fmax(hi, s_mm[w].y); }
+            lo = fmin(lo, s_mm[0].x);
+            hi = fmax(hi, s_mm[0].y);
+            mm_out[blockIdx.x] = make_double2(lo, hi);
+        }
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < 4 * kDigits; i += kRedThreads) {
         const unsigned v = (&h[0][0])[i];
@@ -349,13 +382,22 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
     }
 }
 
-__global__ void k_radix_pick(HistState *st, unsigned int *ghist, int shift) {
+__global__ void k_radix_pick(HistState *st, unsigned int *ghist, int shift, const double2 *mm, int nblk,
+                             int32_t *status) {
     // warp t < 4 picks target t's digit: each lane owns kDigits/32 consecutive
     // digits, a warp scan of the lane sums finds the lane holding rank r
     __shared__ unsigned sh[4 * kDigits];  // coalesced staging, then zero the global counts
     for (int i = threadIdx.x; i < 4 * kDigits; i += blockDim.x) { sh[i] = ghist[i]; ghist[i] = 0u; }
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (mm && w == 4) {  // first pass: finish the fused min/max (k_hist_init's second half)
+        const double2 r = warp_minmax(mm, nblk);
+        if (lane == 0) {
+            st->minv = r.x;
+            st->maxv = r.y;
+            if (*status == EDGC_OK && r.x == r.y) *status = EDGC_EDEGENERATE;
+        }
+    }
     if (w < 4) {
         const long long r = st->rank[w];
         constexpr int kPer = kDigits / 32;
@@ -593,20 +635,27 @@ int run_histogram(const T *x, int64_t n, double inv_cbrt_n, int64_t fixed_bins, 
     HistLayout L = hist_layout(ws);
     const int sms = sm_count();
     const int mmb = (int)std::max<int64_t>(1, std::min<int64_t>(kMinMaxBlocks, ceil_div(n, kRedThreads)));
-    k_minmax<T><<<mmb, kRedThreads, 0, st>>>(x, n, L.mm);
-    EDGC_LAUNCH_CHECK();
-    k_hist_init<<<1, 32, 0, st>>>(L.st, L.mm, mmb, n, fixed_bins > 0, status, result);
+    if (fixed_bins > 0) {  // no select passes: a separate min/max pass
+        k_minmax<T><<<mmb, kRedThreads, 0, st>>>(x, n, L.mm);
+        EDGC_LAUNCH_CHECK();
+    }
+    k_hist_init<<<1, 32, 0, st>>>(L.st, fixed_bins > 0 ? L.mm : nullptr, mmb, n, fixed_bins > 0, status, result);
     EDGC_LAUNCH_CHECK();
     EDGC_CUDA_TRY(cudaMemsetAsync(L.ghist, 0, 4 * kDigits * sizeof(unsigned int), st));
     const int kbits = KeyOf<T>::kBits;
-    const int hb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 4, ceil_div(n, kRedThreads)));
+    const int hb = (int)std::max<int64_t>(
+        1, std::min<int64_t>(std::min<int64_t>((int64_t)sms * 4, kMinMaxBlocks), ceil_div(n, kRedThreads)));
     if (fixed_bins <= 0) {
         // kDigitBits-wide digits, most significant first; the last one takes the rest
         for (int hi = kbits; hi > 0; hi -= kDigitBits) {
             const int width = std::min(kDigitBits, hi), shift = hi - width;
-            k_radix_hist<T><<<hb, kRedThreads, 0, st>>>(x, n, L.st, shift, width, L.ghist);
+            const bool first = hi == kbits;
+            if (first)
+                k_radix_hist<T, true><<<hb, kRedThreads, 0, st>>>(x, n, L.st, shift, width, L.ghist, L.mm);
+            else
+                k_radix_hist<T, false><<<hb, kRedThreads, 0, st>>>(x, n, L.st, shift, width, L.ghist, nullptr);
             EDGC_LAUNCH_CHECK();
-            k_radix_pick<<<1, 256, 0, st>>>(L.st, L.ghist, shift);
+            k_radix_pick<<<1, 256, 0, st>>>(L.st, L.ghist, shift, first ? L.mm : nullptr, hb, status);
             EDGC_LAUNCH_CHECK();
         }
     }

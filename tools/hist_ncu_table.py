@@ -2,7 +2,7 @@
 import collections, csv, sys
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 14 and r[0].isdigit()]
 ids = sorted({int(r[0]) for r in rows})
-first = max(i for i in ids if any(int(r[0]) == i and "k_minmax" in r[4] for r in rows))
+first = max(i for i in ids if any(int(r[0]) == i and ("k_minmax" in r[4] or "k_hist_init" in r[4]) for r in rows))
 agg = collections.OrderedDict()
 for r in rows:
     if int(r[0]) >= first:
