@@ -95,3 +95,19 @@ def test_layer_batch_gaussian_equals_oracle():
     for k, (m, h) in enumerate(zip(mats, got)):
         ref = oracle.gaussian_entropy(oracle.subsample(m, 0.25, oracle.subsample_seed(9, 30, k)))
         assert abs(h - ref) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("df,nbins", [(2.4, 16144), (2.2, 36578), (2.0, 123587), (1.5, 301971)])
+def test_fd_histogram_many_bins_global_path(df, nbins):
+    """Heavy tails: 16144 bins (just inside the 16K shared-memory bins), 36578
+    (global-atomic counting), 123587 and 301971 (global path after the 64K-bin
+    capacity retry)."""
+    from paper_2511_10333_b200.entropy import histogram_fd
+    import torch
+    x = np.random.default_rng(5).standard_t(df, 1_000_000).astype(np.float32)
+    c_ref, e_ref = np.histogram(x.astype(np.float64), bins="fd")
+    assert c_ref.size == nbins
+    c, e, _ = histogram_fd(torch.from_numpy(x).cuda())
+    assert np.array_equal(c.cpu().numpy(), c_ref)
+    assert np.array_equal(e.cpu().numpy(), e_ref)
