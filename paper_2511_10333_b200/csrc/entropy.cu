@@ -315,7 +315,9 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
     __syncthreads();
     const int kbits = KeyOf<T>::kBits;
     const K hi_mask = (shift + width >= kbits) ? (K)0 : (K)(~(K)0) << (shift + width);
-    double lo = INFINITY, hi = -INFINITY;  // min/max fused into the first pass (mm_out)
+    // min/max fused into the first pass (mm_out), in T: exact, and fp32 min/max
+    // avoids the fp64 pipe (the fused pass was SM-bound with double compares)
+    T lo = T(INFINITY), hi = T(-INFINITY);
     const unsigned dmask = (1u << width) - 1u;
     K pre[4];
 #pragma unroll
@@ -339,8 +341,8 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
         for (int u = 0; u < kHistUnroll; ++u) {
         const int64_t i = (it0 + u) * stride + base;
         if (kMinMax && i < n) {
-            lo = fmin(lo, (double)v[u]);
-            hi = fmax(hi, (double)v[u]);
+            lo = fmin(lo, v[u]);
+            hi = fmax(hi, v[u]);
         }
         unsigned tag = 0u;  // bits 0-10 digit, 12-15 matching targets; 0 = nothing to count
         if (i < n) {
@@ -366,13 +368,12 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
             lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
             hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
         }
-        if (lane == 0) s_mm[threadIdx.x >> 5] = make_double2(lo, hi);
+        if (lane == 0) s_mm[threadIdx.x >> 5] = make_double2((double)lo, (double)hi);
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int w = 1; w < kRedThreads / 32; ++w) { lo = fmin(lo, s_mm[w].x); hi = fmax(hi, s_mm[w].y); }
-            lo = fmin(lo, s_mm[0].x);
-            hi = fmax(hi, s_mm[0].y);
-            mm_out[blockIdx.x] = make_double2(lo, hi);
+            double dlo = s_mm[0].x, dhi = s_mm[0].y;
+            for (int w = 1; w < kRedThreads / 32; ++w) { dlo = fmin(dlo, s_mm[w].x); dhi = fmax(dhi, s_mm[w].y); }
+            mm_out[blockIdx.x] = make_double2(dlo, dhi);
         }
     }
     __syncthreads();
