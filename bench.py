@@ -309,6 +309,11 @@ def run_ours(args):
     start.record(stream)
     for t in range(args.warmup, args.warmup + args.steps):
         one_step(t, ev)
+    if tracker is not None and tracker._pf_stream is not None:
+        # the plans prefetched for the next sampled iteration belong to the timed steps: each
+        # period of round(1/alpha) steps carries one plan build, so the window must contain the
+        # build launched inside it (the one before the window finished during warm-up)
+        stream.wait_stream(tracker._pf_stream)
     stop.record(stream)
     barrier()
     launches = L.edgc_launch_count() - launches0

@@ -149,9 +149,11 @@ def compress(matrix, state: CompressorState) -> LowRankFactors:
     status = torch.zeros(1, dtype=torch.int32, device=state.device)
     _lib.check(L.edgc_compress(arr, 1, DEVICE_COLUMN_TOL, _lib.ptr(status), _lib.ptr(ws), ws.numel(), stream),
                "edgc_compress")
+    # the state keeps private copies of the pair: the reference's residual is an array of its own
+    # (compressor.py:112), so in-place edits of the returned factors must not reach the next step
     state._p_res, state._q_res = p, q
     meta = matrix if isinstance(matrix, GradientMatrix) else None
-    return LowRankFactors(p=p, q=q, layer_id=meta.layer_id if meta else 0,
+    return LowRankFactors(p=p.clone(), q=q.clone(), layer_id=meta.layer_id if meta else 0,
                           stage_id=meta.stage_id if meta else 0, iteration=meta.iteration if meta else 0)
 
 

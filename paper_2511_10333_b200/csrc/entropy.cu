@@ -245,8 +245,9 @@ __global__ void __launch_bounds__(kRedThreads) k_minmax(const T *x, int64_t n, d
         }
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u) {
+            // NaN is skipped by fmin/fmax: fold it into the max as +inf so the range is non-finite
             lo = fmin(lo, (double)v[u]);
-            hi = fmax(hi, (double)v[u]);
+            hi = fmax(hi, v[u] != v[u] ? (double)INFINITY : (double)v[u]);
         }
     }
 #pragma unroll
@@ -300,6 +301,7 @@ __global__ void k_hist_init(HistState *st, const double2 *mm, int nblk, int64_t 
     for (int t = 0; t < 4; ++t) st->prefix[t] = 0ull;
     *status = EDGC_OK;
     if (n < 2) *status = EDGC_EINVAL;
+    else if (mm && !(isfinite(lo) && isfinite(hi))) *status = EDGC_ENONFINITE;  // np.histogram: range not finite
     else if (lo == hi) *status = EDGC_EDEGENERATE;
     for (int i = 0; i < 5; ++i) result[i] = NAN;
 }
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(kRedThreads) k_radix_hist(const T *x, int64_t 
         const int64_t i = (it0 + u) * stride + base;
         if (kMinMax && i < n) {
             lo = fmin(lo, v[u]);
-            hi = fmax(hi, v[u]);
+            hi = fmax(hi, v[u] != v[u] ? T(INFINITY) : v[u]);  // NaN -> non-finite range
         }
         unsigned tag = 0u;  // bits 0-10 digit, 12-15 matching targets; 0 = nothing to count
         if (i < n) {
@@ -396,7 +398,8 @@ __global__ void k_radix_pick(HistState *st, unsigned int *ghist, int shift, cons
         if (lane == 0) {
             st->minv = r.x;
             st->maxv = r.y;
-            if (*status == EDGC_OK && r.x == r.y) *status = EDGC_EDEGENERATE;
+            if (*status == EDGC_OK && !(isfinite(r.x) && isfinite(r.y))) *status = EDGC_ENONFINITE;
+            else if (*status == EDGC_OK && r.x == r.y) *status = EDGC_EDEGENERATE;
         }
     }
     if (w < 4) {

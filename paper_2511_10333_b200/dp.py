@@ -27,7 +27,25 @@ from .engine import BucketEngine, broadcast_decision
 from .entropy import EntropyTracker, SamplerConfig
 from .rank_model import g_table
 
-__all__ = ["EdgcDataParallel"]
+__all__ = ["EdgcDataParallel", "edgc_setup"]
+
+
+def edgc_setup(shapes, *, table_trials: int = 64, seed: int = 0, bandwidth: float = 1e9, element_size: int = 4):
+    """train_toy's EDGC setup (grad_source.py:311-327): byte model, Eq. 2 bounds, g-table, r_max < table.m.
+
+    Returns (CommModel, RankBounds, GTable).  Host-only; pinned to the reference by tests/golden/dp.json.
+    """
+    shapes = [(int(m), int(n)) for m, n in shapes]
+    per_rank = sum(m + n for m, n in shapes)
+    raw = sum(m * n for m, n in shapes)
+    model = CommModel(eta=element_size * per_rank / bandwidth, bandwidth=bandwidth, element_size=element_size)
+    bounds = compute_rank_bounds(model, element_size * raw, shapes)
+    big = max(shapes, key=lambda s: s[0] * s[1])
+    table = g_table(min(big), max(big), table_trials, seed)
+    if bounds.r_max >= table.m:
+        r_max = table.m - 1
+        bounds = RankBounds(r_min=min(bounds.r_min, r_max), r_max=r_max)
+    return model, bounds, table
 
 
 class EdgcDataParallel:
@@ -36,16 +54,8 @@ class EdgcDataParallel:
                  warmup_floor: float = 0.10, table_trials: int = 64, bandwidth: float = 1e9, element_size: int = 4):
         self.shapes = [(int(m), int(n)) for m, n in shapes]
         self.world, self.me, self.group = world_size, rank_id, group
-        per_rank = sum(m + n for m, n in self.shapes)
-        raw = sum(m * n for m, n in self.shapes)
-        self.model = CommModel(eta=element_size * per_rank / bandwidth, bandwidth=bandwidth,
-                               element_size=element_size)
-        bounds = compute_rank_bounds(self.model, element_size * raw, self.shapes)
-        big = max(self.shapes, key=lambda s: s[0] * s[1])
-        self.table = g_table(min(big), max(big), table_trials, seed)
-        if bounds.r_max >= self.table.m:
-            r_max = self.table.m - 1
-            bounds = RankBounds(r_min=min(bounds.r_min, r_max), r_max=r_max)
+        self.model, bounds, self.table = edgc_setup(self.shapes, table_trials=table_trials, seed=seed,
+                                                    bandwidth=bandwidth, element_size=element_size)
         self.bounds = bounds
         self.ctl = RankControllerState(bounds=bounds, window=window, step_limit=step_limit,
                                        warmup_floor=warmup_floor, total_iterations=total_iterations)
@@ -95,8 +105,9 @@ class EdgcDataParallel:
             closed = self.tracker.observe(t, eng.grads, fused=fused)
             if closed is not None:
                 decision = self._window_update(closed)
-        if self.world > 1:
-            # every rank learns whether a decision happened (-1 = none / still warm-up)
+        if self.world > 1 and self.closes_window(t):
+            # a window can close only when t // window advances (entropy.py:161-166), which every
+            # rank knows: only those iterations pay for the broadcast (-1 = none / still warm-up)
             decision = broadcast_decision(decision, eng.device, self.group)
         if decision is not None:
             eng.set_rank(decision)
@@ -104,11 +115,23 @@ class EdgcDataParallel:
                 self.ctl.phase = PHASE_ACTIVE  # non-zero ranks mirror rank 0's phase switch
         return outs
 
+    def closes_window(self, t: int) -> bool:
+        """True iff observing iteration t can close a window: t // window advanced past the previous one."""
+        return t > 0 and t // self.ctl.window > (t - 1) // self.ctl.window
+
     def flush(self):
-        if self.tracker is None:
-            return None
-        closed = self.tracker.flush()
-        return None if closed is None else self._window_update(closed)
+        """Close the trailing partial window (entropy.py:180-186); every rank applies the decision."""
+        decision = None
+        if self.tracker is not None:
+            closed = self.tracker.flush()
+            decision = None if closed is None else self._window_update(closed)
+        if self.world > 1:
+            decision = broadcast_decision(decision, self.engine.device, self.group)
+        if decision is not None:
+            self.engine.set_rank(decision)
+            if self.ctl.phase != PHASE_ACTIVE:
+                self.ctl.phase = PHASE_ACTIVE
+        return decision
 
     def _window_update(self, win):
         ctl = self.ctl

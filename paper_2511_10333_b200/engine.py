@@ -242,13 +242,25 @@ class BucketEngine:
                                            _lib.ptr(out_buf[po:]), _lib.ptr(out_buf[qo:]),
                                            _lib.ptr(self.precond[k]), m, n, g.stride(0), r, r_res, self.cap,
                                            self.cap))
+        self._evict("c", ranks, key)
         plan = _Plan("compress", descs, self.device)
-        if res is not None:
-            # the residual-free first-step plan is never used again: release its workspace
-            for k in [k for k in self._plans if k[0] == "c" and k[3] is None]:
-                del self._plans[k]
         self._plans[key] = plan
         return plan
+
+    def _evict(self, kind: str, ranks, keep) -> None:
+        """Release every cached plan of `kind` that the current ranks can no longer use.
+
+        A steady-state compress plan has ranks == residual ranks == the current
+        ranks (one per factor-buffer parity); the residual-free first-step plan
+        and the one-step transition plan after a rank change are used once.  Each
+        plan owns fp64 scratch sized by its ranks, so keeping stale ones would
+        grow HBM use with every controller decision.
+        """
+        for k in list(self._plans):
+            if k[0] != kind or k == keep:
+                continue
+            if k[2] != ranks or (kind == "c" and (k[3] is None or k[3][1] != ranks)):
+                del self._plans[k]
 
     def _recon_plan(self):
         ranks = tuple(self.ranks)
@@ -264,6 +276,7 @@ class BucketEngine:
             o = self.outs[k]
             descs.append(_lib.ReconDesc(_lib.ptr(src[po:]), _lib.ptr(src[qo:]), _lib.ptr(o), m, n, o.stride(0),
                                         size, size, r, self.world, 1.0 / self.world, 0))
+        self._evict("r", ranks, key)
         plan = _Plan("recon", descs, self.device)
         self._plans[key] = plan
         return plan

@@ -319,6 +319,9 @@ def histogram_fd(samples, bins="fd"):
         if code == _lib.EDGC_ECAPACITY:
             cap = int(res[4])
             continue
+        if code == _lib.EDGC_ENONFINITE:
+            # numpy/lib/_histograms_impl.py:_get_outer_edges
+            raise ValueError("autodetected range of the samples is not finite")
         if code == _lib.EDGC_EDEGENERATE:
             raise DegenerateInputError("zero-range sample has no histogram entropy")
         if code == _lib.EDGC_ETOOMANYBINS:

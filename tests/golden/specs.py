@@ -129,3 +129,30 @@ def trace_frames(spec=TRACE_SPEC):
         c = rng.standard_normal(spec["shapes"][2]).astype(np.float32) * s
         frames.append([a, b, c])
     return frames
+
+
+# ---------------------------------------------------------------- DP driver
+# train_toy's EDGC setup (grad_source.py:311-327) on these bucket sets pins the
+# rank bounds (controller.py:111-163); DP_SCENARIO pins the window decisions.
+def _gpt2(layer, layers):
+    return [s for _ in range(layers) for s in layer]
+
+
+DP_BOUND_SETS = {
+    "gpt2_2p5b": _gpt2(((1920, 5760), (1920, 1920), (1920, 7680), (7680, 1920)), 52),
+    "gpt2_12p1b": _gpt2(((3584, 10752), (3584, 3584), (3584, 14336), (14336, 3584)), 76),
+    "gpt2_2p5b_layer": _gpt2(((1920, 5760), (1920, 1920), (1920, 7680), (7680, 1920)), 1),
+    "dp_small": [(128, 512), (512, 128), (256, 256)],
+    "dp_check": [(192, 576), (192, 192), (192, 768), (768, 192), (50, 70)],
+}
+
+DP_SCENARIO = {"shapes": [[128, 512], [512, 128], [256, 256]], "iters": 80, "window": 20, "alpha": 0.1,
+               "beta": 0.25, "sigma0": 1e-2, "tau": 60.0, "synth_seed": 7}
+
+
+def dp_scenario_grads(t: int, w: int):
+    """Worker w's fp32 gradients at iteration t: sigma0 exp(-t / tau) standard normals (oracle.synth_matrix)."""
+    import oracle
+    sc = DP_SCENARIO
+    s = sc["sigma0"] * math.exp(-t / sc["tau"])
+    return [oracle.synth_matrix(sc["synth_seed"], t, k, w, m, n, s) for k, (m, n) in enumerate(sc["shapes"])]

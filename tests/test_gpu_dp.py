@@ -1,76 +1,26 @@
 """GPU: EdgcDataParallel (train_toy's EDGC wiring, grad_source.py:311-479) at W = 1.
 
-The rank history must equal the one the reference's control flow produces from
-the oracle's entropies on the same inputs, and the averaged gradients must match
-the oracle's per-step DP average (uncompressed during warm-up, compressed after).
+The rank history must equal the one the LIVE reference's tracker and controller
+produce on the same inputs (tests/golden/dp.json, make_dp_golden.py), and the
+averaged gradients must match the oracle's per-step DP average (uncompressed
+during warm-up, compressed after).
 """
-
-import math
 
 import numpy as np
 import pytest
 import torch
 
 import oracle
-from tests.helpers import rel_err
+from tests.golden.specs import DP_SCENARIO, dp_scenario_grads
+from tests.helpers import load_json, rel_err
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(128, 512), (512, 128), (256, 256)]
+SHAPES = [tuple(s) for s in DP_SCENARIO["shapes"]]
 
 
-def grads_at(t, tau=60.0):
-    s = 1e-2 * math.exp(-t / tau)
-    return [oracle.synth_matrix(7, t, k, 0, m, n, s) for k, (m, n) in enumerate(SHAPES)]
-
-
-def reference_run(iters, window, alpha, beta):
-    """The reference's train_toy EDGC control flow, on the oracle (host, float64)."""
-    import paper_2511_10333_b200.controller as C
-    from paper_2511_10333_b200.rank_model import g_table
-    per_rank = sum(m + n for m, n in SHAPES)
-    raw = sum(m * n for m, n in SHAPES)
-    model = C.CommModel(eta=4 * per_rank / 1e9, bandwidth=1e9, element_size=4)
-    bounds = C.compute_rank_bounds(model, 4 * raw, SHAPES)
-    big = max(SHAPES, key=lambda s: s[0] * s[1])
-    table = g_table(min(big), max(big), 64, 0)
-    if bounds.r_max >= table.m:
-        bounds = C.RankBounds(min(bounds.r_min, table.m - 1), table.m - 1)
-    ctl = C.RankControllerState(bounds=bounds, window=window, total_iterations=iters)
-    seeds = oracle.state_seeds(0, 1, len(SHAPES))
-    states = [[oracle.OracleState(m, n, min(bounds.r_max, m, n), seeds[(0, k)]) for k, (m, n) in enumerate(SHAPES)]]
-    period = max(1, round(1 / alpha))
-    pending, cur, hist, avgs = [], 0, [], []
-
-    def close(idx, vals):
-        h = float(np.mean(vals))
-        if ctl.phase == C.PHASE_WARMUP:
-            C.warmup_step(ctl, h, (idx + 1) * window, table)
-            r = ctl.r_prev if ctl.phase == C.PHASE_ACTIVE else None
-        else:
-            r, _ = C.adjust_rank_window(ctl, h, table, model)
-        hist.append(r)
-        if r is not None:
-            for s in states[0]:
-                oracle.set_rank(s, min(r, s.m, s.n))
-
-    for t in range(iters):
-        gs = [g.astype(np.float64) for g in grads_at(t)]
-        if ctl.phase == C.PHASE_ACTIVE:
-            avgs.append(oracle.dp_step([gs], states))
-        else:
-            avgs.append(gs)
-        win = t // window
-        if win > cur:
-            close(cur, pending)
-            pending, cur = [], win
-        if t % period == 0:
-            per = [oracle.gaussian_entropy(oracle.subsample(g, beta, oracle.subsample_seed(0, t, k)))
-                   for k, g in enumerate(gs)]
-            pending.append(float(np.mean(per)))
-    if pending:
-        close(cur, pending)
-    return hist, avgs
+def grads_at(t):
+    return dp_scenario_grads(t, 0)
 
 
 def test_dp_driver_rank_history_and_averages():
@@ -83,8 +33,9 @@ def test_dp_driver_rank_history_and_averages():
     from paper_2511_10333_b200.dp import EdgcDataParallel
     from paper_2511_10333_b200.entropy import SamplerConfig
     from tests.test_gpu_debug_rank import resync
-    iters, window, alpha, beta = 80, 20, 0.1, 0.25
-    ref_hist, _ = reference_run(iters, window, alpha, beta)
+    sc = DP_SCENARIO
+    iters, window, alpha, beta = sc["iters"], sc["window"], sc["alpha"], sc["beta"]
+    ref_hist = load_json("dp.json")["driver"]["history"]
     dp = EdgcDataParallel(SHAPES, total_iterations=iters, seed=0, sampler=SamplerConfig(alpha, beta, 0),
                           window=window)
     seeds = oracle.state_seeds(0, 1, len(SHAPES))

@@ -111,3 +111,44 @@ def test_engine_gpt2_layer_one_step():
         ref = oracle.dp_step([[g.astype(np.float64) for g in gs]], ost)
         for o, r in zip(outs, ref):
             assert rel_err(o, r) <= 1e-4
+
+
+def test_rank_changes_do_not_accumulate_plans():
+    """Every controller decision used to leave its transition and steady-state plans (each with its
+    own fp64 scratch) cached forever; now only the current ranks' plans survive, so HBM use is
+    flat across many rank changes."""
+    from paper_2511_10333_b200.engine import BucketEngine
+    shapes = _shapes()
+    eng = BucketEngine(shapes, rank=24, seed=3, rank_cap=48)
+    gs = [torch.from_numpy(oracle.synth_matrix(1, 0, k, 0, m, n, 1e-2)).cuda() for k, (m, n) in enumerate(shapes)]
+    mem = []
+    for i, r in enumerate([24, 30, 17, 48, 9, 33, 24, 40, 12, 36, 20, 44, 28]):
+        eng.set_rank(r)
+        for _ in range(3):
+            eng.step(gs)
+        torch.cuda.synchronize()
+        assert len(eng._plans) <= 4, sorted(k[:3] for k in eng._plans)
+        mem.append(torch.cuda.memory_allocated())
+    eng.check_status()
+    # bounded by the largest configuration visited, not growing with the number of decisions
+    assert mem[-1] <= max(mem[:4]) * 1.05, mem
+
+
+def test_compress_factors_do_not_alias_the_residual():
+    """Editing the returned factors in place (e.g. a caller scaling P) must not change the state's
+    error-feedback residual (compressor.py:112 stores an array of its own)."""
+    import paper_2511_10333_b200 as e
+    m, n, r = 96, 160, 4
+    g = oracle.synth_matrix(2, 0, 0, 0, m, n, 1e-2)
+    st = e.CompressorState(m, n, r, rng_seed=5)
+    f = e.compress(torch.from_numpy(g).cuda(), st)
+    before = st.residual.clone()
+    f.p.mul_(3.0)
+    f.q.zero_()
+    assert torch.equal(st.residual, before)
+    ost = oracle.OracleState(m, n, r, 5)
+    oracle.compress(g.astype(np.float64), ost)
+    g2 = oracle.synth_matrix(2, 1, 0, 0, m, n, 1e-2)
+    f2 = e.compress(torch.from_numpy(g2).cuda(), st)
+    p2, q2, _ = oracle.compress(g2.astype(np.float64), ost)
+    assert rel_err(f2.p @ f2.q.T, p2 @ q2.T) <= 2e-5

@@ -111,3 +111,16 @@ def test_fd_histogram_many_bins_global_path(df, nbins):
     c, e, _ = histogram_fd(torch.from_numpy(x).cuda())
     assert np.array_equal(c.cpu().numpy(), c_ref)
     assert np.array_equal(e.cpu().numpy(), e_ref)
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), float("-inf")])
+def test_histogram_rejects_non_finite_samples(bad):
+    """np.histogram(bins='fd') raises ValueError when the autodetected range is not finite
+    (numpy/lib/_histograms_impl.py:_get_outer_edges); the device histogram does too."""
+    from paper_2511_10333_b200 import entropy as E
+    x = torch.randn(100_003, device="cuda")
+    x[12_345] = bad
+    with pytest.raises(ValueError):
+        E.histogram_fd(x)
+    with pytest.raises(ValueError):
+        E.histogram_fd(x, bins=64)

@@ -21,6 +21,6 @@ def test_multi_gpu_exchange_matches_reference(world):
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={29533 + world}", os.path.join(ROOT, "tools", "dp_check.py")]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
     assert '"ok": true' in res.stdout

@@ -133,3 +133,45 @@ def test_seeds_match_reference_golden():
         assert seeds.subsample_seed(rec["seed"], rec["t"], rec["k"]) == rec["sub_seed"]
     got = {f"{w},{k}": v for (w, k), v in seeds.state_seeds(0, 8, 208).items()}
     assert got == gold["state_seeds_0_8_208"]
+
+
+@pytest.mark.parametrize("name", ["gpt2_2p5b", "gpt2_12p1b", "gpt2_2p5b_layer", "dp_small", "dp_check"])
+def test_dp_setup_bounds_match_reference_golden(name):
+    """train_toy's EDGC setup (grad_source.py:311-327 -> controller.py:111-163) on the GPT-2 bucket
+    sets: our edgc_setup gives the live reference's r_min / r_max (tests/golden/dp.json)."""
+    from paper_2511_10333_b200.dp import edgc_setup
+    from tests.golden.specs import DP_BOUND_SETS
+    rec = load_json("dp.json")["bounds"][name]
+    _, bounds, table = edgc_setup(DP_BOUND_SETS[name])
+    assert (bounds.r_min, bounds.r_max, table.m) == (rec["r_min"], rec["r_max"], rec["table_m"])
+
+
+def test_dp_driver_history_from_oracle_entropies():
+    """The DP scenario's window entropies, computed by the oracle (NumPy choice + std), equal the
+    reference's (dp.json), and our controller turns them into the reference's rank history."""
+    import oracle
+    from paper_2511_10333_b200 import controller as C
+    from paper_2511_10333_b200.dp import edgc_setup
+    from tests.golden.specs import DP_SCENARIO, dp_scenario_grads
+    gold = load_json("dp.json")["driver"]
+    sc = DP_SCENARIO
+    model, bounds, table = edgc_setup([tuple(s) for s in sc["shapes"]])
+    assert [bounds.r_min, bounds.r_max] == gold["bounds"]
+    period = max(1, round(1 / sc["alpha"]))
+    per_win = {}
+    for t in range(0, sc["iters"], period):
+        gs = dp_scenario_grads(t, 0)
+        h = [oracle.gaussian_entropy(oracle.subsample(g.astype(np.float64), sc["beta"], oracle.subsample_seed(0, t, k)))
+             for k, g in enumerate(gs)]
+        per_win.setdefault(t // sc["window"], []).append(float(np.mean(h)))
+    means = [float(np.mean(v)) for _, v in sorted(per_win.items())]
+    assert np.allclose(means, gold["window_entropies"], rtol=0, atol=1e-12)
+    ctl = C.RankControllerState(bounds=bounds, window=sc["window"], total_iterations=sc["iters"])
+    hist = []
+    for i, h in enumerate(gold["window_entropies"]):
+        if ctl.phase == C.PHASE_WARMUP:
+            C.warmup_step(ctl, h, (i + 1) * ctl.window, table)
+            hist.append(ctl.r_prev if ctl.phase == C.PHASE_ACTIVE else None)
+        else:
+            hist.append(C.adjust_rank_window(ctl, h, table, model)[0])
+    assert hist == gold["history"]
