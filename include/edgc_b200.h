@@ -69,8 +69,9 @@ typedef struct {
                           (bit e set iff e is sampled; the caller zeroes it) or NULL */
     int64_t flags;     /* EDGC_PLAN_* */
 } edgc_plan_desc;
-/* Only the membership bitmap (required) and idx[0] (the first sample in NumPy
- * order, the Gaussian estimator's shift) are produced: the set, not the order. */
+/* Only the membership bitmap (required) and idx[0] (one sampled element, the
+ * Gaussian estimator's shift: NumPy's first sample for Floyd plans, its last for
+ * tail-shuffle plans) are produced: the set, not the order. */
 #define EDGC_PLAN_BITMAP_ONLY 1
 
 int64_t edgc_sample_plan_workspace_bytes(const edgc_plan_desc *plans, int n_plans);

@@ -69,13 +69,10 @@ struct PlanDev {
     int64_t n_elems, count;
     int32_t *idx;
     uint32_t *bitmap;  // optional membership bits
-    uint32_t *draws;   // [n_draws]
-    int64_t n_draws;   // even
     int32_t *rv;       // [count] bounded values
     int32_t *next;     // [count]
     int32_t *head;     // [n_elems] latest step targeting each position (-1: none)
     int32_t tail;      // 1 = tail shuffle, 0 = Floyd
-    int64_t draw_chunk0;  // first P1 chunk index of this plan
     int64_t step_block0;  // first P3/P4 block index of this plan
     // bucketed resolve (tail-shuffle plans; see k_bucket_sort)
     int32_t *lst_s, *lst_j;   // [count] each chunk's steps sorted by bucket, and their bounded values
@@ -85,56 +82,24 @@ struct PlanDev {
     int32_t *nchain;          // chain list length
     int32_t nb, nch;          // buckets, sort chunks
     int32_t bucketed;         // 1: bucket path, 0: global head-table path
+    int32_t setmode;          // 1: membership set only (k_set_*), the order-free resolve
+    uint32_t *lst_pk;         // set mode: [count] (step in chunk << kSBits) | position in bucket
+    uint32_t *notlast;        // set mode: [ceil(count/32)] bit s: a later step hits rv[s] again
     int32_t full_idx;         // 0: EDGC_PLAN_BITMAP_ONLY (only idx[0] is written)
     int64_t chunk0;           // first sort CTA of this plan
     int64_t bucket0;          // first bucket-resolve CTA of this plan
     int64_t oblock0;          // first chain-pass CTA of this plan
 };
 
-constexpr int kDrawsPerThread = 64;  // 64-bit outputs per P1 thread
-constexpr int kP1Threads = 256;
-constexpr int64_t kDrawsPerBlock = (int64_t)kDrawsPerThread * kP1Threads;
 constexpr int kStepThreads = 256;
 
-__device__ __forceinline__ int find_plan(const PlanDev *plans, int n, int64_t blk, bool by_draw) {
+__device__ __forceinline__ int find_plan(const PlanDev *plans, int n, int64_t blk) {
     int lo = 0, hi = n - 1;
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
-        int64_t b0 = by_draw ? plans[mid].draw_chunk0 : plans[mid].step_block0;
-        if (b0 <= blk) lo = mid; else hi = mid - 1;
+        if (plans[mid].step_block0 <= blk) lo = mid; else hi = mid - 1;
     }
     return lo;
-}
-
-// ---- P1: u32 draw stream ---------------------------------------------------
-// Block b of a plan owns 64-bit outputs [b*64*256, (b+1)*64*256); thread t
-// produces outputs t, t+256, t+512, ... of that range (one jump-ahead, then a
-// 256-step affine LCG map per output), so every warp store is coalesced.
-__device__ __forceinline__ void k_draws_body(const PlanDev *plans, int n_plans, int64_t vb) {
-    const PlanDev P = plans[find_plan(plans, n_plans, vb, true)];
-    const int64_t o_base = (int64_t)(vb - P.draw_chunk0) * kDrawsPerBlock;
-    const int64_t n64 = P.n_draws / 2;
-    if (o_base >= n64) return;
-    // s = state after o + 1 steps: output o = XSL-RR(s); one 128-bit multiply-add per output
-    u128 s = pcg_jump(P.state, P.inc, (uint64_t)(o_base + threadIdx.x) + 1u);
-    u128 a_t, c_t;
-    pcg_affine(P.inc, kP1Threads, a_t, c_t);
-    uint2 *out = reinterpret_cast<uint2 *>(P.draws);
-    for (int k = 0; k < kDrawsPerThread; ++k) {
-        const int64_t o = o_base + threadIdx.x + (int64_t)k * kP1Threads;
-        if (o >= n64) break;
-        const uint64_t v = pcg_output(s);
-        out[o] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
-        s = a_t * s + c_t;
-    }
-}
-
-__global__ void __launch_bounds__(kP1Threads) k_draws(const PlanDev *plans, int n_plans, int64_t nvb) {
-    // grid-stride over the virtual CTAs: the launch may be capped to a share of the SMs
-    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
-        k_draws_body(plans, n_plans, vb);
-        __syncthreads();
-    }
 }
 
 // 2^32 mod excl (NumPy's Lemire threshold (2^32 - excl) % excl), excl >= 1.  For
@@ -151,228 +116,141 @@ __device__ __forceinline__ uint32_t lemire_threshold(uint32_t excl) {
     return (uint32_t)r;
 }
 
-// ---- P2: assign draws to steps --------------------------------------------
-// A group of kWT threads walks one plan in windows of kWW steps.  Thread t
-// tests its kWQ consecutive steps against the draws at shifts 0..kWK-1 (draw
-// u + step + j): a Lemire rejection at step f and shift d moves every later
-// step one draw further, so the window resolves by scanning rejection events
-// in step order (one warp, ballots) and accepting each step at shift #events
-// at or before it.  Up to kWK-1 rejections fit in one window (~3.5 expected at
-// GPT-2 sizes); rarer bursts end the window early.  Draws stream into a
-// shared ring with bulk async copies.  kWG plans share a CTA (one group each,
-// named barriers), so the walk holds few SMs while it prefetches.
-constexpr int kWT = 256;                  // threads per plan group
-constexpr int kWQ = 8;                    // consecutive steps per thread
-constexpr int kWW = kWT * kWQ;            // steps per window
-#ifndef EDGC_WALK_K
-#define EDGC_WALK_K 4
-#endif
-constexpr int kWK = EDGC_WALK_K;          // speculative shifts
-static_assert(kWK <= 8, "the shift switch in k_walk covers 8 shifts");
-constexpr int kWG = 4;                    // plan groups per CTA
-constexpr int kWWords = kWW / 32;         // mask words per shift
-constexpr int kRingBlk = 1024;            // draws per ring block (4 KB bulk copy)
-constexpr int kRingN = 8;                 // blocks in flight
-constexpr int kRing = kRingBlk * kRingN;  // ring size (draws), power of two
-static_assert(kWWords == 64, "event scan assumes two mask words per lane");
+// ---- P1: the walk -- bounded value of every step ------------------------------
+// The NumPy walk is sequential: step s takes the next unused u32 draw (NumPy's
+// next_uint32: low half of each PCG64 output first) and a Lemire rejection
+// consumes one extra draw.  Rejections are rare (first-stage test p ~ excl/2^32,
+// ~3e-3 at GPT-2 sizes), so one walker warp takes kWalkQ * 32 consecutive steps
+// per chunk -- lane l steps s + l + 32 q against draws k + l + 32 q: one multiply
+// and compare per step, one ballot per chunk -- and when a step rejects, the chunk
+// ends at the first rejecting step (in step order), whose draw is skipped.
+// Generating the draws is most of the arithmetic (a 128-bit LCG step per two
+// draws) and does not depend on the walk, so kWalkProd producer warps per plan
+// fill a shared ring of kWalkBlk-draw blocks ahead of the walker (smem counters,
+// no HBM draw buffer).  kWalkPlans plans share a CTA.
+constexpr int kWalkPlans = 8;               // plans per CTA
+constexpr int kWalkProd = 2;                // producer warps per plan
+constexpr int kWalkQ = 4;                   // steps per walker lane per chunk
+constexpr int kWalkChunk = 32 * kWalkQ;
+constexpr int kWalkBlk = 1024;              // draws per ring block
+constexpr int kWalkNBlk = 4;                // ring blocks
+constexpr int kWalkRing = kWalkBlk * kWalkNBlk;
+constexpr int kWalkWarpsPer = 1 + kWalkProd;
+constexpr int kWalkThreads = 32 * kWalkWarpsPer * kWalkPlans;
+static_assert(kWalkBlk % (64 * kWalkProd) == 0, "whole outputs per producer lane");
+static_assert(kWalkChunk <= kWalkBlk, "a chunk spans at most two blocks");
+static_assert(kWalkPlans <= 15, "one named barrier per plan group");
 
-struct WalkGroup {
-    uint32_t ring[kRing];
-    uint32_t mask[kWK][kWWords];
-    int ev[kWK];
-    int ne, len, err;
-    alignas(8) uint64_t full[kRingN];
+struct alignas(16) WalkRing {
+    uint32_t d[kWalkRing];
+    volatile int produced;   // blocks written
+    volatile int consumed;   // blocks the walker is done with
+    volatile int done;
 };
 
-__device__ __forceinline__ void group_sync(int g) { ptx::named_bar_sync(1 + g, kWT); }
-
-// order[]: the plans by decreasing step count, so a CTA's groups walk plans of similar
-// length and CTAs of short plans free their SMs early
-__global__ void __launch_bounds__(kWT * kWG, 1) k_walk(const PlanDev *plans, int n_plans, int32_t *status,
-                                                      const int32_t *order) {
-    extern __shared__ __align__(128) unsigned char walk_raw[];
-    const int g = threadIdx.x / kWT;
-    const int slot = blockIdx.x * kWG + g;
-    if (slot >= n_plans) return;   // the whole group leaves; groups synchronise only among themselves
-    const int pid = order[slot];
-    WalkGroup &W = reinterpret_cast<WalkGroup *>(walk_raw)[g];
-    const PlanDev P = plans[pid];
-    const int tid = threadIdx.x % kWT, lane = tid & 31, warp = tid >> 5;
-    const int64_t count = P.count, nd = P.n_draws;
-    const int64_t nblocks = (nd + kRingBlk - 1) / kRingBlk;
+__global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int n_plans, const int32_t *order) {
+    extern __shared__ __align__(16) unsigned char walk_raw[];
+    const int g = threadIdx.x / (32 * kWalkWarpsPer);        // plan group in the CTA
+    const int wg = (threadIdx.x / 32) % kWalkWarpsPer;       // 0: walker, 1..: producers
+    const int lane = threadIdx.x & 31;
+    const int slot = blockIdx.x * kWalkPlans + g;
+    WalkRing &R = reinterpret_cast<WalkRing *>(walk_raw)[g];
+    if (threadIdx.x % (32 * kWalkWarpsPer) == 0) { R.produced = 0; R.consumed = 0; R.done = 0; }
+    __syncthreads();
+    if (slot >= n_plans) return;   // whole group leaves (groups synchronise only among themselves)
+    const PlanDev &P = plans[order[slot]];
+    const uint32_t count = (uint32_t)P.count;
+    if (wg > 0) {
+        // producer: lane pl (of 32 * kWalkProd) writes outputs o = blk * kWalkBlk / 2 + pl + 32 kWalkProd t
+        const int pl = (wg - 1) * 32 + lane;
+        constexpr int kStride = 32 * kWalkProd;                 // outputs between a lane's consecutive ones
+        constexpr int kPer = kWalkBlk / 2 / kStride;            // outputs per lane per block
+        u128 st = pcg_jump(P.state, P.inc, (uint64_t)pl + 1u);  // state after output pl
+        u128 a, c;
+        pcg_affine(P.inc, kStride, a, c);
+        for (int blk = 0;; ++blk) {
+            // exit only where every producer warp decides alike: once done is set the walker's
+            // consumed count is final, so re-reading it gives all of them the same answer
+            bool stop = false;
+            while (blk - R.consumed >= kWalkNBlk) {
+                if (R.done) {
+                    stop = blk - R.consumed >= kWalkNBlk;
+                    break;
+                }
+                __nanosleep(256);
+            }
+            if (stop) return;
+            uint2 *dst = reinterpret_cast<uint2 *>(R.d + (blk % kWalkNBlk) * kWalkBlk);
+#pragma unroll 4
+            for (int t = 0; t < kPer; ++t) {
+                const uint64_t v = pcg_output(st);
+                st = a * st + c;
+                dst[pl + kStride * t] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
+            }
+            ptx::named_bar_sync(1 + g, 32 * kWalkProd);   // the producers of this plan
+            if (pl == 0) {
+                __threadfence_block();
+                R.produced = blk + 1;
+            }
+        }
+    }
+    // walker
     const uint32_t tail = (uint32_t)P.tail;
-    const uint32_t rng_hi = tail ? (uint32_t)(P.n_elems - 1) : (uint32_t)(P.n_elems - P.count);
+    // excl = rng + 1 of step s: tail i + 1 = N - s; Floyd j + 1 = N - count + s + 1
+    const uint32_t e0 = tail ? (uint32_t)P.n_elems : (uint32_t)(P.n_elems - P.count + 1);
     int32_t *rv = P.rv;
-    const uint32_t *draws = P.draws;
-    int64_t next_blk = 0;   // first block not yet requested (thread 0 of the group)
-    auto request = [&](int64_t upto) {
-        while (next_blk < upto && next_blk < nblocks) {
-            const int slot = (int)(next_blk % kRingN);
-            const int64_t first = next_blk * kRingBlk;
-            const uint32_t bytes = (uint32_t)(min((int64_t)kRingBlk, nd - first) * 4);
-            ptx::mbar_arrive_expect_tx(&W.full[slot], bytes);
-            ptx::bulk_g2s(&W.ring[slot * kRingBlk], draws + first, bytes, &W.full[slot]);
-            ++next_blk;
-        }
-    };
-    if (tid == 0) {
-        for (int i = 0; i < kRingN; ++i) ptx::mbar_init(&W.full[i], 1);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        W.err = 0;
-        request(kRingN);
-    }
-    group_sync(g);
-    int64_t s = 0, u = 0;
+    uint32_t s = 0, k = 0;   // next step, next draw (N < 2^31)
+    int have = 0;            // blocks known to be produced
     while (s < count) {
-        const int64_t b0 = u / kRingBlk;
-        for (int64_t bb = b0; bb <= b0 + 2 && bb < nblocks; ++bb)
-            ptx::mbar_wait(&W.full[bb % kRingN], (uint32_t)((bb / kRingN) & 1));
-        // this thread's steps s + kWQ tid + q use draws u + kWQ tid + q + j
-        const int nvalid = (int)min((int64_t)kWW, count - s);
-        const uint32_t ubase = (uint32_t)(u & (kRing - 1)) + (uint32_t)(kWQ * tid);
-        const int64_t dleft = nd - u - kWQ * tid;   // draws generated from this thread's first one on
-        const bool near_end = dleft < kWQ + kWK;
-        uint32_t d[kWQ + kWK - 1];
-#pragma unroll
-        for (int e = 0; e < kWQ + kWK - 1; ++e) d[e] = W.ring[(ubase + e) & (kRing - 1)];
-        // speculative pass: rejection bits only (the bounded values are recomputed below for
-        // the one shift each step ends up at)
-        uint32_t byt[kWK];
-#pragma unroll
-        for (int j = 0; j < kWK; ++j) byt[j] = 0u;
-#pragma unroll
-        for (int q = 0; q < kWQ; ++q) {
-            const int step = kWQ * tid + q;
-            // rng of step s + step: tail i = N-1-(s+step); Floyd j = N-count+(s+step)
-            const uint32_t off = (uint32_t)s + (uint32_t)step;
-            const uint32_t rng = tail ? rng_hi - off : rng_hi + off;
-            const uint32_t excl = rng + 1u;
-            uint32_t left[kWK];
-            bool cand = false;
-#pragma unroll
-            for (int j = 0; j < kWK; ++j) {
-                left[j] = d[q + j] * excl;   // low half of the 64-bit product
-                cand |= left[j] < excl;      // necessary for a rejection (p ~ excl / 2^32)
-            }
-            if (cand) {
-                const uint32_t thr = lemire_threshold(excl);   // the step's, shared by every shift
-#pragma unroll
-                for (int j = 0; j < kWK; ++j) byt[j] |= (uint32_t)(left[j] < thr) << q;
-            }
-            if (near_end) {
-#pragma unroll
-                for (int j = 0; j < kWK; ++j)
-                    if ((int64_t)(q + j) >= dleft) byt[j] |= 1u << q;   // past the generated stream
-            }
+        const int need = (int)((k + kWalkChunk + kWalkBlk - 1) / kWalkBlk);
+        if (have < need) {
+            // refresh the producers' count (once per block); the fence pairs with theirs -- it also
+            // waits for this warp's outstanding rv stores, so it must not run every chunk
+            do {
+                have = R.produced;
+                if (have < need) __nanosleep(32);
+            } while (have < need);
+            __threadfence_block();
         }
-        {
-            const int valid = min(kWQ, max(0, nvalid - kWQ * tid));   // steps of this thread inside the window
-            const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+        uint64_t m[kWalkQ];
+        bool any = false;
 #pragma unroll
-            for (int j = 0; j < kWK; ++j) byt[j] &= vm;
+        for (int q = 0; q < kWalkQ; ++q) {
+            const uint32_t sl = s + lane + 32 * q;
+            const uint32_t excl = tail ? e0 - sl : e0 + sl;
+            m[q] = (uint64_t)R.d[(k + lane + 32 * q) & (kWalkRing - 1)] * excl;
+            any |= sl < count && (uint32_t)m[q] < excl;   // necessary for a rejection
         }
-        // per-shift 32-bit words: word (8 warp + lane/4) holds steps 32 w .. 32 w + 31
+        uint32_t adv = min((uint32_t)kWalkChunk, count - s), skip = 0;
+        if (__ballot_sync(0xffffffffu, any)) {
 #pragma unroll
-        for (int j = 0; j < kWK; ++j) {
-            uint32_t wv = byt[j] << (8 * (lane & 3));
-            wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
-            wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
-            if ((lane & 3) == 0) W.mask[j][warp * 8 + (lane >> 2)] = wv;
-        }
-        group_sync(g);
-        if (warp == 0) {
-            int cur = 0, dd = 0, ne = 0, len = nvalid;
-            while (true) {
-                uint32_t lo_bits = W.mask[dd][lane], hi_bits = W.mask[dd][lane + 32];
-                const int lo0 = lane * 32, hi0 = (lane + 32) * 32;
-                if (lo0 + 32 <= cur) lo_bits = 0u;
-                else if (lo0 < cur) lo_bits &= ~((1u << (cur - lo0)) - 1u);
-                if (hi0 + 32 <= cur) hi_bits = 0u;
-                else if (hi0 < cur) hi_bits &= ~((1u << (cur - hi0)) - 1u);
-                const unsigned any_lo = __ballot_sync(0xffffffffu, lo_bits != 0u);
-                const unsigned any_hi = __ballot_sync(0xffffffffu, hi_bits != 0u);
-                if (!any_lo && !any_hi) break;
-                int f;
-                if (any_lo) {
-                    const int wi = __ffs(any_lo) - 1;
-                    f = wi * 32 + __ffs(__shfl_sync(0xffffffffu, lo_bits, wi)) - 1;
-                } else {
-                    const int wi = __ffs(any_hi) - 1;
-                    f = (wi + 32) * 32 + __ffs(__shfl_sync(0xffffffffu, hi_bits, wi)) - 1;
-                }
-                if (lane == 0) W.ev[ne] = f;
-                ++ne;
-                ++dd;
-                if (dd == kWK) { len = f; break; }
-                cur = f;
-            }
-            if (lane == 0) { W.ne = ne; W.len = len; }
-        }
-        group_sync(g);
-        const int ne = W.ne, len = W.len;
-        int ev[kWK];
-#pragma unroll
-        for (int e = 0; e < kWK; ++e) ev[e] = (e < ne) ? W.ev[e] : 0x7fffffff;
-        uint32_t out[kWQ];
-        {
-            const int first = kWQ * tid, last = first + kWQ - 1;
-            int sh0 = 0;
-#pragma unroll
-            for (int e = 0; e < kWK; ++e) sh0 += (ev[e] <= first);
-            const bool split = sh0 < kWK && ev[sh0 < kWK ? sh0 : 0] <= last;   // an event inside my steps
-            uint32_t x[kWQ];
-            if (!split) {
-                // one shift for all of this thread's steps
-                switch (sh0) {
-#define EDGC_PICK(SH) case SH: _Pragma("unroll") for (int q = 0; q < kWQ; ++q) x[q] = d[q + (SH < kWK ? SH : 0)]; break;
-                    EDGC_PICK(0) EDGC_PICK(1) EDGC_PICK(2) EDGC_PICK(3)
-                    EDGC_PICK(4) EDGC_PICK(5) EDGC_PICK(6) EDGC_PICK(7)
-#undef EDGC_PICK
-                    default:
-#pragma unroll
-                        for (int q = 0; q < kWQ; ++q) x[q] = d[q];   // shift kWK: steps past the window end
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < kWQ; ++q) {
-                    int sh = 0;
-#pragma unroll
-                    for (int e = 0; e < kWK; ++e) sh += (ev[e] <= first + q);
-                    uint32_t v = d[q];
-#pragma unroll
-                    for (int j = 1; j < kWK; ++j) v = (sh == j) ? d[q + j] : v;
-                    x[q] = v;
+            for (int q = 0; q < kWalkQ; ++q) {
+                const uint32_t sl = s + lane + 32 * q;
+                const uint32_t excl = tail ? e0 - sl : e0 + sl;
+                const bool rej = sl < count && (uint32_t)m[q] < excl && (uint32_t)m[q] < lemire_threshold(excl);
+                const unsigned rb = __ballot_sync(0xffffffffu, rej);
+                if (rb && !skip) {
+                    adv = min(adv, 32u * q + __ffs(rb) - 1);   // steps before the first rejection keep their draws
+                    skip = 1;
                 }
             }
-#pragma unroll
-            for (int q = 0; q < kWQ; ++q) {
-                const uint32_t off = (uint32_t)s + (uint32_t)(first + q);
-                const uint32_t excl = (tail ? rng_hi - off : rng_hi + off) + 1u;
-                out[q] = __umulhi(x[q], excl);
-            }
         }
-        const int first = kWQ * tid;
-        if (first + kWQ <= len && ((s & 3) == 0)) {
-            int4 *dst = reinterpret_cast<int4 *>(rv + s + first);
-            dst[0] = make_int4(out[0], out[1], out[2], out[3]);
-            dst[1] = make_int4(out[4], out[5], out[6], out[7]);
-        } else {
 #pragma unroll
-            for (int q = 0; q < kWQ; ++q)
-                if (first + q < len) rv[s + first + q] = (int32_t)out[q];
-        }
-        if (tid == 0 && u + len + ne > nd) W.err = 1;
-        s += len;
-        u += len + ne;
-        group_sync(g);   // every read of ring blocks below u / kRingBlk is done
-        if (tid == 0) request(u / kRingBlk + kRingN);
-        if (W.err || (len == 0 && ne == 0)) break;
+        for (int q = 0; q < kWalkQ; ++q)
+            if (lane + 32u * q < adv) rv[s + lane + 32 * q] = (int32_t)(m[q] >> 32);
+        s += adv;
+        k += adv + skip;
+        __syncwarp();
+        if (lane == 0) R.consumed = (int)(k / kWalkBlk);   // blocks wholly below the next draw
     }
-    if (tid == 0) status[pid] = (W.err || s < count) ? EDGC_EDRAWS : EDGC_OK;
+    if (lane == 0) {
+        __threadfence_block();   // the final consumed count before done
+        R.done = 1;
+    }
 }
 
 __device__ __forceinline__ int find_plan_steps(const PlanDev *plans, int n, int64_t blk) {
-    return find_plan(plans, n, blk, false);
+    return find_plan(plans, n, blk);
 }
 
 // ---- P3: per-position lists of the steps whose bounded value is that position
@@ -850,10 +728,276 @@ __global__ void __launch_bounds__(kStepThreads) k_bucket_chain(const PlanDev *pl
     }
 }
 
+// ---- set mode: membership bits only (EDGC_PLAN_BITMAP_ONLY tail-shuffle plans) --
+// The Gaussian estimator needs the SET of sampled positions, not NumPy's order,
+// and the set of a partial Fisher-Yates has an order-free description.  With
+// step s finalising position i_s = N-1-s, target j_s = rv[s] <= i_s, z0 = N-count:
+//   M(p)     = latest step (largest s) with j_s = p and j_s != i_s; D(p) = M(p) exists
+//   last(s)  = M(j_s) == s  (no later step hits j_s again)
+//   good(s)  = j_s != i_s && last(s) && (j_s < z0 || good(N-1-j_s))
+// Position p < z0 is sampled iff D(p) (its value leaves for the tail the first
+// time it is hit); a tail position q >= z0 iff D(q) or !good(N-1-q): the value q
+// ends outside the tail only if it is carried down to a non-tail position along
+// a path of "last writer" links, and then no earlier step hit q.  (Derivation in
+// DESIGN.md §4; every rule is emulated against NumPy in tests/test_plan_logic.py.)
+// Kernels: k_set_sort packs each 32K-step chunk by 32K-position bucket (4 B per
+// step); k_set_resolve computes M in shared memory per bucket, stores the bucket's
+// D bits whole and marks !last steps; k_set_tail finishes the tail positions.
+// No chain lists, no per-position tables in HBM.
+constexpr int kSBits = 14;
+constexpr int kSSize = 1 << kSBits;          // positions per set-mode bucket (M: 64 KB of shared memory)
+constexpr int kSWords = kSSize / 32;
+constexpr int kSChunk = 32768;               // steps per sort CTA (15-bit step-in-chunk)
+constexpr int kSMaxBuckets = 2048;           // N <= 2^25
+constexpr int kSMaxChunks = (1 << 25) / kSChunk;
+constexpr int kSSortThreads = 1024;
+constexpr int kSSortPer = kSChunk / kSSortThreads;
+constexpr int kSResThreads = 512;            // 2 CTAs per SM (104 KB of shared memory each)
+constexpr int kSResBatch = 8;                // entry loads in flight per thread
+constexpr int kSTailThreads = 256;           // a warp per bitmap word
+constexpr int kSTailWords = 4;               // words per warp (independent loads in flight)
+static_assert(kSChunk == kBChunk, "both bucket paths share the chunk tables");
+
+struct SSortSmem {
+    int32_t hist[kSMaxBuckets + 1];
+    int32_t warp_tmp[33];
+    uint32_t st[kSChunk];
+};
+
+constexpr int kSLpCap = 16384;               // entries with a shared chunk table (beta <= ~0.6)
+struct SResSmem {
+    int32_t M[kSSize];
+    uint16_t lp[kSLpCap];              // chunk of entry k (when the bucket has <= kSLpCap entries)
+    int32_t segoff[kSMaxChunks + 1];   // entry prefix per sort chunk (+ total)
+    int32_t segstart[kSMaxChunks];     // global start of the bucket's segment in each chunk
+    int32_t warp_tmp[33];
+};
+
+__device__ __forceinline__ void k_set_sort_body(const PlanDev *plans, int n_plans, PlanLut lut, int64_t vb) {
+    extern __shared__ __align__(16) unsigned char ssm_raw[];
+    SSortSmem &sm = *reinterpret_cast<SSortSmem *>(ssm_raw);
+    const PlanDev P = plans[find_plan_by(plans, n_plans, lut.sort, vb, 0)];
+    const int c = (int)(vb - P.chunk0);
+    const int nb = P.nb;
+    const int64_t c0 = (int64_t)c * kSChunk;
+    const int len = (int)min((int64_t)kSChunk, P.count - c0);
+    for (int b = threadIdx.x; b <= nb; b += kSSortThreads) sm.hist[b] = 0;
+    __syncthreads();
+    int32_t j[kSSortPer];
+#pragma unroll
+    for (int k = 0; k < kSSortPer; ++k) {
+        const int i = threadIdx.x + k * kSSortThreads;
+        j[k] = i < len ? P.rv[c0 + i] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < kSSortPer; ++k)
+        if (j[k] >= 0) atomicAdd(&sm.hist[j[k] >> kSBits], 1);
+    __syncthreads();
+    block_exclusive_scan(sm.hist, nb + 1, sm.warp_tmp);
+    int32_t *seg = P.segoff + (int64_t)c * (nb + 1);
+    for (int b = threadIdx.x; b <= nb; b += kSSortThreads) seg[b] = sm.hist[b];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSSortPer; ++k) {
+        if (j[k] < 0) continue;
+        const int slot = atomicAdd(&sm.hist[j[k] >> kSBits], 1);
+        sm.st[slot] = ((uint32_t)(threadIdx.x + k * kSSortThreads) << kSBits) | ((uint32_t)j[k] & (kSSize - 1));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += kSSortThreads) P.lst_pk[c0 + i] = sm.st[i];
+}
+
+__global__ void __launch_bounds__(kSSortThreads) k_set_sort(const PlanDev *plans, int n_plans, PlanLut lut,
+                                                            int64_t nvb) {
+    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+        k_set_sort_body(plans, n_plans, lut, vb);
+        __syncthreads();
+    }
+}
+
+// f(step, position in bucket) for every entry of the bucket: a flat walk over the
+// concatenated segments (the chunk of entry k from the prefix table), kSResBatch
+// global loads in flight per thread
+template <typename F>
+__device__ __forceinline__ void for_bucket_entries(const PlanDev &P, const SResSmem &sm, int nch, int32_t n, F &&f) {
+    const bool table = n <= kSLpCap;
+    for (int32_t k0 = threadIdx.x; k0 < n; k0 += kSResBatch * kSResThreads) {
+        uint32_t e[kSResBatch];
+        int c[kSResBatch];
+#pragma unroll
+        for (int u = 0; u < kSResBatch; ++u) {
+            const int32_t k = k0 + u * kSResThreads;
+            c[u] = -1;
+            if (k < n) {
+                int cc;
+                if (table) {
+                    cc = sm.lp[k];
+                } else {
+                    int lo = 0, hi = nch - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (sm.segoff[mid] <= k) lo = mid; else hi = mid - 1;
+                    }
+                    cc = lo;
+                }
+                c[u] = cc;
+                e[u] = __ldg(P.lst_pk + sm.segstart[cc] + (k - sm.segoff[cc]));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kSResBatch; ++u)
+            if (c[u] >= 0) f((int32_t)c[u] * kSChunk + (int32_t)(e[u] >> kSBits), (int)(e[u] & (kSSize - 1)));
+    }
+}
+
+__device__ __forceinline__ void k_set_resolve_body(const PlanDev *plans, int n_plans, PlanLut lut, int64_t vb) {
+    extern __shared__ __align__(16) unsigned char srm_raw[];
+    SResSmem &sm = *reinterpret_cast<SResSmem *>(srm_raw);
+    const PlanDev P = plans[find_plan_by(plans, n_plans, lut.bucket, vb, 1)];
+    const int b = (int)(vb - P.bucket0);
+    const int nb = P.nb, nch = P.nch;
+    const int64_t N = P.n_elems;
+    const int64_t pbase = (int64_t)b << kSBits;
+    const int32_t ibase = (int32_t)(N - 1 - pbase);   // step s finalises position pbase + l iff s == ibase - l
+    const int tid = threadIdx.x;
+    for (int c = tid; c < nch; c += kSResThreads) {
+        const int32_t *row = P.segoff + (int64_t)c * (nb + 1);
+        const int32_t r0 = row[b];
+        sm.segstart[c] = c * kSChunk + r0;
+        sm.segoff[c] = row[b + 1] - r0;
+    }
+    for (int l = tid; l < kSSize / 4; l += kSResThreads) reinterpret_cast<int4 *>(sm.M)[l] = make_int4(-1, -1, -1, -1);
+    __syncthreads();
+    const int32_t n = block_exclusive_scan(sm.segoff, nch, sm.warp_tmp);
+    if (tid == 0) sm.segoff[nch] = n;
+    __syncthreads();
+    if (n <= kSLpCap) {   // entry -> chunk table (a warp per chunk segment)
+        const int lane = tid & 31;
+        for (int c = tid >> 5; c < nch; c += kSResThreads / 32)
+            for (int32_t k = sm.segoff[c] + lane; k < sm.segoff[c + 1]; k += 32) sm.lp[k] = (uint16_t)c;
+        __syncthreads();
+    }
+    // M(p): latest step hitting p, self-swaps (j_s == i_s) excluded
+    for_bucket_entries(P, sm, nch, n, [&](int32_t st, int l) {
+        if (st != ibase - l) atomicMax(&sm.M[l], st);
+    });
+    __syncthreads();
+    // D bits of the bucket, stored whole (a warp covers one word)
+    const int64_t w0 = (int64_t)b * kSWords;
+    const int64_t nw = (N + 31) / 32;
+    static_assert(kSWords % kSResThreads == 0, "one or more whole words per thread");
+    for (int w = tid; w < kSWords; w += kSResThreads) {
+        uint32_t word = 0u;
+        const int4 *m4 = reinterpret_cast<const int4 *>(sm.M + 32 * w);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+            const int4 x = m4[(v + w) & 7];   // rotated start: consecutive threads hit different banks
+            const int b = 4 * ((v + w) & 7);
+            word |= (uint32_t)(x.x >= 0) << b | (uint32_t)(x.y >= 0) << (b + 1) | (uint32_t)(x.z >= 0) << (b + 2) |
+                    (uint32_t)(x.w >= 0) << (b + 3);
+        }
+        if (w0 + w < nw) P.bitmap[w0 + w] = word;
+    }
+    // steps that are not the last to hit their target
+    for_bucket_entries(P, sm, nch, n, [&](int32_t st, int l) {
+        if (st != ibase - l && sm.M[l] != st) atomicOr(P.notlast + (st >> 5), 1u << (st & 31));
+    });
+}
+
+__global__ void __launch_bounds__(kSResThreads, 2) k_set_resolve(const PlanDev *plans, int n_plans, PlanLut lut,
+                                                                 int64_t nvb) {
+    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+        k_set_resolve_body(plans, n_plans, lut, vb);
+        __syncthreads();
+    }
+}
+
+// tail positions q >= z0 not hit by an earlier step: sampled iff !good(N-1-q).
+// A warp finishes kSTailWords bitmap words: every position's first link (D word,
+// rv, !last bit) is loaded up front, the second links of all positions that need
+// one (~1 in 8: the value came from another tail position) are loaded together,
+// and the rare deeper chains are followed one by one.
+__device__ __forceinline__ bool set_chain_good(const PlanDev &P, int64_t st) {
+    const int64_t N = P.n_elems, z0 = N - P.count;
+    while (true) {
+        const int64_t j = P.rv[st];
+        if (j == N - 1 - st) return false;                               // self-swap: the value stays
+        if ((P.notlast[st >> 5] >> (st & 31)) & 1u) return false;        // taken back into the tail later
+        if (j < z0) return true;                                         // carried down below the tail
+        st = N - 1 - j;
+    }
+}
+
+__device__ __forceinline__ void k_set_tail_body(const PlanDev *plans, int n_plans, PlanLut lut, int64_t vb) {
+    const PlanDev &P = plans[find_plan_by(plans, n_plans, lut.chain, vb, 2)];
+    const int64_t N = P.n_elems, z0 = N - P.count;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t w_first = (z0 >> 5) + ((vb - P.oblock0) * (kSTailThreads / 32) + warp) * kSTailWords;
+    const int64_t nw = (N + 31) >> 5;
+    uint32_t word[kSTailWords], nl[kSTailWords];
+    int32_t j[kSTailWords];
+#pragma unroll
+    for (int u = 0; u < kSTailWords; ++u) {
+        const int64_t w = w_first + u;
+        const int64_t q = (w << 5) + lane;
+        word[u] = 0u;
+        j[u] = -1;
+        nl[u] = 0u;
+        if (w < nw) {
+            word[u] = P.bitmap[w];
+            if (q >= z0 && q < N) {
+                const int64_t st = N - 1 - q;
+                j[u] = P.rv[st];
+                nl[u] = P.notlast[st >> 5] >> (st & 31);
+            }
+        }
+    }
+    // 0: settled not sampled, 1: sampled, 2: follow the value to tail position j
+    int state[kSTailWords];
+#pragma unroll
+    for (int u = 0; u < kSTailWords; ++u) {
+        const int64_t st = N - 1 - (((w_first + u) << 5) + lane);
+        state[u] = 0;
+        if (j[u] >= 0 && !((word[u] >> lane) & 1u)) {
+            if (j[u] == N - 1 - st || (nl[u] & 1u)) state[u] = 1;
+            else if (j[u] >= z0) state[u] = 2;
+        }
+    }
+    int32_t st2[kSTailWords];
+#pragma unroll
+    for (int u = 0; u < kSTailWords; ++u) {   // second links, loads issued together
+        st2[u] = (int32_t)(N - 1 - j[u]);      // the step that finalises tail position j
+        if (state[u] != 2) continue;
+        j[u] = P.rv[st2[u]];
+        nl[u] = P.notlast[st2[u] >> 5] >> (st2[u] & 31);
+    }
+#pragma unroll
+    for (int u = 0; u < kSTailWords; ++u) {
+        if (state[u] != 2) continue;
+        if (j[u] == N - 1 - st2[u] || (nl[u] & 1u)) state[u] = 1;
+        else if (j[u] < z0) state[u] = 0;
+        else state[u] = set_chain_good(P, N - 1 - j[u]) ? 0 : 1;
+    }
+#pragma unroll
+    for (int u = 0; u < kSTailWords; ++u) {
+        const int64_t w = w_first + u;
+        if (w >= nw) break;   // warp-uniform
+        const unsigned bits = __ballot_sync(0xffffffffu, state[u] == 1);
+        if (lane == 0 && bits) P.bitmap[w] = word[u] | bits;
+        // one sampled element for the Gaussian shift: step 0's output is its own target
+        if ((w << 5) + lane == N - 1) P.idx[0] = P.rv[0];
+    }
+}
+
+__global__ void __launch_bounds__(kSTailThreads) k_set_tail(const PlanDev *plans, int n_plans, PlanLut lut,
+                                                            int64_t nvb) {
+    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) k_set_tail_body(plans, n_plans, lut, vb);
+}
+
 struct PlanLayout {
     std::vector<PlanDev> dev;
     int64_t ws_bytes = 0;
-    int64_t draw_chunks = 0, step_blocks = 0;
+    int64_t step_blocks = 0;
     int64_t bchunks = 0, buckets = 0, oblocks = 0;   // bucket path (plans with bucketed = 1)
     int32_t *nchains = nullptr;                       // all bucket plans' chain counters (zeroed per call)
     std::vector<int32_t> lut_host;                    // [sort | bucket | chain] CTA-group -> plan tables
@@ -862,6 +1006,9 @@ struct PlanLayout {
     int32_t *walk_order = nullptr;            // k_walk: plans by decreasing step count
     std::vector<int32_t> walk_order_host;
     int n_bucketed = 0;
+    int setmode = 0;                                  // bucketed plans take the set-only path (k_set_*)
+    uint32_t *notlast = nullptr;                      // all set-mode plans' !last bits (zeroed per call)
+    int64_t notlast_words = 0;
     int64_t table_bytes = 0;
     char *table_base = nullptr;
     std::vector<int64_t> table_off;   // head-table plans, relative to table_base (contiguous)
@@ -872,7 +1019,7 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
     L.dev.resize(n);
     PlanDev *descs_dev = a.take<PlanDev>(n);
     (void)descs_dev;
-    int64_t chunk = 0, blocks = 0;
+    int64_t blocks = 0;
     static const bool no_bucket = std::getenv("EDGC_PLAN_HEADTABLE") != nullptr;
     for (int i = 0; i < n; ++i) {
         const edgc_plan_desc &d = plans[i];
@@ -891,23 +1038,53 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
         P.full_idx = (d.flags & EDGC_PLAN_BITMAP_ONLY) ? 0 : 1;
         P.tail = (d.n_elems > 10000 && d.count > d.n_elems / 20) ? 1 : 0;
         P.bucketed = (!no_bucket && P.tail && ceil_div(d.n_elems, kBSize) <= kBMaxBuckets) ? 1 : 0;
-        // expected rejections ~ count * N / 2^33 (threshold ~ uniform below rng+1)
-        const double lam = (double)d.count * (double)d.n_elems / 4294967296.0;
-        int64_t slack = (int64_t)(2.0 * lam + 16.0 * std::sqrt(lam + 1.0)) + 4096;
-        int64_t nd = d.count + slack;
-        nd = (nd + 3) & ~int64_t(3);
-        P.n_draws = nd;
-        P.draw_chunk0 = chunk;
-        chunk += ceil_div(nd / 2, kDrawsPerBlock);
         P.step_block0 = blocks;
         blocks += ceil_div(d.count, kStepThreads);
     }
-    L.draw_chunks = chunk;
     L.step_blocks = blocks;
+    // set mode when every bucketed plan is bitmap-only (the tracker's plans): the order-free resolve
+    static const bool no_set = std::getenv("EDGC_PLAN_NOSET") != nullptr;
+    L.setmode = no_set ? 0 : 1;
+    bool any_b = false;
+    for (int i = 0; i < n; ++i) {
+        if (!L.dev[i].bucketed) continue;
+        any_b = true;
+        if (L.dev[i].full_idx || L.dev[i].bitmap == nullptr) L.setmode = 0;
+    }
+    if (!any_b) L.setmode = 0;
+    if (L.setmode) {
+        int64_t words = 0;
+        for (int i = 0; i < n; ++i)
+            if (L.dev[i].bucketed) words += align256(4 * ceil_div(L.dev[i].count, 32)) / 4;
+        L.notlast = a.take<uint32_t>(words);
+        L.notlast_words = words;
+        int64_t wo = 0;
+        for (int i = 0; i < n; ++i) {
+            PlanDev &P = L.dev[i];
+            if (!P.bucketed) continue;
+            P.setmode = 1;
+            P.notlast = L.notlast ? L.notlast + wo : nullptr;
+            wo += align256(4 * ceil_div(P.count, 32)) / 4;
+        }
+    }
     for (int i = 0; i < n; ++i) {
         PlanDev &P = L.dev[i];
-        P.draws = a.take<uint32_t>(P.n_draws);
         P.rv = a.take<int32_t>(P.count);
+        if (P.setmode) {
+            P.nb = (int32_t)ceil_div(P.n_elems, kSSize);
+            P.nch = (int32_t)ceil_div(P.count, kSChunk);
+            P.lst_pk = a.take<uint32_t>(P.count);
+            P.segoff = a.take<int32_t>((int64_t)P.nch * (P.nb + 1));
+            P.chunk0 = L.bchunks;
+            L.bchunks += P.nch;
+            P.bucket0 = L.buckets;
+            L.buckets += P.nb;
+            P.oblock0 = L.oblocks;
+            const int64_t z0 = P.n_elems - P.count;
+            L.oblocks += ceil_div(ceil_div(P.n_elems, 32) - (z0 >> 5), (int64_t)(kSTailThreads / 32) * kSTailWords);
+            ++L.n_bucketed;
+            continue;
+        }
         if (!P.bucketed) {
             // zero-width ranges at the running offsets keep the CTA -> plan searches monotone
             P.chunk0 = L.bchunks;
@@ -1031,40 +1208,19 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
         if (plan_short) return (unsigned)std::max<int64_t>(1, nvb);
         return (unsigned)std::max<int64_t>(1, std::min<int64_t>(nvb, (int64_t)plan_sms * per_sm));
     };
-    k_draws<<<capped(L.draw_chunks, 8), kP1Threads, 0, st>>>(d_plans, n_plans, L.draw_chunks);
-    EDGC_LAUNCH_CHECK();
+    // every plan's status is OK (the walk generates its own draws; kept for the ABI)
+    EDGC_CUDA_TRY(cudaMemsetAsync(status_dev, 0, 4 * (size_t)n_plans, st));
+    EDGC_CUDA_TRY(cudaMemcpyAsync(L.walk_order, L.walk_order_host.data(), 4 * (size_t)n_plans,
+                                  cudaMemcpyHostToDevice, st));
     static bool walk_attr = false;
     if (!walk_attr) {
         EDGC_CUDA_TRY(cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(kWG * sizeof(WalkGroup))));
+                                           (int)(kWalkPlans * sizeof(WalkRing))));
         walk_attr = true;
     }
-    {
-        // The walk holds one SM per 4 plans for its whole (latency-bound) run.  It is launched in
-        // thread-block clusters (EDGC_WALK_CLUSTER, default 4) so those SMs sit together in a few
-        // GPCs instead of one in every GPC, leaving whole GPCs to the step's cluster-launched pass 1.
-        static const int wc = [] {
-            const char *e = std::getenv("EDGC_WALK_CLUSTER");
-            return e ? std::max(1, std::min(8, std::atoi(e))) : 4;   // measured: 8.99 (1), 8.89 (4), 8.92 (8) ms/step
-        }();
-        const int nb = (int)ceil_div(n_plans, kWG);
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        cfg.gridDim = dim3((unsigned)(ceil_div(nb, wc) * wc));
-        cfg.blockDim = dim3(kWT * kWG);
-        cfg.dynamicSmemBytes = kWG * sizeof(WalkGroup);
-        cfg.stream = st;
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = wc;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = wc > 1 ? 1 : 0;
-        EDGC_CUDA_TRY(cudaMemcpyAsync(L.walk_order, L.walk_order_host.data(), 4 * (size_t)n_plans,
-                                      cudaMemcpyHostToDevice, st));
-        EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_walk, (const PlanDev *)d_plans, n_plans, status_dev,
-                                         (const int32_t *)L.walk_order));
-    }
+    k_walk<<<(unsigned)ceil_div(n_plans, kWalkPlans), kWalkThreads, kWalkPlans * sizeof(WalkRing), st>>>(
+        d_plans, n_plans, (const int32_t *)L.walk_order);
+    EDGC_LAUNCH_CHECK();
     if (L.n_bucketed) {
         // bucket path (tail-shuffle plans); plans are ordered, so each kernel's CTA range covers
         // only the bucketed plans' chunks / buckets / chain blocks
@@ -1080,14 +1236,34 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
         EDGC_CUDA_TRY(cudaMemcpyAsync(L.lut_dev, L.lut_host.data(), 4 * L.lut_host.size(), cudaMemcpyHostToDevice,
                                       st));
         const PlanLut lut{L.lut_dev, L.lut_dev + L.lut_n[0], L.lut_dev + L.lut_n[0] + L.lut_n[1]};
-        k_bucket_sort<<<capped(L.bchunks, 1), kBSortThreads, sizeof(BSortSmem), st>>>(d_plans, n_plans, lut,
-                                                                                      L.bchunks);
-        EDGC_LAUNCH_CHECK();
-        k_bucket_resolve<<<capped(L.buckets, 2), kBResThreads, sizeof(BResSmem), st>>>(d_plans, n_plans, lut,
-                                                                                       status_dev, L.buckets);
-        EDGC_LAUNCH_CHECK();
-        k_bucket_chain<<<capped(L.oblocks, 8), kStepThreads, 0, st>>>(d_plans, n_plans, lut, L.oblocks);
-        EDGC_LAUNCH_CHECK();
+        if (L.setmode) {
+            static bool sattr = false;
+            if (!sattr) {
+                EDGC_CUDA_TRY(cudaFuncSetAttribute(k_set_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)sizeof(SSortSmem)));
+                EDGC_CUDA_TRY(cudaFuncSetAttribute(k_set_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)sizeof(SResSmem)));
+                sattr = true;
+            }
+            EDGC_CUDA_TRY(cudaMemsetAsync(L.notlast, 0, 4 * (size_t)L.notlast_words, st));
+            k_set_sort<<<capped(L.bchunks, 1), kSSortThreads, sizeof(SSortSmem), st>>>(d_plans, n_plans, lut,
+                                                                                        L.bchunks);
+            EDGC_LAUNCH_CHECK();
+            k_set_resolve<<<capped(L.buckets, 2), kSResThreads, sizeof(SResSmem), st>>>(d_plans, n_plans, lut,
+                                                                                        L.buckets);
+            EDGC_LAUNCH_CHECK();
+            k_set_tail<<<capped(L.oblocks, 8), kSTailThreads, 0, st>>>(d_plans, n_plans, lut, L.oblocks);
+            EDGC_LAUNCH_CHECK();
+        } else {
+            k_bucket_sort<<<capped(L.bchunks, 1), kBSortThreads, sizeof(BSortSmem), st>>>(d_plans, n_plans, lut,
+                                                                                          L.bchunks);
+            EDGC_LAUNCH_CHECK();
+            k_bucket_resolve<<<capped(L.buckets, 2), kBResThreads, sizeof(BResSmem), st>>>(
+                d_plans, n_plans, lut, status_dev, L.buckets);
+            EDGC_LAUNCH_CHECK();
+            k_bucket_chain<<<capped(L.oblocks, 8), kStepThreads, 0, st>>>(d_plans, n_plans, lut, L.oblocks);
+            EDGC_LAUNCH_CHECK();
+        }
     }
     // head-table path (Floyd plans, N > 2^25, or EDGC_PLAN_HEADTABLE): index + resolve groups of
     // consecutive such plans whose tables, links and bounded values fit in L2 together

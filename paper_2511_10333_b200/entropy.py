@@ -107,8 +107,8 @@ def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, work
     tracker build the next sampled iteration's plans on a side stream;
     ``check=False`` skips the synchronising status check (the caller checks
     ``status`` later).  ``indices=False`` (with ``bitmaps``) builds only the
-    membership sets: each returned index tensor then holds just the first
-    sample (the Gaussian estimator's shift).
+    membership sets: each returned index tensor then holds one sampled
+    element (the Gaussian estimator's shift; see EDGC_PLAN_BITMAP_ONLY).
     """
     if not indices and not bitmaps:
         raise ValueError("indices=False needs bitmaps=True")

@@ -81,7 +81,7 @@ def test_native_library_is_loaded():
 @pytest.mark.parametrize("indices", [True, False])
 def test_membership_bitmaps_match_oracle_sets(indices):
     """Membership bitmaps (full plans and EDGC_PLAN_BITMAP_ONLY plans) equal the oracle's
-    sampled sets; bitmap-only plans still return the first sample (the Gaussian shift).
+    sampled sets; bitmap-only plans still return one sampled element (the Gaussian shift).
     Includes a matrix spanning many 16K-position buckets and Floyd / tail branches."""
     from paper_2511_10333_b200.entropy import sample_count, sample_plans
     specs = [(n, sample_count(n, b), s) for n, b, s in [
@@ -100,4 +100,7 @@ def test_membership_bitmaps_match_oracle_sets(indices):
         if indices:
             assert np.array_equal(got, ref)
         else:
-            assert got.size == 1 and got[0] == ref[0]
+            # bitmap-only: one sampled element (the Gaussian shift) -- Floyd plans give NumPy's first
+            # sample, tail-shuffle plans (set-mode resolve) step 0's output, NumPy's last sample
+            tail = n > 10000 and c > n // 20
+            assert got.size == 1 and got[0] == (ref[-1] if tail else ref[0])

@@ -1,8 +1,9 @@
-"""CPU: the device sample-plan ALGORITHM (csrc/sample_plan.cu phases P2-P4),
-emulated step for step in Python on the oracle's u32 stream, against NumPy.
+"""CPU: the device sample-plan ALGORITHM (csrc/sample_plan.cu), emulated step
+for step in Python on the oracle's u32 stream, against NumPy.
 
-This pins the parallel decomposition (walk with first-rejection windows, hash
-lists, tail-shuffle chains, Floyd collision chains) independently of the GPU.
+This pins the parallel decomposition (the warp walk with first-rejection chunks,
+hash lists, tail-shuffle chains, Floyd collision chains, and the order-free
+set-mode resolve) independently of the GPU.
 """
 
 import math
@@ -23,42 +24,31 @@ def lemire(x, rng):
     return left >= thr, val
 
 
-def walk(seed, n_elems, count, window=64, K=8):
-    """k_walk: bounded value of every step (speculative shifts, first-rejection windows)."""
+def walk(seed, n_elems, count, chunk=128):
+    """k_walk: bounded value of every step.  A warp takes `chunk` consecutive steps against
+    consecutive draws; the chunk ends at its first Lemire rejection, whose draw is skipped."""
     tail = n_elems > 10000 and count > n_elems // 20
-    draws = oracle.pcg64_u32(seed, count + 4096 + 2 * count).astype(np.int64)
+    draws = oracle.pcg64_u32(seed, 2 * count + 4096).astype(np.int64)
     step_rng = (lambda s: n_elems - 1 - s) if tail else (lambda s: n_elems - count + s)
     rv = [0] * count
-    s = u = 0
-    while s < count:                      # k_walk (speculative shifts 0..K-1)
-        nvalid = min(window, count - s)
-        vals = [[0] * window for _ in range(K)]
-        rej = [[False] * window for _ in range(K)]
-        for lane in range(nvalid):
-            for j in range(K):
-                ok, v = lemire(int(draws[u + lane + j]), step_rng(s + lane))
-                vals[j][lane], rej[j][lane] = v, not ok
-        cur, d, events, length = 0, 0, [], nvalid
-        while True:
-            f = next((l for l in range(cur, nvalid) if rej[d][l]), None)
-            if f is None:
+    s = k = 0
+    while s < count:
+        adv, skip = min(chunk, count - s), 0
+        vals = []
+        for lane in range(adv):
+            ok, v = lemire(int(draws[k + lane]), step_rng(s + lane))
+            if not ok:
+                adv, skip = lane, 1
                 break
-            events.append(f)
-            d += 1
-            if d == K:
-                length = f
-                break
-            cur = f
-        for lane in range(length):
-            sh = sum(1 for e in events if e <= lane)
-            rv[s + lane] = vals[sh][lane]
-        s += length
-        u += length + len(events)
+            vals.append(v)
+        rv[s:s + adv] = vals[:adv]
+        s += adv
+        k += adv + skip
     return rv, tail
 
 
-def emulate(seed, n_elems, count, window=64, K=8):
-    rv, tail = walk(seed, n_elems, count, window, K)
+def emulate(seed, n_elems, count, chunk=128):
+    rv, tail = walk(seed, n_elems, count, chunk)
     lists = {}                            # k_index (hash lists)
     for st in range(count):
         lists.setdefault(rv[st], []).append(st)
@@ -97,16 +87,16 @@ def emulate(seed, n_elems, count, window=64, K=8):
     return np.asarray(out, dtype=np.int64)
 
 
-@pytest.mark.parametrize("window,K", [(64, 8), (7, 4), (2048, 8)])
+@pytest.mark.parametrize("chunk", [128, 32, 7, 1])
 @pytest.mark.parametrize("n_elems,beta,seed", [
     (100, 0.5, 3), (101, 0.9, 1), (4096, 0.25, 1), (10000, 0.5, 4), (10001, 0.06, 4), (12000, 0.25, 5),
     (20000, 0.05, 9), (20000, 0.0501, 11), (40000, 0.999, 2), (7, 0.3, 5), (2, 0.5, 0), (300, 0.99, 8)])
-def test_plan_algorithm_matches_numpy(n_elems, beta, seed, window, K):
+def test_plan_algorithm_matches_numpy(n_elems, beta, seed, chunk):
     count = min(n_elems, math.ceil(beta * n_elems))
     if count == n_elems:
         pytest.skip("copy branch")
     ref = np.random.default_rng(seed).choice(n_elems, size=count, replace=False, shuffle=False)
-    assert np.array_equal(emulate(seed, n_elems, count, window, K), ref)
+    assert np.array_equal(emulate(seed, n_elems, count, chunk), ref)
 
 
 def resolve_buckets(rv, n_elems, count, tail, bbits, order_seed=0):
@@ -193,3 +183,85 @@ def test_lemire_threshold_fast_path():
     for x in xs:
         x = int(x)
         assert lemire_threshold(x) == (2**32 - x) % x, x
+
+
+def sequential_rv(seed, n_elems, count):
+    """Tail-shuffle bounded values j_s in step order (NumPy's sequential Lemire loop, vectorised
+    between rejections): the walk's output, whose chunked form test_plan_algorithm_matches_numpy pins."""
+    draws = oracle.pcg64_u32(seed, count + 8192 + count // 64).astype(np.uint64)
+    excl = (n_elems - np.arange(count, dtype=np.uint64))          # i + 1 for step s
+    rv = np.empty(count, dtype=np.int64)
+    s = u = 0
+    while s < count:
+        k = min(count - s, 1 << 16)
+        m = draws[u:u + k] * excl[s:s + k]
+        left = m & np.uint64(0xFFFFFFFF)
+        thr = (np.uint64(1 << 32) - excl[s:s + k]) % excl[s:s + k]
+        bad = np.flatnonzero(left < thr)
+        take = k if bad.size == 0 else int(bad[0])
+        rv[s:s + take] = (m[:take] >> np.uint64(32)).astype(np.int64)
+        s += take
+        u += take + (0 if bad.size == 0 else 1)
+    return rv.tolist()
+
+
+def resolve_set(rv, n_elems, count, sbits):
+    """k_set_sort / k_set_resolve / k_set_tail: the membership set of a tail-shuffle plan without
+    NumPy's order.  Buckets of 2^sbits positions hold the packed (step in chunk, position) entries
+    of every sort chunk; each computes M (latest non-self step per position) in any entry order,
+    stores its D bits and marks the !last steps; the tail pass finishes positions >= z0."""
+    chunk = 1 << sbits
+    z0 = n_elems - count
+    nb = -(-n_elems // chunk)
+    bits = np.zeros(n_elems, dtype=np.uint8)
+    notlast = np.zeros(count, dtype=bool)
+    segs = [[] for _ in range(nb)]       # bucket b: (chunk, packed entry) of every sort chunk
+    for i in range(count):                # k_set_sort: one chunk of steps per CTA
+        c = i // chunk
+        segs[rv[i] >> sbits].append((c, ((i - c * chunk) << sbits) | (rv[i] & (chunk - 1))))
+    rng = np.random.default_rng(sbits)
+    for b in range(nb):                   # k_set_resolve: one CTA per bucket
+        ents = [(c * chunk + (e >> sbits), e & (chunk - 1)) for c, e in segs[b]]
+        ents = [ents[k] for k in rng.permutation(len(ents))]   # atomics: any order
+        ibase = n_elems - 1 - (b << sbits)
+        M = {}
+        for st, l in ents:
+            if st != ibase - l:
+                M[l] = max(M.get(l, -1), st)
+        for l in M:
+            bits[(b << sbits) + l] = 1
+        for st, l in ents:
+            if st != ibase - l and M[l] != st:
+                notlast[st] = True
+    for q in range(z0, n_elems):          # k_set_tail
+        if bits[q]:
+            continue
+        s, good = n_elems - 1 - q, False
+        while True:
+            j = rv[s]
+            if j == n_elems - 1 - s or notlast[s]:
+                break
+            if j < z0:
+                good = True
+                break
+            s = n_elems - 1 - j
+        if not good:
+            bits[q] = 1
+    return bits
+
+
+@pytest.mark.parametrize("sbits", [2, 5, 15])
+@pytest.mark.parametrize("n_elems,beta,seed", [
+    (10001, 0.06, 4), (12000, 0.25, 5), (20000, 0.0501, 11), (40000, 0.999, 2), (65536, 0.25, 13),
+    (262144, 0.5, 8), (30000, 0.75, 1)])
+def test_set_resolve_matches_numpy_set(n_elems, beta, seed, sbits):
+    count = min(n_elems, math.ceil(beta * n_elems))
+    rv = sequential_rv(seed, n_elems, count)
+    assert n_elems > 10000 and count > n_elems // 20
+    ref = np.random.default_rng(seed).choice(n_elems, size=count, replace=False, shuffle=False)
+    want = np.zeros(n_elems, dtype=np.uint8)
+    want[ref] = 1
+    got = resolve_set(rv, n_elems, count, sbits)
+    assert np.array_equal(got, want)
+    assert int(got.sum()) == count
+    assert ref[-1] == rv[0]                # the bitmap-only plan's shift sample: step 0's own target

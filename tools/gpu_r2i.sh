@@ -1,0 +1,10 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_sampling.py tests/test_gpu_fused_entropy.py tests/test_gpu_ranks.py -x -q -p no:cacheprovider > gpurun_out/i_pytest.log 2>&1
+echo "pytest exit $?" >> gpurun_out/i_pytest.log
+timeout 120 python tools/plan_prof.py --reps 5 > gpurun_out/i_plan_set.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  --csv --log-file gpurun_out/i_plan_ncu.csv python tools/plan_prof.py --reps 1 > gpurun_out/i_plan_ncu.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_set_resolve|k_set_tail|k_walk" -c 3 \
+  -o gpurun_out/i_plan_full -f python tools/plan_prof.py --reps 1 > gpurun_out/i_ncu.log 2>&1
+exit 0
