@@ -39,7 +39,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-TF32_PEAK = 1100.0   # TFLOP/s dense, B200_PROFILING.md (no measured tf32 figure)
+TF32_FALLBACK = 1100.0   # TFLOP/s dense, B200_PROFILING.md (used only if the measurement fails)
 METRIC = "EDGC grad GB/s (entropy+compress+AR+decompress) @1/2/4/8 B200; % HBM roofline"
 UNIT = "GB/s"
 SMI_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -82,6 +82,33 @@ def load_peak():
             return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def measure_tf32_peak(dev, n: int = 8192, reps: int = 10):
+    """Dense TF32 tensor-core throughput measured here: cuBLAS fp32 GEMM with TF32 math, n^3.
+
+    MEASURED_PEAKS.json carries HBM and bf16 figures only; the wide path's roofline is TF32.
+    """
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    try:
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        for _ in range(3):
+            a @ b
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            a @ b
+        e1.record()
+        torch.cuda.synchronize(dev)
+        tf = 2.0 * n ** 3 * reps / (e0.elapsed_time(e1) / 1e3) / 1e12
+        return tf, f"measured here: cuBLAS TF32 GEMM {n}^3, mean of {reps} back-to-back launches"
+    except Exception as exc:   # pragma: no cover
+        return TF32_FALLBACK, f"fallback (B200_PROFILING.md; measurement failed: {exc})"
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
 
 
 def load_traffic(kernel: str):
@@ -331,6 +358,16 @@ def run_ours(args):
     for mk in ev["marks"]:
         for i, n in enumerate(names):
             ph[n] += mk[i].elapsed_time(mk[i + 1]) / len(ev["marks"])
+    # sampled vs other steps (timed step t = warmup + i): pass 1 and whole-step device time
+    starts_all = [mk[0] for mk in ev["marks"]] + [stop]
+    samp = {"pass1": [], "step": []}
+    rest = {"pass1": [], "step": []}
+    for i, mk in enumerate(ev["marks"]):
+        dst = samp if (args.warmup + i) % period == 0 else rest
+        dst["pass1"].append(mk[0].elapsed_time(mk[1]))
+        dst["step"].append(starts_all[i].elapsed_time(starts_all[i + 1]))
+    ph["sampled_steps_ms"] = {k: statistics.mean(v) for k, v in samp.items() if v}
+    ph["other_steps_ms"] = {k: statistics.mean(v) for k, v in rest.items() if v}
     ent_ms = [a.elapsed_time(b) for a, b in ev["ent"]]
     ph["entropy_per_sampled_step"] = statistics.mean(ent_ms) if ent_ms else 0.0
     ph["entropy_sampled_steps"] = len(ent_ms)
@@ -354,10 +391,10 @@ def run_ours(args):
         tfl = {"pass1": 3 * 4.0 * total * args.rank, "pass2_finalize": 3 * 2.0 * total * args.rank,
                "reconstruct": 3 * 2.0 * total * args.rank * world}
         tdom = max(tfl, key=lambda k: ph[k])
+        tf32_peak, tf32_src = measure_tf32_peak(dev)
         tensor = {"bound": "tensor", "kernel": tdom, "achieved": tfl[tdom] / (ph[tdom] / 1e3) / 1e12,
-                  "peak": TF32_PEAK, "unit": "TFLOP/s", "frac": tfl[tdom] / (ph[tdom] / 1e3) / 1e12 / TF32_PEAK,
-                  "traffic": None, "flop_per_launch": tfl[tdom],
-                  "peak_source": "B200_PROFILING.md fallback (tf32 dense 1.1 PFLOP/s; MEASURED_PEAKS.json has bf16 only)",
+                  "peak": tf32_peak, "unit": "TFLOP/s", "frac": tfl[tdom] / (ph[tdom] / 1e3) / 1e12 / tf32_peak,
+                  "traffic": None, "flop_per_launch": tfl[tdom], "peak_source": tf32_src,
                   "flop_accounting": "tensor-core FLOP incl. the 3xTF32 split (3 MMAs per fp32 product)"}
     n_sampled = len(ent_ms)
     ent_bytes = 4.0 * sum(sample_count(m * n, args.beta) for m, n in shapes) * n_sampled / max(1, args.steps)

@@ -512,6 +512,20 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
         };
         float4 pcur[kTRB];
         load_pres(0, pcur);
+        // membership bits of a round's 4 x 4 elements, loaded a round ahead (like p_res): a load
+        // consumed in its own round would stall every round on a global round trip
+        auto load_bits = [&](int bb, uint32_t (&sw)[kTRB]) {
+            const int64_t r0 = t.row0 + (int64_t)bb * kTRB;
+            const int nrow = (int)min((int64_t)kTRB, t.row1 - r0);   // <= 0 past the strip
+#pragma unroll
+            for (int rr = 0; rr < kTRB; ++rr) {
+                const int lr = rr ^ fr;
+                const int64_t e = (r0 + lr) * n + col0;   // 4-aligned: the 4 bits share a word
+                sw[rr] = (active && lr < nrow) ? (__ldg(sbits + (e >> 5)) >> (e & 31)) & 0xFu : 0u;
+            }
+        };
+        uint32_t swcur[kTRB] = {0u, 0u, 0u, 0u};
+        if (SAMPLE && sbits) load_bits(0, swcur);
 #pragma unroll 1
         for (int b = 0; b < nrounds; ++b) {
             const int s = b % kTStages, q = b % kTRing;
@@ -519,17 +533,13 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             const int rows = (int)min((int64_t)kTRB, t.row1 - i0);
             float4 pnext[kTRB];
             load_pres(b + 1, pnext);
+            uint32_t swnext[kTRB] = {0u, 0u, 0u, 0u};
+            if (SAMPLE && sbits) load_bits(b + 1, swnext);
             if (chunk_cols > 0) ptx::mbar_wait_sleep<EDGC_CONS_SLEEP>(&sm.full[s], (b / kTStages) & 1);
             if (EDGC_P1_EARLYZ && !EDGC_P1_NOEXCH && b >= kTLag) consume(b - kTLag);
             uint32_t sw[kTRB];
-            if (SAMPLE && sbits) {
 #pragma unroll
-                for (int rr = 0; rr < kTRB; ++rr) {
-                    const int lr = rr ^ fr;
-                    const int64_t e = (i0 + lr) * n + col0;   // 4-aligned: the 4 bits share a word
-                    sw[rr] = (active && lr < rows) ? (__ldg(sbits + (e >> 5)) >> (e & 31)) & 0xFu : 0u;
-                }
-            }
+            for (int rr = 0; rr < kTRB; ++rr) sw[rr] = swcur[rr];
             double acc[kTV];
 #pragma unroll
             for (int rr = 0; rr < kTRB; ++rr) {
@@ -588,7 +598,10 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass1t(const MatDev *mats, con
             ptx::named_bar_arrive(2 + q, kTCons + 32);   // hand red[q] to the exchange warp
             if (!EDGC_P1_EARLYZ && !EDGC_P1_NOEXCH && b >= kTLag) consume(b - kTLag);
 #pragma unroll
-            for (int rr = 0; rr < kTRB; ++rr) pcur[rr] = pnext[rr];
+            for (int rr = 0; rr < kTRB; ++rr) {
+                pcur[rr] = pnext[rr];
+                swcur[rr] = swnext[rr];
+            }
         }
         if (EDGC_P1_MEMONLY || EDGC_P1_NOEXCH) goto done;
         for (int bb = max(0, nrounds - kTLag); bb < nrounds; ++bb) consume(bb);

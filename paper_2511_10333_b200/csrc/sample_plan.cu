@@ -125,73 +125,87 @@ __device__ __forceinline__ uint32_t lemire_threshold(uint32_t excl) {
 // and compare per step, one ballot per chunk -- and when a step rejects, the chunk
 // ends at the first rejecting step (in step order), whose draw is skipped.
 // Generating the draws is most of the arithmetic (a 128-bit LCG step per two
-// draws) and does not depend on the walk, so kWalkProd producer warps per plan
-// fill a shared ring of kWalkBlk-draw blocks ahead of the walker (smem counters,
-// no HBM draw buffer).  kWalkPlans plans share a CTA.
-constexpr int kWalkPlans = 8;               // plans per CTA
-constexpr int kWalkProd = 2;                // producer warps per plan
-constexpr int kWalkQ = 4;                   // steps per walker lane per chunk
+// draws) and does not depend on the walk, so a producer warp per plan fills a
+// shared ring of kWalkBlk-draw blocks ahead of the walker (smem counters, no HBM
+// draw buffer).  kWalkPlans plans share a CTA.
+constexpr int kWalkPlans = 16;              // plans per CTA (a walker and a producer warp each)
+constexpr int kWalkQ = 8;                   // steps per walker lane per chunk
 constexpr int kWalkChunk = 32 * kWalkQ;
-constexpr int kWalkBlk = 1024;              // draws per ring block
+constexpr int kWalkMaxRej = 8;              // rejections settled inside one chunk (ring lookahead)
+constexpr int kWalkBlk = 512;               // draws per ring block
 constexpr int kWalkNBlk = 4;                // ring blocks
 constexpr int kWalkRing = kWalkBlk * kWalkNBlk;
-constexpr int kWalkWarpsPer = 1 + kWalkProd;
-constexpr int kWalkThreads = 32 * kWalkWarpsPer * kWalkPlans;
-static_assert(kWalkBlk % (64 * kWalkProd) == 0, "whole outputs per producer lane");
-static_assert(kWalkChunk <= kWalkBlk, "a chunk spans at most two blocks");
-static_assert(kWalkPlans <= 15, "one named barrier per plan group");
+constexpr int kWalkThreads = 64 * kWalkPlans;
+static_assert(kWalkBlk % 64 == 0, "whole outputs per producer lane");
+static_assert(kWalkChunk + kWalkMaxRej <= kWalkBlk, "a chunk spans at most two blocks");
 
 struct alignas(16) WalkRing {
     uint32_t d[kWalkRing];
-    volatile int produced;   // blocks written
-    volatile int consumed;   // blocks the walker is done with
+    uint64_t full[kWalkNBlk];    // producer -> walker: block written
+    uint64_t empty[kWalkNBlk];   // walker -> producer: block consumed
     volatile int done;
 };
 
+// mbarrier probe that suspends the thread up to the hint (ns) while the phase is pending
+__device__ __forceinline__ bool walk_try_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 2000;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(ptx::smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void walk_wait(uint64_t *bar, uint32_t parity) {
+    while (!walk_try_wait(bar, parity)) {
+    }
+}
+
 __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int n_plans, const int32_t *order) {
     extern __shared__ __align__(16) unsigned char walk_raw[];
-    const int g = threadIdx.x / (32 * kWalkWarpsPer);        // plan group in the CTA
-    const int wg = (threadIdx.x / 32) % kWalkWarpsPer;       // 0: walker, 1..: producers
+    const int g = threadIdx.x >> 6;                 // plan group in the CTA
+    const bool producer = (threadIdx.x >> 5) & 1;
     const int lane = threadIdx.x & 31;
     const int slot = blockIdx.x * kWalkPlans + g;
     WalkRing &R = reinterpret_cast<WalkRing *>(walk_raw)[g];
-    if (threadIdx.x % (32 * kWalkWarpsPer) == 0) { R.produced = 0; R.consumed = 0; R.done = 0; }
+    if ((threadIdx.x & 63) == 0) {
+        for (int i = 0; i < kWalkNBlk; ++i) {
+            ptx::mbar_init(&R.full[i], 1);
+            ptx::mbar_init(&R.empty[i], 1);
+        }
+        R.done = 0;
+    }
     __syncthreads();
     if (slot >= n_plans) return;   // whole group leaves (groups synchronise only among themselves)
     const PlanDev &P = plans[order[slot]];
     const uint32_t count = (uint32_t)P.count;
-    if (wg > 0) {
-        // producer: lane pl (of 32 * kWalkProd) writes outputs o = blk * kWalkBlk / 2 + pl + 32 kWalkProd t
-        const int pl = (wg - 1) * 32 + lane;
-        constexpr int kStride = 32 * kWalkProd;                 // outputs between a lane's consecutive ones
-        constexpr int kPer = kWalkBlk / 2 / kStride;            // outputs per lane per block
-        u128 st = pcg_jump(P.state, P.inc, (uint64_t)pl + 1u);  // state after output pl
+    if (producer) {
+        // lane l writes outputs o = blk * kWalkBlk / 2 + l + 32 t of each block
+        constexpr int kPer = kWalkBlk / 64;                        // outputs per lane per block
+        u128 st = pcg_jump(P.state, P.inc, (uint64_t)lane + 1u);   // state after output `lane`
         u128 a, c;
-        pcg_affine(P.inc, kStride, a, c);
-        for (int blk = 0;; ++blk) {
-            // exit only where every producer warp decides alike: once done is set the walker's
-            // consumed count is final, so re-reading it gives all of them the same answer
-            bool stop = false;
-            while (blk - R.consumed >= kWalkNBlk) {
-                if (R.done) {
-                    stop = blk - R.consumed >= kWalkNBlk;
-                    break;
+        pcg_affine(P.inc, 32, a, c);
+        for (uint32_t blk = 0;; ++blk) {
+            const uint32_t sl = blk % kWalkNBlk;
+            // block blk - kWalkNBlk handed back?  The walker may finish first: it only sets done
+            if (blk >= kWalkNBlk)
+                while (!walk_try_wait(&R.empty[sl], ((blk / kWalkNBlk) - 1) & 1)) {
+                    if (R.done) return;
+                    __nanosleep(1000);   // try_wait suspends only ~0.1 us: back off so the walkers issue
                 }
-                __nanosleep(256);
-            }
-            if (stop) return;
-            uint2 *dst = reinterpret_cast<uint2 *>(R.d + (blk % kWalkNBlk) * kWalkBlk);
-#pragma unroll 4
+            if (R.done) return;
+            uint2 *dst = reinterpret_cast<uint2 *>(R.d + sl * kWalkBlk);
+#pragma unroll
             for (int t = 0; t < kPer; ++t) {
                 const uint64_t v = pcg_output(st);
                 st = a * st + c;
-                dst[pl + kStride * t] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
+                dst[lane + 32 * t] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
             }
-            ptx::named_bar_sync(1 + g, 32 * kWalkProd);   // the producers of this plan
-            if (pl == 0) {
-                __threadfence_block();
-                R.produced = blk + 1;
-            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&R.full[sl]);   // release: the block's writes before the arrival
         }
     }
     // walker
@@ -199,54 +213,63 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int
     // excl = rng + 1 of step s: tail i + 1 = N - s; Floyd j + 1 = N - count + s + 1
     const uint32_t e0 = tail ? (uint32_t)P.n_elems : (uint32_t)(P.n_elems - P.count + 1);
     int32_t *rv = P.rv;
-    uint32_t s = 0, k = 0;   // next step, next draw (N < 2^31)
-    int have = 0;            // blocks known to be produced
+    uint32_t s = 0, k = 0;       // next step, next draw (N < 2^31)
+    uint32_t have = 0, freed = 0; // blocks waited for / handed back
     while (s < count) {
-        const int need = (int)((k + kWalkChunk + kWalkBlk - 1) / kWalkBlk);
-        if (have < need) {
-            // refresh the producers' count (once per block); the fence pairs with theirs -- it also
-            // waits for this warp's outstanding rv stores, so it must not run every chunk
-            do {
-                have = R.produced;
-                if (have < need) __nanosleep(32);
-            } while (have < need);
-            __threadfence_block();
-        }
+        const uint32_t need = (k + kWalkChunk + kWalkMaxRej + kWalkBlk) / kWalkBlk;
+        for (; have < need; ++have) walk_wait(&R.full[have % kWalkNBlk], (have / kWalkNBlk) & 1);
+        const uint32_t base = s + lane;
         uint64_t m[kWalkQ];
-        bool any = false;
+        uint32_t excl[kWalkQ];
+        uint32_t cm = 0;   // bit q: step base + 32 q is a rejection candidate
 #pragma unroll
         for (int q = 0; q < kWalkQ; ++q) {
-            const uint32_t sl = s + lane + 32 * q;
-            const uint32_t excl = tail ? e0 - sl : e0 + sl;
-            m[q] = (uint64_t)R.d[(k + lane + 32 * q) & (kWalkRing - 1)] * excl;
-            any |= sl < count && (uint32_t)m[q] < excl;   // necessary for a rejection
+            excl[q] = tail ? e0 - base - 32 * q : e0 + base + 32 * q;
+            m[q] = (uint64_t)R.d[(k + lane + 32 * q) & (kWalkRing - 1)] * excl[q];
+            cm |= (uint32_t)(base + 32 * q < count && (uint32_t)m[q] < excl[q]) << q;
         }
-        uint32_t adv = min((uint32_t)kWalkChunk, count - s), skip = 0;
-        if (__ballot_sync(0xffffffffu, any)) {
-#pragma unroll
-            for (int q = 0; q < kWalkQ; ++q) {
-                const uint32_t sl = s + lane + 32 * q;
-                const uint32_t excl = tail ? e0 - sl : e0 + sl;
-                const bool rej = sl < count && (uint32_t)m[q] < excl && (uint32_t)m[q] < lemire_threshold(excl);
-                const unsigned rb = __ballot_sync(0xffffffffu, rej);
-                if (rb && !skip) {
-                    adv = min(adv, 32u * q + __ffs(rb) - 1);   // steps before the first rejection keep their draws
-                    skip = 1;
+        const uint32_t len = min((uint32_t)kWalkChunk, count - s);
+        uint32_t adv = len, shift = 0, skip = 0;   // shift: rejections so far in this chunk
+        if (__ballot_sync(0xffffffffu, cm != 0)) {
+            // settle rejections in step order: from the first rejecting step f on, every step
+            // moves to the next draw (f itself retries) and is tested again
+            uint32_t from = 0;
+            while (true) {
+                uint32_t first = 0xFFFFFFFFu;
+                for (uint32_t c = cm; c; c &= c - 1) {   // candidates in step order
+                    const int q = __ffs(c) - 1;
+                    const uint32_t p = 32u * q + lane;
+                    if (p >= from && (uint32_t)m[q] < lemire_threshold(excl[q])) { first = p; break; }
                 }
+                first = __reduce_min_sync(0xffffffffu, first);
+                if (first == 0xFFFFFFFFu) break;
+                if (shift == kWalkMaxRej) {   // burst beyond the ring's lookahead: end the chunk here
+                    adv = first;
+                    skip = 1;
+                    break;
+                }
+                ++shift;
+#pragma unroll
+                for (int q = 0; q < kWalkQ; ++q) {
+                    const uint32_t p = 32u * q + lane;
+                    if (p >= first) {
+                        m[q] = (uint64_t)R.d[(k + p + shift) & (kWalkRing - 1)] * excl[q];
+                        cm = (cm & ~(1u << q)) | ((uint32_t)(p < len && (uint32_t)m[q] < excl[q]) << q);
+                    }
+                }
+                from = first;
             }
         }
 #pragma unroll
         for (int q = 0; q < kWalkQ; ++q)
-            if (lane + 32u * q < adv) rv[s + lane + 32 * q] = (int32_t)(m[q] >> 32);
+            if (lane + 32u * q < adv) rv[base + 32 * q] = (int32_t)(m[q] >> 32);
         s += adv;
-        k += adv + skip;
-        __syncwarp();
-        if (lane == 0) R.consumed = (int)(k / kWalkBlk);   // blocks wholly below the next draw
+        k += adv + shift + skip;
+        __syncwarp();   // every lane's ring reads before blocks are handed back
+        for (; freed < k / kWalkBlk; ++freed)
+            if (lane == 0) ptx::mbar_arrive(&R.empty[freed % kWalkNBlk]);
     }
-    if (lane == 0) {
-        __threadfence_block();   // the final consumed count before done
-        R.done = 1;
-    }
+    if (lane == 0) R.done = 1;
 }
 
 __device__ __forceinline__ int find_plan_steps(const PlanDev *plans, int n, int64_t blk) {
@@ -753,7 +776,7 @@ constexpr int kSMaxChunks = (1 << 25) / kSChunk;
 constexpr int kSSortThreads = 1024;
 constexpr int kSSortPer = kSChunk / kSSortThreads;
 constexpr int kSResThreads = 512;            // 2 CTAs per SM (104 KB of shared memory each)
-constexpr int kSResBatch = 8;                // entry loads in flight per thread
+constexpr int kSResBatch = 4;                // segments whose loads a warp keeps in flight
 constexpr int kSTailThreads = 256;           // a warp per bitmap word
 constexpr int kSTailWords = 4;               // words per warp (independent loads in flight)
 static_assert(kSChunk == kBChunk, "both bucket paths share the chunk tables");
@@ -762,15 +785,6 @@ struct SSortSmem {
     int32_t hist[kSMaxBuckets + 1];
     int32_t warp_tmp[33];
     uint32_t st[kSChunk];
-};
-
-constexpr int kSLpCap = 16384;               // entries with a shared chunk table (beta <= ~0.6)
-struct SResSmem {
-    int32_t M[kSSize];
-    uint16_t lp[kSLpCap];              // chunk of entry k (when the bucket has <= kSLpCap entries)
-    int32_t segoff[kSMaxChunks + 1];   // entry prefix per sort chunk (+ total)
-    int32_t segstart[kSMaxChunks];     // global start of the bucket's segment in each chunk
-    int32_t warp_tmp[33];
 };
 
 __device__ __forceinline__ void k_set_sort_body(const PlanDev *plans, int n_plans, PlanLut lut, int64_t vb) {
@@ -805,6 +819,8 @@ __device__ __forceinline__ void k_set_sort_body(const PlanDev *plans, int n_plan
     }
     __syncthreads();
     for (int i = threadIdx.x; i < len; i += kSSortThreads) P.lst_pk[c0 + i] = sm.st[i];
+    // one sampled element for the Gaussian shift: step 0's output is its own target
+    if (c == 0 && threadIdx.x == 0) P.idx[0] = j[0];
 }
 
 __global__ void __launch_bounds__(kSSortThreads) k_set_sort(const PlanDev *plans, int n_plans, PlanLut lut,
@@ -815,51 +831,24 @@ __global__ void __launch_bounds__(kSSortThreads) k_set_sort(const PlanDev *plans
     }
 }
 
-// f(step, position in bucket) for every entry of the bucket: a flat walk over the
-// concatenated segments (the chunk of entry k from the prefix table), kSResBatch
-// global loads in flight per thread
-template <typename F>
-__device__ __forceinline__ void for_bucket_entries(const PlanDev &P, const SResSmem &sm, int nch, int32_t n, F &&f) {
-    const bool table = n <= kSLpCap;
-    for (int32_t k0 = threadIdx.x; k0 < n; k0 += kSResBatch * kSResThreads) {
-        uint32_t e[kSResBatch];
-        int c[kSResBatch];
-#pragma unroll
-        for (int u = 0; u < kSResBatch; ++u) {
-            const int32_t k = k0 + u * kSResThreads;
-            c[u] = -1;
-            if (k < n) {
-                int cc;
-                if (table) {
-                    cc = sm.lp[k];
-                } else {
-                    int lo = 0, hi = nch - 1;
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (sm.segoff[mid] <= k) lo = mid; else hi = mid - 1;
-                    }
-                    cc = lo;
-                }
-                c[u] = cc;
-                e[u] = __ldg(P.lst_pk + sm.segstart[cc] + (k - sm.segoff[cc]));
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kSResBatch; ++u)
-            if (c[u] >= 0) f((int32_t)c[u] * kSChunk + (int32_t)(e[u] >> kSBits), (int)(e[u] & (kSSize - 1)));
-    }
-}
+struct SResSmem {
+    int32_t M[kSSize];
+    uint32_t bits[kSWords];            // D bits of the bucket
+    int32_t segoff[kSMaxChunks + 1];   // the bucket's segment length per sort chunk
+    int32_t segstart[kSMaxChunks];     // global start of the bucket's segment in each chunk
+};
 
 __device__ __forceinline__ void k_set_resolve_body(const PlanDev *plans, int n_plans, PlanLut lut, int64_t vb) {
     extern __shared__ __align__(16) unsigned char srm_raw[];
     SResSmem &sm = *reinterpret_cast<SResSmem *>(srm_raw);
-    const PlanDev P = plans[find_plan_by(plans, n_plans, lut.bucket, vb, 1)];
+    const PlanDev &P = plans[find_plan_by(plans, n_plans, lut.bucket, vb, 1)];
     const int b = (int)(vb - P.bucket0);
     const int nb = P.nb, nch = P.nch;
     const int64_t N = P.n_elems;
     const int64_t pbase = (int64_t)b << kSBits;
     const int32_t ibase = (int32_t)(N - 1 - pbase);   // step s finalises position pbase + l iff s == ibase - l
-    const int tid = threadIdx.x;
+    uint32_t *notlast = P.notlast;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int c = tid; c < nch; c += kSResThreads) {
         const int32_t *row = P.segoff + (int64_t)c * (nb + 1);
         const int32_t r0 = row[b];
@@ -867,44 +856,51 @@ __device__ __forceinline__ void k_set_resolve_body(const PlanDev *plans, int n_p
         sm.segoff[c] = row[b + 1] - r0;
     }
     for (int l = tid; l < kSSize / 4; l += kSResThreads) reinterpret_cast<int4 *>(sm.M)[l] = make_int4(-1, -1, -1, -1);
+    for (int w = tid; w < kSWords; w += kSResThreads) sm.bits[w] = 0u;
     __syncthreads();
-    const int32_t n = block_exclusive_scan(sm.segoff, nch, sm.warp_tmp);
-    if (tid == 0) sm.segoff[nch] = n;
-    __syncthreads();
-    if (n <= kSLpCap) {   // entry -> chunk table (a warp per chunk segment)
-        const int lane = tid & 31;
-        for (int c = tid >> 5; c < nch; c += kSResThreads / 32)
-            for (int32_t k = sm.segoff[c] + lane; k < sm.segoff[c + 1]; k += 32) sm.lp[k] = (uint16_t)c;
-        __syncthreads();
+    // One pass over the bucket's entries (a warp per sort-chunk segment, kSResBatch segments'
+    // loads in flight).  old = atomicMax(M[l], s) settles "last" without a second pass: if
+    // old > s a later step hits l, so s is not last; otherwise s displaces old, which is not
+    // last -- every step but the final maximum is marked exactly once, in any arrival order.
+    // D(l) is set by the first arrival.  Self-swaps (s finalises l itself) take no part.
+    for (int c0 = warp * kSResBatch; c0 < nch; c0 += (kSResThreads / 32) * kSResBatch) {
+        int32_t len[kSResBatch];
+        int32_t mx = 0;
+#pragma unroll
+        for (int u = 0; u < kSResBatch; ++u) {
+            len[u] = c0 + u < nch ? sm.segoff[c0 + u] : 0;
+            mx = max(mx, len[u]);
+        }
+        for (int32_t k0 = 0; k0 < mx; k0 += 32) {
+            uint32_t e[kSResBatch];
+#pragma unroll
+            for (int u = 0; u < kSResBatch; ++u)
+                if (k0 + lane < len[u]) e[u] = __ldg(P.lst_pk + sm.segstart[c0 + u] + k0 + lane);
+#pragma unroll
+            for (int u = 0; u < kSResBatch; ++u) {
+                if (k0 + lane >= len[u]) continue;
+                const int32_t st = (c0 + u) * kSChunk + (int32_t)(e[u] >> kSBits);
+                const int l = (int)(e[u] & (kSSize - 1));
+                if (st == ibase - l) continue;
+                const int32_t old = atomicMax(&sm.M[l], st);
+                if (old > st) {
+                    atomicOr(notlast + (st >> 5), 1u << (st & 31));
+                } else if (old >= 0) {
+                    atomicOr(notlast + (old >> 5), 1u << (old & 31));
+                } else {
+                    atomicOr(&sm.bits[l >> 5], 1u << (l & 31));
+                }
+            }
+        }
     }
-    // M(p): latest step hitting p, self-swaps (j_s == i_s) excluded
-    for_bucket_entries(P, sm, nch, n, [&](int32_t st, int l) {
-        if (st != ibase - l) atomicMax(&sm.M[l], st);
-    });
     __syncthreads();
-    // D bits of the bucket, stored whole (a warp covers one word)
     const int64_t w0 = (int64_t)b * kSWords;
     const int64_t nw = (N + 31) / 32;
-    static_assert(kSWords % kSResThreads == 0, "one or more whole words per thread");
-    for (int w = tid; w < kSWords; w += kSResThreads) {
-        uint32_t word = 0u;
-        const int4 *m4 = reinterpret_cast<const int4 *>(sm.M + 32 * w);
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-            const int4 x = m4[(v + w) & 7];   // rotated start: consecutive threads hit different banks
-            const int b = 4 * ((v + w) & 7);
-            word |= (uint32_t)(x.x >= 0) << b | (uint32_t)(x.y >= 0) << (b + 1) | (uint32_t)(x.z >= 0) << (b + 2) |
-                    (uint32_t)(x.w >= 0) << (b + 3);
-        }
-        if (w0 + w < nw) P.bitmap[w0 + w] = word;
-    }
-    // steps that are not the last to hit their target
-    for_bucket_entries(P, sm, nch, n, [&](int32_t st, int l) {
-        if (st != ibase - l && sm.M[l] != st) atomicOr(P.notlast + (st >> 5), 1u << (st & 31));
-    });
+    for (int w = tid; w < kSWords; w += kSResThreads)
+        if (w0 + w < nw) P.bitmap[w0 + w] = sm.bits[w];
 }
 
-__global__ void __launch_bounds__(kSResThreads, 2) k_set_resolve(const PlanDev *plans, int n_plans, PlanLut lut,
+__global__ void __launch_bounds__(kSResThreads, 3) k_set_resolve(const PlanDev *plans, int n_plans, PlanLut lut,
                                                                  int64_t nvb) {
     for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
         k_set_resolve_body(plans, n_plans, lut, vb);
@@ -917,81 +913,77 @@ __global__ void __launch_bounds__(kSResThreads, 2) k_set_resolve(const PlanDev *
 // rv, !last bit) is loaded up front, the second links of all positions that need
 // one (~1 in 8: the value came from another tail position) are loaded together,
 // and the rare deeper chains are followed one by one.
-__device__ __forceinline__ bool set_chain_good(const PlanDev &P, int64_t st) {
-    const int64_t N = P.n_elems, z0 = N - P.count;
+__device__ __forceinline__ bool set_chain_good(const int32_t *rv, const uint32_t *notlast, int32_t n1, int32_t z0,
+                                               int32_t st) {
     while (true) {
-        const int64_t j = P.rv[st];
-        if (j == N - 1 - st) return false;                               // self-swap: the value stays
-        if ((P.notlast[st >> 5] >> (st & 31)) & 1u) return false;        // taken back into the tail later
-        if (j < z0) return true;                                         // carried down below the tail
-        st = N - 1 - j;
+        const int32_t j = rv[st];
+        if (j == n1 - st) return false;                         // self-swap: the value stays
+        if ((notlast[st >> 5] >> (st & 31)) & 1u) return false; // taken back into the tail later
+        if (j < z0) return true;                                // carried down below the tail
+        st = n1 - j;
     }
 }
 
-__device__ __forceinline__ void k_set_tail_body(const PlanDev *plans, int n_plans, PlanLut lut, int64_t vb) {
-    const PlanDev &P = plans[find_plan_by(plans, n_plans, lut.chain, vb, 2)];
-    const int64_t N = P.n_elems, z0 = N - P.count;
+__device__ __forceinline__ void k_set_tail_body(const PlanDev &P, int64_t vb) {
+    // 32-bit index arithmetic: N < 2^31 on this path
+    const int32_t N = (int32_t)P.n_elems, n1 = N - 1, z0 = (int32_t)(P.n_elems - P.count);
+    const int32_t *rv = P.rv;
+    const uint32_t *notlast = P.notlast;
+    uint32_t *bitmap = P.bitmap;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t w_first = (z0 >> 5) + ((vb - P.oblock0) * (kSTailThreads / 32) + warp) * kSTailWords;
-    const int64_t nw = (N + 31) >> 5;
+    const int32_t w_first = (z0 >> 5) + ((int32_t)(vb - P.oblock0) * (kSTailThreads / 32) + warp) * kSTailWords;
+    const int32_t nw = (int32_t)((P.n_elems + 31) >> 5);
     uint32_t word[kSTailWords], nl[kSTailWords];
     int32_t j[kSTailWords];
 #pragma unroll
     for (int u = 0; u < kSTailWords; ++u) {
-        const int64_t w = w_first + u;
-        const int64_t q = (w << 5) + lane;
-        word[u] = 0u;
-        j[u] = -1;
-        nl[u] = 0u;
-        if (w < nw) {
-            word[u] = P.bitmap[w];
-            if (q >= z0 && q < N) {
-                const int64_t st = N - 1 - q;
-                j[u] = P.rv[st];
-                nl[u] = P.notlast[st >> 5] >> (st & 31);
-            }
-        }
+        const int32_t w = w_first + u, q = (w << 5) + lane;
+        const bool in = w < nw && q >= z0 && q < N;
+        word[u] = w < nw ? bitmap[w] : 0u;
+        const int32_t st = in ? n1 - q : 0;
+        j[u] = in ? rv[st] : -1;
+        nl[u] = in ? notlast[st >> 5] >> (st & 31) : 0u;
     }
-    // 0: settled not sampled, 1: sampled, 2: follow the value to tail position j
+    // state: 1 sampled, 0 not, 2 follow the value to the tail position j came from
     int state[kSTailWords];
-#pragma unroll
-    for (int u = 0; u < kSTailWords; ++u) {
-        const int64_t st = N - 1 - (((w_first + u) << 5) + lane);
-        state[u] = 0;
-        if (j[u] >= 0 && !((word[u] >> lane) & 1u)) {
-            if (j[u] == N - 1 - st || (nl[u] & 1u)) state[u] = 1;
-            else if (j[u] >= z0) state[u] = 2;
-        }
-    }
     int32_t st2[kSTailWords];
 #pragma unroll
-    for (int u = 0; u < kSTailWords; ++u) {   // second links, loads issued together
-        st2[u] = (int32_t)(N - 1 - j[u]);      // the step that finalises tail position j
+    for (int u = 0; u < kSTailWords; ++u) {
+        const int32_t st = n1 - ((w_first + u) << 5) - lane;
+        state[u] = 0;
+        if (j[u] >= 0 && !((word[u] >> lane) & 1u))
+            state[u] = (j[u] == n1 - st || (nl[u] & 1u)) ? 1 : (j[u] >= z0 ? 2 : 0);
+        st2[u] = n1 - j[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kSTailWords; ++u) {   // second links of every position that needs one, together
         if (state[u] != 2) continue;
-        j[u] = P.rv[st2[u]];
-        nl[u] = P.notlast[st2[u] >> 5] >> (st2[u] & 31);
+        j[u] = rv[st2[u]];
+        nl[u] = notlast[st2[u] >> 5] >> (st2[u] & 31);
     }
 #pragma unroll
     for (int u = 0; u < kSTailWords; ++u) {
         if (state[u] != 2) continue;
-        if (j[u] == N - 1 - st2[u] || (nl[u] & 1u)) state[u] = 1;
+        if (j[u] == n1 - st2[u] || (nl[u] & 1u)) state[u] = 1;
         else if (j[u] < z0) state[u] = 0;
-        else state[u] = set_chain_good(P, N - 1 - j[u]) ? 0 : 1;
+        else state[u] = set_chain_good(rv, notlast, n1, z0, n1 - j[u]) ? 0 : 1;
     }
 #pragma unroll
     for (int u = 0; u < kSTailWords; ++u) {
-        const int64_t w = w_first + u;
-        if (w >= nw) break;   // warp-uniform
         const unsigned bits = __ballot_sync(0xffffffffu, state[u] == 1);
-        if (lane == 0 && bits) P.bitmap[w] = word[u] | bits;
-        // one sampled element for the Gaussian shift: step 0's output is its own target
-        if ((w << 5) + lane == N - 1) P.idx[0] = P.rv[0];
+        if (lane == 0 && bits) bitmap[w_first + u] = word[u] | bits;
     }
 }
 
 __global__ void __launch_bounds__(kSTailThreads) k_set_tail(const PlanDev *plans, int n_plans, PlanLut lut,
                                                             int64_t nvb) {
-    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) k_set_tail_body(plans, n_plans, lut, vb);
+    __shared__ int pi;
+    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+        if (threadIdx.x == 0) pi = find_plan_by(plans, n_plans, lut.chain, vb, 2);
+        __syncthreads();
+        k_set_tail_body(plans[pi], vb);
+        __syncthreads();
+    }
 }
 
 struct PlanLayout {
@@ -1249,7 +1241,7 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
             k_set_sort<<<capped(L.bchunks, 1), kSSortThreads, sizeof(SSortSmem), st>>>(d_plans, n_plans, lut,
                                                                                         L.bchunks);
             EDGC_LAUNCH_CHECK();
-            k_set_resolve<<<capped(L.buckets, 2), kSResThreads, sizeof(SResSmem), st>>>(d_plans, n_plans, lut,
+            k_set_resolve<<<capped(L.buckets, 3), kSResThreads, sizeof(SResSmem), st>>>(d_plans, n_plans, lut,
                                                                                         L.buckets);
             EDGC_LAUNCH_CHECK();
             k_set_tail<<<capped(L.oblocks, 8), kSTailThreads, 0, st>>>(d_plans, n_plans, lut, L.oblocks);

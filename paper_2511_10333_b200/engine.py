@@ -328,6 +328,46 @@ class BucketEngine:
             self.check_status()
         return self.outs
 
+    def capture_graphs(self):
+        """Record the steady-state step (compress, exchange, reconstruct) as two CUDA graphs, one per
+        factor-buffer parity; `graph_step` then replays the current parity's graph.
+
+        Needs one eager step first (the residual-free first step uses its own plan).  The graphs hold
+        the current plans' device pointers, so `set_rank` drops them.
+        """
+        if self._res is None:
+            raise ValueError("run one eager step before capturing the step graphs")
+        saved = (self._parity, self._res, self.steps)
+        graphs = {}
+        cap = torch.cuda.Stream(self.device)
+        cap.wait_stream(torch.cuda.current_stream(self.device))
+        for _ in range(2):
+            par = self._parity
+            # plans are built (allocations, uploads) before capture; capture only records launches
+            self._compress_plan()
+            self._recon_plan()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                self.compress()
+                self.exchange()
+                self.reconstruct()
+            graphs[par] = g
+            self.advance()   # host bookkeeping only: which buffer holds the residual pair
+        torch.cuda.current_stream(self.device).wait_stream(cap)
+        self._parity, self._res, self.steps = saved
+        self._graphs = graphs
+
+    def graph_step(self, check: bool = False):
+        """One DP step by graph replay (capture_graphs); same results as `step`."""
+        g = getattr(self, "_graphs", None)
+        if not g:
+            raise ValueError("capture_graphs() first")
+        g[self._parity].replay()
+        self.advance()
+        if check:
+            self.check_status()
+        return self.outs
+
     def advance(self):
         """Close a step issued phase by phase: the factors just written become the residual pair."""
         offs, _ = self._packed_offsets(self.ranks)
@@ -346,6 +386,7 @@ class BucketEngine:
         """Apply a controller decision to every matrix: r_k = min(r, min(m, n)) (grad_source.py:469-471)."""
         if r < 1:
             raise ValueError(f"rank must be >= 1, got {r}")
+        self._graphs = None   # captured plans no longer match
         if r > self.cap:
             old = {"cap": self.cap, "basis": [b.clone() for b in self.basis],
                    "q_warm": [q.clone() for q in self.q_warm], "factors": self.factors,

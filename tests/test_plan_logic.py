@@ -24,31 +24,39 @@ def lemire(x, rng):
     return left >= thr, val
 
 
-def walk(seed, n_elems, count, chunk=128):
+def walk(seed, n_elems, count, chunk=256, max_rej=8):
     """k_walk: bounded value of every step.  A warp takes `chunk` consecutive steps against
-    consecutive draws; the chunk ends at its first Lemire rejection, whose draw is skipped."""
+    consecutive draws; rejections are settled in step order inside the chunk (from a rejecting
+    step on, every step moves to the next draw and is tested again), up to `max_rej` per chunk,
+    beyond which the chunk ends at the rejecting step."""
     tail = n_elems > 10000 and count > n_elems // 20
     draws = oracle.pcg64_u32(seed, 2 * count + 4096).astype(np.int64)
     step_rng = (lambda s: n_elems - 1 - s) if tail else (lambda s: n_elems - count + s)
     rv = [0] * count
     s = k = 0
     while s < count:
-        adv, skip = min(chunk, count - s), 0
-        vals = []
-        for lane in range(adv):
-            ok, v = lemire(int(draws[k + lane]), step_rng(s + lane))
-            if not ok:
-                adv, skip = lane, 1
+        ln = min(chunk, count - s)
+        vals = [lemire(int(draws[k + p]), step_rng(s + p)) for p in range(ln)]
+        adv, shift, skip, frm = ln, 0, 0, 0
+        while True:
+            first = next((p for p in range(frm, ln) if not vals[p][0]), None)
+            if first is None:
                 break
-            vals.append(v)
-        rv[s:s + adv] = vals[:adv]
+            if shift == max_rej:
+                adv, skip = first, 1
+                break
+            shift += 1
+            for p in range(first, ln):
+                vals[p] = lemire(int(draws[k + p + shift]), step_rng(s + p))
+            frm = first
+        rv[s:s + adv] = [v for _, v in vals[:adv]]
         s += adv
-        k += adv + skip
+        k += adv + shift + skip
     return rv, tail
 
 
-def emulate(seed, n_elems, count, chunk=128):
-    rv, tail = walk(seed, n_elems, count, chunk)
+def emulate(seed, n_elems, count, chunk=256, max_rej=8):
+    rv, tail = walk(seed, n_elems, count, chunk, max_rej)
     lists = {}                            # k_index (hash lists)
     for st in range(count):
         lists.setdefault(rv[st], []).append(st)
@@ -87,16 +95,17 @@ def emulate(seed, n_elems, count, chunk=128):
     return np.asarray(out, dtype=np.int64)
 
 
-@pytest.mark.parametrize("chunk", [128, 32, 7, 1])
+@pytest.mark.parametrize("chunk,max_rej", [(256, 8), (32, 1), (7, 0), (1, 0), (300, 2)])
 @pytest.mark.parametrize("n_elems,beta,seed", [
     (100, 0.5, 3), (101, 0.9, 1), (4096, 0.25, 1), (10000, 0.5, 4), (10001, 0.06, 4), (12000, 0.25, 5),
-    (20000, 0.05, 9), (20000, 0.0501, 11), (40000, 0.999, 2), (7, 0.3, 5), (2, 0.5, 0), (300, 0.99, 8)])
-def test_plan_algorithm_matches_numpy(n_elems, beta, seed, chunk):
+    (20000, 0.05, 9), (20000, 0.0501, 11), (40000, 0.999, 2), (7, 0.3, 5), (2, 0.5, 0), (300, 0.99, 8),
+    (2_000_000_000, 0.00001, 6)])
+def test_plan_algorithm_matches_numpy(n_elems, beta, seed, chunk, max_rej):
     count = min(n_elems, math.ceil(beta * n_elems))
     if count == n_elems:
         pytest.skip("copy branch")
     ref = np.random.default_rng(seed).choice(n_elems, size=count, replace=False, shuffle=False)
-    assert np.array_equal(emulate(seed, n_elems, count, chunk), ref)
+    assert np.array_equal(emulate(seed, n_elems, count, chunk, max_rej), ref)
 
 
 def resolve_buckets(rv, n_elems, count, tail, bbits, order_seed=0):

@@ -16,7 +16,8 @@ def main(path):
         d = dict(zip(hdr, r))
         k = d["Kernel Name"].split("(")[0][-40:]
         a = agg.setdefault(k, collections.defaultdict(float))
-        a[d["Metric Name"]] += float(d["Metric Value"].replace(",", ""))
+        v = d["Metric Value"].replace(",", "")
+        a[d["Metric Name"]] += float(v) if v not in ("n/a", "") else 0.0
         if d["Metric Name"] == "gpu__time_duration.sum":
             a["n"] += 1
     for k, a in agg.items():
