@@ -70,8 +70,10 @@ def parse_args():
                          "tracker's plan kernels run on a low-priority side stream and yield SMs to the step)")
     ap.add_argument("--alias-output", action="store_true",
                     help="averaged gradients overwrite the raw ones (default for the 12.1B set, to fit in HBM)")
-    ap.add_argument("--no-fuse-entropy", dest="fuse_entropy", action="store_false",
-                    help="diagnostics: separate Gaussian pass instead of gathering the statistics in pass 1")
+    ap.add_argument("--fuse-entropy", dest="fuse_entropy", action="store_true",
+                    help="gather the sampled-iteration statistics inside pass 1 instead of a separate Gaussian "
+                         "pass over the bitmaps (measured: the separate pass is cheaper -- 9.2 GB at ~HBM speed "
+                         "vs +47%% instructions in pass 1)")
     ap.add_argument("--cpu-steps", type=int, default=6, help="EF steps in the bounded CPU sample")
     return ap.parse_args()
 

@@ -73,6 +73,9 @@ typedef struct {
  * Gaussian estimator's shift: NumPy's first sample for Floyd plans, its last for
  * tail-shuffle plans) are produced: the set, not the order. */
 #define EDGC_PLAN_BITMAP_ONLY 1
+/* The plans are on the caller's critical path (built inline, not ahead on a side
+ * stream): spread the sequential walk over all SMs instead of packing it onto few. */
+#define EDGC_PLAN_LATENCY 2
 
 int64_t edgc_sample_plan_workspace_bytes(const edgc_plan_desc *plans, int n_plans);
 /* status_dev: device int32[n_plans]; nonzero = EDGC_EDRAWS for that plan. */

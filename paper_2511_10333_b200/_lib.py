@@ -30,6 +30,7 @@ EDGC_EDRAWS = 8
 
 PHASE_PASS1, PHASE_FACTOR, PHASE_PASS2, PHASE_FINALIZE, PHASE_ALL = 1, 2, 4, 8, 15
 PLAN_BITMAP_ONLY = 1
+PLAN_LATENCY = 2
 
 c_i32, c_i64, c_u64, c_f32, c_f64, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float,
                                            ctypes.c_double, ctypes.c_void_p)

@@ -1552,6 +1552,16 @@ struct TcEF {
 
 // EDGC_TC_MIN_RANK (default 16): wide-path ranks above it use the tensor cores;
 // EDGC_NO_TC disables them (A/B runs)
+// averaged reconstruction on the tensor cores from this W r on (EDGC_TC_RECON_MIN)
+int tc_recon_min() {
+    static const int v = [] {
+        if (std::getenv("EDGC_NO_TC")) return 1 << 30;
+        const char *e = std::getenv("EDGC_TC_RECON_MIN");
+        return e ? std::atoi(e) : 33;
+    }();
+    return v;
+}
+
 int tc_min_rank() {
     static const int v = [] {
         if (std::getenv("EDGC_NO_TC")) return 1 << 30;
@@ -1621,36 +1631,65 @@ __global__ void __launch_bounds__(kP2Threads) k_pass2(const MatDev *mats, const 
 }
 
 // ---------------------------------------------------------------- finalize
-__global__ void k_finalize(const MatDev *mats, const int32_t *status) {
+// One thread per Q element (j, k): the Z (or Q) partials of every strip summed in a fixed
+// order (deterministic), then Q = Z T through shared memory.  Sized by n r so a single
+// matrix still spreads over the GPU.
+constexpr int kFinThreads = 256;
+__global__ void __launch_bounds__(kFinThreads) k_finalize(const MatDev *mats, const int32_t *status) {
     const MatDev &M = mats[blockIdx.y];
     const int st = status[blockIdx.y];
     if (st & 1) return;
     const int r = M.r;
     const int64_t n = M.n;
     const bool zq = M.zmode && !(st & 2);
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * r; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = e / r;
-        const int k = (int)(e % r);
-        float q;
-        if (M.dead[k]) {
-            q = M.basis[j * M.ld_q + k];   // compressor.py:113-114
-        } else if (zq) {
-            // Q = Z T (T upper triangular): sum_l Z[j, l] T[l, k]
-            double a = 0.0;
-            for (int l = 0; l <= k; ++l) {
-                double z = 0.0;
-                for (int b = 0; b < M.nitems; ++b) z += M.zpart[((int64_t)b * n + j) * r + l];
-                a += z * M.tmat[(int64_t)k * r + l];
-            }
-            q = (float)a;
-        } else {
-            double a = 0.0;
-            for (int b = 0; b < M.nblk2; ++b) a += M.q_part[((int64_t)b * n + j) * r + k];
-            q = (float)a;
+    const int64_t e = (int64_t)blockIdx.x * kFinThreads + threadIdx.x;
+    if ((int64_t)blockIdx.x * kFinThreads >= n * r) return;   // whole CTA past this matrix
+    const bool live = e < n * r;
+    const int64_t j = e / r;
+    const int k = (int)(e % r);
+    const int nb = zq ? M.nitems : M.nblk2;
+    const double *part = zq ? M.zpart : M.q_part;
+    double z = 0.0;
+    if (live) {
+        int b = 0;
+        for (; b + 4 <= nb; b += 4) {   // four strips' loads in flight, summed in strip order
+            const double z0 = part[((int64_t)b * n + j) * r + k], z1 = part[((int64_t)(b + 1) * n + j) * r + k];
+            const double z2 = part[((int64_t)(b + 2) * n + j) * r + k], z3 = part[((int64_t)(b + 3) * n + j) * r + k];
+            z += z0;
+            z += z1;
+            z += z2;
+            z += z3;
         }
-        M.q_out[j * r + k] = q;
-        M.q_warm[j * M.ld_q + k] = q;
+        for (; b < nb; ++b) z += part[((int64_t)b * n + j) * r + k];
     }
+    __shared__ double zs[kFinThreads];
+    zs[threadIdx.x] = z;
+    __syncthreads();
+    if (!live) return;
+    float q;
+    if (M.dead[k]) {
+        q = M.basis[j * M.ld_q + k];   // compressor.py:113-114
+    } else if (zq) {
+        // Q = Z T (T upper triangular): sum_l Z[j, l] T[l, k]; row j's Z values sit in this CTA
+        // unless the row straddles two CTAs (r does not divide 256): then reload them
+        const int base = (int)(threadIdx.x - k);
+        double a = 0.0;
+        for (int l = 0; l <= k; ++l) {
+            double zl;
+            if (base >= 0) {
+                zl = zs[base + l];
+            } else {
+                zl = 0.0;
+                for (int b = 0; b < nb; ++b) zl += part[((int64_t)b * n + j) * r + l];
+            }
+            a += zl * M.tmat[(int64_t)k * r + l];
+        }
+        q = (float)a;
+    } else {
+        q = (float)z;
+    }
+    M.q_out[j * r + k] = q;
+    M.q_warm[j * M.ld_q + k] = q;
 }
 
 struct Plan {
@@ -1663,6 +1702,7 @@ struct Plan {
     std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles
     int64_t nfxg64 = 0, nfxr64 = 0;   // the first n are 64-edge tiles, the rest kFxBig-edge   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
     int64_t bytes = 0;
+    int64_t max_nr = 1;                // largest n r of the plan (k_finalize grid)
     MatDev *d_mats = nullptr;
     Tile *d_t1v4 = nullptr, *d_t1v1 = nullptr, *d_t2v4 = nullptr, *d_t2v1 = nullptr;
     ZTile *d_tz[9] = {};
@@ -1682,6 +1722,20 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     P.mats.resize(n);
     P.d_mats = a.take<MatDev>(n);
     std::vector<FxTile> fxg_big, fxr_big;   // kFxBig-edge factorisation tiles, appended after the 64-edge ones
+    // Z-path strip height: kZRows, unless the plan's clusters would not fill one wave of the GPU
+    // (a single matrix through the reference's per-matrix compress): then thinner strips, so
+    // more clusters stream it (more Z partials to sum, a few KB each)
+    int64_t zrows = kZRows;
+    {
+        int64_t ctas = 0;
+        for (int k = 0; k < n; ++k) {
+            int zc = (int)ceil_div(std::max<int64_t>(descs[k].n, 1), kTCW);
+            if (zc == 4 || zc == 5) zc = 6;
+            ctas += ceil_div(std::max<int64_t>(descs[k].m, 1), kZRows) * zc;
+        }
+        const int64_t want = (int64_t)sm_count();
+        if (ctas < want) zrows = std::max<int64_t>(16, (kZRows * ctas / want) / 4 * 4);
+    }
     for (int k = 0; k < n; ++k) {
         const edgc_compress_desc &d = descs[k];
         EDGC_REQUIRE(d.m >= 1 && d.n >= 1, "compress desc %d: dims must be positive", k);
@@ -1695,6 +1749,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         EDGC_REQUIRE(d.g && d.w && d.q_warm && d.basis && d.p_out && d.q_out && d.ld_q >= d.r && d.ld_g >= d.n,
                      "compress desc %d: null pointer or bad leading dimension", k);
         MatDev &M = P.mats[k];
+        P.max_nr = std::max<int64_t>(P.max_nr, d.n * (int64_t)d.r);
         M.g = d.g; M.w = d.w; M.p_res = d.p_res; M.q_res = d.q_res; M.q_warm = d.q_warm; M.basis = d.basis;
         M.p_out = d.p_out; M.q_out = d.q_out;
         M.m = d.m; M.n = d.n; M.ld_g = d.ld_g; M.r = d.r; M.r_res = d.r_res; M.ld_q = d.ld_q;
@@ -1711,10 +1766,10 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.zw = (int32_t)(ceil_div(ceil_div(d.n, zc), 4) * 4);
         M.zmode = (!z_off && v4 && std::max(d.r, d.r_res) <= 4 && zc <= 8) ? 1 : 0;
         M.zc = zc;
-        M.nitems = M.zmode ? (int32_t)ceil_div(d.m, kZRows) : 0;
+        M.nitems = M.zmode ? (int32_t)ceil_div(d.m, zrows) : 0;
         if (M.zmode)
             for (int32_t it = 0; it < M.nitems; ++it)
-                P.tz[zc].push_back(ZTile{k, it, (int64_t)it * kZRows, std::min(d.m, (int64_t)(it + 1) * kZRows)});
+                P.tz[zc].push_back(ZTile{k, it, (int64_t)it * zrows, std::min(d.m, (int64_t)(it + 1) * zrows)});
         const int64_t slots = d.n / M.vec;
         const int64_t threads1 = kP1Threads;
         M.wide = std::max(d.r, d.r_res) > kNarrow ? 1 : 0;
@@ -2165,13 +2220,14 @@ __global__ void k_residual(const float *w, const float *p, const float *q, int r
 
 __global__ void k_check_work(const float *g, int64_t ld_g, const float *w, const float *p, const float *q, int r,
                              int64_t m, int64_t n, int32_t *flag) {
+    // rows over grid.y, columns over grid.x: no per-element division
     bool bad = false;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < m * n; x += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = x / n, j = x % n;
-        float dot = 0.f;
-        for (int k = 0; k < r; ++k) dot = fmaf(p[i * r + k], q[j * r + k], dot);
-        bad |= !isfinite(g[i * ld_g + j] + (w[x] - dot));
-    }
+    for (int64_t i = blockIdx.y; i < m; i += gridDim.y)
+        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+            float dot = 0.f;
+            for (int k = 0; k < r; ++k) dot = fmaf(p[i * r + k], q[j * r + k], dot);
+            bad |= !isfinite(g[i * ld_g + j] + (w[i * n + j] - dot));
+        }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
@@ -2369,7 +2425,7 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
             EDGC_CUDA_TRY((tc::launch<128, 4>(TcQ{P.d_mats, P.d_tcq[1], status_dev, (int)P.tcq[1].size()}, sm_count(), st)));
     }
     if (phases & EDGC_PHASE_FINALIZE) {
-        k_finalize<<<dim3(16, n), 256, 0, st>>>(P.d_mats, status_dev);
+        k_finalize<<<dim3((unsigned)ceil_div(P.max_nr, kFinThreads), n), kFinThreads, 0, st>>>(P.d_mats, status_dev);
         EDGC_LAUNCH_CHECK();
     }
     return EDGC_OK;
@@ -2440,10 +2496,9 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
         P.d[k] = ReconDev{s.p, s.q, s.out, s.m, s.n, s.ld_out, s.p_rank_stride, s.q_rank_stride, s.r, s.n_ranks,
                           s.scale};
         const bool v4 = s.r * s.n_ranks <= 32 && s.n % 4 == 0 && s.ld_out % 4 == 0 && ((uintptr_t)s.out % 16 == 0);
-        // tensor cores above the wide-path threshold; rank blocks must not straddle a
-        // 32-wide K block (single rank, or r % 32 == 0)
-        const bool tcr = s.r * s.n_ranks > std::max(32, tc_min_rank()) && s.r % 4 == 0 &&
-                         (s.n_ranks == 1 || s.r % 32 == 0);
+        // tensor cores once W r passes the recon threshold (CUDA-core FMA bound beyond it); with
+        // W > 1 the K index concatenates the ranks' r-wide blocks (float4 loads per block: 4 | r)
+        const bool tcr = s.r * s.n_ranks >= tc_recon_min() && s.r % 4 == 0;
         if (tcr) {
             for (int64_t r0 = 0; r0 < s.m; r0 += tc::kBM)
                 for (int64_t c0 = 0; c0 < s.n; c0 += 128)
@@ -2580,8 +2635,9 @@ extern "C" int edgc_check_work_finite(const float *g, int64_t ld_g, const float 
                                       void *stream) {
     EDGC_REQUIRE(g && w && flag_dev && m >= 1 && n >= 1 && ld_g >= n && (r_res == 0 || (p_res && q_res)),
                  "edgc_check_work_finite: bad arguments");
-    k_check_work<<<elementwise_blocks(m * n), 256, 0, (cudaStream_t)stream>>>(g, ld_g, w, p_res, q_res, r_res, m, n,
-                                                                             flag_dev);
+    const unsigned gx = (unsigned)std::min<int64_t>(ceil_div(n, 256), 8);
+    const unsigned gy = (unsigned)std::min<int64_t>(m, std::max<int64_t>(1, (int64_t)sm_count() * 8 / gx));
+    k_check_work<<<dim3(gx, gy), 256, 0, (cudaStream_t)stream>>>(g, ld_g, w, p_res, q_res, r_res, m, n, flag_dev);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }

@@ -127,7 +127,9 @@ __device__ __forceinline__ uint32_t lemire_threshold(uint32_t excl) {
 // Generating the draws is most of the arithmetic (a 128-bit LCG step per two
 // draws) and does not depend on the walk, so a producer warp per plan fills a
 // shared ring of kWalkBlk-draw blocks ahead of the walker (smem counters, no HBM
-// draw buffer).  kWalkPlans plans share a CTA.
+// draw buffer).  Plans per CTA: kWalkPlans for plans built ahead on a side stream
+// (few SMs held for the longer walk), 1 with EDGC_PLAN_LATENCY (the walk is on
+// the step's critical path: every SM to itself).
 constexpr int kWalkPlans = 16;              // plans per CTA (a walker and a producer warp each)
 constexpr int kWalkQ = 8;                   // steps per walker lane per chunk
 constexpr int kWalkChunk = 32 * kWalkQ;
@@ -138,9 +140,11 @@ constexpr int kWalkRing = kWalkBlk * kWalkNBlk;
 constexpr int kWalkThreads = 64 * kWalkPlans;
 static_assert(kWalkBlk % 64 == 0, "whole outputs per producer lane");
 static_assert(kWalkChunk + kWalkMaxRej <= kWalkBlk, "a chunk spans at most two blocks");
+static_assert((kWalkChunk + kWalkMaxRej) % 2 == 0, "the mirror copies whole outputs");
 
+constexpr int kWalkPad = kWalkChunk + kWalkMaxRej;   // ring head mirrored past its end: no index wrap
 struct alignas(16) WalkRing {
-    uint32_t d[kWalkRing];
+    uint32_t d[kWalkRing + kWalkPad];
     uint64_t full[kWalkNBlk];    // producer -> walker: block written
     uint64_t empty[kWalkNBlk];   // walker -> producer: block consumed
     volatile int done;
@@ -164,12 +168,13 @@ __device__ __forceinline__ void walk_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
-__global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int n_plans, const int32_t *order) {
+__global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int n_plans, const int32_t *order,
+                                                       int ppc) {
     extern __shared__ __align__(16) unsigned char walk_raw[];
     const int g = threadIdx.x >> 6;                 // plan group in the CTA
     const bool producer = (threadIdx.x >> 5) & 1;
     const int lane = threadIdx.x & 31;
-    const int slot = blockIdx.x * kWalkPlans + g;
+    const int slot = blockIdx.x * ppc + g;
     WalkRing &R = reinterpret_cast<WalkRing *>(walk_raw)[g];
     if ((threadIdx.x & 63) == 0) {
         for (int i = 0; i < kWalkNBlk; ++i) {
@@ -202,7 +207,11 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int
             for (int t = 0; t < kPer; ++t) {
                 const uint64_t v = pcg_output(st);
                 st = a * st + c;
-                dst[lane + 32 * t] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
+                const uint2 w = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
+                dst[lane + 32 * t] = w;
+                // the ring's first kWalkPad draws again past its end, so a chunk reads one straight run
+                if (sl == 0 && 2 * (lane + 32 * t) < kWalkPad)
+                    *reinterpret_cast<uint2 *>(R.d + kWalkRing + 2 * (lane + 32 * t)) = w;
             }
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&R.full[sl]);   // release: the block's writes before the arrival
@@ -219,16 +228,20 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int
         const uint32_t need = (k + kWalkChunk + kWalkMaxRej + kWalkBlk) / kWalkBlk;
         for (; have < need; ++have) walk_wait(&R.full[have % kWalkNBlk], (have / kWalkNBlk) & 1);
         const uint32_t base = s + lane;
+        const uint32_t len = min((uint32_t)kWalkChunk, count - s);
+        const bool full = len == kWalkChunk;
+        const uint32_t *rp = R.d + (k & (kWalkRing - 1)) + lane;   // draw of step base + 32 q: rp[32 q]
+        const uint32_t ex0 = tail ? e0 - base : e0 + base;
+        const uint32_t dex = tail ? 0u - 32u : 32u;
         uint64_t m[kWalkQ];
         uint32_t excl[kWalkQ];
         uint32_t cm = 0;   // bit q: step base + 32 q is a rejection candidate
 #pragma unroll
         for (int q = 0; q < kWalkQ; ++q) {
-            excl[q] = tail ? e0 - base - 32 * q : e0 + base + 32 * q;
-            m[q] = (uint64_t)R.d[(k + lane + 32 * q) & (kWalkRing - 1)] * excl[q];
-            cm |= (uint32_t)(base + 32 * q < count && (uint32_t)m[q] < excl[q]) << q;
+            excl[q] = ex0 + dex * q;
+            m[q] = (uint64_t)rp[32 * q] * excl[q];
+            cm |= (uint32_t)((uint32_t)m[q] < excl[q] && (full || lane + 32u * q < len)) << q;
         }
-        const uint32_t len = min((uint32_t)kWalkChunk, count - s);
         uint32_t adv = len, shift = 0, skip = 0;   // shift: rejections so far in this chunk
         if (__ballot_sync(0xffffffffu, cm != 0)) {
             // settle rejections in step order: from the first rejecting step f on, every step
@@ -253,16 +266,22 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int
                 for (int q = 0; q < kWalkQ; ++q) {
                     const uint32_t p = 32u * q + lane;
                     if (p >= first) {
-                        m[q] = (uint64_t)R.d[(k + p + shift) & (kWalkRing - 1)] * excl[q];
+                        m[q] = (uint64_t)rp[32 * q + shift] * excl[q];
                         cm = (cm & ~(1u << q)) | ((uint32_t)(p < len && (uint32_t)m[q] < excl[q]) << q);
                     }
                 }
                 from = first;
             }
         }
+        int32_t *out = rv + base;
+        if (adv == kWalkChunk) {
 #pragma unroll
-        for (int q = 0; q < kWalkQ; ++q)
-            if (lane + 32u * q < adv) rv[base + 32 * q] = (int32_t)(m[q] >> 32);
+            for (int q = 0; q < kWalkQ; ++q) out[32 * q] = (int32_t)(m[q] >> 32);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kWalkQ; ++q)
+                if (lane + 32u * q < adv) out[32 * q] = (int32_t)(m[q] >> 32);
+        }
         s += adv;
         k += adv + shift + skip;
         __syncwarp();   // every lane's ring reads before blocks are handed back
@@ -1210,8 +1229,11 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
                                            (int)(kWalkPlans * sizeof(WalkRing))));
         walk_attr = true;
     }
-    k_walk<<<(unsigned)ceil_div(n_plans, kWalkPlans), kWalkThreads, kWalkPlans * sizeof(WalkRing), st>>>(
-        d_plans, n_plans, (const int32_t *)L.walk_order);
+    bool latency = false;
+    for (int i = 0; i < n_plans; ++i) latency |= (plans[i].flags & EDGC_PLAN_LATENCY) != 0;
+    const int ppc = latency ? 1 : kWalkPlans;
+    k_walk<<<(unsigned)ceil_div(n_plans, ppc), 64 * ppc, ppc * sizeof(WalkRing), st>>>(
+        d_plans, n_plans, (const int32_t *)L.walk_order, ppc);
     EDGC_LAUNCH_CHECK();
     if (L.n_bucketed) {
         // bucket path (tail-shuffle plans); plans are ordered, so each kernel's CTA range covers

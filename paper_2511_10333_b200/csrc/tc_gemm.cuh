@@ -243,6 +243,20 @@ __device__ __forceinline__ void load_plane(const View &v, bool vec, int64_t kbas
             if (PL::kVec % kGroupThreads != 0 && tid + u * kGroupThreads >= PL::kVec) break;
             x[u] = __ldg(reinterpret_cast<const float4 *>(p + (uint32_t)u * step));
         }
+    } else if (!MN && vec && v.rows >= ROWS && v.kblk % 4 == 0) {
+        // K-major operand whose K is the concatenation of narrow rank blocks (the averaged
+        // reconstruction at W ranks of rank r, 4 | r): the thread's 4 consecutive k lie in one
+        // rank block, so every row is one float4 at kmap(k0); k past K (K < a 32-wide block) is 0
+        const int64_t k = kbase + k0;
+        const bool in = k < v.K;
+        const float *p = v.p + (int64_t)r0 * v.ld + (in ? kmap(v, k) : 0);
+        uint32_t step = (uint32_t)(PL::kStep * v.ld);
+        asm volatile("" : "+r"(step));
+#pragma unroll
+        for (int u = 0; u < PL::kPer; ++u) {
+            if (PL::kVec % kGroupThreads != 0 && tid + u * kGroupThreads >= PL::kVec) break;
+            x[u] = in ? __ldg(reinterpret_cast<const float4 *>(p + (uint32_t)u * step)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     } else {
 #pragma unroll
         for (int u = 0; u < PL::kPer; ++u) {

@@ -97,7 +97,7 @@ def sample_count(n_elems: int, beta: float) -> int:
 
 
 def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, workspace=None, check: bool = True,
-                 indices: bool = True):
+                 indices: bool = True, ahead: bool = False):
     """Device index plans for many (n_elems, count, seed) at once.
 
     Returns a list of int32 CUDA tensors (None where count == n_elems, i.e. the
@@ -109,6 +109,9 @@ def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, work
     ``status`` later).  ``indices=False`` (with ``bitmaps``) builds only the
     membership sets: each returned index tensor then holds one sampled
     element (the Gaussian estimator's shift; see EDGC_PLAN_BITMAP_ONLY).
+    ``ahead=True``: the plans are built ahead of use on a side stream, so the
+    sequential walk is packed onto few SMs; otherwise (EDGC_PLAN_LATENCY) it is
+    spread over all of them, as the result is waited for.
     """
     if not indices and not bitmaps:
         raise ValueError("indices=False needs bitmaps=True")
@@ -147,7 +150,8 @@ def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, work
         for i in todo:
             n_elems, count, seed = specs[i]
             descs[i] = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]), _lib.ptr(bms[i]),
-                                     0 if indices else _lib.PLAN_BITMAP_ONLY)
+                                     (0 if indices else _lib.PLAN_BITMAP_ONLY) |
+                                     (0 if ahead else _lib.PLAN_LATENCY))
             sizes[i] = L.edgc_sample_plan_workspace_bytes((_lib.PlanDesc * 1)(descs[i]), 1) + 4096
         status_all = torch.zeros(max(1, len(todo)), dtype=torch.int32, device=dev)
         k = 0
@@ -453,7 +457,7 @@ class EntropyTracker:
         ready = torch.cuda.Event()
         ready.record(torch.cuda.current_stream(dev))
         self._pf_stream.wait_event(ready)
-        plans, bms, status = sample_plans(specs, dev, bitmaps=True, stream=self._pf_stream,
+        plans, bms, status = sample_plans(specs, dev, bitmaps=True, stream=self._pf_stream, ahead=True,
                                           workspace=self._pf_ws, check=False, indices=False)
         ev = torch.cuda.Event()
         ev.record(self._pf_stream)

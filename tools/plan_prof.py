@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--full-idx", action="store_true")
+    ap.add_argument("--ahead", action="store_true", help="side-stream packing (the tracker's prefetch)")
     args = ap.parse_args()
     import torch
     from paper_2511_10333_b200.engine import gpt2_shapes
@@ -26,12 +27,13 @@ def main():
     for _ in range(args.reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        _, _, st = sample_plans(specs, bitmaps=True, indices=args.full_idx, check=False)
+        _, _, st = sample_plans(specs, bitmaps=True, indices=args.full_idx, check=False, ahead=args.ahead)
         b.record()
         torch.cuda.synchronize()
         assert int(st.max()) == 0
         ts.append(a.elapsed_time(b))
-    print(json.dumps({"plan_ms": ts, "steps": sum(c for _, c, _ in specs)}))
+    print(json.dumps({"plan_ms": ts, "steps": sum(c for _, c, _ in specs), "ahead": args.ahead,
+                      "full_idx": args.full_idx}))
 
 
 if __name__ == "__main__":
