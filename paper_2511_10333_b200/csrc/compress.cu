@@ -117,6 +117,13 @@ template <> struct VecT<4> {
     }
     __device__ static void unpack(const float4 &x, float (&v)[4]) { v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; }
 };
+template <> struct VecT<2> {
+    typedef float2 T;
+    __device__ static float2 ld(const float *p) { return __ldg(reinterpret_cast<const float2 *>(p)); }
+    __device__ static float2 ld_cs(const float *p) { return __ldcs(reinterpret_cast<const float2 *>(p)); }
+    __device__ static void st(float *p, const float (&v)[2]) { *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]); }
+    __device__ static void unpack(const float2 &x, float (&v)[2]) { v[0] = x.x; v[1] = x.y; }
+};
 template <> struct VecT<1> {
     typedef float T;
     __device__ static float ld(const float *p) { return __ldg(p); }
@@ -1575,7 +1582,7 @@ int tc_min_rank() {
 // Q partial over this tile's rows: thread owns VEC columns x RMAX ranks;
 // fp32 FMA over 32-row groups, fp64 across groups.
 template <int VEC, int RMAX>
-__global__ void __launch_bounds__(kP2Threads) k_pass2(const MatDev *mats, const Tile *tiles, const int32_t *status) {
+__global__ void __launch_bounds__(kP2Threads, VEC == 2 ? 3 : 1) k_pass2(const MatDev *mats, const Tile *tiles, const int32_t *status) {
     const Tile t = tiles[blockIdx.x];
     const MatDev &M = mats[t.mat];
     const int st = status[t.mat];
@@ -1726,6 +1733,12 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     // (a single matrix through the reference's per-matrix compress): then thinner strips, so
     // more clusters stream it (more Z partials to sum, a few KB each)
     int64_t zrows = kZRows;
+    int vec_rmax = 0;   // largest rank of the vector group (aligned, r <= kNarrow)
+    for (int k = 0; k < n; ++k) {
+        const edgc_compress_desc &d = descs[k];
+        const bool al4 = (d.n % 4 == 0) && (d.ld_g % 4 == 0) && ((uintptr_t)d.g % 16 == 0) && ((uintptr_t)d.w % 16 == 0);
+        if (al4 && std::max(d.r, d.r_res) <= kNarrow) vec_rmax = std::max(vec_rmax, std::max(d.r, d.r_res));
+    }
     {
         int64_t ctas = 0;
         for (int k = 0; k < n; ++k) {
@@ -1757,7 +1770,11 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.al4 = (d.n % 4 == 0) && (d.ld_g % 4 == 0) && ((uintptr_t)d.g % 16 == 0) &&
                         ((uintptr_t)d.w % 16 == 0);
         const bool v4 = M.al4 && std::max(d.r, d.r_res) <= kNarrow;
+        // vector group: float4 columns; pass 2 above rank 4 (r <= 8) takes float2 columns, so its
+        // per-thread fp64 Q partials halve and three CTAs fit an SM (measured: 4.8 -> 2.5 ms on
+        // the GPT2-2.5B set at r = 8; pass 1 stays float4, its row-block reduction dominates)
         M.vec = v4 ? 4 : 1;
+        const int vec2 = v4 ? (vec_rmax <= 4 ? 4 : 2) : 1;
         static const bool z_off = std::getenv("EDGC_NO_ZPATH") != nullptr;
         // cluster size: smallest of {1, 2, 3, 6, 7, 8} covering n with <= kTCW columns per CTA
         // (GPCs hold 18-20 SMs: 4- and 5-CTA clusters would strand SMs); balanced chunks
@@ -1839,7 +1856,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                 Tile t{k, c, c * threads1, std::min(slots, (c + 1) * threads1), r0, std::min(d.m, r0 + kP1Rows)};
                 (v4 ? P.t1v4 : P.t1v1).push_back(t);
             }
-        const int64_t slots2 = slots;
+        const int64_t slots2 = d.n / vec2;
         for (int32_t b = 0; b < M.nblk2; ++b)
             for (int64_t s0 = 0; s0 < slots2; s0 += kP2Threads) {
                 Tile t{k, b, s0, std::min(slots2, s0 + kP2Threads), (int64_t)b * kP2Rows,
@@ -2008,7 +2025,7 @@ int launch_pass2(const Plan &P, bool v4, const int32_t *status, cudaStream_t st)
     const unsigned grid = (unsigned)h.size();
     const int rmax = v4 ? P.rmax4 : P.rmax1;
     if (v4 && rmax <= 4) k_pass2<4, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
-    else if (v4) k_pass2<4, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
+    else if (v4) k_pass2<2, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
     else if (rmax <= 4) k_pass2<1, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
     else k_pass2<1, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
     EDGC_LAUNCH_CHECK();
