@@ -790,8 +790,9 @@ constexpr int kSBits = 14;
 constexpr int kSSize = 1 << kSBits;          // positions per set-mode bucket (M: 64 KB of shared memory)
 constexpr int kSWords = kSSize / 32;
 constexpr int kSChunk = 32768;               // steps per sort CTA (15-bit step-in-chunk)
-constexpr int kSMaxBuckets = 2048;           // N <= 2^25
-constexpr int kSMaxChunks = (1 << 25) / kSChunk;
+constexpr int kSMaxLog2N = 26;               // N <= 2^26 (GPT2-12.1B's largest, 51.4M, included)
+constexpr int kSMaxBuckets = (1 << kSMaxLog2N) / kSSize;
+constexpr int kSMaxChunks = (1 << kSMaxLog2N) / kSChunk;
 constexpr int kSSortThreads = 1024;
 constexpr int kSSortPer = kSChunk / kSSortThreads;
 constexpr int kSResThreads = 512;            // 2 CTAs per SM (104 KB of shared memory each)
@@ -850,12 +851,17 @@ __global__ void __launch_bounds__(kSSortThreads) k_set_sort(const PlanDev *plans
     }
 }
 
+// dynamic shared memory: M, the bucket's D bits, then the per-chunk segment tables sized by
+// the call's largest chunk count (3 CTAs per SM at GPT2-2.5B sizes, 2 at the largest N)
 struct SResSmem {
     int32_t M[kSSize];
     uint32_t bits[kSWords];            // D bits of the bucket
-    int32_t segoff[kSMaxChunks + 1];   // the bucket's segment length per sort chunk
-    int32_t segstart[kSMaxChunks];     // global start of the bucket's segment in each chunk
+    int32_t tab[1];                    // segoff[max_nch + 1] (segment lengths, then their prefix), segstart[max_nch]
 };
+
+inline size_t set_resolve_smem(int max_nch) {
+    return offsetof(SResSmem, tab) + sizeof(int32_t) * (2 * (size_t)max_nch + 1);
+}
 
 __device__ __forceinline__ void k_set_resolve_body(const PlanDev *plans, int n_plans, PlanLut lut, int64_t vb) {
     extern __shared__ __align__(16) unsigned char srm_raw[];
@@ -867,12 +873,13 @@ __device__ __forceinline__ void k_set_resolve_body(const PlanDev *plans, int n_p
     const int64_t pbase = (int64_t)b << kSBits;
     const int32_t ibase = (int32_t)(N - 1 - pbase);   // step s finalises position pbase + l iff s == ibase - l
     uint32_t *notlast = P.notlast;
+    int32_t *segoff = sm.tab, *segstart = sm.tab + nch + 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int c = tid; c < nch; c += kSResThreads) {
         const int32_t *row = P.segoff + (int64_t)c * (nb + 1);
         const int32_t r0 = row[b];
-        sm.segstart[c] = c * kSChunk + r0;
-        sm.segoff[c] = row[b + 1] - r0;
+        segstart[c] = c * kSChunk + r0;
+        segoff[c] = row[b + 1] - r0;
     }
     for (int l = tid; l < kSSize / 4; l += kSResThreads) reinterpret_cast<int4 *>(sm.M)[l] = make_int4(-1, -1, -1, -1);
     for (int w = tid; w < kSWords; w += kSResThreads) sm.bits[w] = 0u;
@@ -887,14 +894,14 @@ __device__ __forceinline__ void k_set_resolve_body(const PlanDev *plans, int n_p
         int32_t mx = 0;
 #pragma unroll
         for (int u = 0; u < kSResBatch; ++u) {
-            len[u] = c0 + u < nch ? sm.segoff[c0 + u] : 0;
+            len[u] = c0 + u < nch ? segoff[c0 + u] : 0;
             mx = max(mx, len[u]);
         }
         for (int32_t k0 = 0; k0 < mx; k0 += 32) {
             uint32_t e[kSResBatch];
 #pragma unroll
             for (int u = 0; u < kSResBatch; ++u)
-                if (k0 + lane < len[u]) e[u] = __ldg(P.lst_pk + sm.segstart[c0 + u] + k0 + lane);
+                if (k0 + lane < len[u]) e[u] = __ldg(P.lst_pk + segstart[c0 + u] + k0 + lane);
 #pragma unroll
             for (int u = 0; u < kSResBatch; ++u) {
                 if (k0 + lane >= len[u]) continue;
@@ -1032,6 +1039,11 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
     (void)descs_dev;
     int64_t blocks = 0;
     static const bool no_bucket = std::getenv("EDGC_PLAN_HEADTABLE") != nullptr;
+    // set mode when every plan of the call is bitmap-only (the tracker's plans): the order-free resolve
+    static const bool no_set = std::getenv("EDGC_PLAN_NOSET") != nullptr;
+    bool call_set = !no_set;
+    for (int i = 0; i < n; ++i)
+        if (!(plans[i].flags & EDGC_PLAN_BITMAP_ONLY) || plans[i].bitmap == nullptr) call_set = false;
     for (int i = 0; i < n; ++i) {
         const edgc_plan_desc &d = plans[i];
         EDGC_REQUIRE(d.n_elems >= 2 && d.n_elems < (int64_t(1) << 31), "plan %d: N=%lld outside [2, 2^31)", i,
@@ -1048,21 +1060,17 @@ int layout_plans(const edgc_plan_desc *plans, int n, void *ws, int64_t ws_bytes,
         P.bitmap = d.bitmap;
         P.full_idx = (d.flags & EDGC_PLAN_BITMAP_ONLY) ? 0 : 1;
         P.tail = (d.n_elems > 10000 && d.count > d.n_elems / 20) ? 1 : 0;
-        P.bucketed = (!no_bucket && P.tail && ceil_div(d.n_elems, kBSize) <= kBMaxBuckets) ? 1 : 0;
+        // bucket paths: the list resolve up to 2^25 positions, the set resolve (a call whose plans
+        // are all bitmap-only) up to 2^26
+        const int64_t bmax = call_set ? (int64_t(1) << kSMaxLog2N) : (int64_t)kBMaxBuckets * kBSize;
+        P.bucketed = (!no_bucket && P.tail && d.n_elems <= bmax) ? 1 : 0;
         P.step_block0 = blocks;
         blocks += ceil_div(d.count, kStepThreads);
     }
     L.step_blocks = blocks;
-    // set mode when every bucketed plan is bitmap-only (the tracker's plans): the order-free resolve
-    static const bool no_set = std::getenv("EDGC_PLAN_NOSET") != nullptr;
-    L.setmode = no_set ? 0 : 1;
     bool any_b = false;
-    for (int i = 0; i < n; ++i) {
-        if (!L.dev[i].bucketed) continue;
-        any_b = true;
-        if (L.dev[i].full_idx || L.dev[i].bitmap == nullptr) L.setmode = 0;
-    }
-    if (!any_b) L.setmode = 0;
+    for (int i = 0; i < n; ++i) any_b |= L.dev[i].bucketed != 0;
+    L.setmode = (call_set && any_b) ? 1 : 0;
     if (L.setmode) {
         int64_t words = 0;
         for (int i = 0; i < n; ++i)
@@ -1256,14 +1264,17 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
                 EDGC_CUDA_TRY(cudaFuncSetAttribute(k_set_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)sizeof(SSortSmem)));
                 EDGC_CUDA_TRY(cudaFuncSetAttribute(k_set_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)sizeof(SResSmem)));
+                                                   (int)set_resolve_smem(kSMaxChunks)));
                 sattr = true;
             }
             EDGC_CUDA_TRY(cudaMemsetAsync(L.notlast, 0, 4 * (size_t)L.notlast_words, st));
             k_set_sort<<<capped(L.bchunks, 1), kSSortThreads, sizeof(SSortSmem), st>>>(d_plans, n_plans, lut,
                                                                                         L.bchunks);
             EDGC_LAUNCH_CHECK();
-            k_set_resolve<<<capped(L.buckets, 3), kSResThreads, sizeof(SResSmem), st>>>(d_plans, n_plans, lut,
+            int max_nch = 1;
+            for (int i = 0; i < n_plans; ++i)
+                if (L.dev[i].setmode) max_nch = std::max(max_nch, (int)L.dev[i].nch);
+            k_set_resolve<<<capped(L.buckets, 3), kSResThreads, set_resolve_smem(max_nch), st>>>(d_plans, n_plans, lut,
                                                                                         L.buckets);
             EDGC_LAUNCH_CHECK();
             k_set_tail<<<capped(L.oblocks, 8), kSTailThreads, 0, st>>>(d_plans, n_plans, lut, L.oblocks);

@@ -478,7 +478,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
     }
 }
 
-// launch helper: persistent grid of min(tiles, SMs) CTAs
+// launch helper: persistent grid of min(tiles, SMs) CTAs (measured: a 4-wave grid, meant to let
+// free SMs absorb the CTAs of SMs the side-stream plans hold, is 3-10% slower alone and did not
+// remove the plan interference at GPT2-12.1B r = 256)
 template <int BN, int KCH, class Op>
 inline cudaError_t launch(const Op &op, int sms, cudaStream_t st) {
     using C = Cfg<BN, KCH, Op::kPF>;

@@ -104,3 +104,20 @@ def test_membership_bitmaps_match_oracle_sets(indices):
             # sample, tail-shuffle plans (set-mode resolve) step 0's output, NumPy's last sample
             tail = n > 10000 and c > n // 20
             assert got.size == 1 and got[0] == (ref[-1] if tail else ref[0])
+
+
+def test_set_resolve_beyond_2p25_positions():
+    """GPT2-12.1B's largest matrices (3584 x 14336 = 51.4M elements > 2^25) take the order-free set
+    resolve when the plans are bitmap-only: the bitmap equals NumPy's sampled set."""
+    from paper_2511_10333_b200.entropy import sample_count, sample_plans
+    n = 3584 * 14336
+    c = sample_count(n, 0.25)
+    plans, bms, status = sample_plans([(n, c, 41)], bitmaps=True, indices=False, ahead=True)
+    assert int(status.max()) == 0
+    ref = np.random.default_rng(41).choice(n, size=c, replace=False, shuffle=False)
+    words = to_np(bms[0]).astype(np.uint32)
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:n]
+    want = np.zeros(n, dtype=np.uint8)
+    want[ref] = 1
+    assert np.array_equal(bits, want)
+    assert int(to_np(plans[0])[0]) == int(ref[-1])
