@@ -155,12 +155,19 @@ __global__ void __launch_bounds__(kRedThreads) k_gauss_partial(const GaussDev *d
 
 __global__ void k_gauss_finish(const GaussDev *descs, int n, const double2 *partial, int nblk, double *h_out,
                                int32_t *status) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    // a warp per descriptor: lane-strided partial sums, then a fixed shuffle tree (deterministic)
+    const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
     if (i >= n) return;
     const int64_t cnt = descs[i].count;
-    if (cnt < 2) { status[i] = EDGC_EINVAL; h_out[i] = NAN; return; }
     double s1 = 0.0, s2 = 0.0;
-    for (int b = 0; b < nblk; ++b) { s1 += partial[(int64_t)i * nblk + b].x; s2 += partial[(int64_t)i * nblk + b].y; }
+    for (int b = lane; b < nblk; b += 32) { s1 += partial[(int64_t)i * nblk + b].x; s2 += partial[(int64_t)i * nblk + b].y; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane != 0) return;
+    if (cnt < 2) { status[i] = EDGC_EINVAL; h_out[i] = NAN; return; }
     const double nn = (double)cnt;
     double var = (s2 - s1 * (s1 / nn)) / (nn - 1.0);
     if (var < 0.0) var = 0.0;
@@ -719,7 +726,7 @@ extern "C" int edgc_entropy_gaussian(int src_dtype, const edgc_gauss_desc *descs
     else
         k_gauss_partial<double><<<kGaussBlocksPerDesc, kRedThreads, 0, st>>>(d, n, part);
     EDGC_LAUNCH_CHECK();
-    k_gauss_finish<<<(n + 127) / 128, 128, 0, st>>>(d, n, part, kGaussBlocksPerDesc, h_out, status_dev);
+    k_gauss_finish<<<(n + 3) / 4, 128, 0, st>>>(d, n, part, kGaussBlocksPerDesc, h_out, status_dev);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }
