@@ -786,7 +786,10 @@ __global__ void __launch_bounds__(kStepThreads) k_bucket_chain(const PlanDev *pl
 // step); k_set_resolve computes M in shared memory per bucket, stores the bucket's
 // D bits whole and marks !last steps; k_set_tail finishes the tail positions.
 // No chain lists, no per-position tables in HBM.
-constexpr int kSBits = 14;
+#ifndef EDGC_SET_BITS
+#define EDGC_SET_BITS 14
+#endif
+constexpr int kSBits = EDGC_SET_BITS;
 constexpr int kSSize = 1 << kSBits;          // positions per set-mode bucket (M: 64 KB of shared memory)
 constexpr int kSWords = kSSize / 32;
 constexpr int kSChunk = 32768;               // steps per sort CTA (15-bit step-in-chunk)
@@ -795,7 +798,10 @@ constexpr int kSMaxBuckets = (1 << kSMaxLog2N) / kSSize;
 constexpr int kSMaxChunks = (1 << kSMaxLog2N) / kSChunk;
 constexpr int kSSortThreads = 1024;
 constexpr int kSSortPer = kSChunk / kSSortThreads;
-constexpr int kSResThreads = 512;            // 2 CTAs per SM (104 KB of shared memory each)
+// measured (plan_prof, GPT2-2.5B): 16K-position buckets, 512 threads, 3 CTAs/SM 2.78 ms;
+// 8K buckets, 256 threads, 6/SM 2.88 ms; 16K, 256 threads 3.30 ms
+constexpr int kSResThreads = (1 << kSBits) <= 8192 ? 256 : 512;
+constexpr int kSResPerSM = (1 << kSBits) <= 8192 ? 6 : 3;
 constexpr int kSResBatch = 4;                // segments whose loads a warp keeps in flight
 constexpr int kSTailThreads = 256;           // a warp per bitmap word
 constexpr int kSTailWords = 4;               // words per warp (independent loads in flight)
@@ -926,7 +932,7 @@ __device__ __forceinline__ void k_set_resolve_body(const PlanDev *plans, int n_p
         if (w0 + w < nw) P.bitmap[w0 + w] = sm.bits[w];
 }
 
-__global__ void __launch_bounds__(kSResThreads, 3) k_set_resolve(const PlanDev *plans, int n_plans, PlanLut lut,
+__global__ void __launch_bounds__(kSResThreads, kSResPerSM) k_set_resolve(const PlanDev *plans, int n_plans, PlanLut lut,
                                                                  int64_t nvb) {
     for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
         k_set_resolve_body(plans, n_plans, lut, vb);
@@ -1274,7 +1280,7 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
             int max_nch = 1;
             for (int i = 0; i < n_plans; ++i)
                 if (L.dev[i].setmode) max_nch = std::max(max_nch, (int)L.dev[i].nch);
-            k_set_resolve<<<capped(L.buckets, 3), kSResThreads, set_resolve_smem(max_nch), st>>>(d_plans, n_plans, lut,
+            k_set_resolve<<<capped(L.buckets, kSResPerSM), kSResThreads, set_resolve_smem(max_nch), st>>>(d_plans, n_plans, lut,
                                                                                         L.buckets);
             EDGC_LAUNCH_CHECK();
             k_set_tail<<<capped(L.oblocks, 8), kSTailThreads, 0, st>>>(d_plans, n_plans, lut, L.oblocks);
