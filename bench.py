@@ -205,31 +205,56 @@ def cpu_reference_sample(shapes, rank, alpha, beta, seed, steps):
 
 
 def run_reference(args):
+    """The reference's CPU path (oracle port) for W + K steps, each a bounded sample of the workload:
+    one GPT-2 layer (4 matrices) through train_toy's per-step calls -- compress -> decompress with
+    error feedback (compressor.py:94-133) and, on every round(1/alpha)-th step, the worker-0 entropy
+    of the layer (Generator.choice + std, entropy.py:67-90) -- timed per step on the host."""
     rank_env = int(os.environ.get("RANK", "0"))
     if rank_env != 0:
         return 0
+    import numpy as np
+
+    import oracle
     from paper_2511_10333_b200.engine import gpt2_shapes
     shapes = gpt2_shapes(args.model, args.layers)
-    total = sum(m * n for m, n in shapes)
-    vals = []
-    det = None
-    for _ in range(max(1, args.warmup and 1)):
-        cpu_reference_sample(shapes, args.rank, args.alpha, args.beta, args.seed, 1)
-    for _ in range(max(1, min(args.steps, 3))):
-        v, det = cpu_reference_sample(shapes, args.rank, args.alpha, args.beta, args.seed, args.cpu_steps)
-        vals.append(v)
-    value = statistics.median(vals)
-    ms = 4.0 * total / (value * 1e9) * 1e3
+    layer = shapes[:4]
+    elems = sum(m * n for m, n in layer)
+    cores = len(os.sched_getaffinity(0))
+    grads = [oracle.synth_matrix(args.seed, 0, k, 0, m, n, 1e-2).astype(np.float64) for k, (m, n) in enumerate(layer)]
+    seeds = oracle.state_seeds(args.seed, 1, len(layer))
+    states = [[oracle.OracleState(m, n, min(args.rank, m, n), seeds[(0, k)]) for k, (m, n) in enumerate(layer)]]
+    period = max(1, round(1.0 / args.alpha))
+
+    def one_step(t):
+        oracle.dp_step([grads], states)
+        if t % period == 0:
+            for k, g in enumerate(grads):
+                cnt = oracle.sample_count(g.size, args.beta)
+                sub = g.ravel() if cnt == g.size else g.ravel()[np.random.default_rng(
+                    oracle.subsample_seed(args.seed, t, k)).choice(g.size, size=cnt, replace=False, shuffle=False)]
+                oracle.gaussian_entropy(sub)
+
+    for t in range(args.warmup):
+        one_step(t)
+    t0 = time.perf_counter()
+    for t in range(args.warmup, args.warmup + args.steps):
+        one_step(t)
+    dt = time.perf_counter() - t0
+    value = 4.0 * elems * args.steps / dt / 1e9
+    sample = (f"each step: 1 GPT-2 layer ({len(layer)} matrices, {elems / 1e6:.1f}M fp64 elements) of the "
+              f"{len(shapes)}-matrix set through compress+decompress with error feedback at r={args.rank} "
+              f"(NumPy f64 / OpenBLAS), plus the layer's entropy (Generator.choice + std, beta={args.beta}) on "
+              f"every {period}th step; {args.steps} timed steps after {args.warmup} warm-up steps")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(args, shapes),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": det["cores"], "kind": "port",
-                         "sample": det["sample"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference CPU path = oracle port (NumPy float64, OpenBLAS on all host cores; choice/MGS "
-                "single-threaded as in NumPy); ms_per_step scaled from the one-layer sample to the full set",
+                "single-threaded as in NumPy); a step is the one-layer sample, so ms_per_step is measured, "
+                "not extrapolated",
     }
     print(json.dumps(line), flush=True)
     return 0
