@@ -74,6 +74,9 @@ def parse_args():
                     help="gather the sampled-iteration statistics inside pass 1 instead of a separate Gaussian "
                          "pass over the bitmaps (measured: the separate pass is cheaper -- 9.2 GB at ~HBM speed "
                          "vs +47%% instructions in pass 1)")
+    ap.add_argument("--exchange", choices=["auto", "p2p", "nccl"], default="auto",
+                    help="N > 1: read the peers' factors in place over NVLink (p2p, the default where the "
+                         "reconstruction allows it) or all-gather them with NCCL first")
     ap.add_argument("--cpu-steps", type=int, default=6, help="EF steps in the bounded CPU sample")
     return ap.parse_args()
 
@@ -267,6 +270,8 @@ def config_dict(args, shapes):
             "rank": args.rank, "alpha": args.alpha, "beta": args.beta, "estimator": "gaussian_plugin",
             "l2": "inputs 9.2 GB/GPU >> 126 MB L2 (no flush needed)" if args.model == "2.5B" and args.layers is None
             else "inputs larger than L2", "parallelism": f"dp{args.gpus}",
+            "exchange": getattr(args, "exchange_eff", getattr(args, "exchange", "auto")) if args.gpus > 1
+            else "none (1 rank)",
             "entropy_stats": "gathered in pass 1" if getattr(args, "fuse_entropy", True) else "separate Gaussian pass",
             "entropy_plans": {"prefetch": "side stream, built during the preceding iterations",
                               "inline": "built inside the sampled iteration", "off": "tracker disabled"}[args.entropy],
@@ -296,7 +301,11 @@ def run_ours(args):
     shapes = gpt2_shapes(args.model, args.layers)
     total = sum(m * n for m, n in shapes)
     alias = args.alias_output or args.model == "12.1B"
-    eng = BucketEngine(shapes, rank=args.rank, seed=args.seed, world_size=world, rank_id=me, alias_output=alias)
+    eng = BucketEngine(shapes, rank=args.rank, seed=args.seed, world_size=world, rank_id=me, alias_output=alias,
+                       exchange=args.exchange)
+    if world > 1:
+        args.exchange_eff = ("p2p: device-initiated pull of every rank's factors over NVLink (CUDA IPC, "
+                             "device flags), no collective call" if eng._p2p else "nccl all_gather_into_tensor")
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + me)
     chunk = 1 << 28

@@ -29,6 +29,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstring>
 #include <cmath>
 #include <cstdlib>
 #include <type_traits>
@@ -2153,6 +2154,12 @@ __host__ __device__ constexpr int v4_tile_rows(int wr) { return wr <= 8 ? 64 : 2
 #ifndef EDGC_RECON32_MINB
 #define EDGC_RECON32_MINB 2   // CTAs per SM for W*r = 32 (2 caps registers at 128: Q partly spills)
 #endif
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
+    int64_t v;
+    asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <int WR, int VC>
 __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1) k_recon4(const ReconDev *descs, const RTile *tiles) {
     constexpr int NT = kV4Cols / VC;
@@ -2162,13 +2169,16 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
     const int r = D.r, wr = D.r * D.n_ranks;
     const int64_t j0 = t.col0 + VC * threadIdx.x;
     const bool active = j0 < t.col1;
+    // rank w's P_k / Q_k in the gathered buffer
+    auto p_of = [&](int w) -> const float * { return D.p + (int64_t)w * D.p_stride; };
+    auto q_of = [&](int w) -> const float * { return D.q + (int64_t)w * D.q_stride; };
     // P tile transposed ([k][row]): one 16-byte shared read gives 4 rows of one k
     __shared__ __align__(16) float s_pT[WR][kV4TileRows];
     // thread = (row, rank): its r consecutive P values; (worker, k) indexed incrementally (no div/mod)
     for (int e = threadIdx.x; e < kV4TileRows * D.n_ranks; e += NT) {
         const int rr = e % kV4TileRows, w = e / kV4TileRows;
         const int64_t i = t.row0 + rr;
-        const float *src = D.p + (int64_t)w * D.p_stride + i * r;
+        const float *src = p_of(w) + i * r;
         for (int k = 0; k < r; ++k) s_pT[w * r + k][rr] = i < t.row1 ? src[k] : 0.f;
     }
     for (int e = threadIdx.x; e < kV4TileRows * (WR - wr); e += NT)   // zero padding columns
@@ -2176,13 +2186,16 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
     float q[VC][WR];
 #pragma unroll
     for (int v = 0; v < VC; ++v) {
-        const float *qp = D.q + (j0 + v) * r;
-        int k = 0;
-        int64_t wo = 0;
+        int k = 0, w = 0;
+        const float *qp = q_of(0) + (j0 + v) * r;
 #pragma unroll
         for (int c = 0; c < WR; ++c) {
-            q[v][c] = (active && c < wr) ? __ldg(qp + wo + k) : 0.f;
-            if (++k == r) { k = 0; wo += D.q_stride; }
+            q[v][c] = (active && c < wr) ? __ldg(qp + k) : 0.f;
+            if (++k == r) {
+                k = 0;
+                ++w;
+                if (c + 1 < wr) qp = q_of(w) + (j0 + v) * r;
+            }
         }
     }
     __syncthreads();
@@ -2616,6 +2629,107 @@ extern "C" int edgc_recon_plan_run(edgc_recon_plan *h, void *stream) {
     }
     if (!h->P.tilesC.empty())
         EDGC_CUDA_TRY((tc::launch<128, 4>(TcRecon{h->P.dd, h->P.dtc, (int)h->P.tilesC.size()}, sm_count(), st)));
+    return EDGC_OK;
+}
+
+namespace edgc {
+namespace {
+__global__ void k_p2p_signal(int64_t *const *peer_flags, int me, int nranks, int64_t epoch) {
+    // this rank's factors (written by the kernels before this one on the stream) are complete:
+    // publish the step number into slot `me` of every rank's flags, release at system scope
+    const int w = threadIdx.x;
+    if (w >= nranks) return;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(peer_flags[w] + me), "l"(epoch) : "memory");
+}
+}  // namespace
+}  // namespace edgc
+
+namespace edgc {
+namespace {
+// gathered[w * n .. (w + 1) * n) <- rank w's buffer, read over NVLink once rank w's flag for this
+// step is up: kPullCtas CTAs per rank, 16-byte loads (8 in flight per thread), local stores
+constexpr int kPullCtas = 32, kPullThreads = 256;
+__global__ void __launch_bounds__(kPullThreads) k_p2p_pull(const float *const *bases, float *gathered, int64_t n,
+                                                           const int64_t *flags, int64_t epoch) {
+    const int w = blockIdx.y;
+    if (threadIdx.x == 0)
+        while (ld_acquire_sys(flags + w) < epoch) __nanosleep(64);
+    __syncthreads();
+    const float *src = bases[w];
+    float *dst = gathered + (int64_t)w * n;
+    const int64_t n4 = ((uintptr_t)src % 16 == 0 && (uintptr_t)dst % 16 == 0) ? n / 4 : 0;
+    const int64_t stride = (int64_t)kPullCtas * kPullThreads;
+    const float4 *s4 = reinterpret_cast<const float4 *>(src);
+    float4 *d4 = reinterpret_cast<float4 *>(dst);
+    for (int64_t i0 = (int64_t)blockIdx.x * kPullThreads + threadIdx.x; i0 < n4; i0 += 8 * stride) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (i0 + u * stride < n4) v[u] = __ldcv(s4 + i0 + u * stride);   // volatile: never a stale L1 line
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (i0 + u * stride < n4) d4[i0 + u * stride] = v[u];
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * kPullThreads + threadIdx.x; i < n; i += stride)
+        dst[i] = __ldcv(src + i);
+}
+}  // namespace
+}  // namespace edgc
+
+extern "C" int edgc_p2p_pull(const float *const *bases_dev, float *gathered, int64_t n, int nranks,
+                             const int64_t *flags_dev, int64_t epoch, void *stream) {
+    EDGC_REQUIRE(bases_dev && gathered && flags_dev && n >= 0 && nranks >= 1, "edgc_p2p_pull: bad arguments");
+    if (n == 0) return EDGC_OK;
+    k_p2p_pull<<<dim3(kPullCtas, nranks), kPullThreads, 0, (cudaStream_t)stream>>>(bases_dev, gathered, n, flags_dev,
+                                                                                  epoch);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+extern "C" int edgc_p2p_signal(int64_t *const *peer_flags_dev, int me, int nranks, int64_t epoch, void *stream) {
+    EDGC_REQUIRE(peer_flags_dev && nranks >= 1 && nranks <= 1024 && me >= 0 && me < nranks,
+                 "edgc_p2p_signal: bad arguments");
+    k_p2p_signal<<<1, ((nranks + 31) / 32) * 32, 0, (cudaStream_t)stream>>>(peer_flags_dev, me, nranks, epoch);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (no libcuda link)
+typedef int (*MemRangeFn)(unsigned long long *base, size_t *size, unsigned long long dptr);
+
+extern "C" int edgc_ipc_handle(const void *ptr, void *handle64, int64_t *offset) {
+    EDGC_REQUIRE(ptr && handle64 && offset, "edgc_ipc_handle: bad arguments");
+    static MemRangeFn range = nullptr;
+    if (!range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        EDGC_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        EDGC_REQUIRE(fn && q == cudaDriverEntryPointSuccess, "edgc_ipc_handle: cuMemGetAddressRange unavailable");
+        range = (MemRangeFn)fn;
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    EDGC_REQUIRE(range(&base, &size, (unsigned long long)(uintptr_t)ptr) == 0,
+                 "edgc_ipc_handle: cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    EDGC_CUDA_TRY(cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base));
+    memcpy(handle64, &h, sizeof(h));
+    *offset = (int64_t)((uintptr_t)ptr - (uintptr_t)base);
+    return EDGC_OK;
+}
+
+extern "C" int edgc_ipc_open(const void *handle64, void **ptr) {
+    EDGC_REQUIRE(handle64 && ptr, "edgc_ipc_open: bad arguments");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    EDGC_CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return EDGC_OK;
+}
+
+extern "C" int edgc_ipc_close(void *ptr) {
+    EDGC_REQUIRE(ptr, "edgc_ipc_close: null pointer");
+    EDGC_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
     return EDGC_OK;
 }
 

@@ -51,7 +51,8 @@ def edgc_setup(shapes, *, table_trials: int = 64, seed: int = 0, bandwidth: floa
 class EdgcDataParallel:
     def __init__(self, shapes, *, total_iterations: int, seed: int = 0, world_size: int = 1, rank_id: int = 0,
                  group=None, sampler: SamplerConfig = SamplerConfig(), window: int = 100, step_limit: int = 8,
-                 warmup_floor: float = 0.10, table_trials: int = 64, bandwidth: float = 1e9, element_size: int = 4):
+                 warmup_floor: float = 0.10, table_trials: int = 64, bandwidth: float = 1e9, element_size: int = 4,
+                 exchange: str = "auto"):
         self.shapes = [(int(m), int(n)) for m, n in shapes]
         self.world, self.me, self.group = world_size, rank_id, group
         self.model, bounds, self.table = edgc_setup(self.shapes, table_trials=table_trials, seed=seed,
@@ -61,7 +62,7 @@ class EdgcDataParallel:
                                        warmup_floor=warmup_floor, total_iterations=total_iterations)
         self.tracker = EntropyTracker(sampler, window) if rank_id == 0 else None
         self.engine = BucketEngine(self.shapes, rank=bounds.r_max, seed=seed, world_size=world_size,
-                                   rank_id=rank_id, group=group, rank_cap=bounds.r_max)
+                                   rank_id=rank_id, group=group, rank_cap=bounds.r_max, exchange=exchange)
         self.rank_history: list[RankDecision] = []
         self.bytes_per_step: list[float] = []
         self._raw_avg = None

@@ -137,13 +137,24 @@ class BucketEngine:
 
     def __init__(self, shapes, rank: int, seed: int = 0, *, world_size: int = 1, rank_id: int = 0, group=None,
                  rank_cap: int | None = None, col_tol: float = DEVICE_COLUMN_TOL, device=None,
-                 alias_output: bool = False):
+                 alias_output: bool = False, exchange: str = "auto"):
+        """exchange (W > 1): "p2p" gathers every rank's packed factors with a device-initiated pull over
+        NVLink (CUDA IPC mappings, a device flag per rank and step, no collective call); "nccl" with
+        all_gather_into_tensor; "auto" = p2p on an NCCL process group (one node)."""
         self.L = _lib.lib()
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.shapes = [(int(m), int(n)) for m, n in shapes]
         if not self.shapes:
             raise ValueError("need at least one matrix")
         self.world, self.me, self.group = int(world_size), int(rank_id), group
+        if exchange not in ("auto", "p2p", "nccl"):
+            raise ValueError(f"exchange must be 'auto', 'p2p' or 'nccl', got {exchange!r}")
+        self._p2p = False
+        if self.world > 1 and exchange != "nccl":
+            import torch.distributed as dist
+            self._p2p = exchange == "p2p" or dist.get_backend(group) == "nccl"
+        self._flags = None          # p2p: int64[W] completion flags, written by the peers
+        self._epoch = 0             # p2p: steps published so far
         self.col_tol = float(col_tol)
         self.cap = max(int(rank), int(rank_cap or rank))
         seeds = state_seeds(seed, self.world, len(self.shapes))
@@ -209,8 +220,63 @@ class BucketEngine:
         self.factors = new_fac
         self.cap = cap
         self._gathered = None
-        if self.world > 1:
+        self._fsz = fsz
+        if self.world > 1 and not self._p2p:
             self._gathered = torch.empty(self.world * fsz, dtype=torch.float32, device=dev)
+        if self._p2p:
+            self._share_factors()
+
+    def _share_factors(self):
+        """Map every rank's two factor buffers and flag array into this process on this rank's device
+        (CUDA IPC handles of the allocations holding them, exchanged once per buffer allocation
+        through the process group) and build the device pointer tables."""
+        import torch.distributed as dist
+        dev = self.device
+        if self._flags is None:
+            self._flags = torch.zeros(self.world, dtype=torch.int64, device=dev)
+        mine = []
+        for t in (self.factors[0], self.factors[1], self._flags):
+            handle = ctypes.create_string_buffer(64)
+            off = ctypes.c_int64()
+            _lib.check(self.L.edgc_ipc_handle(ctypes.c_void_p(t.data_ptr()), handle, ctypes.byref(off)),
+                       "edgc_ipc_handle")
+            mine.append((handle.raw, int(off.value)))
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=self.group)
+        self._close_peers()
+        opened = {}
+        table = []
+        for w, recs in enumerate(everyone):
+            if w == self.me:
+                table.append([t.data_ptr() for t in (self.factors[0], self.factors[1], self._flags)])
+                continue
+            row = []
+            for handle, off in recs:
+                if handle not in opened:   # one mapping per allocation (buffers may share one)
+                    p = ctypes.c_void_p()
+                    _lib.check(self.L.edgc_ipc_open(ctypes.c_char_p(handle), ctypes.byref(p)), "edgc_ipc_open")
+                    opened[handle] = p.value
+                row.append(opened[handle] + off)
+            table.append(row)
+        self._ipc_mapped = list(opened.values())
+        self._peer_bases = [torch.tensor([row[par] for row in table], dtype=torch.int64, device=dev)
+                            for par in (0, 1)]
+        self._peer_flags = torch.tensor([row[2] for row in table], dtype=torch.int64, device=dev)
+        torch.cuda.synchronize(dev)
+        # every rank must hold its mappings before any rank starts publishing into them
+        dist.barrier(group=self.group)
+
+    def _close_peers(self):
+        for p in getattr(self, "_ipc_mapped", []):
+            try:
+                self.L.edgc_ipc_close(ctypes.c_void_p(p))
+            except Exception:
+                pass
+        self._ipc_mapped = []
+
+    def _ensure_gathered(self):
+        if self._gathered is None:
+            self._gathered = torch.empty(self.world * self._fsz, dtype=torch.float32, device=self.device)
 
     def _packed_offsets(self, ranks):
         return packed_offsets(self.shapes, ranks)
@@ -269,6 +335,8 @@ class BucketEngine:
         if plan is not None:
             return plan
         offs, size = self._packed_offsets(ranks)
+        if self.world > 1:
+            self._ensure_gathered()
         src = self.factors[self._parity] if self.world == 1 else self._gathered
         descs = []
         for k, ((m, n), r) in enumerate(zip(self.shapes, ranks)):
@@ -304,10 +372,24 @@ class BucketEngine:
         self._compress_plan().set_sampling(descs, partials, _lib.stream_ptr(self.device))
 
     def exchange(self):
-        """Phase 2: all-gather the packed factors of every rank (NCCL); no-op at W = 1."""
+        """Phase 2, W > 1: every rank's packed factors into the gathered buffer, in rank order.
+        p2p: publish a device flag into every rank's flag array, then pull each rank's buffer over
+        NVLink once its flag for this step is up (no host synchronisation, no collective call);
+        nccl: one all_gather_into_tensor.  No-op at W = 1."""
         if self.world == 1:
             return
+        self._ensure_gathered()
         _, size = self._packed_offsets(self.ranks)
+        if self._p2p:
+            self._epoch += 1
+            stream = _lib.stream_ptr(self.device)
+            _lib.check(self.L.edgc_p2p_signal(_lib.ptr(self._peer_flags), self.me, self.world, self._epoch, stream),
+                       "edgc_p2p_signal")
+            # each rank's packed buffer is laid out identically: copy the first `size` floats of each
+            # into slots of self._fsz (the gathered layout's rank stride is the packed size)
+            _lib.check(self.L.edgc_p2p_pull(_lib.ptr(self._peer_bases[self._parity]), _lib.ptr(self._gathered), size,
+                                            self.world, _lib.ptr(self._flags), self._epoch, stream), "edgc_p2p_pull")
+            return
         gather_packed(self.factors[self._parity][:size], self._gathered, self.world, self.group)
 
     def reconstruct(self):

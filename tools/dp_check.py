@@ -6,9 +6,10 @@ oracle.dp_step) computed from the same per-worker gradients and basis seeds
 (grad_source.py:440-447).  Cases:
 
 * ``engine_*``: BucketEngine chained over a few steps at r well below
-  min(m, n): r = 4 (CUDA-core reconstruction), r = 32 (W r >= 64: the
-  rank-blocked tcgen05 reconstruction), r = 128 (tcgen05 compress + recon), and
-  one full GPT2-2.5B layer per rank at r = 4;
+  min(m, n): r = 4 (CUDA-core reconstruction; the factors gathered by the
+  device-initiated NVLink pull, and the same through NCCL), r = 8, r = 32
+  (W r >= 64: the rank-blocked tcgen05 reconstruction), r = 128 (tcgen05
+  compress + recon), and one full GPT2-2.5B layer per rank at r = 4;
 * ``driver``: EdgcDataParallel through warm-up (uncompressed NCCL average) into
   the active phase, with the window decisions broadcast from rank 0 only on
   window-close iterations.  The rank history must equal the LIVE reference's
@@ -43,6 +44,8 @@ WIDE = [(1024, 3072), (1024, 1024), (1024, 4096), (4096, 1024)]
 
 CASES = {
     "engine_r4": dict(shapes=SMALL, rank=4, steps=4, tol=5e-5),
+    "engine_r4_nccl": dict(shapes=SMALL, rank=4, steps=4, tol=5e-5, exchange="nccl"),
+    "engine_r8_p2p": dict(shapes=MID, rank=8, steps=4, tol=5e-5, exchange="p2p"),
     "engine_r32": dict(shapes=MID, rank=32, steps=4, tol=5e-5),
     "engine_r128": dict(shapes=WIDE, rank=128, steps=3, tol=5e-5),
     "engine_gpt2_layer_r4": dict(shapes=list(GPT2_2P5B_LAYER), rank=4, steps=2, tol=5e-5),
@@ -67,7 +70,8 @@ def engine_case(name, spec, world, me, dev):
     shapes, rank, steps = spec["shapes"], spec["rank"], spec["steps"]
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    eng = BucketEngine(shapes, rank=rank, seed=0, world_size=world, rank_id=me)
+    eng = BucketEngine(shapes, rank=rank, seed=0, world_size=world, rank_id=me,
+                       exchange=spec.get("exchange", "auto"))
     seeds = oracle.state_seeds(0, world, len(shapes))
     ost = [[oracle.OracleState(m, n, min(rank, m, n), seeds[(w, k)]) for k, (m, n) in enumerate(shapes)]
            for w in range(world)] if me == 0 else None
@@ -83,8 +87,9 @@ def engine_case(name, spec, world, me, dev):
                 worst = max(worst, rel(o.double().cpu().numpy(), r))
     copies = gather_np(eng.out_arena[:1 << 16].clone(), world)  # every rank must hold the same average
     same = all(np.array_equal(c, copies[0]) for c in copies)
+    mode = "p2p" if eng._p2p else "nccl"
     rec = {"case": name, "world": world, "rank": rank, "shapes": [list(s) for s in shapes], "steps": steps,
-           "worst_rel_err": worst, "tol": spec["tol"], "ranks_identical": same,
+           "exchange": mode, "worst_rel_err": worst, "tol": spec["tol"], "ranks_identical": same,
            "recon_rank": world * rank, "wall_s": round(time.perf_counter() - t0, 2)}
     rec["ok"] = bool(worst <= spec["tol"] and same) if me == 0 else None
     return rec
