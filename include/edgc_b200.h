@@ -238,14 +238,16 @@ void edgc_recon_plan_destroy(edgc_recon_plan *plan);
 /* Device-initiated all-gather over NVLink (replaces the NCCL all-gather in front
  * of edgc_recon_plan_run, grad_source.py:404-408): every rank's packed factor
  * buffer and int64 flag array are mapped into every process by CUDA IPC.
- * edgc_p2p_signal publishes "my factors of step `epoch` are complete" into slot
- * `me` of every rank's flags (peer_flags_dev[w] = rank w's flags as mapped here;
- * release, system scope); edgc_p2p_pull waits for each rank's slot in its own
- * flags (acquire) and copies rank w's n floats from bases_dev[w] into
- * gathered[w n ..) -- the gathered layout the reconstruction plans read. */
+ * edgc_p2p_signal publishes "my factors of step *counter_dev + 1 are complete"
+ * into slot `me` of every rank's flags (peer_flags_dev[w] = rank w's flags as
+ * mapped here; release, system scope) and advances the device counter;
+ * edgc_p2p_pull waits until each rank's slot in its own flags reaches the counter
+ * (acquire) and copies rank w's n floats from bases_dev[w] into gathered[w n ..)
+ * -- the gathered layout the reconstruction plans read.  The step number lives on
+ * the device, so the pair can be captured in a CUDA graph. */
 int edgc_p2p_pull(const float *const *bases_dev, float *gathered, int64_t n, int nranks,
-                  const int64_t *flags_dev, int64_t epoch, void *stream);
-int edgc_p2p_signal(int64_t *const *peer_flags_dev, int me, int nranks, int64_t epoch, void *stream);
+                  const int64_t *flags_dev, const int64_t *counter_dev, void *stream);
+int edgc_p2p_signal(int64_t *const *peer_flags_dev, int me, int nranks, int64_t *counter_dev, void *stream);
 /* The 64-byte cudaIpcMemHandle of the allocation holding device pointer ptr,
  * and ptr's byte offset in it; map a peer process's allocation into this
  * process on the current device, peer access enabled; and unmap it. */

@@ -90,8 +90,8 @@ SIGNATURES = {
     "edgc_recon_plan_bind": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "edgc_recon_plan_run": (c_i32, [c_vp, c_vp]),
     "edgc_recon_plan_destroy": (None, [c_vp]),
-    "edgc_p2p_pull": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
-    "edgc_p2p_signal": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_vp]),
+    "edgc_p2p_pull": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "edgc_p2p_signal": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
     "edgc_ipc_handle": (c_i32, [c_vp, c_vp, c_vp]),
     "edgc_ipc_open": (c_i32, [c_vp, c_vp]),
     "edgc_ipc_close": (c_i32, [c_vp]),

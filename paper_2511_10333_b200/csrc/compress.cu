@@ -2634,13 +2634,19 @@ extern "C" int edgc_recon_plan_run(edgc_recon_plan *h, void *stream) {
 
 namespace edgc {
 namespace {
-__global__ void k_p2p_signal(int64_t *const *peer_flags, int me, int nranks, int64_t epoch) {
+__global__ void k_p2p_signal(int64_t *const *peer_flags, int me, int nranks, int64_t *counter) {
     // this rank's factors (written by the kernels before this one on the stream) are complete:
-    // publish the step number into slot `me` of every rank's flags, release at system scope
+    // publish the next step number into slot `me` of every rank's flags, release at system
+    // scope, and advance this rank's device counter (graph replays see the live count)
     const int w = threadIdx.x;
-    if (w >= nranks) return;
-    __threadfence_system();
-    asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(peer_flags[w] + me), "l"(epoch) : "memory");
+    const int64_t epoch = *counter + 1;
+    __syncthreads();
+    if (w < nranks) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(peer_flags[w] + me), "l"(epoch) : "memory");
+    }
+    __syncthreads();
+    if (w == 0) *counter = epoch;
 }
 }  // namespace
 }  // namespace edgc
@@ -2651,10 +2657,12 @@ namespace {
 // step is up: kPullCtas CTAs per rank, 16-byte loads (8 in flight per thread), local stores
 constexpr int kPullCtas = 32, kPullThreads = 256;
 __global__ void __launch_bounds__(kPullThreads) k_p2p_pull(const float *const *bases, float *gathered, int64_t n,
-                                                           const int64_t *flags, int64_t epoch) {
+                                                           const int64_t *flags, const int64_t *counter) {
     const int w = blockIdx.y;
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
+        const int64_t epoch = *counter;   // this rank's step number, advanced by its k_p2p_signal
         while (ld_acquire_sys(flags + w) < epoch) __nanosleep(64);
+    }
     __syncthreads();
     const float *src = bases[w];
     float *dst = gathered + (int64_t)w * n;
@@ -2678,19 +2686,20 @@ __global__ void __launch_bounds__(kPullThreads) k_p2p_pull(const float *const *b
 }  // namespace edgc
 
 extern "C" int edgc_p2p_pull(const float *const *bases_dev, float *gathered, int64_t n, int nranks,
-                             const int64_t *flags_dev, int64_t epoch, void *stream) {
-    EDGC_REQUIRE(bases_dev && gathered && flags_dev && n >= 0 && nranks >= 1, "edgc_p2p_pull: bad arguments");
+                             const int64_t *flags_dev, const int64_t *counter_dev, void *stream) {
+    EDGC_REQUIRE(bases_dev && gathered && flags_dev && counter_dev && n >= 0 && nranks >= 1,
+                 "edgc_p2p_pull: bad arguments");
     if (n == 0) return EDGC_OK;
     k_p2p_pull<<<dim3(kPullCtas, nranks), kPullThreads, 0, (cudaStream_t)stream>>>(bases_dev, gathered, n, flags_dev,
-                                                                                  epoch);
+                                                                                  counter_dev);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }
 
-extern "C" int edgc_p2p_signal(int64_t *const *peer_flags_dev, int me, int nranks, int64_t epoch, void *stream) {
-    EDGC_REQUIRE(peer_flags_dev && nranks >= 1 && nranks <= 1024 && me >= 0 && me < nranks,
+extern "C" int edgc_p2p_signal(int64_t *const *peer_flags_dev, int me, int nranks, int64_t *counter_dev, void *stream) {
+    EDGC_REQUIRE(peer_flags_dev && counter_dev && nranks >= 1 && nranks <= 1024 && me >= 0 && me < nranks,
                  "edgc_p2p_signal: bad arguments");
-    k_p2p_signal<<<1, ((nranks + 31) / 32) * 32, 0, (cudaStream_t)stream>>>(peer_flags_dev, me, nranks, epoch);
+    k_p2p_signal<<<1, ((nranks + 31) / 32) * 32, 0, (cudaStream_t)stream>>>(peer_flags_dev, me, nranks, counter_dev);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }

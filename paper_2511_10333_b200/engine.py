@@ -154,7 +154,6 @@ class BucketEngine:
             import torch.distributed as dist
             self._p2p = exchange == "p2p" or dist.get_backend(group) == "nccl"
         self._flags = None          # p2p: int64[W] completion flags, written by the peers
-        self._epoch = 0             # p2p: steps published so far
         self.col_tol = float(col_tol)
         self.cap = max(int(rank), int(rank_cap or rank))
         seeds = state_seeds(seed, self.world, len(self.shapes))
@@ -234,6 +233,7 @@ class BucketEngine:
         dev = self.device
         if self._flags is None:
             self._flags = torch.zeros(self.world, dtype=torch.int64, device=dev)
+            self._epoch_dev = torch.zeros(1, dtype=torch.int64, device=dev)   # steps published (device)
         mine = []
         for t in (self.factors[0], self.factors[1], self._flags):
             handle = ctypes.create_string_buffer(64)
@@ -381,14 +381,14 @@ class BucketEngine:
         self._ensure_gathered()
         _, size = self._packed_offsets(self.ranks)
         if self._p2p:
-            self._epoch += 1
             stream = _lib.stream_ptr(self.device)
-            _lib.check(self.L.edgc_p2p_signal(_lib.ptr(self._peer_flags), self.me, self.world, self._epoch, stream),
-                       "edgc_p2p_signal")
-            # each rank's packed buffer is laid out identically: copy the first `size` floats of each
-            # into slots of self._fsz (the gathered layout's rank stride is the packed size)
+            _lib.check(self.L.edgc_p2p_signal(_lib.ptr(self._peer_flags), self.me, self.world,
+                                              _lib.ptr(self._epoch_dev), stream), "edgc_p2p_signal")
+            # every rank's packed buffer has the same layout: rank w's first `size` floats go to
+            # gathered[w size ..) (the gathered layout's rank stride is the packed size)
             _lib.check(self.L.edgc_p2p_pull(_lib.ptr(self._peer_bases[self._parity]), _lib.ptr(self._gathered), size,
-                                            self.world, _lib.ptr(self._flags), self._epoch, stream), "edgc_p2p_pull")
+                                            self.world, _lib.ptr(self._flags), _lib.ptr(self._epoch_dev), stream),
+                       "edgc_p2p_pull")
             return
         gather_packed(self.factors[self._parity][:size], self._gathered, self.world, self.group)
 

@@ -46,6 +46,7 @@ CASES = {
     "engine_r4": dict(shapes=SMALL, rank=4, steps=4, tol=5e-5),
     "engine_r4_nccl": dict(shapes=SMALL, rank=4, steps=4, tol=5e-5, exchange="nccl"),
     "engine_r8_p2p": dict(shapes=MID, rank=8, steps=4, tol=5e-5, exchange="p2p"),
+    "engine_r4_graph": dict(shapes=MID, rank=4, steps=5, tol=5e-5, graph=True),
     "engine_r32": dict(shapes=MID, rank=32, steps=4, tol=5e-5),
     "engine_r128": dict(shapes=WIDE, rank=128, steps=3, tol=5e-5),
     "engine_gpt2_layer_r4": dict(shapes=list(GPT2_2P5B_LAYER), rank=4, steps=2, tol=5e-5),
@@ -78,7 +79,15 @@ def engine_case(name, spec, world, me, dev):
     worst = 0.0
     for t in range(steps):
         mine = [oracle.synth_matrix(3, t, k, me, m, n, 1e-2) for k, (m, n) in enumerate(shapes)]
-        outs = eng.step([torch.from_numpy(g).to(dev) for g in mine], check=True)
+        if spec.get("graph") and t >= 1:
+            # the steady-state step as CUDA graphs (compress, NVLink exchange, reconstruction)
+            if t == 1:
+                eng.capture_graphs()
+            for dst, g in zip(eng.grads, mine):
+                dst.copy_(torch.from_numpy(g))
+            outs = eng.graph_step(check=True)
+        else:
+            outs = eng.step([torch.from_numpy(g).to(dev) for g in mine], check=True)
         if me == 0:
             allg = [[oracle.synth_matrix(3, t, k, w, m, n, 1e-2).astype(np.float64) for k, (m, n) in
                      enumerate(shapes)] for w in range(world)]
