@@ -188,11 +188,18 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int
     const PlanDev &P = plans[order[slot]];
     const uint32_t count = (uint32_t)P.count;
     if (producer) {
-        // lane l writes outputs o = blk * kWalkBlk / 2 + l + 32 t of each block
+        // lane l writes outputs o = blk * kWalkBlk / 2 + l + 32 t of each block; output t comes from
+        // chain t % kChains, each chain stepping 32 kChains outputs at a time, so the 128-bit LCG
+        // steps of a block form kChains independent dependency chains instead of one
         constexpr int kPer = kWalkBlk / 64;                        // outputs per lane per block
-        u128 st = pcg_jump(P.state, P.inc, (uint64_t)lane + 1u);   // state after output `lane`
+        constexpr int kChains = 4;
+        static_assert(kPer % kChains == 0, "whole chain rounds per block");
+        u128 stc[kChains];
+#pragma unroll
+        for (int ch = 0; ch < kChains; ++ch)
+            stc[ch] = pcg_jump(P.state, P.inc, (uint64_t)lane + 1u + 32u * ch);   // state after output lane + 32 ch
         u128 a, c;
-        pcg_affine(P.inc, 32, a, c);
+        pcg_affine(P.inc, 32 * kChains, a, c);
         for (uint32_t blk = 0;; ++blk) {
             const uint32_t sl = blk % kWalkNBlk;
             // block blk - kWalkNBlk handed back?  The walker may finish first: it only sets done
@@ -205,6 +212,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int
             uint2 *dst = reinterpret_cast<uint2 *>(R.d + sl * kWalkBlk);
 #pragma unroll
             for (int t = 0; t < kPer; ++t) {
+                u128 &st = stc[t % kChains];
                 const uint64_t v = pcg_output(st);
                 st = a * st + c;
                 const uint2 w = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
