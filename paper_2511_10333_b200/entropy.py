@@ -449,7 +449,10 @@ class EntropyTracker:
             return
         dev = flats[0].device
         if self._pf_stream is None:
-            self._pf_stream = torch.cuda.Stream(dev)
+            # alpha = 1: the plans are needed by the very next iteration, so they run at the step's
+            # (high) priority and overlap it; otherwise low priority, yielding SMs to the step
+            prio = -1 if sampling_period(self.config.alpha) == 1 else 0
+            self._pf_stream = torch.cuda.Stream(dev, priority=prio)
         specs = _layer_specs(flats, iteration, self.config)
         if any(c < 2 for _, c, _ in specs):
             return
@@ -457,7 +460,10 @@ class EntropyTracker:
         ready = torch.cuda.Event()
         ready.record(torch.cuda.current_stream(dev))
         self._pf_stream.wait_event(ready)
-        plans, bms, status = sample_plans(specs, dev, bitmaps=True, stream=self._pf_stream, ahead=True,
+        # packed onto few SMs when several iterations of slack remain; spread when the plan is
+        # needed by the very next iteration (alpha = 1)
+        ahead = sampling_period(self.config.alpha) > 1
+        plans, bms, status = sample_plans(specs, dev, bitmaps=True, stream=self._pf_stream, ahead=ahead,
                                           workspace=self._pf_ws, check=False, indices=False)
         ev = torch.cuda.Event()
         ev.record(self._pf_stream)
@@ -536,10 +542,11 @@ class EntropyTracker:
                 per_layer = layer_entropies(mats, iteration, self.config, self.estimator, prefetched=pre)
                 if per_layer:
                     self._pending.append(float(np.mean(per_layer)))
-        if self.prefetch and mats and not should_sample_iteration(iteration, self.config.alpha):
+        period = sampling_period(self.config.alpha)
+        if self.prefetch and mats and (period == 1 or not should_sample_iteration(iteration, self.config.alpha)):
             # build the next sampled iteration's plans on the side stream; launched from a
-            # non-sampled iteration so the sampled one stays a single short device pass
-            period = sampling_period(self.config.alpha)
+            # non-sampled iteration so the sampled one stays a single short device pass -- or,
+            # when every iteration is sampled (alpha = 1), from this one, overlapping the next step
             nxt = (iteration // period + 1) * period
             if nxt not in self._pf:
                 self._launch_prefetch(nxt, mats)
