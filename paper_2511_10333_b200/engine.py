@@ -246,19 +246,31 @@ class BucketEngine:
         self._close_peers()
         opened = {}
         table = []
-        for w, recs in enumerate(everyone):
-            if w == self.me:
-                table.append([t.data_ptr() for t in (self.factors[0], self.factors[1], self._flags)])
-                continue
-            row = []
-            for handle, off in recs:
-                if handle not in opened:   # one mapping per allocation (buffers may share one)
-                    p = ctypes.c_void_p()
-                    _lib.check(self.L.edgc_ipc_open(ctypes.c_char_p(handle), ctypes.byref(p)), "edgc_ipc_open")
-                    opened[handle] = p.value
-                row.append(opened[handle] + off)
-            table.append(row)
+        ok = True
+        try:
+            for w, recs in enumerate(everyone):
+                if w == self.me:
+                    table.append([t.data_ptr() for t in (self.factors[0], self.factors[1], self._flags)])
+                    continue
+                row = []
+                for handle, off in recs:
+                    if handle not in opened:   # one mapping per allocation (buffers may share one)
+                        p = ctypes.c_void_p()
+                        _lib.check(self.L.edgc_ipc_open(ctypes.c_char_p(handle), ctypes.byref(p)), "edgc_ipc_open")
+                        opened[handle] = p.value
+                    row.append(opened[handle] + off)
+                table.append(row)
+        except RuntimeError:
+            ok = False
         self._ipc_mapped = list(opened.values())
+        # all ranks agree: if any rank could not map its peers, every rank uses the NCCL all-gather
+        agree = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(agree, op=dist.ReduceOp.MIN, group=self.group)
+        if not int(agree.item()):
+            self._close_peers()
+            self._p2p = False
+            self._ensure_gathered()
+            return
         self._peer_bases = [torch.tensor([row[par] for row in table], dtype=torch.int64, device=dev)
                             for par in (0, 1)]
         self._peer_flags = torch.tensor([row[2] for row in table], dtype=torch.int64, device=dev)
