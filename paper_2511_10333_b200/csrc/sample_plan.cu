@@ -202,13 +202,20 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int
         pcg_affine(P.inc, 32 * kChains, a, c);
         for (uint32_t blk = 0;; ++blk) {
             const uint32_t sl = blk % kWalkNBlk;
-            // block blk - kWalkNBlk handed back?  The walker may finish first: it only sets done
-            if (blk >= kWalkNBlk)
-                while (!walk_try_wait(&R.empty[sl], ((blk / kWalkNBlk) - 1) & 1)) {
-                    if (R.done) return;
-                    __nanosleep(1000);   // try_wait suspends only ~0.1 us: back off so the walkers issue
-                }
-            if (R.done) return;
+            // block blk - kWalkNBlk handed back?  The walker may finish first: it only sets done.
+            // Lane 0 waits and decides for the warp (a lane-divergent exit would leave the others'
+            // __syncwarp waiting on exited lanes); the __syncwarp orders its acquire before the writes
+            int stop = 0;
+            if (lane == 0) {
+                if (blk >= kWalkNBlk)
+                    while (!walk_try_wait(&R.empty[sl], ((blk / kWalkNBlk) - 1) & 1)) {
+                        if (R.done) { stop = 1; break; }
+                        __nanosleep(1000);   // try_wait suspends only ~0.1 us: back off so the walkers issue
+                    }
+                if (R.done) stop = 1;
+            }
+            if (__shfl_sync(0xffffffffu, stop, 0)) return;
+            __syncwarp();
             uint2 *dst = reinterpret_cast<uint2 *>(R.d + sl * kWalkBlk);
 #pragma unroll
             for (int t = 0; t < kPer; ++t) {
