@@ -1343,10 +1343,20 @@ __global__ void __launch_bounds__(kGThreads) k_gemm(const MatDev *mats, const Ge
 // to the rank: OP 0 P_raw partial = W[:, K-chunk] q_warm[K-chunk, :], OP 1 Q
 // partial = W[K-chunk, :]^T P[K-chunk, :].  BM x BN outputs per CTA (BM * BN =
 // 4096, 4x4 per thread); A staged as fp32, the small B tile pre-converted to fp64.
+// Skinny GEMMs of the 8 < r <= 32 path: P_raw partial (OP 0: M = m, N = r, K = n) and Q partial
+// (OP 1: M = n, N = r, K = m).  BM x BN outputs per CTA, 4 x 4 per thread; K in 32-wide steps
+// with the next step's w tile loaded into registers (float4, coalesced along the contiguous
+// dimension) while the current one is multiplied from shared memory.  fp32 products are summed
+// in fp32 over one K step and folded into fp64 accumulators (the tensor-core path accumulates
+// 128-wide K chunks in fp32 the same way).
+constexpr int kSkK = 32;
+template <int OP, int BM>
+constexpr int skinny_smem() { return 2 * (OP == 0 ? BM * (kSkK + 4) : kSkK * (BM + 4)) * (int)sizeof(float); }
 template <int OP, int BM, int BN>
-__global__ void __launch_bounds__(kGThreads) k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
+__global__ void __launch_bounds__(kGThreads, 2) k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
     constexpr int TX = BN / 4;
     static_assert((BM / 4) * TX == kGThreads, "4x4 outputs per thread");
+    constexpr int kAV = BM * kSkK / 4 / kGThreads;   // float4 of the w tile per thread
     const GemmTile t = tiles[blockIdx.x];
     const MatDev &M = mats[t.mat];
     if (OP == 1) {
@@ -1359,38 +1369,91 @@ __global__ void __launch_bounds__(kGThreads) k_skinny(const MatDev *mats, const 
     const float *__restrict__ w = M.w;
     const float *__restrict__ bsrc = OP == 0 ? M.q_warm : M.p_out;
     const int64_t ldb = OP == 0 ? M.ld_q : r;
-    __shared__ __align__(16) float As[kGK][BM + 4];
-    __shared__ __align__(16) float Bs[kGK][BN + 4];
+    // OP 0 keeps the w tile row-major (rows i, 32 k + 4 pad: float4 stores and loads conflict-free),
+    // OP 1 k-major (rows k, BM i + 4 pad)
+    constexpr int AR = OP == 0 ? BM : kSkK, AC = OP == 0 ? kSkK + 4 : BM + 4;
+    constexpr int kBV = BN * kSkK / kGThreads;        // q / P elements of one K step per thread
+    extern __shared__ __align__(16) float sk_smem[];
+    float (*As)[AR][AC] = reinterpret_cast<float (*)[AR][AC]>(sk_smem);   // two stages
+    __shared__ __align__(16) float Bs[kSkK][BN + 4];
     const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-    // fp32 products summed in fp32 over one kGK block, blocks folded in fp64: the FP32 pipe instead
-    // of the FP64 one (measured on the GPT2-2.5B set at r = 16: P_raw 7.3 -> 6.4 ms, Q 6.5 -> 5.9 ms;
-    // the rest is the tile loop's latency); the tensor-core path accumulates 128-wide K chunks in fp32 too
-    double acc[4][4] = {};
-    for (int64_t k0 = t.k0; k0 < t.k1; k0 += kGK) {
-        for (int e = tid; e < BM * kGK; e += kGThreads) {
+    // float4 e of the w tile: OP 0 rows i (contiguous along k): e -> (row e / 8, k quad e % 8);
+    // OP 1 rows k (contiguous along i): e -> (k e / (BM/4), i quad e % (BM/4)).  Copied with
+    // cp.async into the stage not being multiplied (no registers held across the multiply).
+    const bool vec = (n % 4 == 0) && ((uintptr_t)w % 16 == 0);
+    auto issue_a = [&](int64_t k0, int buf) {
+#pragma unroll
+        for (int u = 0; u < kAV; ++u) {
+            const int e = tid + u * kGThreads;
             int ii, kk;
-            if (OP == 1) { ii = e % BM; kk = e / BM; } else { kk = e % kGK; ii = e / kGK; }
-            const int64_t gi = t.i0 + ii, gk = k0 + kk;
-            float v = 0.f;
-            if (gi < MM && gk < t.k1) v = OP == 0 ? w[gi * n + gk] : w[gk * n + gi];
-            As[kk][ii] = v;
+            int64_t gi, gk;
+            if (OP == 0) { ii = e / (kSkK / 4); kk = 4 * (e % (kSkK / 4)); }
+            else { kk = e / (BM / 4); ii = 4 * (e % (BM / 4)); }
+            gi = t.i0 + ii; gk = k0 + kk;
+            float *dst = OP == 0 ? &As[buf][ii][kk] : &As[buf][kk][ii];
+            const bool in = OP == 0 ? gi < MM : gk < t.k1;
+            const int64_t lim = OP == 0 ? t.k1 - gk : MM - gi;   // valid of the 4 contiguous
+            const float *src = OP == 0 ? w + gi * n + gk : w + gk * n + gi;
+            if (vec && in && lim >= 4) {
+                tc::cp_async16(dst, src);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) dst[c] = (in && c < lim) ? src[c] : 0.f;
+            }
         }
-        for (int e = tid; e < BN * kGK; e += kGThreads) {
-            const int jj = e % BN, kk = e / BN;
-            const int64_t gj = t.j0 + jj, gk = k0 + kk;
-            Bs[kk][jj] = (gj < r && gk < t.k1) ? bsrc[gk * ldb + gj] : 0.f;
+        tc::cp_async_commit();
+    };
+    auto load_b = [&](int64_t k0, float (&b)[kBV]) {
+#pragma unroll
+        for (int u = 0; u < kBV; ++u) {
+            const int e = tid + u * kGThreads;
+            const int64_t gj = t.j0 + e % BN, gk = k0 + e / BN;
+            b[u] = (gj < r && gk < t.k1) ? bsrc[gk * ldb + gj] : 0.f;
         }
+    };
+    double acc[4][4] = {};
+    float b_next[kBV];
+    issue_a(t.k0, 0);
+    load_b(t.k0, b_next);
+    int buf = 0;
+    for (int64_t k0 = t.k0; k0 < t.k1; k0 += kSkK, buf ^= 1) {
+        const bool more = k0 + kSkK < t.k1;
+        if (more) issue_a(k0 + kSkK, buf ^ 1);   // next step's tile in flight during the multiply
+#pragma unroll
+        for (int u = 0; u < kBV; ++u) {
+            const int e = tid + u * kGThreads;
+            Bs[e / BN][e % BN] = b_next[u];
+        }
+        if (more) tc::cp_async_wait<1>();
+        else tc::cp_async_wait<0>();
         __syncthreads();
+        if (more) load_b(k0 + kSkK, b_next);
         float accf[4][4] = {};
 #pragma unroll
-        for (int kk = 0; kk < kGK; ++kk) {
-            const float4 a4 = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
-            const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[kk][tx * 4]);
-            const float a[4] = {a4.x, a4.y, a4.z, a4.w}, b[4] = {b4.x, b4.y, b4.z, b4.w};
+        for (int k4 = 0; k4 < kSkK; k4 += 4) {
+            float a[4][4];   // a[u][c]: row ty*4+u, k k4+c
+            if (OP == 0) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < 4; ++u) {   // rows ty + u BM/4: 8 rows of a warp on distinct banks
+                    const float4 x = *reinterpret_cast<const float4 *>(&As[buf][ty + u * (BM / 4)][k4]);
+                    a[u][0] = x.x; a[u][1] = x.y; a[u][2] = x.z; a[u][3] = x.w;
+                }
+            } else {
 #pragma unroll
-                for (int v = 0; v < 4; ++v) accf[u][v] = fmaf(a[u], b[v], accf[u][v]);
+                for (int c = 0; c < 4; ++c) {
+                    const float4 x = *reinterpret_cast<const float4 *>(&As[buf][k4 + c][ty * 4]);
+                    a[0][c] = x.x; a[1][c] = x.y; a[2][c] = x.z; a[3][c] = x.w;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[k4 + c][tx * 4]);
+                const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) accf[u][v] = fmaf(a[u][c], b[v], accf[u][v]);
+            }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -1402,11 +1465,31 @@ __global__ void __launch_bounds__(kGThreads) k_skinny(const MatDev *mats, const 
     for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-            const int64_t gi = t.i0 + ty * 4 + u, gj = t.j0 + tx * 4 + v;
+            const int64_t gi = t.i0 + (OP == 0 ? ty + u * (BM / 4) : ty * 4 + u), gj = t.j0 + tx * 4 + v;
             if (gi >= MM || gj >= r) continue;
             if (OP == 0) M.p_part[((int64_t)t.split * m + gi) * r + gj] = acc[u][v];
             else M.q_part[((int64_t)t.split * n + gi) * r + gj] = acc[u][v];
         }
+}
+
+// cudaFuncSetAttribute applies to the current device: remember which devices have it
+template <typename K>
+int smem_attr_once(K kernel, int bytes, uint64_t &done_mask) {
+    int dev = 0;
+    EDGC_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 64 && (done_mask >> dev & 1)) return EDGC_OK;
+    EDGC_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    if (dev < 64) done_mask |= 1ull << dev;
+    return EDGC_OK;
+}
+
+template <int OP, int BM, int BN>
+int launch_skinny(unsigned grid, cudaStream_t st, const MatDev *mats, const GemmTile *tiles, int32_t *status) {
+    static uint64_t attr = 0;
+    const int rc = smem_attr_once(k_skinny<OP, BM, BN>, skinny_smem<OP, BM>(), attr);
+    if (rc != EDGC_OK) return rc;
+    k_skinny<OP, BM, BN><<<grid, kGThreads, skinny_smem<OP, BM>(), st>>>(mats, tiles, status);
+    return EDGC_OK;
 }
 
 // ------------------------------------------------- wide path on tcgen05
@@ -2003,14 +2086,10 @@ int launch_pass1z(const Plan &P, int32_t *status, bool sample, cudaStream_t st) 
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        static bool attr_set = false;
-        if (!attr_set) {
-            EDGC_CUDA_TRY(cudaFuncSetAttribute(k_pass1t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)sizeof(TSmem)));
-            EDGC_CUDA_TRY(cudaFuncSetAttribute(k_pass1t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)sizeof(TSmem)));
-            attr_set = true;
-        }
+        static uint64_t attr_f = 0, attr_t = 0;
+        int arc = smem_attr_once(k_pass1t<false>, (int)sizeof(TSmem), attr_f);
+        if (arc == EDGC_OK) arc = smem_attr_once(k_pass1t<true>, (int)sizeof(TSmem), attr_t);
+        if (arc != EDGC_OK) return arc;
         if (sample)
             EDGC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pass1t<true>, (const MatDev *)P.d_mats,
                                              (const ZTile *)P.d_tz[c], status, (const SampDev *)P.d_samp));
@@ -2413,11 +2492,11 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if (!P.tcp[1].empty())
             EDGC_CUDA_TRY((tc::launch<128, 4>(TcPraw{P.d_mats, P.d_tcp[1], (int)P.tcp[1].size()}, sm_count(), st)));
         if (!P.sp[0].empty()) {
-            k_skinny<0, 256, 16><<<(unsigned)P.sp[0].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sp[0], status_dev);
+            if ((rc = launch_skinny<0, 256, 16>((unsigned)P.sp[0].size(), st, P.d_mats, P.d_sp[0], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if (!P.sp[1].empty()) {
-            k_skinny<0, 128, 32><<<(unsigned)P.sp[1].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sp[1], status_dev);
+            if ((rc = launch_skinny<0, 128, 32>((unsigned)P.sp[1].size(), st, P.d_mats, P.d_sp[1], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if ((rc = launch_gemm<0>(P, P.gp, P.d_gp, status_dev, st))) return rc;
@@ -2449,11 +2528,11 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if ((rc = launch_pass2(P, true, status_dev, st))) return rc;
         if ((rc = launch_pass2(P, false, status_dev, st))) return rc;
         if (!P.sq[0].empty()) {
-            k_skinny<1, 256, 16><<<(unsigned)P.sq[0].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sq[0], status_dev);
+            if ((rc = launch_skinny<1, 256, 16>((unsigned)P.sq[0].size(), st, P.d_mats, P.d_sq[0], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if (!P.sq[1].empty()) {
-            k_skinny<1, 128, 32><<<(unsigned)P.sq[1].size(), kGThreads, 0, st>>>(P.d_mats, P.d_sq[1], status_dev);
+            if ((rc = launch_skinny<1, 128, 32>((unsigned)P.sq[1].size(), st, P.d_mats, P.d_sq[1], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if ((rc = launch_gemm<1>(P, P.gq, P.d_gq, status_dev, st))) return rc;
