@@ -1353,10 +1353,10 @@ constexpr int kSkK = 32;
 template <int OP, int BM>
 constexpr int skinny_smem() { return 2 * (OP == 0 ? BM * (kSkK + 4) : kSkK * (BM + 4)) * (int)sizeof(float); }
 template <int OP, int BM, int BN>
-__global__ void __launch_bounds__(kGThreads, 2) k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
-    constexpr int TX = BN / 4;
-    static_assert((BM / 4) * TX == kGThreads, "4x4 outputs per thread");
-    constexpr int kAV = BM * kSkK / 4 / kGThreads;   // float4 of the w tile per thread
+__global__ void __launch_bounds__((BM / 4) * (BN / 4), 512 / ((BM / 4) * (BN / 4)))
+k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
+    constexpr int TX = BN / 4, NT = (BM / 4) * TX;   // 4 x 4 outputs per thread
+    constexpr int kAV = BM * kSkK / 4 / NT;          // float4 of the w tile per thread
     const GemmTile t = tiles[blockIdx.x];
     const MatDev &M = mats[t.mat];
     if (OP == 1) {
@@ -1372,7 +1372,7 @@ __global__ void __launch_bounds__(kGThreads, 2) k_skinny(const MatDev *mats, con
     // OP 0 keeps the w tile row-major (rows i, 32 k + 4 pad: float4 stores and loads conflict-free),
     // OP 1 k-major (rows k, BM i + 4 pad)
     constexpr int AR = OP == 0 ? BM : kSkK, AC = OP == 0 ? kSkK + 4 : BM + 4;
-    constexpr int kBV = BN * kSkK / kGThreads;        // q / P elements of one K step per thread
+    constexpr int kBV = BN * kSkK / NT;        // q / P elements of one K step per thread
     extern __shared__ __align__(16) float sk_smem[];
     float (*As)[AR][AC] = reinterpret_cast<float (*)[AR][AC]>(sk_smem);   // two stages
     __shared__ __align__(16) float Bs[kSkK][BN + 4];
@@ -1384,7 +1384,7 @@ __global__ void __launch_bounds__(kGThreads, 2) k_skinny(const MatDev *mats, con
     auto issue_a = [&](int64_t k0, int buf) {
 #pragma unroll
         for (int u = 0; u < kAV; ++u) {
-            const int e = tid + u * kGThreads;
+            const int e = tid + u * NT;
             int ii, kk;
             int64_t gi, gk;
             if (OP == 0) { ii = e / (kSkK / 4); kk = 4 * (e % (kSkK / 4)); }
@@ -1406,7 +1406,7 @@ __global__ void __launch_bounds__(kGThreads, 2) k_skinny(const MatDev *mats, con
     auto load_b = [&](int64_t k0, float (&b)[kBV]) {
 #pragma unroll
         for (int u = 0; u < kBV; ++u) {
-            const int e = tid + u * kGThreads;
+            const int e = tid + u * NT;
             const int64_t gj = t.j0 + e % BN, gk = k0 + e / BN;
             b[u] = (gj < r && gk < t.k1) ? bsrc[gk * ldb + gj] : 0.f;
         }
@@ -1421,7 +1421,7 @@ __global__ void __launch_bounds__(kGThreads, 2) k_skinny(const MatDev *mats, con
         if (more) issue_a(k0 + kSkK, buf ^ 1);   // next step's tile in flight during the multiply
 #pragma unroll
         for (int u = 0; u < kBV; ++u) {
-            const int e = tid + u * kGThreads;
+            const int e = tid + u * NT;
             Bs[e / BN][e % BN] = b_next[u];
         }
         if (more) tc::cp_async_wait<1>();
@@ -1488,7 +1488,7 @@ int launch_skinny(unsigned grid, cudaStream_t st, const MatDev *mats, const Gemm
     static uint64_t attr = 0;
     const int rc = smem_attr_once(k_skinny<OP, BM, BN>, skinny_smem<OP, BM>(), attr);
     if (rc != EDGC_OK) return rc;
-    k_skinny<OP, BM, BN><<<grid, kGThreads, skinny_smem<OP, BM>(), st>>>(mats, tiles, status);
+    k_skinny<OP, BM, BN><<<grid, (BM / 4) * (BN / 4), skinny_smem<OP, BM>(), st>>>(mats, tiles, status);
     return EDGC_OK;
 }
 
@@ -1661,6 +1661,17 @@ int tc_recon_min() {
     return v;
 }
 
+// EDGC_NARROW_MAX (4..kNarrow, default 4): largest rank on the register-tiled passes.  Ranks 5..8
+// measured faster on the skinny GEMMs (GPT2-2.5B set, r = 6: 548 -> 629 GB/s, r = 8: 481 -> 604
+// with 256 x 16 tiles): the narrow pass 1 holds 8 ranks per thread at 25% occupancy
+int narrow_max() {
+    static const int v = [] {
+        const char *e = std::getenv("EDGC_NARROW_MAX");
+        return e ? std::max(4, std::min(kNarrow, std::atoi(e))) : 4;
+    }();
+    return v;
+}
+
 int tc_min_rank() {
     static const int v = [] {
         if (std::getenv("EDGC_NO_TC")) return 1 << 30;
@@ -1796,7 +1807,7 @@ struct Plan {
     std::vector<Tile> t1v4, t1v1, t2v4, t2v1;
     std::vector<ZTile> tz[9];          // Z-path items grouped by cluster size 1..8
     std::vector<GemmTile> gw, gp, gq;  // wide path: EF update, P_raw and Q tiles for r > 32
-    std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles for r <= 16 (256x16) and <= 32 (128x32)
+    std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles: r <= 16 (256x16), <= 32 (128x32), <= 8 (256x8)
     std::vector<GemmTile> tce, tcp[2], tcq[2];
     std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles
     int64_t nfxg64 = 0, nfxr64 = 0;   // the first n are 64-edge tiles, the rest kFxBig-edge   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
@@ -1829,7 +1840,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     for (int k = 0; k < n; ++k) {
         const edgc_compress_desc &d = descs[k];
         const bool al4 = (d.n % 4 == 0) && (d.ld_g % 4 == 0) && ((uintptr_t)d.g % 16 == 0) && ((uintptr_t)d.w % 16 == 0);
-        if (al4 && std::max(d.r, d.r_res) <= kNarrow) vec_rmax = std::max(vec_rmax, std::max(d.r, d.r_res));
+        if (al4 && std::max(d.r, d.r_res) <= narrow_max()) vec_rmax = std::max(vec_rmax, std::max(d.r, d.r_res));
     }
     {
         int64_t ctas = 0;
@@ -1861,7 +1872,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.precond = d.precond; M.ld_s = d.ld_s;
         M.al4 = (d.n % 4 == 0) && (d.ld_g % 4 == 0) && ((uintptr_t)d.g % 16 == 0) &&
                         ((uintptr_t)d.w % 16 == 0);
-        const bool v4 = M.al4 && std::max(d.r, d.r_res) <= kNarrow;
+        const bool v4 = M.al4 && std::max(d.r, d.r_res) <= narrow_max();
         // vector group: float4 columns; pass 2 above rank 4 (r <= 8) takes float2 columns, so its
         // per-thread fp64 Q partials halve and three CTAs fit an SM (measured: 4.8 -> 2.5 ms on
         // the GPT2-2.5B set at r = 8; pass 1 stays float4, its row-block reduction dominates)
@@ -1881,7 +1892,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                 P.tz[zc].push_back(ZTile{k, it, (int64_t)it * zrows, std::min(d.m, (int64_t)(it + 1) * zrows)});
         const int64_t slots = d.n / M.vec;
         const int64_t threads1 = kP1Threads;
-        M.wide = std::max(d.r, d.r_res) > kNarrow ? 1 : 0;
+        M.wide = std::max(d.r, d.r_res) > narrow_max() ? 1 : 0;
         M.tc = (M.wide && d.r > tc_min_rank()) ? 1 : 0;
         static const bool fx_off = std::getenv("EDGC_NO_FX") != nullptr;
         M.fx = (M.wide && d.r >= 32 && (M.tc || d.r > 32) && !fx_off) ? 1 : 0;   // single P_raw chunk
@@ -1929,9 +1940,11 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                 continue;
             }
             // skinny GEMM tile shape matched to the rank (r > 32: the 64x64 k_gemm tiles)
-            const int cfg = d.r <= 16 ? 0 : (d.r <= 32 ? 1 : 2);
-            const int BM = cfg == 0 ? 256 : (cfg == 1 ? 128 : kGT), BN = cfg == 0 ? 16 : (cfg == 1 ? 32 : kGT);
-            std::vector<GemmTile> &tp = cfg == 2 ? P.gp : P.sp[cfg], &tq = cfg == 2 ? P.gq : P.sq[cfg];
+            // (cfg 2: r <= 8, 256 x 8; 0: r <= 16, 256 x 16; 1: r <= 32, 128 x 32)
+            const int cfg = d.r <= 8 ? 2 : (d.r <= 16 ? 0 : (d.r <= 32 ? 1 : 3));
+            const int BM = cfg == 0 || cfg == 2 ? 256 : (cfg == 1 ? 128 : kGT);
+            const int BN = cfg == 2 ? 8 : (cfg == 0 ? 16 : (cfg == 1 ? 32 : kGT));
+            std::vector<GemmTile> &tp = cfg == 3 ? P.gp : P.sp[cfg], &tq = cfg == 3 ? P.gq : P.sq[cfg];
             for (int32_t c = 0; c < M.nchunk1; ++c)
                 for (int64_t i0 = 0; i0 < d.m; i0 += BM)
                     for (int64_t j0 = 0; j0 < d.r; j0 += BN)
@@ -2499,6 +2512,10 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
             if ((rc = launch_skinny<0, 128, 32>((unsigned)P.sp[1].size(), st, P.d_mats, P.d_sp[1], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
+        if (!P.sp[2].empty()) {
+            if ((rc = launch_skinny<0, 256, 8>((unsigned)P.sp[2].size(), st, P.d_mats, P.d_sp[2], status_dev))) return rc;
+            EDGC_LAUNCH_CHECK();
+        }
         if ((rc = launch_gemm<0>(P, P.gp, P.d_gp, status_dev, st))) return rc;
     }
     if (phases & EDGC_PHASE_FACTOR) {
@@ -2533,6 +2550,10 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         }
         if (!P.sq[1].empty()) {
             if ((rc = launch_skinny<1, 128, 32>((unsigned)P.sq[1].size(), st, P.d_mats, P.d_sq[1], status_dev))) return rc;
+            EDGC_LAUNCH_CHECK();
+        }
+        if (!P.sq[2].empty()) {
+            if ((rc = launch_skinny<1, 256, 8>((unsigned)P.sq[2].size(), st, P.d_mats, P.d_sq[2], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if ((rc = launch_gemm<1>(P, P.gq, P.d_gq, status_dev, st))) return rc;

@@ -6,6 +6,10 @@ seeds them (grad_source.py:440-447), so a W-rank engine's rank-w factors are
 the reference worker w's.
 """
 
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -20,7 +24,7 @@ def _shapes():
     return [(256, 768), (256, 256), (256, 1024), (1024, 256), (48, 36), (7, 9)]
 
 
-@pytest.mark.parametrize("rank", [1, 4, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("rank", [1, 4, 5, 6, 8, 16, 32, 64, 128])
 def test_engine_matches_oracle_dp_step_chained(rank):
     from paper_2511_10333_b200.engine import BucketEngine
     shapes = _shapes()
@@ -43,6 +47,18 @@ def test_engine_matches_oracle_dp_step_chained(rank):
                 else:  # full-rank compression: the reference residual is fp64 round-off
                     assert float(torch.linalg.norm(eng.residual(k))) <= 1e-5 * np.linalg.norm(gs[k])
     assert worst <= 5e-5, worst
+
+
+@pytest.mark.parametrize("rank", [6, 8])
+def test_engine_narrow_passes_match_oracle(rank):
+    """Ranks 5..8 run the skinny GEMMs by default; EDGC_NARROW_MAX=8 pins them to the
+    register-tiled narrow passes (k_pass1 / k_pass2 with 8 ranks per thread)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EDGC_NARROW_MAX="8")
+    code = (f"import sys; sys.path.insert(0, {root!r}); "
+            f"from tests.test_gpu_engine import test_engine_matches_oracle_dp_step_chained as t; t({rank})")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
 
 
 @pytest.mark.parametrize("rank", [96, 256])
