@@ -135,18 +135,22 @@ constexpr int kWalkQ = 8;                   // steps per walker lane per chunk
 constexpr int kWalkChunk = 32 * kWalkQ;
 constexpr int kWalkMaxRej = 8;              // rejections settled inside one chunk (ring lookahead)
 constexpr int kWalkBlk = 512;               // draws per ring block
-constexpr int kWalkNBlk = 4;                // ring blocks
-constexpr int kWalkRing = kWalkBlk * kWalkNBlk;
+// ring blocks: 4 with kWalkPlans rings per CTA (plans built ahead), 32 with one (latency mode:
+// the producer runs up to 16K draws ahead, so its back-off while the ring is full never
+// starves the walker)
+constexpr int kWalkNBlkAhead = 4, kWalkNBlkLat = 32;
 constexpr int kWalkThreads = 64 * kWalkPlans;
 static_assert(kWalkBlk % 64 == 0, "whole outputs per producer lane");
 static_assert(kWalkChunk + kWalkMaxRej <= kWalkBlk, "a chunk spans at most two blocks");
 static_assert((kWalkChunk + kWalkMaxRej) % 2 == 0, "the mirror copies whole outputs");
 
 constexpr int kWalkPad = kWalkChunk + kWalkMaxRej;   // ring head mirrored past its end: no index wrap
+template <int NBLK>
 struct alignas(16) WalkRing {
-    uint32_t d[kWalkRing + kWalkPad];
-    uint64_t full[kWalkNBlk];    // producer -> walker: block written
-    uint64_t empty[kWalkNBlk];   // walker -> producer: block consumed
+    static constexpr int kRing = kWalkBlk * NBLK;
+    uint32_t d[kRing + kWalkPad];
+    uint64_t full[NBLK];    // producer -> walker: block written
+    uint64_t empty[NBLK];   // walker -> producer: block consumed
     volatile int done;
 };
 
@@ -168,14 +172,16 @@ __device__ __forceinline__ void walk_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
+template <int NBLK, int BACKOFF_NS>
 __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int n_plans, const int32_t *order,
                                                        int ppc) {
+    constexpr int kWalkNBlk = NBLK, kWalkRing = WalkRing<NBLK>::kRing;
     extern __shared__ __align__(16) unsigned char walk_raw[];
     const int g = threadIdx.x >> 6;                 // plan group in the CTA
     const bool producer = (threadIdx.x >> 5) & 1;
     const int lane = threadIdx.x & 31;
     const int slot = blockIdx.x * ppc + g;
-    WalkRing &R = reinterpret_cast<WalkRing *>(walk_raw)[g];
+    WalkRing<NBLK> &R = reinterpret_cast<WalkRing<NBLK> *>(walk_raw)[g];
     if ((threadIdx.x & 63) == 0) {
         for (int i = 0; i < kWalkNBlk; ++i) {
             ptx::mbar_init(&R.full[i], 1);
@@ -210,7 +216,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const PlanDev *plans, int
                 if (blk >= kWalkNBlk)
                     while (!walk_try_wait(&R.empty[sl], ((blk / kWalkNBlk) - 1) & 1)) {
                         if (R.done) { stop = 1; break; }
-                        __nanosleep(1000);   // try_wait suspends only ~0.1 us: back off so the walkers issue
+                        __nanosleep(BACKOFF_NS);   // try_wait suspends only ~0.1 us: back off so the walkers issue
                     }
                 if (R.done) stop = 1;
             }
@@ -1254,15 +1260,21 @@ extern "C" int edgc_sample_plan(const edgc_plan_desc *plans, int n_plans, int32_
                                   cudaMemcpyHostToDevice, st));
     static bool walk_attr = false;
     if (!walk_attr) {
-        EDGC_CUDA_TRY(cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(kWalkPlans * sizeof(WalkRing))));
+        EDGC_CUDA_TRY(cudaFuncSetAttribute(k_walk<kWalkNBlkAhead, 1000>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(kWalkPlans * sizeof(WalkRing<kWalkNBlkAhead>))));
+        EDGC_CUDA_TRY(cudaFuncSetAttribute(k_walk<kWalkNBlkLat, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sizeof(WalkRing<kWalkNBlkLat>)));
         walk_attr = true;
     }
     bool latency = false;
     for (int i = 0; i < n_plans; ++i) latency |= (plans[i].flags & EDGC_PLAN_LATENCY) != 0;
-    const int ppc = latency ? 1 : kWalkPlans;
-    k_walk<<<(unsigned)ceil_div(n_plans, ppc), 64 * ppc, ppc * sizeof(WalkRing), st>>>(
-        d_plans, n_plans, (const int32_t *)L.walk_order, ppc);
+    if (latency)
+        k_walk<kWalkNBlkLat, 100><<<(unsigned)n_plans, 64, sizeof(WalkRing<kWalkNBlkLat>), st>>>(
+            d_plans, n_plans, (const int32_t *)L.walk_order, 1);
+    else
+        k_walk<kWalkNBlkAhead, 1000><<<(unsigned)ceil_div(n_plans, kWalkPlans), 64 * kWalkPlans,
+                                       kWalkPlans * sizeof(WalkRing<kWalkNBlkAhead>), st>>>(
+            d_plans, n_plans, (const int32_t *)L.walk_order, kWalkPlans);
     EDGC_LAUNCH_CHECK();
     if (L.n_bucketed) {
         // bucket path (tail-shuffle plans); plans are ordered, so each kernel's CTA range covers

@@ -24,7 +24,7 @@ import torch
 from . import _lib
 from .errors import DegenerateInputError
 from .matrix_core import as_device_array, as_device_matrix
-from .seeds import pcg64_words, subsample_seed
+from .seeds import pcg64_words_many, subsample_seeds
 
 __all__ = ["GAUSSIAN_ENTROPY_CONST", "SamplerConfig", "EntropyWindow", "should_sample_iteration",
            "sampling_period", "sample_count", "sample_indices", "sample_plans", "subsample_entries",
@@ -147,9 +147,10 @@ def sample_plans(specs, device=None, *, bitmaps: bool = False, stream=None, work
                 bo += pad(words)
         cap_bytes = _plan_ws_cap(dev)
         descs, sizes = {}, {}
+        words = dict(zip(todo, pcg64_words_many([specs[i][2] for i in todo])))
         for i in todo:
             n_elems, count, seed = specs[i]
-            descs[i] = _lib.PlanDesc(*pcg64_words(seed), n_elems, count, _lib.ptr(out[i]), _lib.ptr(bms[i]),
+            descs[i] = _lib.PlanDesc(*words[i], n_elems, count, _lib.ptr(out[i]), _lib.ptr(bms[i]),
                                      (0 if indices else _lib.PLAN_BITMAP_ONLY) |
                                      (0 if ahead else _lib.PLAN_LATENCY))
             sizes[i] = L.edgc_sample_plan_workspace_bytes((_lib.PlanDesc * 1)(descs[i]), 1) + 4096
@@ -363,8 +364,8 @@ def relative_change_rate(series_sampled, series_full) -> np.ndarray:
 
 
 def _layer_specs(flats, iteration: int, config: SamplerConfig):
-    return [(f.numel(), sample_count(f.numel(), config.beta), subsample_seed(config.rng_seed, iteration, k))
-            for k, f in enumerate(flats)]
+    seeds = subsample_seeds(config.rng_seed, iteration, len(flats))
+    return [(f.numel(), sample_count(f.numel(), config.beta), seeds[k]) for k, f in enumerate(flats)]
 
 
 def layer_entropies(matrices, iteration: int, config: SamplerConfig, estimator=None, prefetched=None,

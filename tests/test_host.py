@@ -131,8 +131,22 @@ def test_seeds_match_reference_golden():
     gold = load_json("seeds.json")
     for rec in gold["subsample"]:
         assert seeds.subsample_seed(rec["seed"], rec["t"], rec["k"]) == rec["sub_seed"]
+        assert seeds.subsample_seeds(rec["seed"], rec["t"], rec["k"] + 1)[rec["k"]] == rec["sub_seed"]
     got = {f"{w},{k}": v for (w, k), v in seeds.state_seeds(0, 8, 208).items()}
     assert got == gold["state_seeds_0_8_208"]
+
+
+def test_batched_seed_derivation_matches_numpy():
+    """pcg64_words_many / subsample_seeds (restated SeedSequence + PCG64 seeding) equal
+    NumPy's default_rng word for word: single-word, multi-word (>= 2^32) and list entropy."""
+    from paper_2511_10333_b200.seeds import pcg64_words, pcg64_words_many, subsample_seed, subsample_seeds
+    r = np.random.default_rng(11)
+    seeds = [0, 1, 2**31 - 1, 2**32 - 1, 2**32, 2**63 + 5, 2**64, 2**100 + 7] + [int(x) for x in r.integers(0, 2**31, 40)]
+    lists = [[0, 2, 0, 0], [7, 2, 10, 207], [2**40, 2, 3, 1], [5], [1, 2, 3, 4, 5, 6, 7], []]
+    assert pcg64_words_many(seeds) == [pcg64_words(s) for s in seeds]
+    assert pcg64_words_many(lists) == [pcg64_words(l) for l in lists]
+    for run_seed, it in [(0, 0), (0, 10), (12345, 3), (2**33 + 1, 7)]:
+        assert subsample_seeds(run_seed, it, 30) == [subsample_seed(run_seed, it, k) for k in range(30)]
 
 
 @pytest.mark.parametrize("name", ["gpt2_2p5b", "gpt2_12p1b", "gpt2_2p5b_layer", "dp_small", "dp_check"])

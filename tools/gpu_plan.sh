@@ -9,6 +9,8 @@ timeout 120 python tools/plan_prof.py --reps 5 > gpurun_out/${T}_plan.log 2>&1
 timeout 120 python tools/plan_prof.py --reps 5 --ahead >> gpurun_out/${T}_plan.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file gpurun_out/${T}_plan_ncu.csv python tools/plan_prof.py --reps 1 --ahead > gpurun_out/${T}_plan_ncu.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  --csv --log-file gpurun_out/${T}_plan_ncu_lat.csv python tools/plan_prof.py --reps 1 > /dev/null 2>&1
 #timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_set_resolve|k_set_tail|k_walk" -c 3 \
 #  -o gpurun_out/${T}_plan_full -f python tools/plan_prof.py --reps 1 --ahead > gpurun_out/${T}_ncu.log 2>&1
 exit 0
