@@ -443,6 +443,11 @@ class EntropyTracker:
         self._pf = {}              # iteration -> (specs, plans, bitmaps, status, event)
         self._pf_stream = None
         self._pf_ws = _lib.Workspace()
+        # the plan workspace is shared by the side-stream prefetches and the (rare) inline builds on
+        # the step stream: each side waits only for the other's last use, not for the whole stream
+        # (at alpha = 1 the next plan then overlaps this step instead of queueing behind it)
+        self._ws_pf_done = None      # event after the last prefetch
+        self._ws_inline_done = None  # event after the last inline build
 
     def _launch_prefetch(self, iteration: int, matrices) -> None:
         flats = [as_device_matrix(m).reshape(-1) for m in matrices]
@@ -457,10 +462,8 @@ class EntropyTracker:
         specs = _layer_specs(flats, iteration, self.config)
         if any(c < 2 for _, c, _ in specs):
             return
-        # the workspace is shared with the inline (main-stream) builds: order after them
-        ready = torch.cuda.Event()
-        ready.record(torch.cuda.current_stream(dev))
-        self._pf_stream.wait_event(ready)
+        if self._ws_inline_done is not None:
+            self._pf_stream.wait_event(self._ws_inline_done)
         # packed onto few SMs when several iterations of slack remain; spread when the plan is
         # needed by the very next iteration (alpha = 1)
         ahead = sampling_period(self.config.alpha) > 1
@@ -468,7 +471,19 @@ class EntropyTracker:
                                           workspace=self._pf_ws, check=False, indices=False)
         ev = torch.cuda.Event()
         ev.record(self._pf_stream)
+        self._ws_pf_done = ev
         self._pf[iteration] = (specs, plans, bms, status, ev)
+
+    def _inline_ws(self, dev):
+        """The shared plan workspace for a build on the current stream (after the last prefetch)."""
+        if self._ws_pf_done is not None:
+            torch.cuda.current_stream(dev).wait_event(self._ws_pf_done)
+        return self._pf_ws
+
+    def _inline_done(self, dev):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dev))
+        self._ws_inline_done = ev
 
     def _take_prefetch(self, iteration: int):
         rec = self._pf.pop(iteration, None)
@@ -503,7 +518,8 @@ class EntropyTracker:
             _, plans, bms, status = pre
         else:
             plans, bms, status = sample_plans(specs, dev, bitmaps=True, check=False, indices=False,
-                                              workspace=self._pf_ws)
+                                              workspace=self._inline_ws(dev))
+            self._inline_done(dev)
         # slots beyond a matrix's own CTA count stay zero
         partials = torch.zeros((len(specs), slots, 2), dtype=torch.float64, device=dev)
         engine.set_sampling(bms, plans, partials)
@@ -537,8 +553,13 @@ class EntropyTracker:
             pre = self._take_prefetch(iteration)
             if self.estimator is entropy_gaussian_plugin and mats:
                 # read back lazily: the host needs the value only when the window closes
+                dev = as_device_matrix(mats[0]).device
+                inline = pre is None or [n for n, _, _ in pre[0]] != [as_device_matrix(m).numel() for m in mats]
                 self._pending.append(layer_entropies(mats, iteration, self.config, self.estimator,
-                                                     prefetched=pre, deferred=True, workspace=self._pf_ws))
+                                                     prefetched=pre, deferred=True,
+                                                     workspace=self._inline_ws(dev)))
+                if inline:
+                    self._inline_done(dev)
             else:
                 per_layer = layer_entropies(mats, iteration, self.config, self.estimator, prefetched=pre)
                 if per_layer:
