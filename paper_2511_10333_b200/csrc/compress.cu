@@ -1343,6 +1343,87 @@ __global__ void __launch_bounds__(kGThreads) k_gemm(const MatDev *mats, const Ge
 // to the rank: OP 0 P_raw partial = W[:, K-chunk] q_warm[K-chunk, :], OP 1 Q
 // partial = W[K-chunk, :]^T P[K-chunk, :].  BM x BN outputs per CTA (BM * BN =
 // 4096, 4x4 per thread); A staged as fp32, the small B tile pre-converted to fp64.
+// EF update of the wide path on CUDA cores, w <- g + (w - p_res q_res^T), r_res <= RK: one
+// 64 x 64 tile per CTA, 4 x 4 per thread.  The thread's g and w are requested first (float4,
+// streaming), so their HBM latency overlaps the factor loads and the FMAs (k_gemm<2> loaded
+// them after the products); the products are summed in the same order, so w is bit-identical.
+template <int RK>
+__global__ void __launch_bounds__(kGThreads) k_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
+    constexpr int FV = kGT * RK / kGThreads;   // factor elements per thread and operand
+    const GemmTile t = tiles[blockIdx.x];
+    const MatDev &M = mats[t.mat];
+    const int64_t n = M.n, m = M.m;
+    const int rres = M.r_res;
+    __shared__ __align__(16) float As[RK][kGT + 4];
+    __shared__ __align__(16) float Bs[RK][kGT + 4];
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    // factor rows first (L2-resident, needed before the FMAs), then the streaming g and w
+    float fa[FV], fb[FV];
+#pragma unroll
+    for (int u = 0; u < FV; ++u) {
+        const int e = tid + u * kGThreads;
+        const int ii = e / RK, k = e % RK;   // consecutive threads read one contiguous factor row
+        const int64_t gi = t.i0 + ii, gjj = t.j0 + ii;
+        fa[u] = (k < rres && gi < m) ? M.p_res[gi * rres + k] : 0.f;
+        fb[u] = (k < rres && gjj < n) ? M.q_res[gjj * rres + k] : 0.f;
+    }
+    const int64_t gj = t.j0 + tx * 4;
+    const bool v4 = M.al4 && gj < n;   // al4: n % 4 == 0, so the thread's 4 columns are in range
+    float4 g4[4], w4[4];
+    if (v4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t gi = t.i0 + ty * 4 + u;
+            if (gi < m) {
+                g4[u] = __ldcs(reinterpret_cast<const float4 *>(M.g + gi * M.ld_g + gj));
+                w4[u] = __ldcs(reinterpret_cast<const float4 *>(M.w + gi * n + gj));
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < FV; ++u) {
+        const int e = tid + u * kGThreads;
+        As[e % RK][e / RK] = fa[u];
+        Bs[e % RK][e / RK] = fb[u];
+    }
+    __syncthreads();
+    float acc[4][4] = {};
+#pragma unroll
+    for (int k = 0; k < RK; ++k) {
+        const float4 a4 = *reinterpret_cast<const float4 *>(&As[k][ty * 4]);
+        const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[k][tx * 4]);
+        const float a[4] = {a4.x, a4.y, a4.z, a4.w}, b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = a[u] * b[v] + acc[u][v];
+    }
+    bool bad = false;
+    if (v4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t gi = t.i0 + ty * 4 + u;
+            if (gi >= m) continue;
+            const float x0 = g4[u].x + (w4[u].x - acc[u][0]), x1 = g4[u].y + (w4[u].y - acc[u][1]);
+            const float x2 = g4[u].z + (w4[u].z - acc[u][2]), x3 = g4[u].w + (w4[u].w - acc[u][3]);
+            bad |= !(isfinite(x0) && isfinite(x1) && isfinite(x2) && isfinite(x3));
+            __stcs(reinterpret_cast<float4 *>(M.w + gi * n + gj), make_float4(x0, x1, x2, x3));
+        }
+    } else if (!M.al4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int64_t gi = t.i0 + ty * 4 + u, gc = gj + v;
+                if (gi >= m || gc >= n) continue;
+                const float x = M.g[gi * M.ld_g + gc] + (M.w[gi * n + gc] - acc[u][v]);
+                bad |= !isfinite(x);
+                M.w[gi * n + gc] = x;
+            }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
+}
+
 // Skinny GEMMs of the 8 < r <= 32 path: P_raw partial (OP 0: M = m, N = r, K = n) and Q partial
 // (OP 1: M = n, N = r, K = m).  BM x BN outputs per CTA, 4 x 4 per thread; K in 32-wide steps
 // with the next step's w tile loaded into registers (float4, coalesced along the contiguous
@@ -1672,11 +1753,23 @@ int narrow_max() {
     return v;
 }
 
+// EDGC_TC_EF_MIN_RANK (default EDGC_TC_MIN_RANK): the EF update uses the tensor cores above it
+int tc_ef_min_rank();
+
 int tc_min_rank() {
     static const int v = [] {
         if (std::getenv("EDGC_NO_TC")) return 1 << 30;
         const char *e = std::getenv("EDGC_TC_MIN_RANK");
         return e ? std::atoi(e) : 16;
+    }();
+    return v;
+}
+
+int tc_ef_min_rank() {
+    static const int v = [] {
+        if (std::getenv("EDGC_NO_TC")) return 1 << 30;
+        const char *e = std::getenv("EDGC_TC_EF_MIN_RANK");
+        return e ? std::atoi(e) : tc_min_rank();
     }();
     return v;
 }
@@ -1807,6 +1900,7 @@ struct Plan {
     std::vector<Tile> t1v4, t1v1, t2v4, t2v1;
     std::vector<ZTile> tz[9];          // Z-path items grouped by cluster size 1..8
     std::vector<GemmTile> gw, gp, gq;  // wide path: EF update, P_raw and Q tiles for r > 32
+    int ef_rk = 0;                     // largest r_res of the CUDA-core EF tiles (gw)
     std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles: r <= 16 (256x16), <= 32 (128x32), <= 8 (256x8)
     std::vector<GemmTile> tce, tcp[2], tcq[2];
     std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles
@@ -1923,12 +2017,13 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         const int64_t k2 = (M.wide && (M.tc || d.r > 32)) ? d.m : kP2Rows;
         M.nblk2 = (int32_t)ceil_div(d.m, k2);
         if (M.wide) {
-            if (d.r_res > tc_min_rank()) {
+            if (d.r_res > tc_ef_min_rank()) {
                 for (int64_t i0 = 0; i0 < d.m; i0 += tc::kBM)
                     for (int64_t j0 = 0; j0 < d.n; j0 += kTcEFN) P.tce.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
             } else {
                 for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
                     for (int64_t j0 = 0; j0 < d.n; j0 += kGT) P.gw.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
+                P.ef_rk = std::max(P.ef_rk, d.r_res);
             }
             if (M.tc) {
                 // rank blocks of one row block adjacent: co-resident CTAs share the w rows in L2
@@ -2039,6 +2134,19 @@ template <int OP>
 int launch_gemm(const Plan &P, const std::vector<GemmTile> &h, const GemmTile *d, int32_t *status, cudaStream_t st) {
     if (h.empty()) return EDGC_OK;
     k_gemm<OP><<<(unsigned)h.size(), kGThreads, 0, st>>>(P.d_mats, d, status);
+    EDGC_LAUNCH_CHECK();
+    return EDGC_OK;
+}
+
+int launch_ef(const Plan &P, cudaStream_t st, int32_t *status) {
+    if (P.gw.empty()) return EDGC_OK;
+    const unsigned grid = (unsigned)P.gw.size();
+    static const bool gemm = std::getenv("EDGC_EF_GEMM") != nullptr;   // A/B: the generic tile kernel
+    if (gemm) k_gemm<2><<<grid, kGThreads, 0, st>>>(P.d_mats, P.d_gw, status);
+    else if (P.ef_rk <= 8) k_ef<8><<<grid, kGThreads, 0, st>>>(P.d_mats, P.d_gw, status);
+    else if (P.ef_rk <= 16) k_ef<16><<<grid, kGThreads, 0, st>>>(P.d_mats, P.d_gw, status);
+    else if (P.ef_rk <= 32) k_ef<32><<<grid, kGThreads, 0, st>>>(P.d_mats, P.d_gw, status);
+    else k_gemm<2><<<grid, kGThreads, 0, st>>>(P.d_mats, P.d_gw, status);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }
@@ -2497,7 +2605,7 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if ((rc = launch_pass1(P, false, status_dev, st))) return rc;
         if ((rc = launch_pass1z(P, status_dev, P.sample_armed, st))) return rc;
         h->P.sample_armed = false;   // set_sampling arms exactly one pass 1
-        if ((rc = launch_gemm<2>(P, P.gw, P.d_gw, status_dev, st))) return rc;
+        if ((rc = launch_ef(P, st, status_dev))) return rc;
         if (!P.tce.empty())
             EDGC_CUDA_TRY((tc::launch<kTcEFN, 4>(TcEF{P.d_mats, P.d_tce, status_dev, (int)P.tce.size()}, sm_count(), st)));
         if (!P.tcp[0].empty())
