@@ -16,6 +16,7 @@ from __future__ import annotations
 import csv
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -36,6 +37,9 @@ GAUSSIAN_ENTROPY_CONST = 0.5 * math.log(2.0 * math.pi * math.e)
 
 
 _WS_CAP = {}
+
+
+_PF_AFTER_STEP = os.environ.get("EDGC_PF_AFTER_STEP") is not None
 
 
 def _plan_ws_cap(device) -> int:
@@ -464,6 +468,10 @@ class EntropyTracker:
             return
         if self._ws_inline_done is not None:
             self._pf_stream.wait_event(self._ws_inline_done)
+        if _PF_AFTER_STEP:   # A/B: start the build only after the work queued on the step stream
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream(dev))
+            self._pf_stream.wait_event(ready)
         # packed onto few SMs when several iterations of slack remain; spread when the plan is
         # needed by the very next iteration (alpha = 1)
         ahead = sampling_period(self.config.alpha) > 1
