@@ -265,6 +265,12 @@ constexpr int kTRB = 4;
 #ifndef EDGC_P1_NOZ
 #define EDGC_P1_NOZ 0       // diagnostics: full exchange, Z update skipped
 #endif
+#ifndef EDGC_TCEF_PFD
+#define EDGC_TCEF_PFD 3
+#endif
+#ifndef EDGC_TCEF_STAGES
+#define EDGC_TCEF_STAGES 1
+#endif
 #ifndef EDGC_PROD_SLEEP
 #define EDGC_PROD_SLEEP 64
 #endif
@@ -1587,7 +1593,7 @@ __device__ __forceinline__ int tc_rows4(int64_t rem) { return rem <= 0 ? 0 : rem
 
 struct TcPraw {
     static constexpr bool kAMN = false, kBMN = true;
-    static constexpr int kPF = 0;
+    static constexpr int kPF = 0, kPFDepth = 2, kStages = 0;
     using Tile = GemmTile;
     const MatDev *mats;
     const GemmTile *tiles;
@@ -1619,7 +1625,7 @@ struct TcPraw {
 
 struct TcQ {
     static constexpr bool kAMN = true, kBMN = true;
-    static constexpr int kPF = 0;
+    static constexpr int kPF = 0, kPFDepth = 2, kStages = 0;
     using Tile = GemmTile;
     const MatDev *mats;
     const GemmTile *tiles;
@@ -1663,7 +1669,9 @@ constexpr int kTcEFN = 128;
 
 struct TcEF {
     static constexpr bool kAMN = false, kBMN = false;
-    static constexpr int kPF = 16;   // g and w of the slice, one slice ahead
+    // g and w of the slice, EDGC_TCEF_PFD - 1 slices ahead; the operands (p_res, q_res: K = r_res)
+    // are small, so one stage leaves the shared memory to the prefetch slots
+    static constexpr int kPF = 16, kPFDepth = EDGC_TCEF_PFD, kStages = EDGC_TCEF_STAGES;
     using Tile = GemmTile;
     const MatDev *mats;
     const GemmTile *tiles;
@@ -2483,7 +2491,7 @@ int elementwise_blocks(int64_t count) { return (int)std::max<int64_t>(1, std::mi
 // per-rank factor blocks are the K index's rank blocks)
 struct TcRecon {
     static constexpr bool kAMN = false, kBMN = false;
-    static constexpr int kPF = 0;
+    static constexpr int kPF = 0, kPFDepth = 2, kStages = 0;
     using Tile = RTile;
     const ReconDev *descs;
     const RTile *tiles;

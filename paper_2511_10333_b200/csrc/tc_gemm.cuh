@@ -68,14 +68,17 @@ struct View {
     int64_t ld, rows, K, kblk, kstride;
 };
 
-template <int BN, int KCH, int PF = 0>
+// PFD: prefetch depth (slices of epilogue input in flight per warp); STAGES: operand stages
+// (0: by tile width)
+template <int BN, int KCH, int PF = 0, int PFD = 2, int STAGES = 0>
 struct Cfg {
     static_assert(BN == 64 || BN == 128, "tile N");
+    static_assert(PFD >= 2 && PFD <= 4, "prefetch depth");
     static constexpr int kAPlane = kBM * kBK * 4;          // bytes of one (hi or lo) plane
     static constexpr int kBPlane = BN * kBK * 4;
     static constexpr int kStageBytes = 2 * (kAPlane + kBPlane);
-    static constexpr int kStages = BN == 128 ? (PF > 0 ? 2 : 3) : 4;
-    static constexpr int kPFBytes = 2 * PF * kEpiWarps * 32 * 16;   // double-buffered prefetch slots
+    static constexpr int kStages = STAGES > 0 ? STAGES : BN == 128 ? (PF > 0 ? 2 : 3) : 4;
+    static constexpr int kPFBytes = PFD * PF * kEpiWarps * 32 * 16;   // PFD prefetch slot buffers
     static constexpr int kBarBytes = 8 * (2 * kStages + 4) + 16;
     static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;   // per-warp 32 x 32 transpose slices
     static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kPFBytes + kBarBytes + 1024;
@@ -293,8 +296,8 @@ __device__ __forceinline__ bool view_vec(const View &v) {
 // KCH = K blocks (of 32) per accumulation chunk; 0 = the whole tile in one chunk
 template <int BN, int KCH, class Op>
 __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
-    constexpr int PF = Op::kPF;
-    using C = Cfg<BN, KCH, PF>;
+    constexpr int PF = Op::kPF, PFD = Op::kPFDepth;
+    using C = Cfg<BN, KCH, PF, PFD, Op::kStages>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *epi_smem = smem + C::kStages * C::kStageBytes;
@@ -335,7 +338,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
             op.views(t, av, bv);
             const bool avec = view_vec(av), bvec = view_vec(bv);
             for (int kb = 0; kb < nkb; ++kb, ++q) {
-                if ((q & 1) != grp) continue;
+                // two groups take alternate K blocks; with one operand stage a single group
+                // (two would share the stage's barrier phases and one could run two phases ahead)
+                if (C::kStages == 1 ? grp != 0 : (q & 1) != grp) continue;
                 const int s = (int)(q % C::kStages);
                 const uint32_t use = (uint32_t)(q / C::kStages);
                 float4 va[Plane<Op::kAMN, kBM>::kPer], vb[Plane<Op::kBMN, BN>::kPer];
@@ -413,17 +418,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
                 const int b = (int)(cc & 1);
                 const bool first = c0 == 0, last = c0 + kch >= nkb;
                 if (PF > 0 && last) {
-                    op.prefetch(t, row0, lcol, pf);
-                    cp_async_commit();
+                    // the first PFD - 1 slices of the tile (one group each, empty past the tile)
+#pragma unroll
+                    for (int s = 0; s < PFD - 1; ++s) {
+                        if (s * 32 < BN) op.prefetch(t, row0, s * 32 + lcol, pf + s * kPFBuf);
+                        cp_async_commit();
+                    }
                 }
                 ptx::mbar_wait(tfull + b, (uint32_t)(cc >> 1) & 1);
                 fence_after();
                 const uint32_t acc = tmem + lane_off + b * BN;
 #pragma unroll 1
                 for (int col = 0; col < BN; col += 32) {
-                    const bool more = col + 32 < BN;
-                    if (PF > 0 && last && more) {
-                        op.prefetch(t, row0, col + 32 + lcol, pf + (((col >> 5) + 1) & 1) * kPFBuf);
+                    if (PF > 0 && last) {
+                        // slice + PFD - 1 into the buffer the previous slice released (a group per
+                        // slice even past the tile, so the wait below is always PFD - 1 deep)
+                        const int ahead = (col >> 5) + PFD - 1;
+                        if (ahead * 32 < BN) op.prefetch(t, row0, ahead * 32 + lcol, pf + (ahead % PFD) * kPFBuf);
                         cp_async_commit();
                     }
                     float v[32];
@@ -453,11 +464,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
                             x[u] = ptx::ld_shared_v4(xs + r * 128 + (((lane & 7) ^ (r & 7)) << 4));
                         }
                         __syncwarp();
-                        if (PF > 0) {
-                            if (more) cp_async_wait<1>();
-                            else cp_async_wait<0>();
-                        }
-                        op.epilogue(t, row0, col + lcol, x, pf + ((col >> 5) & 1) * kPFBuf);
+                        if (PF > 0) cp_async_wait<PFD - 1>();
+                        op.epilogue(t, row0, col + lcol, x, pf + ((col >> 5) % PFD) * kPFBuf);
                     } else {
                         tmem_st16(run + col, v);
                         tmem_st16(run + col + 16, v + 16);
@@ -483,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(const Op op) {
 // remove the plan interference at GPT2-12.1B r = 256)
 template <int BN, int KCH, class Op>
 inline cudaError_t launch(const Op &op, int sms, cudaStream_t st) {
-    using C = Cfg<BN, KCH, Op::kPF>;
+    using C = Cfg<BN, KCH, Op::kPF, Op::kPFDepth, Op::kStages>;
     if (op.ntiles <= 0) return cudaSuccess;
     static bool attr_set = false;
     if (!attr_set) {
