@@ -130,7 +130,10 @@ __device__ __forceinline__ uint32_t lemire_threshold(uint32_t excl) {
 // draw buffer).  Plans per CTA: kWalkPlans for plans built ahead on a side stream
 // (few SMs held for the longer walk), 1 with EDGC_PLAN_LATENCY (the walk is on
 // the step's critical path: every SM to itself).
-constexpr int kWalkPlans = 16;              // plans per CTA (a walker and a producer warp each)
+#ifndef EDGC_WALK_PLANS
+#define EDGC_WALK_PLANS 16
+#endif
+constexpr int kWalkPlans = EDGC_WALK_PLANS;  // plans per CTA (a walker and a producer warp each)
 constexpr int kWalkQ = 8;                   // steps per walker lane per chunk
 constexpr int kWalkChunk = 32 * kWalkQ;
 constexpr int kWalkMaxRej = 8;              // rejections settled inside one chunk (ring lookahead)
