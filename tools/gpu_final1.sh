@@ -18,4 +18,5 @@ timeout 300 python tools/plan_prof.py --reps 5 >> $O/plan_prof.log 2>&1
 timeout 300 python tools/recon_probe.py --rank 4 > $O/recon_r4.log 2>&1
 timeout 300 python tools/api_probe.py > $O/api.log 2>&1
 timeout 1200 python bench.py --model 12.1B --rank 256 --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > $O/bench_12b_r256.log 2>&1
+for b in 0.25 0.05; do timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --alpha 1 --beta $b > $O/bench_alpha1_b$b.log 2>&1; done
 exit 0
