@@ -1667,11 +1667,14 @@ struct TcQ {
 // 13.6 vs 11.0 ms at r = 128)
 constexpr int kTcEFN = 128;
 
-struct TcEF {
+// PFD - 1 slices of g and w prefetched ahead; STAGES operand stages.  Up to r_res = 128 (K of at
+// most four 32-wide blocks) one stage and three slot buffers (the operands p_res, q_res are small);
+// above, the earlier two stages and two buffers (measured: r = 32 375 -> 388 GB/s with the first,
+// GPT2-12.1B at r = 256 166 vs 162 GB/s with the second)
+template <int PFD, int STAGES>
+struct TcEFT {
     static constexpr bool kAMN = false, kBMN = false;
-    // g and w of the slice, EDGC_TCEF_PFD - 1 slices ahead; the operands (p_res, q_res: K = r_res)
-    // are small, so one stage leaves the shared memory to the prefetch slots
-    static constexpr int kPF = 16, kPFDepth = EDGC_TCEF_PFD, kStages = EDGC_TCEF_STAGES;
+    static constexpr int kPF = 16, kPFDepth = PFD, kStages = STAGES;
     using Tile = GemmTile;
     const MatDev *mats;
     const GemmTile *tiles;
@@ -1737,6 +1740,8 @@ struct TcEF {
         if (bad) atomicOr(status + t.mat, 1);
     }
 };
+using TcEF = TcEFT<EDGC_TCEF_PFD, EDGC_TCEF_STAGES>;   // r_res <= 128
+using TcEFWide = TcEFT<2, 0>;
 
 // EDGC_TC_MIN_RANK (default 16): wide-path ranks above it use the tensor cores;
 // EDGC_NO_TC disables them (A/B runs)
@@ -1909,6 +1914,7 @@ struct Plan {
     std::vector<ZTile> tz[9];          // Z-path items grouped by cluster size 1..8
     std::vector<GemmTile> gw, gp, gq;  // wide path: EF update, P_raw and Q tiles for r > 32
     int ef_rk = 0;                     // largest r_res of the CUDA-core EF tiles (gw)
+    int tce_rk = 0;                    // largest r_res of the tcgen05 EF tiles (tce)
     std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles: r <= 16 (256x16), <= 32 (128x32), <= 8 (256x8)
     std::vector<GemmTile> tce, tcp[2], tcq[2];
     std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles
@@ -2028,6 +2034,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
             if (d.r_res > tc_ef_min_rank()) {
                 for (int64_t i0 = 0; i0 < d.m; i0 += tc::kBM)
                     for (int64_t j0 = 0; j0 < d.n; j0 += kTcEFN) P.tce.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
+                P.tce_rk = std::max(P.tce_rk, d.r_res);
             } else {
                 for (int64_t i0 = 0; i0 < d.m; i0 += kGT)
                     for (int64_t j0 = 0; j0 < d.n; j0 += kGT) P.gw.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
@@ -2614,8 +2621,13 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if ((rc = launch_pass1z(P, status_dev, P.sample_armed, st))) return rc;
         h->P.sample_armed = false;   // set_sampling arms exactly one pass 1
         if ((rc = launch_ef(P, st, status_dev))) return rc;
-        if (!P.tce.empty())
-            EDGC_CUDA_TRY((tc::launch<kTcEFN, 4>(TcEF{P.d_mats, P.d_tce, status_dev, (int)P.tce.size()}, sm_count(), st)));
+        if (!P.tce.empty()) {
+            if (P.tce_rk <= 128)
+                EDGC_CUDA_TRY((tc::launch<kTcEFN, 4>(TcEF{P.d_mats, P.d_tce, status_dev, (int)P.tce.size()}, sm_count(), st)));
+            else
+                EDGC_CUDA_TRY(
+                    (tc::launch<kTcEFN, 4>(TcEFWide{P.d_mats, P.d_tce, status_dev, (int)P.tce.size()}, sm_count(), st)));
+        }
         if (!P.tcp[0].empty())
             EDGC_CUDA_TRY((tc::launch<64, 4>(TcPraw{P.d_mats, P.d_tcp[0], (int)P.tcp[0].size()}, sm_count(), st)));
         if (!P.tcp[1].empty())

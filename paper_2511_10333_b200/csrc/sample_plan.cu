@@ -826,9 +826,15 @@ constexpr int kSSortPer = kSChunk / kSSortThreads;
 // 8K buckets, 256 threads, 6/SM 2.88 ms; 16K, 256 threads 3.30 ms
 constexpr int kSResThreads = (1 << kSBits) <= 8192 ? 256 : 512;
 constexpr int kSResPerSM = (1 << kSBits) <= 8192 ? 6 : 3;
-constexpr int kSResBatch = 4;                // segments whose loads a warp keeps in flight
+#ifndef EDGC_SRES_BATCH
+#define EDGC_SRES_BATCH 4
+#endif
+#ifndef EDGC_STAIL_WORDS
+#define EDGC_STAIL_WORDS 4
+#endif
+constexpr int kSResBatch = EDGC_SRES_BATCH;  // segments whose loads a warp keeps in flight
 constexpr int kSTailThreads = 256;           // a warp per bitmap word
-constexpr int kSTailWords = 4;               // words per warp (independent loads in flight)
+constexpr int kSTailWords = EDGC_STAIL_WORDS;  // words per warp (independent loads in flight)
 static_assert(kSChunk == kBChunk, "both bucket paths share the chunk tables");
 
 struct SSortSmem {
