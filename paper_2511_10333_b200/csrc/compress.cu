@@ -1559,6 +1559,167 @@ k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
         }
 }
 
+// P_raw partials with the EF update fused in (4 < r <= 16, r_res <= BN, float4-aligned rows):
+// the K step's g and w tiles arrive together by cp.async, the step first applies
+// w <- g + (w - p_res q_resᵀ) in shared memory -- each thread a 4-row x 8-column block,
+// products summed over s ascending exactly as k_ef, so w is bit-identical -- streams the
+// new w back to HBM, and then multiplies it into the P_raw partials as k_skinny<0> does.
+// One pass over w instead of two (12 B/elem for EF + P_raw instead of 16).
+#ifndef EDGC_SKEF_ROWS
+#define EDGC_SKEF_ROWS 128
+#endif
+constexpr int kSkEfRows = EDGC_SKEF_ROWS;   // rows per fused CTA
+template <int BM, int BN>
+struct SkEfSmem {
+    float a[2][BM][kSkK + 4];   // w -> x (new w) per stage
+    float g[2][BM][kSkK + 4];
+    float pt[BN][BM + 4];       // p_res rows of the CTA, transposed
+    float qt[BN][kSkK + 4];     // q_res rows of the K step, transposed
+    float b[kSkK][BN + 4];      // q_warm rows of the K step
+};
+template <int BM, int BN>
+__global__ void __launch_bounds__((BM / 4) * (BN / 4))
+k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
+    constexpr int TX = BN / 4, NT = (BM / 4) * TX;
+    constexpr int kAV = BM * kSkK / 4 / NT;          // float4 of one tile per thread
+    constexpr int kBV = BN * kSkK / NT;               // q_warm / q_res elements of one K step per thread
+    constexpr int kEB = BM / NT;                      // 4 x 8 EF blocks per thread (BM*32 / 32 / NT)
+    extern __shared__ __align__(16) unsigned char skef_raw[];
+    SkEfSmem<BM, BN> &S = *reinterpret_cast<SkEfSmem<BM, BN> *>(skef_raw);
+    const GemmTile t = tiles[blockIdx.x];
+    const MatDev &M = mats[t.mat];
+    const int64_t n = M.n, m = M.m, ldg = M.ld_g;
+    const int r = M.r, rres = M.r_res;
+    float *__restrict__ w = M.w;
+    const float *__restrict__ g = M.g;
+    const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+    for (int e = tid; e < BN * BM; e += NT) {
+        const int s = e / BM, ii = e % BM;
+        const int64_t gi = t.i0 + ii;
+        S.pt[s][ii] = (s < rres && gi < m) ? M.p_res[gi * rres + s] : 0.f;
+    }
+    auto issue = [&](int64_t k0, int buf) {
+#pragma unroll
+        for (int u = 0; u < kAV; ++u) {
+            const int e = tid + u * NT;
+            const int ii = e / (kSkK / 4), kk = 4 * (e % (kSkK / 4));
+            const int64_t gi = t.i0 + ii, gk = k0 + kk;
+            if (gi < m && gk + 4 <= t.k1) {   // rows are float4-aligned and K chunks multiples of 4
+                tc::cp_async16(&S.a[buf][ii][kk], w + gi * n + gk);
+                tc::cp_async16(&S.g[buf][ii][kk], g + gi * ldg + gk);
+            } else {
+                *reinterpret_cast<float4 *>(&S.a[buf][ii][kk]) = make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4 *>(&S.g[buf][ii][kk]) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        tc::cp_async_commit();
+    };
+    auto load_b = [&](int64_t k0, float (&b)[kBV], float (&q)[kBV]) {
+#pragma unroll
+        for (int u = 0; u < kBV; ++u) {
+            const int e = tid + u * NT;
+            const int64_t gj = t.j0 + e % BN, gk = k0 + e / BN;
+            b[u] = (gj < r && gk < t.k1) ? M.q_warm[gk * M.ld_q + gj] : 0.f;
+            const int s = e % BN;
+            q[u] = (s < rres && gk < t.k1) ? M.q_res[gk * rres + s] : 0.f;
+        }
+    };
+    double acc[4][4] = {};
+    float b_next[kBV], q_next[kBV];
+    issue(t.k0, 0);
+    load_b(t.k0, b_next, q_next);
+    bool bad = false;
+    int buf = 0;
+    for (int64_t k0 = t.k0; k0 < t.k1; k0 += kSkK, buf ^= 1) {
+        const bool more = k0 + kSkK < t.k1;
+        if (more) issue(k0 + kSkK, buf ^ 1);
+#pragma unroll
+        for (int u = 0; u < kBV; ++u) {
+            const int e = tid + u * NT;
+            S.b[e / BN][e % BN] = b_next[u];
+            S.qt[e % BN][e / BN] = q_next[u];
+        }
+        if (more) tc::cp_async_wait<1>();
+        else tc::cp_async_wait<0>();
+        __syncthreads();
+        if (more) load_b(k0 + kSkK, b_next, q_next);
+        // EF on the tile: block (rows 4 rb .. +3, columns 8 cb .. +7)
+#pragma unroll
+        for (int eb = 0; eb < kEB; ++eb) {
+            const int bid = tid + eb * NT, rb = bid / 4, cb = bid % 4;
+            float c[4][8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 8; ++v) c[u][v] = 0.f;
+            for (int s2 = 0; s2 < rres; ++s2) {
+                const float4 a4 = *reinterpret_cast<const float4 *>(&S.pt[s2][rb * 4]);
+                const float4 q0 = *reinterpret_cast<const float4 *>(&S.qt[s2][cb * 8]);
+                const float4 q1 = *reinterpret_cast<const float4 *>(&S.qt[s2][cb * 8 + 4]);
+                const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+                const float q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) c[u][v] = a[u] * q[v] + c[u][v];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int ii = rb * 4 + u;
+                const int64_t gi = t.i0 + ii, gk = k0 + cb * 8;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float4 *ap = reinterpret_cast<float4 *>(&S.a[buf][ii][cb * 8 + 4 * h]);
+                    const float4 w4 = *ap;
+                    const float4 g4 = *reinterpret_cast<const float4 *>(&S.g[buf][ii][cb * 8 + 4 * h]);
+                    const float x0 = g4.x + (w4.x - c[u][4 * h]), x1 = g4.y + (w4.y - c[u][4 * h + 1]);
+                    const float x2 = g4.z + (w4.z - c[u][4 * h + 2]), x3 = g4.w + (w4.w - c[u][4 * h + 3]);
+                    const float4 x = make_float4(x0, x1, x2, x3);
+                    *ap = x;
+                    if (gi < m && gk + 4 * h + 4 <= t.k1) {
+                        bad |= !(isfinite(x0) && isfinite(x1) && isfinite(x2) && isfinite(x3));
+                        __stcs(reinterpret_cast<float4 *>(w + gi * n + gk + 4 * h), x);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        float accf[4][4] = {};
+#pragma unroll
+        for (int k4 = 0; k4 < kSkK; k4 += 4) {
+            float a[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {   // rows ty + u BM/4: 8 rows of a warp on distinct banks
+                const float4 x = *reinterpret_cast<const float4 *>(&S.a[buf][ty + u * (BM / 4)][k4]);
+                a[u][0] = x.x; a[u][1] = x.y; a[u][2] = x.z; a[u][3] = x.w;
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float4 b4 = *reinterpret_cast<const float4 *>(&S.b[k4 + c][tx * 4]);
+                const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) accf[u][v] = fmaf(a[u][c], b[v], accf[u][v]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] += (double)accf[u][v];
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t gi = t.i0 + ty + u * (BM / 4), gj = t.j0 + tx * 4 + v;
+            if (gi >= m || gj >= r) continue;
+            M.p_part[((int64_t)t.split * m + gi) * r + gj] = acc[u][v];
+        }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
+}
+
 // cudaFuncSetAttribute applies to the current device: remember which devices have it
 template <typename K>
 int smem_attr_once(K kernel, int bytes, uint64_t &done_mask) {
@@ -1576,6 +1737,15 @@ int launch_skinny(unsigned grid, cudaStream_t st, const MatDev *mats, const Gemm
     const int rc = smem_attr_once(k_skinny<OP, BM, BN>, skinny_smem<OP, BM>(), attr);
     if (rc != EDGC_OK) return rc;
     k_skinny<OP, BM, BN><<<grid, (BM / 4) * (BN / 4), skinny_smem<OP, BM>(), st>>>(mats, tiles, status);
+    return EDGC_OK;
+}
+
+template <int BM, int BN>
+int launch_skinny_ef(unsigned grid, cudaStream_t st, const MatDev *mats, const GemmTile *tiles, int32_t *status) {
+    static uint64_t attr = 0;
+    const int rc = smem_attr_once(k_skinny_ef<BM, BN>, (int)sizeof(SkEfSmem<BM, BN>), attr);
+    if (rc != EDGC_OK) return rc;
+    k_skinny_ef<BM, BN><<<grid, (BM / 4) * (BN / 4), sizeof(SkEfSmem<BM, BN>), st>>>(mats, tiles, status);
     return EDGC_OK;
 }
 
@@ -1769,6 +1939,13 @@ int narrow_max() {
 // EDGC_TC_EF_MIN_RANK (default EDGC_TC_MIN_RANK): the EF update uses the tensor cores above it
 int tc_ef_min_rank();
 
+// EDGC_SKINNY_EF_OFF: keep the EF update of 4 < r <= 16 as its own pass (k_ef) instead of fused
+// into the P_raw partials
+bool skef_off() {
+    static const bool v = std::getenv("EDGC_SKINNY_EF_OFF") != nullptr;
+    return v;
+}
+
 int tc_min_rank() {
     static const int v = [] {
         if (std::getenv("EDGC_NO_TC")) return 1 << 30;
@@ -1916,6 +2093,8 @@ struct Plan {
     int ef_rk = 0;                     // largest r_res of the CUDA-core EF tiles (gw)
     int tce_rk = 0;                    // largest r_res of the tcgen05 EF tiles (tce)
     std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles: r <= 16 (256x16), <= 32 (128x32), <= 8 (256x8)
+    std::vector<GemmTile> spf[2];         // P_raw with the EF update fused: r <= 8 (x8), <= 16 (x16)
+    GemmTile *d_spf[2] = {};
     std::vector<GemmTile> tce, tcp[2], tcq[2];
     std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles
     int64_t nfxg64 = 0, nfxr64 = 0;   // the first n are 64-edge tiles, the rest kFxBig-edge   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
@@ -2031,6 +2210,21 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         const int64_t k2 = (M.wide && (M.tc || d.r > 32)) ? d.m : kP2Rows;
         M.nblk2 = (int32_t)ceil_div(d.m, k2);
         if (M.wide) {
+            // 4 < r <= 16, aligned, residual rank within the rank block: EF fused into P_raw
+            const int fbn = d.r <= 8 ? 8 : 16;
+            const bool fuse = !skef_off() && M.al4 && d.r > 4 && d.r <= 16 && d.r_res <= fbn && !M.tc;
+            if (fuse) {
+                for (int32_t c = 0; c < M.nchunk1; ++c)
+                    for (int64_t i0 = 0; i0 < d.m; i0 += kSkEfRows)
+                        P.spf[fbn == 8 ? 0 : 1].push_back(GemmTile{k, c, i0, 0, c * k1, std::min(d.n, (c + 1) * k1)});
+                const int BM = 256, BN = fbn;
+                std::vector<GemmTile> &tq = P.sq[fbn == 8 ? 2 : 0];
+                for (int32_t b = 0; b < M.nblk2; ++b)
+                    for (int64_t i0 = 0; i0 < d.n; i0 += BM)
+                        for (int64_t j0 = 0; j0 < d.r; j0 += BN)
+                            tq.push_back(GemmTile{k, b, i0, j0, (int64_t)b * k2, std::min(d.m, (int64_t)(b + 1) * k2)});
+                continue;
+            }
             if (d.r_res > tc_ef_min_rank()) {
                 for (int64_t i0 = 0; i0 < d.m; i0 += tc::kBM)
                     for (int64_t j0 = 0; j0 < d.n; j0 += kTcEFN) P.tce.push_back(GemmTile{k, 0, i0, j0, 0, d.r_res});
@@ -2115,6 +2309,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     for (int c = 1; c <= 8; ++c) P.d_tz[c] = a.take<ZTile>(P.tz[c].size());
     for (int c = 0; c < 3; ++c) {
         P.d_sp[c] = a.take<GemmTile>(P.sp[c].size());
+        if (c < 2) P.d_spf[c] = a.take<GemmTile>(P.spf[c].size());
         P.d_sq[c] = a.take<GemmTile>(P.sq[c].size());
     }
     P.d_tce = a.take<GemmTile>(P.tce.size());
@@ -2599,6 +2794,7 @@ extern "C" int edgc_compress_plan_bind(edgc_compress_plan *h, void *ws, int64_t 
     EDGC_CUDA_TRY(upg(P.d_gq, P.gq));
     for (int c = 0; c < 3; ++c) {
         EDGC_CUDA_TRY(upg(P.d_sp[c], P.sp[c]));
+        if (c < 2) EDGC_CUDA_TRY(upg(P.d_spf[c], P.spf[c]));
         EDGC_CUDA_TRY(upg(P.d_sq[c], P.sq[c]));
     }
     // the host staging vectors stay alive in the plan; make the upload complete
@@ -2632,6 +2828,14 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
             EDGC_CUDA_TRY((tc::launch<64, 4>(TcPraw{P.d_mats, P.d_tcp[0], (int)P.tcp[0].size()}, sm_count(), st)));
         if (!P.tcp[1].empty())
             EDGC_CUDA_TRY((tc::launch<128, 4>(TcPraw{P.d_mats, P.d_tcp[1], (int)P.tcp[1].size()}, sm_count(), st)));
+        if (!P.spf[0].empty()) {
+            if ((rc = launch_skinny_ef<kSkEfRows, 8>((unsigned)P.spf[0].size(), st, P.d_mats, P.d_spf[0], status_dev))) return rc;
+            EDGC_LAUNCH_CHECK();
+        }
+        if (!P.spf[1].empty()) {
+            if ((rc = launch_skinny_ef<kSkEfRows, 16>((unsigned)P.spf[1].size(), st, P.d_mats, P.d_spf[1], status_dev))) return rc;
+            EDGC_LAUNCH_CHECK();
+        }
         if (!P.sp[0].empty()) {
             if ((rc = launch_skinny<0, 256, 16>((unsigned)P.sp[0].size(), st, P.d_mats, P.d_sp[0], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
