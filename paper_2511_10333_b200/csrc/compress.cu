@@ -1565,10 +1565,9 @@ k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
 // products summed over s ascending exactly as k_ef, so w is bit-identical -- streams the
 // new w back to HBM, and then multiplies it into the P_raw partials as k_skinny<0> does.
 // One pass over w instead of two (12 B/elem for EF + P_raw instead of 16).
-#ifndef EDGC_SKEF_ROWS
-#define EDGC_SKEF_ROWS 128
-#endif
-constexpr int kSkEfRows = EDGC_SKEF_ROWS;   // rows per fused CTA
+// rows per fused CTA: 64 for 8-rank blocks (32 threads, 5 CTAs per SM by shared memory),
+// 128 for 16 (measured at r = 8: 64 / 128 / 256 rows 772 / 747 / 701 GB/s; r = 16: 611 / 630 / 573)
+constexpr int kSkEfRows8 = 64, kSkEfRows16 = 128;
 template <int BM, int BN>
 struct SkEfSmem {
     float a[2][BM][kSkK + 4];   // w -> x (new w) per stage
@@ -2215,7 +2214,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
             const bool fuse = !skef_off() && M.al4 && d.r > 4 && d.r <= 16 && d.r_res <= fbn && !M.tc;
             if (fuse) {
                 for (int32_t c = 0; c < M.nchunk1; ++c)
-                    for (int64_t i0 = 0; i0 < d.m; i0 += kSkEfRows)
+                    for (int64_t i0 = 0; i0 < d.m; i0 += (fbn == 8 ? kSkEfRows8 : kSkEfRows16))
                         P.spf[fbn == 8 ? 0 : 1].push_back(GemmTile{k, c, i0, 0, c * k1, std::min(d.n, (c + 1) * k1)});
                 const int BM = 256, BN = fbn;
                 std::vector<GemmTile> &tq = P.sq[fbn == 8 ? 2 : 0];
@@ -2829,11 +2828,11 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if (!P.tcp[1].empty())
             EDGC_CUDA_TRY((tc::launch<128, 4>(TcPraw{P.d_mats, P.d_tcp[1], (int)P.tcp[1].size()}, sm_count(), st)));
         if (!P.spf[0].empty()) {
-            if ((rc = launch_skinny_ef<kSkEfRows, 8>((unsigned)P.spf[0].size(), st, P.d_mats, P.d_spf[0], status_dev))) return rc;
+            if ((rc = launch_skinny_ef<kSkEfRows8, 8>((unsigned)P.spf[0].size(), st, P.d_mats, P.d_spf[0], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if (!P.spf[1].empty()) {
-            if ((rc = launch_skinny_ef<kSkEfRows, 16>((unsigned)P.spf[1].size(), st, P.d_mats, P.d_spf[1], status_dev))) return rc;
+            if ((rc = launch_skinny_ef<kSkEfRows16, 16>((unsigned)P.spf[1].size(), st, P.d_mats, P.d_spf[1], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if (!P.sp[0].empty()) {
