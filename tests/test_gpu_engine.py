@@ -61,6 +61,18 @@ def test_engine_narrow_passes_match_oracle(rank):
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
 
 
+@pytest.mark.parametrize("rank", [8, 16])
+def test_engine_separate_ef_pass_matches_oracle(rank):
+    """4 < r <= 16 fuse the EF update into the P_raw partials (k_skinny_ef) by default;
+    EDGC_SKINNY_EF_OFF=1 keeps the separate EF pass (k_ef) that rank transitions still use."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EDGC_SKINNY_EF_OFF="1")
+    code = (f"import sys; sys.path.insert(0, {root!r}); "
+            f"from tests.test_gpu_engine import test_engine_matches_oracle_dp_step_chained as t; t({rank})")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+
+
 @pytest.mark.parametrize("rank", [96, 256])
 def test_engine_tensor_core_ranks_match_oracle(rank):
     """Wide ranks on the tcgen05 path (EF update, P_raw, Q, reconstruction: 3xTF32 with
