@@ -2561,7 +2561,18 @@ constexpr int kV4Threads = 128;
 constexpr int kV4Cols = 4 * kV4Threads;
 constexpr int kV4Rows = 8;
 // rows per tile: 64 while Q (W*r <= 8 per column) is cheap to load, 256 above to amortise it
-__host__ __device__ constexpr int v4_tile_rows(int wr) { return wr <= 8 ? 64 : 256; }
+// rows per reconstruction tile (x 512 columns): one tile's Q columns stay in registers across
+// them.  W r = 5..8: 256 (measured 64 / 128 / 256 rows: r = 8 at W = 1 1.96 / 1.52 / 1.39 ms,
+// r = 4 at W = 2 1.50 / 1.35 / 1.37 ms)
+#ifndef EDGC_RECON4_ROWS
+#define EDGC_RECON4_ROWS 64
+#endif
+#ifndef EDGC_RECON8_ROWS
+#define EDGC_RECON8_ROWS 256
+#endif
+__host__ __device__ constexpr int v4_tile_rows(int wr) {
+    return wr <= 4 ? EDGC_RECON4_ROWS : wr <= 8 ? EDGC_RECON8_ROWS : 256;
+}
 
 // VC adjacent columns per thread (4, or 2 when W*r = 32 to keep Q in registers);
 // kV4Cols = 512 columns per tile either way.
