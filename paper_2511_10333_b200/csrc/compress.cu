@@ -2570,8 +2570,14 @@ constexpr int kV4Rows = 8;
 #ifndef EDGC_RECON8_ROWS
 #define EDGC_RECON8_ROWS 256
 #endif
+#ifndef EDGC_RECON16_TROWS
+#define EDGC_RECON16_TROWS 512   // W r = 9..16 (256 rows: r = 16 at W = 1 2.32 ms, 512: 2.08 ms)
+#endif
+#ifndef EDGC_RECON32_TROWS
+#define EDGC_RECON32_TROWS 256
+#endif
 __host__ __device__ constexpr int v4_tile_rows(int wr) {
-    return wr <= 4 ? EDGC_RECON4_ROWS : wr <= 8 ? EDGC_RECON8_ROWS : 256;
+    return wr <= 4 ? EDGC_RECON4_ROWS : wr <= 8 ? EDGC_RECON8_ROWS : wr <= 16 ? EDGC_RECON16_TROWS : EDGC_RECON32_TROWS;
 }
 
 // VC adjacent columns per thread (4, or 2 when W*r = 32 to keep Q in registers);
@@ -2969,6 +2975,9 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
     P.tilesC.clear();
     P.d.resize(n);
     P.dd = a.take<ReconDev>(n);
+    int wr4max = 0;   // as edgc_recon_plan_create's wr4
+    for (int k = 0; k < n; ++k)
+        if (descs[k].r * descs[k].n_ranks <= 32) wr4max = std::max(wr4max, descs[k].r * descs[k].n_ranks);
     for (int k = 0; k < n; ++k) {
         const edgc_recon_desc &s = descs[k];
         EDGC_REQUIRE(s.m >= 1 && s.n >= 1 && s.r >= 1 && s.n_ranks >= 1 && s.p && s.q && s.out && s.ld_out >= s.n,
@@ -2984,7 +2993,9 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
                 for (int64_t c0 = 0; c0 < s.n; c0 += 128)
                     P.tilesC.push_back(RTile{k, c0, std::min(s.n, c0 + 128), r0, std::min(s.m, r0 + tc::kBM)});
         } else if (v4) {
-            const int64_t tr = v4_tile_rows(s.r * s.n_ranks <= 4 ? 4 : s.r * s.n_ranks <= 8 ? 8 : 16);
+            // the launch's kernel is chosen by the largest W r of the float4 tiles: its tile height
+            // (shared-memory P tile) bounds every tile's rows
+            const int64_t tr = v4_tile_rows(wr4max <= 4 ? 4 : wr4max <= 8 ? 8 : wr4max <= 16 ? 16 : 32);
             for (int64_t c0 = 0; c0 < s.n; c0 += kV4Cols)
                 for (int64_t r0 = 0; r0 < s.m; r0 += tr)
                     P.tiles4.push_back(RTile{k, c0, std::min(s.n, c0 + kV4Cols), r0, std::min(s.m, r0 + tr)});
