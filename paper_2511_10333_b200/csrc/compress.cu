@@ -2574,7 +2574,7 @@ constexpr int kV4Rows = 8;
 #define EDGC_RECON16_TROWS 512   // W r = 9..16 (256 rows: r = 16 at W = 1 2.32 ms, 512: 2.08 ms)
 #endif
 #ifndef EDGC_RECON32_TROWS
-#define EDGC_RECON32_TROWS 256
+#define EDGC_RECON32_TROWS 512   // W r = 17..32 (64 / 128 / 256 / 512 rows at W = 8, r = 4: 4.79 / 4.20 / 3.92 / 3.79 ms)
 #endif
 __host__ __device__ constexpr int v4_tile_rows(int wr) {
     return wr <= 4 ? EDGC_RECON4_ROWS : wr <= 8 ? EDGC_RECON8_ROWS : wr <= 16 ? EDGC_RECON16_TROWS : EDGC_RECON32_TROWS;
@@ -2607,7 +2607,8 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
     auto p_of = [&](int w) -> const float * { return D.p + (int64_t)w * D.p_stride; };
     auto q_of = [&](int w) -> const float * { return D.q + (int64_t)w * D.q_stride; };
     // P tile transposed ([k][row]): one 16-byte shared read gives 4 rows of one k
-    __shared__ __align__(16) float s_pT[WR][kV4TileRows];
+    extern __shared__ __align__(16) float recon4_smem[];   // [WR][kV4TileRows], dynamic (64 KB at W r = 32)
+    float (*s_pT)[kV4TileRows] = reinterpret_cast<float (*)[kV4TileRows]>(recon4_smem);
     // thread = (row, rank): its r consecutive P values; (worker, k) indexed incrementally (no div/mod)
     for (int e = threadIdx.x; e < kV4TileRows * D.n_ranks; e += NT) {
         const int rr = e % kV4TileRows, w = e / kV4TileRows;
@@ -3070,10 +3071,17 @@ extern "C" int edgc_recon_plan_run(edgc_recon_plan *h, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (!h->P.tiles4.empty()) {
         const unsigned g4 = (unsigned)h->P.tiles4.size();
-        if (h->wr4 <= 4) k_recon4<4, 4><<<g4, kV4Cols / 4, 0, st>>>(h->P.dd, h->P.dt4);
-        else if (h->wr4 <= 8) k_recon4<8, 4><<<g4, kV4Cols / 4, 0, st>>>(h->P.dd, h->P.dt4);
-        else if (h->wr4 <= 16) k_recon4<16, 4><<<g4, kV4Cols / 4, 0, st>>>(h->P.dd, h->P.dt4);
-        else k_recon4<32, 2><<<g4, kV4Cols / 2, 0, st>>>(h->P.dd, h->P.dt4);
+        constexpr size_t s4 = 4 * v4_tile_rows(4) * sizeof(float), s8 = 8 * v4_tile_rows(8) * sizeof(float);
+        constexpr size_t s16 = 16 * v4_tile_rows(16) * sizeof(float), s32 = 32 * v4_tile_rows(32) * sizeof(float);
+        static uint64_t a32 = 0;
+        int rc;
+        if (h->wr4 <= 4) k_recon4<4, 4><<<g4, kV4Cols / 4, s4, st>>>(h->P.dd, h->P.dt4);
+        else if (h->wr4 <= 8) k_recon4<8, 4><<<g4, kV4Cols / 4, s8, st>>>(h->P.dd, h->P.dt4);
+        else if (h->wr4 <= 16) k_recon4<16, 4><<<g4, kV4Cols / 4, s16, st>>>(h->P.dd, h->P.dt4);
+        else {
+            if ((rc = smem_attr_once(k_recon4<32, 2>, (int)s32, a32))) return rc;
+            k_recon4<32, 2><<<g4, kV4Cols / 2, s32, st>>>(h->P.dd, h->P.dt4);
+        }
         EDGC_LAUNCH_CHECK();
     }
     if (!h->P.tiles.empty()) {
