@@ -1568,6 +1568,14 @@ k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
 // rows per fused CTA: 64 for 8-rank blocks (32 threads, 5 CTAs per SM by shared memory),
 // 128 for 16 (measured at r = 8: 64 / 128 / 256 rows 772 / 747 / 701 GB/s; r = 16: 611 / 630 / 573)
 constexpr int kSkEfRows8 = 64, kSkEfRows16 = 128;
+// Q partials (k_skinny<1>) rows (columns j of w) per CTA
+#ifndef EDGC_SKQ_ROWS8
+#define EDGC_SKQ_ROWS8 256
+#endif
+#ifndef EDGC_SKQ_ROWS16
+#define EDGC_SKQ_ROWS16 128   // measured r = 16: 128 / 256 / 512 rows 656 / 647 / 619 GB/s; r = 8 best at 256
+#endif
+constexpr int kSkQRows8 = EDGC_SKQ_ROWS8, kSkQRows16 = EDGC_SKQ_ROWS16;
 template <int BM, int BN>
 struct SkEfSmem {
     float a[2][BM][kSkK + 4];   // w -> x (new w) per stage
@@ -2216,7 +2224,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                 for (int32_t c = 0; c < M.nchunk1; ++c)
                     for (int64_t i0 = 0; i0 < d.m; i0 += (fbn == 8 ? kSkEfRows8 : kSkEfRows16))
                         P.spf[fbn == 8 ? 0 : 1].push_back(GemmTile{k, c, i0, 0, c * k1, std::min(d.n, (c + 1) * k1)});
-                const int BM = 256, BN = fbn;
+                const int BM = fbn == 8 ? kSkQRows8 : kSkQRows16, BN = fbn;
                 std::vector<GemmTile> &tq = P.sq[fbn == 8 ? 2 : 0];
                 for (int32_t b = 0; b < M.nblk2; ++b)
                     for (int64_t i0 = 0; i0 < d.n; i0 += BM)
@@ -2252,8 +2260,9 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                 for (int64_t i0 = 0; i0 < d.m; i0 += BM)
                     for (int64_t j0 = 0; j0 < d.r; j0 += BN)
                         tp.push_back(GemmTile{k, c, i0, j0, c * k1, std::min(d.n, (c + 1) * k1)});
+            const int QBM = cfg == 2 ? kSkQRows8 : (cfg == 0 ? kSkQRows16 : BM);
             for (int32_t b = 0; b < M.nblk2; ++b)
-                for (int64_t i0 = 0; i0 < d.n; i0 += BM)
+                for (int64_t i0 = 0; i0 < d.n; i0 += QBM)
                     for (int64_t j0 = 0; j0 < d.r; j0 += BN)
                         tq.push_back(GemmTile{k, b, i0, j0, (int64_t)b * k2, std::min(d.m, (int64_t)(b + 1) * k2)});
             continue;
@@ -2894,7 +2903,7 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if ((rc = launch_pass2(P, true, status_dev, st))) return rc;
         if ((rc = launch_pass2(P, false, status_dev, st))) return rc;
         if (!P.sq[0].empty()) {
-            if ((rc = launch_skinny<1, 256, 16>((unsigned)P.sq[0].size(), st, P.d_mats, P.d_sq[0], status_dev))) return rc;
+            if ((rc = launch_skinny<1, kSkQRows16, 16>((unsigned)P.sq[0].size(), st, P.d_mats, P.d_sq[0], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if (!P.sq[1].empty()) {
@@ -2902,7 +2911,7 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
             EDGC_LAUNCH_CHECK();
         }
         if (!P.sq[2].empty()) {
-            if ((rc = launch_skinny<1, 256, 8>((unsigned)P.sq[2].size(), st, P.d_mats, P.d_sq[2], status_dev))) return rc;
+            if ((rc = launch_skinny<1, kSkQRows8, 8>((unsigned)P.sq[2].size(), st, P.d_mats, P.d_sq[2], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if ((rc = launch_gemm<1>(P, P.gq, P.d_gq, status_dev, st))) return rc;
