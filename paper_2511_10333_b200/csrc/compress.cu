@@ -3086,7 +3086,11 @@ extern "C" int edgc_recon_plan_run(edgc_recon_plan *h, void *stream) {
         int rc;
         if (h->wr4 <= 4) k_recon4<4, 4><<<g4, kV4Cols / 4, s4, st>>>(h->P.dd, h->P.dt4);
         else if (h->wr4 <= 8) k_recon4<8, 4><<<g4, kV4Cols / 4, s8, st>>>(h->P.dd, h->P.dt4);
-        else if (h->wr4 <= 16) k_recon4<16, 4><<<g4, kV4Cols / 4, s16, st>>>(h->P.dd, h->P.dt4);
+        else if (h->wr4 <= 16) {
+            static uint64_t a16 = 0;
+            if ((rc = smem_attr_once(k_recon4<16, 4>, (int)s16, a16))) return rc;
+            k_recon4<16, 4><<<g4, kV4Cols / 4, s16, st>>>(h->P.dd, h->P.dt4);
+        }
         else {
             if ((rc = smem_attr_once(k_recon4<32, 2>, (int)s32, a32))) return rc;
             k_recon4<32, 2><<<g4, kV4Cols / 2, s32, st>>>(h->P.dd, h->P.dt4);
