@@ -42,7 +42,6 @@ __device__ __forceinline__ double load_sample(const GaussDev &d, int64_t i) {
 // partial[desc][block] = {sum(x-K), sum((x-K)^2)} with the shift K = first sample
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_gauss_partial(const GaussDev *descs, int ndesc, double2 *partial) {
-    __shared__ double2 s_red[kRedThreads / 32];
     // one persistent grid walks the layers in order (layer-major: the whole GPU
     // works on one matrix at a time, which keeps a gather's sectors in L2)
     for (int di = 0; di < ndesc; ++di) {
@@ -139,17 +138,13 @@ __global__ void __launch_bounds__(kRedThreads) k_gauss_partial(const GaussDev *d
             s2 += v * v;
         }
     }
+    // one partial per warp (no block barrier between layers, so the load stream does not drain
+    // at every matrix boundary); k_gauss_finish sums them in a fixed order
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) s_red[warp] = make_double2(s1, s2);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (int w = 0; w < kRedThreads / 32; ++w) { a += s_red[w].x; b += s_red[w].y; }
-        partial[(int64_t)di * gridDim.x + blockIdx.x] = make_double2(a, b);
-    }
-    __syncthreads();
+    if (lane == 0)
+        partial[((int64_t)di * gridDim.x + blockIdx.x) * (kRedThreads / 32) + warp] = make_double2(s1, s2);
     }
 }
 
@@ -702,7 +697,7 @@ using namespace edgc;
 extern "C" int64_t edgc_entropy_gaussian_workspace_bytes(const edgc_gauss_desc *descs, int n) {
     (void)descs;
     return align256(sizeof(GaussDev) * (int64_t)std::max(n, 1)) +
-           align256(sizeof(double2) * (int64_t)std::max(n, 1) * kGaussBlocksPerDesc);
+           align256(sizeof(double2) * (int64_t)std::max(n, 1) * kGaussBlocksPerDesc * (kRedThreads / 32));
 }
 
 extern "C" int edgc_entropy_gaussian(int src_dtype, const edgc_gauss_desc *descs, int n, double *h_out,
@@ -713,7 +708,7 @@ extern "C" int edgc_entropy_gaussian(int src_dtype, const edgc_gauss_desc *descs
     EDGC_REQUIRE(ws_bytes >= edgc_entropy_gaussian_workspace_bytes(descs, n), "edgc_entropy_gaussian: workspace");
     Arena a(ws, ws_bytes);
     GaussDev *d = a.take<GaussDev>(n);
-    double2 *part = a.take<double2>((int64_t)n * kGaussBlocksPerDesc);
+    double2 *part = a.take<double2>((int64_t)n * kGaussBlocksPerDesc * (kRedThreads / 32));
     std::vector<GaussDev> h(n);
     for (int i = 0; i < n; ++i) {
         EDGC_REQUIRE(!descs[i].bitmap || descs[i].idx, "gauss desc %d: a bitmap needs idx (for the shift)", i);
@@ -726,7 +721,8 @@ extern "C" int edgc_entropy_gaussian(int src_dtype, const edgc_gauss_desc *descs
     else
         k_gauss_partial<double><<<kGaussBlocksPerDesc, kRedThreads, 0, st>>>(d, n, part);
     EDGC_LAUNCH_CHECK();
-    k_gauss_finish<<<(n + 3) / 4, 128, 0, st>>>(d, n, part, kGaussBlocksPerDesc, h_out, status_dev);
+    k_gauss_finish<<<(n + 3) / 4, 128, 0, st>>>(d, n, part, kGaussBlocksPerDesc * (kRedThreads / 32), h_out,
+                                                 status_dev);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }
