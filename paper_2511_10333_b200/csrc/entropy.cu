@@ -22,7 +22,13 @@ constexpr int kRedThreads = 256;
 // one or two matrices at a time, so their sectors stay in L2 and each matrix is
 // read from DRAM about once (a scattered gather over all layers at once thrashes
 // L2 and moves ~30x the algorithmic bytes).
-constexpr int kGaussBlocksPerDesc = 1184;   // 8 x 148 SMs, persistent over layers
+#ifndef EDGC_GAUSS_UNROLL
+#define EDGC_GAUSS_UNROLL 8   // measured 4: 2.16 ms, 2: 1.75, 8: 1.74 (GPT2-2.5B set)
+#endif
+#ifndef EDGC_GAUSS_BLOCKS
+#define EDGC_GAUSS_BLOCKS 1184
+#endif
+constexpr int kGaussBlocksPerDesc = EDGC_GAUSS_BLOCKS;   // 8 x 148 SMs, persistent over layers
 
 // ---------------------------------------------------------------- Gaussian
 struct GaussDev {
@@ -65,17 +71,18 @@ __global__ void __launch_bounds__(kRedThreads) k_gauss_partial(const GaussDev *d
                     s2 += x * x;
                 }
         };
-        for (; q + 3 * stride < nq; q += 4 * stride) {
-            float4 v[4];
-            uint32_t bw[4];
+        constexpr int U = EDGC_GAUSS_UNROLL;   // float4 loads in flight per thread
+        for (; q + (U - 1) * stride < nq; q += U * stride) {
+            float4 v[U];
+            uint32_t bw[U];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < U; ++k) {
                 const int64_t qq = q + k * stride;
                 v[k] = __ldg(src4 + qq);
                 bw[k] = __ldg(d.bitmap + (qq >> 3)) >> ((qq & 7) * 4);
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) take(v[k], bw[k]);
+            for (int k = 0; k < U; ++k) take(v[k], bw[k]);
         }
         for (; q < nq; q += stride) take(__ldg(src4 + q), __ldg(d.bitmap + (q >> 3)) >> ((q & 7) * 4));
         const int64_t e = 4 * nq + threadIdx.x;   // ragged tail (< 4 elements)
