@@ -2121,6 +2121,35 @@ struct Plan {
     int64_t sample_slots = 0;           // partial slots per matrix (0: some matrix off the Z path)
 };
 
+// Clusters of c pass-1 CTAs that can be resident at once (cudaOccupancyMaxActiveClusters: a
+// cluster must sit inside one GPC of 18-20 SMs, so a 148-SM part holds fewer than 24 six-CTA
+// clusters, not 148 / 6); cached per width.  0 if the query fails.
+int pass1_max_clusters(int c) {
+    static int cached[9] = {};
+    if (c < 1 || c > 8) return 0;
+    if (cached[c]) return cached[c];
+    static uint64_t attr_f = 0;
+    if (smem_attr_once(k_pass1t<false>, (int)sizeof(TSmem), attr_f) != EDGC_OK) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(c * 64));
+    cfg.blockDim = dim3(kTThreads);
+    cfg.dynamicSmemBytes = sizeof(TSmem);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int num = 0;
+    if (cudaOccupancyMaxActiveClusters(&num, k_pass1t<false>, &cfg) != cudaSuccess || num <= 0) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    cached[c] = num;
+    return num;
+}
+
 int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes, Plan &P) {
     Arena a(ws, ws_bytes);
     P.mats.resize(n);
@@ -2144,7 +2173,30 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
             ctas += ceil_div(std::max<int64_t>(descs[k].m, 1), kZRows) * zc;
         }
         const int64_t want = (int64_t)sm_count();
-        if (ctas < want) zrows = std::max<int64_t>(16, (kZRows * ctas / want) / 4 * 4);
+        if (ctas < want) {
+            // thinner strips, but no more clusters than one wave holds: every width's clusters
+            // within its resident-cluster limit and all CTAs within the SM count (a second wave
+            // of a few clusters would double the kernel: 1024 x 4096 at 40 rows gave 26 six-CTA
+            // clusters, 41 us; 48 rows, 22 clusters: 25.5 us)
+            zrows = std::max<int64_t>(16, ceil_div(kZRows * ctas, want * 4) * 4);
+            for (; zrows < kZRows; zrows += 4) {
+                int64_t cl[9] = {}, tot = 0;
+                for (int k = 0; k < n; ++k) {
+                    int zc = (int)ceil_div(std::max<int64_t>(descs[k].n, 1), kTCW);
+                    if (zc == 4 || zc == 5) zc = 6;
+                    if (zc > 8) continue;
+                    const int64_t c = ceil_div(std::max<int64_t>(descs[k].m, 1), zrows);
+                    cl[zc] += c;
+                    tot += c * zc;
+                }
+                bool fits = tot <= want;
+                for (int c = 1; c <= 8 && fits; ++c) {
+                    const int lim = cl[c] ? pass1_max_clusters(c) : 0;
+                    if (cl[c] && lim > 0 && cl[c] > lim) fits = false;
+                }
+                if (fits) break;
+            }
+        }
     }
     for (int k = 0; k < n; ++k) {
         const edgc_compress_desc &d = descs[k];
