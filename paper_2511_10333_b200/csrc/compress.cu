@@ -1561,13 +1561,25 @@ k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
 
 // P_raw partials with the EF update fused in (4 < r <= 16, r_res <= BN, float4-aligned rows):
 // the K step's g and w tiles arrive together by cp.async, the step first applies
-// w <- g + (w - p_res q_resᵀ) in shared memory -- each thread a 4-row x 8-column block,
+// w <- g + (w - p_res q_resᵀ) in shared memory -- each thread 4-row x 4-column blocks,
 // products summed over s ascending exactly as k_ef, so w is bit-identical -- streams the
 // new w back to HBM, and then multiplies it into the P_raw partials as k_skinny<0> does.
 // One pass over w instead of two (12 B/elem for EF + P_raw instead of 16).
-// rows per fused CTA: 64 for 8-rank blocks (32 threads, 5 CTAs per SM by shared memory),
-// 128 for 16 (measured at r = 8: 64 / 128 / 256 rows 772 / 747 / 701 GB/s; r = 16: 611 / 630 / 573)
-constexpr int kSkEfRows8 = 64, kSkEfRows16 = 128;
+// rows per fused CTA: 64, the product split over KS thread groups (KS = 4 for 8-rank blocks,
+// 2 for 16: 128 threads, 128 registers, 4 CTAs per SM).  Measured (GPT2-2.5B, pass 1 per step):
+// r = 8 7.2 -> 5.6 ms (785 -> 901 GB/s; KS = 1 / 2 / 4: 9.4 / 5.9 / 5.6 ms, 96 registers at
+// 5 CTAs per SM 8.1 ms), r = 16 7.6 -> 7.1 ms (128 rows: KS = 1 / 2 7.6 / 7.4 ms).
+#ifndef EDGC_SKEF_ROWS16
+#define EDGC_SKEF_ROWS16 64
+#endif
+constexpr int kSkEfRows8 = 64, kSkEfRows16 = EDGC_SKEF_ROWS16;
+#ifndef EDGC_SKEF_KS8
+#define EDGC_SKEF_KS8 4
+#endif
+#ifndef EDGC_SKEF_KS16
+#define EDGC_SKEF_KS16 2
+#endif
+constexpr int kSkEfKS8 = EDGC_SKEF_KS8, kSkEfKS16 = EDGC_SKEF_KS16;   // product K-split (k_skinny_ef)
 // Q partials (k_skinny<1>) rows (columns j of w) per CTA
 #ifndef EDGC_SKQ_ROWS8
 #define EDGC_SKQ_ROWS8 256
@@ -1584,13 +1596,26 @@ struct SkEfSmem {
     float qt[BN][kSkK + 4];     // q_res rows of the K step, transposed
     float b[kSkK][BN + 4];      // q_warm rows of the K step
 };
-template <int BM, int BN>
-__global__ void __launch_bounds__((BM / 4) * (BN / 4))
+// KS: K-split of the product -- KS thread groups each multiply kSkK / KS columns of the step
+// into their own 4 x 4 register tiles (fp32 per step, folded into fp64), summed group by group
+// in fixed order at the end.  KS = 4 at 8-rank blocks: 128 threads per 64-row CTA instead of 32
+// (measured: 255 registers and 1.25 warps per scheduler at KS = 1, DRAM 50% -- latency bound).
+#ifndef EDGC_SKEF_THREADS_SM
+#define EDGC_SKEF_THREADS_SM 512   // K-split CTAs: registers capped for this many threads per SM (128 each)
+#endif
+template <int BM, int BN, int KS>
+__global__ void __launch_bounds__((BM / 4) * (BN / 4) * KS,
+                                  KS > 1 ? EDGC_SKEF_THREADS_SM / ((BM / 4) * (BN / 4) * KS) : 1)
 k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
-    constexpr int TX = BN / 4, NT = (BM / 4) * TX;
+    constexpr int TX = BN / 4, NG = (BM / 4) * TX, NT = NG * KS;
     constexpr int kAV = BM * kSkK / 4 / NT;          // float4 of one tile per thread
     constexpr int kBV = BN * kSkK / NT;               // q_warm / q_res elements of one K step per thread
-    constexpr int kEB = BM / NT;                      // 4 x 8 EF blocks per thread (BM*32 / 32 / NT)
+    constexpr int kCB = kSkK / 4;                     // 4-column EF blocks per row block
+    constexpr int kEB = (BM / 4) * kCB / NT;          // 4 x 4 EF blocks per thread
+    constexpr int kKG = kSkK / KS;                    // product columns per group and step
+    static_assert(kAV >= 1 && kBV >= 1 && kEB >= 1 && kKG % 4 == 0, "skinny EF thread layout");
+    static_assert(KS * BM * BN * (int)sizeof(double) <= (int)sizeof(float) * 2 * BM * (kSkK + 4),
+                  "K-split partials reuse the w stages");
     extern __shared__ __align__(16) unsigned char skef_raw[];
     SkEfSmem<BM, BN> &S = *reinterpret_cast<SkEfSmem<BM, BN> *>(skef_raw);
     const GemmTile t = tiles[blockIdx.x];
@@ -1599,7 +1624,7 @@ k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
     const int r = M.r, rres = M.r_res;
     float *__restrict__ w = M.w;
     const float *__restrict__ g = M.g;
-    const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+    const int tid = threadIdx.x, kg = tid / NG, tx = (tid % NG) % TX, ty = (tid % NG) / TX;
     for (int e = tid; e < BN * BM; e += NT) {
         const int s = e / BM, ii = e % BM;
         const int64_t gi = t.i0 + ii;
@@ -1650,50 +1675,47 @@ k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
         else tc::cp_async_wait<0>();
         __syncthreads();
         if (more) load_b(k0 + kSkK, b_next, q_next);
-        // EF on the tile: block (rows 4 rb .. +3, columns 8 cb .. +7)
+        // EF on the tile: block (rows 4 rb .. +3, columns 4 cb .. +3); a quarter warp covers
+        // one row's 8 blocks (128 contiguous bytes)
 #pragma unroll
         for (int eb = 0; eb < kEB; ++eb) {
-            const int bid = tid + eb * NT, rb = bid / 4, cb = bid % 4;
-            float c[4][8];
+            const int bid = tid + eb * NT, rb = bid / kCB, cb = bid % kCB;
+            float c[4][4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int v = 0; v < 8; ++v) c[u][v] = 0.f;
+                for (int v = 0; v < 4; ++v) c[u][v] = 0.f;
             for (int s2 = 0; s2 < rres; ++s2) {
                 const float4 a4 = *reinterpret_cast<const float4 *>(&S.pt[s2][rb * 4]);
-                const float4 q0 = *reinterpret_cast<const float4 *>(&S.qt[s2][cb * 8]);
-                const float4 q1 = *reinterpret_cast<const float4 *>(&S.qt[s2][cb * 8 + 4]);
+                const float4 q4 = *reinterpret_cast<const float4 *>(&S.qt[s2][cb * 4]);
                 const float a[4] = {a4.x, a4.y, a4.z, a4.w};
-                const float q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+                const float q[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
 #pragma unroll
-                    for (int v = 0; v < 8; ++v) c[u][v] = a[u] * q[v] + c[u][v];
+                    for (int v = 0; v < 4; ++v) c[u][v] = a[u] * q[v] + c[u][v];
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int ii = rb * 4 + u;
-                const int64_t gi = t.i0 + ii, gk = k0 + cb * 8;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    float4 *ap = reinterpret_cast<float4 *>(&S.a[buf][ii][cb * 8 + 4 * h]);
-                    const float4 w4 = *ap;
-                    const float4 g4 = *reinterpret_cast<const float4 *>(&S.g[buf][ii][cb * 8 + 4 * h]);
-                    const float x0 = g4.x + (w4.x - c[u][4 * h]), x1 = g4.y + (w4.y - c[u][4 * h + 1]);
-                    const float x2 = g4.z + (w4.z - c[u][4 * h + 2]), x3 = g4.w + (w4.w - c[u][4 * h + 3]);
-                    const float4 x = make_float4(x0, x1, x2, x3);
-                    *ap = x;
-                    if (gi < m && gk + 4 * h + 4 <= t.k1) {
-                        bad |= !(isfinite(x0) && isfinite(x1) && isfinite(x2) && isfinite(x3));
-                        __stcs(reinterpret_cast<float4 *>(w + gi * n + gk + 4 * h), x);
-                    }
+                const int64_t gi = t.i0 + ii, gk = k0 + cb * 4;
+                float4 *ap = reinterpret_cast<float4 *>(&S.a[buf][ii][cb * 4]);
+                const float4 w4 = *ap;
+                const float4 g4 = *reinterpret_cast<const float4 *>(&S.g[buf][ii][cb * 4]);
+                const float x0 = g4.x + (w4.x - c[u][0]), x1 = g4.y + (w4.y - c[u][1]);
+                const float x2 = g4.z + (w4.z - c[u][2]), x3 = g4.w + (w4.w - c[u][3]);
+                const float4 x = make_float4(x0, x1, x2, x3);
+                *ap = x;
+                if (gi < m && gk + 4 <= t.k1) {
+                    bad |= !(isfinite(x0) && isfinite(x1) && isfinite(x2) && isfinite(x3));
+                    __stcs(reinterpret_cast<float4 *>(w + gi * n + gk), x);
                 }
             }
         }
         __syncthreads();
         float accf[4][4] = {};
 #pragma unroll
-        for (int k4 = 0; k4 < kSkK; k4 += 4) {
+        for (int k4 = kg * kKG; k4 < (kg + 1) * kKG; k4 += 4) {
             float a[4][4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {   // rows ty + u BM/4: 8 rows of a warp on distinct banks
@@ -1716,14 +1738,36 @@ k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
             for (int v = 0; v < 4; ++v) acc[u][v] += (double)accf[u][v];
         __syncthreads();
     }
+    if (KS > 1) {
+        // group partials through the (now idle) w stages, summed in group order
+        double *red = reinterpret_cast<double *>(&S.a[0][0][0]);   // [KS][BM][BN]
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int64_t gi = t.i0 + ty + u * (BM / 4), gj = t.j0 + tx * 4 + v;
-            if (gi >= m || gj >= r) continue;
-            M.p_part[((int64_t)t.split * m + gi) * r + gj] = acc[u][v];
+            for (int v = 0; v < 4; ++v) red[((int64_t)kg * BM + ty + u * (BM / 4)) * BN + tx * 4 + v] = acc[u][v];
+        __syncthreads();
+        if (kg == 0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (int h = 0; h < KS; ++h) sum += red[((int64_t)h * BM + ty + u * (BM / 4)) * BN + tx * 4 + v];
+                    acc[u][v] = sum;
+                }
         }
+    }
+    if (kg == 0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int64_t gi = t.i0 + ty + u * (BM / 4), gj = t.j0 + tx * 4 + v;
+                if (gi >= m || gj >= r) continue;
+                M.p_part[((int64_t)t.split * m + gi) * r + gj] = acc[u][v];
+            }
+    }
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status + t.mat, 1);
 }
 
@@ -1747,12 +1791,12 @@ int launch_skinny(unsigned grid, cudaStream_t st, const MatDev *mats, const Gemm
     return EDGC_OK;
 }
 
-template <int BM, int BN>
+template <int BM, int BN, int KS>
 int launch_skinny_ef(unsigned grid, cudaStream_t st, const MatDev *mats, const GemmTile *tiles, int32_t *status) {
     static uint64_t attr = 0;
-    const int rc = smem_attr_once(k_skinny_ef<BM, BN>, (int)sizeof(SkEfSmem<BM, BN>), attr);
+    const int rc = smem_attr_once(k_skinny_ef<BM, BN, KS>, (int)sizeof(SkEfSmem<BM, BN>), attr);
     if (rc != EDGC_OK) return rc;
-    k_skinny_ef<BM, BN><<<grid, (BM / 4) * (BN / 4), sizeof(SkEfSmem<BM, BN>), st>>>(mats, tiles, status);
+    k_skinny_ef<BM, BN, KS><<<grid, (BM / 4) * (BN / 4) * KS, sizeof(SkEfSmem<BM, BN>), st>>>(mats, tiles, status);
     return EDGC_OK;
 }
 
@@ -2907,11 +2951,11 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if (!P.tcp[1].empty())
             EDGC_CUDA_TRY((tc::launch<128, 4>(TcPraw{P.d_mats, P.d_tcp[1], (int)P.tcp[1].size()}, sm_count(), st)));
         if (!P.spf[0].empty()) {
-            if ((rc = launch_skinny_ef<kSkEfRows8, 8>((unsigned)P.spf[0].size(), st, P.d_mats, P.d_spf[0], status_dev))) return rc;
+            if ((rc = launch_skinny_ef<kSkEfRows8, 8, kSkEfKS8>((unsigned)P.spf[0].size(), st, P.d_mats, P.d_spf[0], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if (!P.spf[1].empty()) {
-            if ((rc = launch_skinny_ef<kSkEfRows16, 16>((unsigned)P.spf[1].size(), st, P.d_mats, P.d_spf[1], status_dev))) return rc;
+            if ((rc = launch_skinny_ef<kSkEfRows16, 16, kSkEfKS16>((unsigned)P.spf[1].size(), st, P.d_mats, P.d_spf[1], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if (!P.sp[0].empty()) {
