@@ -1579,7 +1579,15 @@ constexpr int kSkEfRows8 = 64, kSkEfRows16 = EDGC_SKEF_ROWS16;
 #ifndef EDGC_SKEF_KS16
 #define EDGC_SKEF_KS16 2
 #endif
+#ifndef EDGC_SKEF_KS32
+#define EDGC_SKEF_KS32 1
+#endif
 constexpr int kSkEfKS8 = EDGC_SKEF_KS8, kSkEfKS16 = EDGC_SKEF_KS16;   // product K-split (k_skinny_ef)
+constexpr int kSkEfKS32 = EDGC_SKEF_KS32, kSkEfRows32 = 64;
+#ifndef EDGC_SKEF32_DEFAULT
+#define EDGC_SKEF32_DEFAULT 1
+#endif
+constexpr bool kSkEf32Default = EDGC_SKEF32_DEFAULT != 0;
 // Q partials (k_skinny<1>) rows (columns j of w) per CTA
 #ifndef EDGC_SKQ_ROWS8
 #define EDGC_SKQ_ROWS8 256
@@ -1603,9 +1611,13 @@ struct SkEfSmem {
 #ifndef EDGC_SKEF_THREADS_SM
 #define EDGC_SKEF_THREADS_SM 512   // K-split CTAs: registers capped for this many threads per SM (128 each)
 #endif
+#ifndef EDGC_SKEF32_THREADS_SM
+#define EDGC_SKEF32_THREADS_SM 384   // 64 x 32 tiles: 3 CTAs per SM at 168 registers (4 at 128 spill: 14.97 vs 11.65 ms at r = 32)
+#endif
 template <int BM, int BN, int KS>
 __global__ void __launch_bounds__((BM / 4) * (BN / 4) * KS,
-                                  KS > 1 ? EDGC_SKEF_THREADS_SM / ((BM / 4) * (BN / 4) * KS) : 1)
+                                  BN > 16 ? EDGC_SKEF32_THREADS_SM / ((BM / 4) * (BN / 4) * KS)
+                                  : KS > 1 ? EDGC_SKEF_THREADS_SM / ((BM / 4) * (BN / 4) * KS) : 1)
 k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
     constexpr int TX = BN / 4, NG = (BM / 4) * TX, NT = NG * KS;
     constexpr int kAV = BM * kSkK / 4 / NT;          // float4 of one tile per thread
@@ -1997,6 +2009,18 @@ bool skef_off() {
     return v;
 }
 
+// Ranks 16 < r <= 32 also take the fused CUDA-core EF + P_raw pass (64 x 32 tiles) instead of
+// the tcgen05 TcEF + TcPraw pair, with the multi-CTA factorisation (EDGC_SKEF32=0: tensor cores).
+// Measured on the GPT2-2.5B set: pass 1 at r = 24 12.3 -> 10.5 ms (410 -> 439 GB/s), r = 32
+// 12.4 -> 11.6 ms (393 -> 403 GB/s)
+bool skef32() {
+    static const bool v = [] {
+        const char *e = std::getenv("EDGC_SKEF32");
+        return e ? std::atoi(e) != 0 : kSkEf32Default;
+    }();
+    return v && !skef_off();
+}
+
 int tc_min_rank() {
     static const int v = [] {
         if (std::getenv("EDGC_NO_TC")) return 1 << 30;
@@ -2144,8 +2168,8 @@ struct Plan {
     int ef_rk = 0;                     // largest r_res of the CUDA-core EF tiles (gw)
     int tce_rk = 0;                    // largest r_res of the tcgen05 EF tiles (tce)
     std::vector<GemmTile> sp[3], sq[3];   // skinny P_raw / Q tiles: r <= 16 (256x16), <= 32 (128x32), <= 8 (256x8)
-    std::vector<GemmTile> spf[2];         // P_raw with the EF update fused: r <= 8 (x8), <= 16 (x16)
-    GemmTile *d_spf[2] = {};
+    std::vector<GemmTile> spf[3];         // P_raw with the EF update fused: r <= 8 (x8), <= 16 (x16), <= 32 (x32)
+    GemmTile *d_spf[3] = {};
     std::vector<GemmTile> tce, tcp[2], tcq[2];
     std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles
     int64_t nfxg64 = 0, nfxr64 = 0;   // the first n are 64-edge tiles, the rest kFxBig-edge   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
@@ -2283,9 +2307,11 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         const int64_t slots = d.n / M.vec;
         const int64_t threads1 = kP1Threads;
         M.wide = std::max(d.r, d.r_res) > narrow_max() ? 1 : 0;
-        M.tc = (M.wide && d.r > tc_min_rank()) ? 1 : 0;
+        // fused CUDA-core EF + P_raw up to rank 32 (EDGC_SKEF32) keeps those ranks off the tensor cores
+        const bool fuse32 = skef32() && M.al4 && d.r > 16 && d.r <= 32 && d.r_res <= 32;
+        M.tc = (M.wide && d.r > tc_min_rank() && !fuse32) ? 1 : 0;
         static const bool fx_off = std::getenv("EDGC_NO_FX") != nullptr;
-        M.fx = (M.wide && d.r >= 32 && (M.tc || d.r > 32) && !fx_off) ? 1 : 0;   // single P_raw chunk
+        M.fx = (M.wide && d.r >= 32 && (M.tc || d.r > 32 || fuse32) && !fx_off) ? 1 : 0;   // single P_raw chunk
         if (M.fx) {
             // Gram K splits: >= 512 rows, and few enough that [gsplit][r][r] fits in q_part when possible
             const int64_t want = std::max<int64_t>(512, ceil_div((int64_t)d.m * d.r, d.n));
@@ -2306,7 +2332,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         }
         // wide path K split of P_raw = w q_warm: 2048 columns up to r = 32; above, one K block
         // (the fp64 partials [nchunk1][m][r] scale with r while the tile count already suffices)
-        const int64_t k1 = (M.tc || d.r > 32) ? d.n : kWideSplitK;
+        const int64_t k1 = (M.tc || d.r > 32 || M.fx) ? d.n : kWideSplitK;
         M.nchunk1 = M.wide ? (int32_t)ceil_div(d.n, k1) : (int32_t)ceil_div(slots, threads1);
         // Q partials: 256-row K blocks, or 2048 for the wide path above r = 32 (the fp64
         // partials [nblk2][n][r] would otherwise take ~1 GB per GPT2-12.1B layer at r = 256)
@@ -2314,14 +2340,16 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.nblk2 = (int32_t)ceil_div(d.m, k2);
         if (M.wide) {
             // 4 < r <= 16, aligned, residual rank within the rank block: EF fused into P_raw
-            const int fbn = d.r <= 8 ? 8 : 16;
-            const bool fuse = !skef_off() && M.al4 && d.r > 4 && d.r <= 16 && d.r_res <= fbn && !M.tc;
+            const int fbn = d.r <= 8 ? 8 : (d.r <= 16 ? 16 : 32);
+            const bool fuse = !skef_off() && M.al4 && d.r > 4 && (d.r <= 16 || fuse32) && d.r_res <= fbn && !M.tc;
             if (fuse) {
+                const int fi = fbn == 8 ? 0 : (fbn == 16 ? 1 : 2);
+                const int rows = fbn == 8 ? kSkEfRows8 : (fbn == 16 ? kSkEfRows16 : kSkEfRows32);
                 for (int32_t c = 0; c < M.nchunk1; ++c)
-                    for (int64_t i0 = 0; i0 < d.m; i0 += (fbn == 8 ? kSkEfRows8 : kSkEfRows16))
-                        P.spf[fbn == 8 ? 0 : 1].push_back(GemmTile{k, c, i0, 0, c * k1, std::min(d.n, (c + 1) * k1)});
-                const int BM = fbn == 8 ? kSkQRows8 : kSkQRows16, BN = fbn;
-                std::vector<GemmTile> &tq = P.sq[fbn == 8 ? 2 : 0];
+                    for (int64_t i0 = 0; i0 < d.m; i0 += rows)
+                        P.spf[fi].push_back(GemmTile{k, c, i0, 0, c * k1, std::min(d.n, (c + 1) * k1)});
+                const int BM = fbn == 8 ? kSkQRows8 : (fbn == 16 ? kSkQRows16 : 128), BN = fbn;
+                std::vector<GemmTile> &tq = P.sq[fbn == 8 ? 2 : (fbn == 16 ? 0 : 1)];
                 for (int32_t b = 0; b < M.nblk2; ++b)
                     for (int64_t i0 = 0; i0 < d.n; i0 += BM)
                         for (int64_t j0 = 0; j0 < d.r; j0 += BN)
@@ -2413,7 +2441,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     for (int c = 1; c <= 8; ++c) P.d_tz[c] = a.take<ZTile>(P.tz[c].size());
     for (int c = 0; c < 3; ++c) {
         P.d_sp[c] = a.take<GemmTile>(P.sp[c].size());
-        if (c < 2) P.d_spf[c] = a.take<GemmTile>(P.spf[c].size());
+        P.d_spf[c] = a.take<GemmTile>(P.spf[c].size());
         P.d_sq[c] = a.take<GemmTile>(P.sq[c].size());
     }
     P.d_tce = a.take<GemmTile>(P.tce.size());
@@ -2916,7 +2944,7 @@ extern "C" int edgc_compress_plan_bind(edgc_compress_plan *h, void *ws, int64_t 
     EDGC_CUDA_TRY(upg(P.d_gq, P.gq));
     for (int c = 0; c < 3; ++c) {
         EDGC_CUDA_TRY(upg(P.d_sp[c], P.sp[c]));
-        if (c < 2) EDGC_CUDA_TRY(upg(P.d_spf[c], P.spf[c]));
+        EDGC_CUDA_TRY(upg(P.d_spf[c], P.spf[c]));
         EDGC_CUDA_TRY(upg(P.d_sq[c], P.sq[c]));
     }
     // the host staging vectors stay alive in the plan; make the upload complete
@@ -2956,6 +2984,10 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         }
         if (!P.spf[1].empty()) {
             if ((rc = launch_skinny_ef<kSkEfRows16, 16, kSkEfKS16>((unsigned)P.spf[1].size(), st, P.d_mats, P.d_spf[1], status_dev))) return rc;
+            EDGC_LAUNCH_CHECK();
+        }
+        if (!P.spf[2].empty()) {
+            if ((rc = launch_skinny_ef<kSkEfRows32, 32, kSkEfKS32>((unsigned)P.spf[2].size(), st, P.d_mats, P.d_spf[2], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if (!P.sp[0].empty()) {

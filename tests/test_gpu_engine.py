@@ -24,7 +24,7 @@ def _shapes():
     return [(256, 768), (256, 256), (256, 1024), (1024, 256), (48, 36), (7, 9)]
 
 
-@pytest.mark.parametrize("rank", [1, 4, 5, 6, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("rank", [1, 4, 5, 6, 8, 12, 16, 24, 32, 64, 128])
 def test_engine_matches_oracle_dp_step_chained(rank):
     from paper_2511_10333_b200.engine import BucketEngine
     shapes = _shapes()
@@ -55,6 +55,18 @@ def test_engine_narrow_passes_match_oracle(rank):
     register-tiled narrow passes (k_pass1 / k_pass2 with 8 ranks per thread)."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, EDGC_NARROW_MAX="8")
+    code = (f"import sys; sys.path.insert(0, {root!r}); "
+            f"from tests.test_gpu_engine import test_engine_matches_oracle_dp_step_chained as t; t({rank})")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+
+
+@pytest.mark.parametrize("rank", [24, 32])
+def test_engine_rank32_tensor_core_path_matches_oracle(rank):
+    """16 < r <= 32 take the fused CUDA-core EF + P_raw pass (k_skinny_ef, 64 x 32 tiles) by
+    default; EDGC_SKEF32=0 keeps them on the tcgen05 TcEF / TcPraw / TcQ kernels."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EDGC_SKEF32="0")
     code = (f"import sys; sys.path.insert(0, {root!r}); "
             f"from tests.test_gpu_engine import test_engine_matches_oracle_dp_step_chained as t; t({rank})")
     res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
