@@ -1596,6 +1596,13 @@ constexpr bool kSkEf32Default = EDGC_SKEF32_DEFAULT != 0;
 #define EDGC_SKQ_ROWS16 128   // measured r = 16: 128 / 256 / 512 rows 656 / 647 / 619 GB/s; r = 8 best at 256
 #endif
 constexpr int kSkQRows8 = EDGC_SKQ_ROWS8, kSkQRows16 = EDGC_SKQ_ROWS16;
+#ifndef EDGC_SKQ_K
+#define EDGC_SKQ_K 1024
+#endif
+// K (rows of w) per skinny Q tile = one fp64 partial [n][r] per block: 256 / 512 / 1024 / 2048 rows
+// measured (GPT2-2.5B, pass 2 + finalize): r = 8 2.16 / 1.92 / 1.86 / 1.87 ms, r = 16 3.03 / 2.74 /
+// 2.61 / 2.57, r = 32 5.70 / 5.10 / 4.81 / 4.69 (fewer fp64 partials to write and sum)
+constexpr int kSkQK = EDGC_SKQ_K;
 template <int BM, int BN>
 struct SkEfSmem {
     float a[2][BM][kSkK + 4];   // w -> x (new w) per stage
@@ -2336,7 +2343,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
         M.nchunk1 = M.wide ? (int32_t)ceil_div(d.n, k1) : (int32_t)ceil_div(slots, threads1);
         // Q partials: 256-row K blocks, or 2048 for the wide path above r = 32 (the fp64
         // partials [nblk2][n][r] would otherwise take ~1 GB per GPT2-12.1B layer at r = 256)
-        const int64_t k2 = (M.wide && (M.tc || d.r > 32)) ? d.m : kP2Rows;
+        const int64_t k2 = (M.wide && (M.tc || d.r > 32)) ? d.m : (M.wide ? (int64_t)kSkQK : kP2Rows);
         M.nblk2 = (int32_t)ceil_div(d.m, k2);
         if (M.wide) {
             // 4 < r <= 16, aligned, residual rank within the rank block: EF fused into P_raw
