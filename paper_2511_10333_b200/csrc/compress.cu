@@ -2716,6 +2716,13 @@ constexpr int kV4Rows = 8;
 #ifndef EDGC_RECON32_TROWS
 #define EDGC_RECON32_TROWS 512   // W r = 17..32 (64 / 128 / 256 / 512 rows at W = 8, r = 4: 4.79 / 4.20 / 3.92 / 3.79 ms)
 #endif
+// 512-column blocks per tile at W r = 17..32 (one P tile load for all of them; measured 1 / 2 /
+// 4 / 8 blocks: r = 32 at W = 1 4.34 / 4.15 / 4.07 / 4.32 ms, r = 4 at W = 8 3.74 / 3.68 / 3.68 /
+// 3.97 ms -- the FMA loop, not the P tile load, bounds this kernel)
+#ifndef EDGC_RECON_CB32
+#define EDGC_RECON_CB32 4
+#endif
+constexpr int v4_col_blocks(int wr) { return wr <= 16 ? 1 : EDGC_RECON_CB32; }
 __host__ __device__ constexpr int v4_tile_rows(int wr) {
     return wr <= 4 ? EDGC_RECON4_ROWS : wr <= 8 ? EDGC_RECON8_ROWS : wr <= 16 ? EDGC_RECON16_TROWS : EDGC_RECON32_TROWS;
 }
@@ -2741,8 +2748,6 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
     const RTile t = tiles[blockIdx.x];
     const ReconDev D = descs[t.d];
     const int r = D.r, wr = D.r * D.n_ranks;
-    const int64_t j0 = t.col0 + VC * threadIdx.x;
-    const bool active = j0 < t.col1;
     // rank w's P_k / Q_k in the gathered buffer
     auto p_of = [&](int w) -> const float * { return D.p + (int64_t)w * D.p_stride; };
     auto q_of = [&](int w) -> const float * { return D.q + (int64_t)w * D.q_stride; };
@@ -2758,6 +2763,13 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
     }
     for (int e = threadIdx.x; e < kV4TileRows * (WR - wr); e += NT)   // zero padding columns
         s_pT[wr + e / kV4TileRows][e % kV4TileRows] = 0.f;
+    __syncthreads();
+    // the tile may span several 512-column blocks (W r = 17..32): the P tile above is loaded
+    // once for all of them, each block reloads only its Q columns (registers)
+    auto block = [&](int64_t cb0) {
+    const int64_t j0 = cb0 + VC * threadIdx.x;
+    const bool active = j0 < t.col1;
+    if (!active) return;
     float q[VC][WR];
 #pragma unroll
     for (int v = 0; v < VC; ++v) {
@@ -2773,8 +2785,6 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
             }
         }
     }
-    __syncthreads();
-    if (!active) return;
     // rows per pass: 8, or EDGC_RECON32_ROWS for W*r = 32 (fewer live accumulators next to Q)
     constexpr int RP = WR == 32 ? EDGC_RECON32_ROWS : kV4Rows;
     for (int64_t row = t.row0; row < t.row1; row += RP) {
@@ -2810,6 +2820,12 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
                 __stcs(reinterpret_cast<float2 *>(D.out + i * D.ld_out + j0),
                        make_float2(acc[rr][0] * D.scale, acc[rr][VC > 1 ? 1 : 0] * D.scale));
         }
+    }
+    };
+    if (WR == 32) {
+        for (int64_t cb0 = t.col0; cb0 < t.col1; cb0 += kV4Cols) block(cb0);
+    } else {
+        block(t.col0);   // one column block per tile
     }
 }
 
@@ -3140,10 +3156,11 @@ int make_rplan(const edgc_recon_desc *descs, int n, void *ws, RPlan &P) {
         } else if (v4) {
             // the launch's kernel is chosen by the largest W r of the float4 tiles: its tile height
             // (shared-memory P tile) bounds every tile's rows
-            const int64_t tr = v4_tile_rows(wr4max <= 4 ? 4 : wr4max <= 8 ? 8 : wr4max <= 16 ? 16 : 32);
-            for (int64_t c0 = 0; c0 < s.n; c0 += kV4Cols)
+            const int wrc = wr4max <= 4 ? 4 : wr4max <= 8 ? 8 : wr4max <= 16 ? 16 : 32;
+            const int64_t tr = v4_tile_rows(wrc), tc = (int64_t)kV4Cols * v4_col_blocks(wrc);
+            for (int64_t c0 = 0; c0 < s.n; c0 += tc)
                 for (int64_t r0 = 0; r0 < s.m; r0 += tr)
-                    P.tiles4.push_back(RTile{k, c0, std::min(s.n, c0 + kV4Cols), r0, std::min(s.m, r0 + tr)});
+                    P.tiles4.push_back(RTile{k, c0, std::min(s.n, c0 + tc), r0, std::min(s.m, r0 + tr)});
         } else if (s.n % 4 == 0 && s.ld_out % 4 == 0 && ((uintptr_t)s.out % 16 == 0)) {
             for (int64_t r0 = 0; r0 < s.m; r0 += kGT)
                 for (int64_t c0 = 0; c0 < s.n; c0 += kGT)
