@@ -1439,6 +1439,32 @@ __global__ void __launch_bounds__(kGThreads) k_ef(const MatDev *mats, const Gemm
 constexpr int kSkK = 32;
 template <int OP, int BM>
 constexpr int skinny_smem() { return 2 * (OP == 0 ? BM * (kSkK + 4) : kSkK * (BM + 4)) * (int)sizeof(float); }
+// 4 x 4 register tile update acc[u][v] += a[u][c] b[v] (fp32 FMA per element, fixed order): on
+// FFMA2 the columns go in pairs with a[u][c] as the broadcast scalar operand (same rounding per
+// lane, half the FMA instructions)
+#ifndef EDGC_SKINNY_FFMA2
+#define EDGC_SKINNY_FFMA2 1
+#endif
+template <bool F2 = EDGC_SKINNY_FFMA2 != 0>
+__device__ __forceinline__ void skinny_fma4x4(float (&acc)[4][4], const float (&a)[4][4], int c, const float4 b4) {
+    if constexpr (F2) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const float2 lo = __ffma2_rn(make_float2(a[u][c], a[u][c]), make_float2(b4.x, b4.y),
+                                     make_float2(acc[u][0], acc[u][1]));
+        const float2 hi = __ffma2_rn(make_float2(a[u][c], a[u][c]), make_float2(b4.z, b4.w),
+                                     make_float2(acc[u][2], acc[u][3]));
+        acc[u][0] = lo.x; acc[u][1] = lo.y; acc[u][2] = hi.x; acc[u][3] = hi.y;
+    }
+    } else {
+    const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u][c], b[v], acc[u][v]);
+    }
+}
+
 template <int OP, int BM, int BN>
 __global__ void __launch_bounds__((BM / 4) * (BN / 4), 512 / ((BM / 4) * (BN / 4)))
 k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
@@ -1535,11 +1561,7 @@ k_skinny(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[k4 + c][tx * 4]);
-                const float b[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) accf[u][v] = fmaf(a[u][c], b[v], accf[u][v]);
+                skinny_fma4x4(accf, a, c, b4);
             }
         }
 #pragma unroll
@@ -1633,6 +1655,9 @@ k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
     constexpr int kEB = (BM / 4) * kCB / NT;          // 4 x 4 EF blocks per thread
     constexpr int kKG = kSkK / KS;                    // product columns per group and step
     static_assert(kAV >= 1 && kBV >= 1 && kEB >= 1 && kKG % 4 == 0, "skinny EF thread layout");
+    // FFMA2 tiles except at 16-rank blocks (there they spill at the 128-register cap: measured
+    // r = 16 pass 1 7.05 -> 8.19 ms; r = 8 / 32 gain 2%)
+    constexpr bool kF2 = EDGC_SKINNY_FFMA2 != 0 && BN != 16;
     static_assert(KS * BM * BN * (int)sizeof(double) <= (int)sizeof(float) * 2 * BM * (kSkK + 4),
                   "K-split partials reuse the w stages");
     extern __shared__ __align__(16) unsigned char skef_raw[];
@@ -1708,11 +1733,22 @@ k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
                 const float4 a4 = *reinterpret_cast<const float4 *>(&S.pt[s2][rb * 4]);
                 const float4 q4 = *reinterpret_cast<const float4 *>(&S.qt[s2][cb * 4]);
                 const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+                if constexpr (kF2) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 lo = __ffma2_rn(make_float2(a[u], a[u]), make_float2(q4.x, q4.y),
+                                                 make_float2(c[u][0], c[u][1]));
+                    const float2 hi = __ffma2_rn(make_float2(a[u], a[u]), make_float2(q4.z, q4.w),
+                                                 make_float2(c[u][2], c[u][3]));
+                    c[u][0] = lo.x; c[u][1] = lo.y; c[u][2] = hi.x; c[u][3] = hi.y;
+                }
+                } else {
                 const float q[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
 #pragma unroll
                     for (int v = 0; v < 4; ++v) c[u][v] = a[u] * q[v] + c[u][v];
+                }
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -1744,11 +1780,7 @@ k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const float4 b4 = *reinterpret_cast<const float4 *>(&S.b[k4 + c][tx * 4]);
-                const float b[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) accf[u][v] = fmaf(a[u][c], b[v], accf[u][v]);
+                skinny_fma4x4<kF2>(accf, a, c, b4);
             }
         }
 #pragma unroll
@@ -2732,6 +2764,11 @@ __host__ __device__ constexpr int v4_tile_rows(int wr) {
 #ifndef EDGC_RECON32_ROWS
 #define EDGC_RECON32_ROWS 8
 #endif
+// W r from which k_recon4 multiplies on FFMA2 (measured W r = 32: r = 4 at W = 8 3.68 -> 2.79 ms,
+// r = 32 at W = 1 4.06 -> 3.29 ms)
+#ifndef EDGC_RECON_FFMA2_MIN
+#define EDGC_RECON_FFMA2_MIN 8
+#endif
 #ifndef EDGC_RECON32_MINB
 #define EDGC_RECON32_MINB 2   // CTAs per SM for W*r = 32 (2 caps registers at 128: Q partly spills)
 #endif
@@ -2795,6 +2832,39 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
 #pragma unroll
             for (int v = 0; v < VC; ++v) acc[rr][v] = 0.f;
         // per output the fma order over (worker, k) is c ascending
+        if constexpr (WR >= EDGC_RECON_FFMA2_MIN && VC % 2 == 0) {
+            // paired columns on the packed FP32 pipe (FFMA2 with the P value as a broadcast scalar
+            // operand: same rounding per lane, half the FMA instructions to issue)
+            float2 acc2[RP][VC / 2];
+#pragma unroll
+            for (int rr = 0; rr < RP; ++rr)
+#pragma unroll
+                for (int v = 0; v < VC / 2; ++v) acc2[rr][v] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int c = 0; c < WR; ++c) {
+                float pr[RP];
+#pragma unroll
+                for (int h = 0; h < RP; h += 4) {
+                    const float4 pa = *reinterpret_cast<const float4 *>(&s_pT[c][lr + h]);
+                    pr[h] = pa.x; pr[h + 1] = pa.y; pr[h + 2] = pa.z; pr[h + 3] = pa.w;
+                }
+#pragma unroll
+                for (int v = 0; v < VC / 2; ++v) {
+                    const float2 qc = make_float2(q[2 * v][c], q[2 * v + 1][c]);
+#pragma unroll
+                    for (int rr = 0; rr < RP; ++rr)
+                        acc2[rr][v] = __ffma2_rn(make_float2(pr[rr], pr[rr]), qc, acc2[rr][v]);
+                }
+            }
+#pragma unroll
+            for (int rr = 0; rr < RP; ++rr)
+#pragma unroll
+                for (int v = 0; v < VC / 2; ++v) {
+                    acc[rr][2 * v] = acc2[rr][v].x;
+                    acc[rr][2 * v + 1] = acc2[rr][v].y;
+                }
+        } else
+        {
 #pragma unroll
         for (int c = 0; c < WR; ++c) {
             float pr[RP];
@@ -2807,6 +2877,7 @@ __global__ void __launch_bounds__(kV4Cols / VC, VC == 2 ? EDGC_RECON32_MINB : 1)
             for (int rr = 0; rr < RP; ++rr)
 #pragma unroll
                 for (int v = 0; v < VC; ++v) acc[rr][v] = fmaf(pr[rr], q[v][c], acc[rr][v]);
+        }
         }
 #pragma unroll
         for (int rr = 0; rr < RP; ++rr) {
