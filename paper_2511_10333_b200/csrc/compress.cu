@@ -1640,12 +1640,21 @@ struct SkEfSmem {
 #ifndef EDGC_SKEF_THREADS_SM
 #define EDGC_SKEF_THREADS_SM 512   // K-split CTAs: registers capped for this many threads per SM (128 each)
 #endif
+// 16-rank blocks: 4 CTAs per SM on FFMA measured best (3 CTAs at 168 registers, with or without
+// FFMA2: r = 16 pass 1 7.12 -> 7.45 ms; tools/probe_skef16.sh)
+#ifndef EDGC_SKEF16_THREADS_SM
+#define EDGC_SKEF16_THREADS_SM 512
+#endif
+#ifndef EDGC_SKEF16_FFMA2
+#define EDGC_SKEF16_FFMA2 0
+#endif
 #ifndef EDGC_SKEF32_THREADS_SM
 #define EDGC_SKEF32_THREADS_SM 384   // 64 x 32 tiles: 3 CTAs per SM at 168 registers (4 at 128 spill: 14.97 vs 11.65 ms at r = 32)
 #endif
 template <int BM, int BN, int KS>
 __global__ void __launch_bounds__((BM / 4) * (BN / 4) * KS,
                                   BN > 16 ? EDGC_SKEF32_THREADS_SM / ((BM / 4) * (BN / 4) * KS)
+                                  : BN == 16 ? EDGC_SKEF16_THREADS_SM / ((BM / 4) * (BN / 4) * KS)
                                   : KS > 1 ? EDGC_SKEF_THREADS_SM / ((BM / 4) * (BN / 4) * KS) : 1)
 k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
     constexpr int TX = BN / 4, NG = (BM / 4) * TX, NT = NG * KS;
@@ -1657,7 +1666,7 @@ k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
     static_assert(kAV >= 1 && kBV >= 1 && kEB >= 1 && kKG % 4 == 0, "skinny EF thread layout");
     // FFMA2 tiles except at 16-rank blocks (there they spill at the 128-register cap: measured
     // r = 16 pass 1 7.05 -> 8.19 ms; r = 8 / 32 gain 2%)
-    constexpr bool kF2 = EDGC_SKINNY_FFMA2 != 0 && BN != 16;
+    constexpr bool kF2 = EDGC_SKINNY_FFMA2 != 0 && (BN != 16 || EDGC_SKEF16_FFMA2 != 0);
     static_assert(KS * BM * BN * (int)sizeof(double) <= (int)sizeof(float) * 2 * BM * (kSkK + 4),
                   "K-split partials reuse the w stages");
     extern __shared__ __align__(16) unsigned char skef_raw[];
