@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2 closing validation on 1 GPU: full GPU suite, smoke, driver-like bench lines (ours + reference arm), launch list
-mkdir -p gpurun_out/f3
-O=gpurun_out/f3
+mkdir -p gpurun_out/f4
+O=gpurun_out/f4
 timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
 timeout 900 python bench.py > $O/bench_default.log 2>&1
