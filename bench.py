@@ -420,7 +420,10 @@ def run_ours(args):
     traffic = (load_traffic({"pass1": "k_pass1t", "pass2_finalize": "k_pass2", "reconstruct": "k_recon4"}[dom])
                if args.rank <= 4 else None)
     tensor = None
-    if args.rank > 16:
+    # ranks up to 32 run on CUDA cores (HBM roofline above); the tcgen05 path above 32, or above
+    # 16 with EDGC_SKEF32=0
+    tc_min = 16 if os.environ.get("EDGC_SKEF32", "1") == "0" else 32
+    if args.rank > tc_min:
         # wide path on tcgen05 (3xTF32: three MMAs per product): the bound is the tensor pipe.
         # tensor FLOP per phase: pass 1 = EF update (2 N r_res) + P_raw (2 N r); pass 2 = Q (2 N r);
         # reconstruct = 2 N (W r); x3 for the hi/lo split
