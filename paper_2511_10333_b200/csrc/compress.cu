@@ -1617,7 +1617,10 @@ constexpr bool kSkEf32Default = EDGC_SKEF32_DEFAULT != 0;
 #ifndef EDGC_SKQ_ROWS16
 #define EDGC_SKQ_ROWS16 128   // measured r = 16: 128 / 256 / 512 rows 656 / 647 / 619 GB/s; r = 8 best at 256
 #endif
-constexpr int kSkQRows8 = EDGC_SKQ_ROWS8, kSkQRows16 = EDGC_SKQ_ROWS16;
+#ifndef EDGC_SKQ_ROWS32
+#define EDGC_SKQ_ROWS32 128   // measured r = 32 pass 2: 64 / 128 / 256 rows 4.50 / 4.53 / 5.42 ms
+#endif
+constexpr int kSkQRows8 = EDGC_SKQ_ROWS8, kSkQRows16 = EDGC_SKQ_ROWS16, kSkQRows32 = EDGC_SKQ_ROWS32;
 #ifndef EDGC_SKQ_K
 #define EDGC_SKQ_K 1024
 #endif
@@ -2396,7 +2399,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                 for (int32_t c = 0; c < M.nchunk1; ++c)
                     for (int64_t i0 = 0; i0 < d.m; i0 += rows)
                         P.spf[fi].push_back(GemmTile{k, c, i0, 0, c * k1, std::min(d.n, (c + 1) * k1)});
-                const int BM = fbn == 8 ? kSkQRows8 : (fbn == 16 ? kSkQRows16 : 128), BN = fbn;
+                const int BM = fbn == 8 ? kSkQRows8 : (fbn == 16 ? kSkQRows16 : kSkQRows32), BN = fbn;
                 std::vector<GemmTile> &tq = P.sq[fbn == 8 ? 2 : (fbn == 16 ? 0 : 1)];
                 for (int32_t b = 0; b < M.nblk2; ++b)
                     for (int64_t i0 = 0; i0 < d.n; i0 += BM)
@@ -2432,7 +2435,7 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
                 for (int64_t i0 = 0; i0 < d.m; i0 += BM)
                     for (int64_t j0 = 0; j0 < d.r; j0 += BN)
                         tp.push_back(GemmTile{k, c, i0, j0, c * k1, std::min(d.n, (c + 1) * k1)});
-            const int QBM = cfg == 2 ? kSkQRows8 : (cfg == 0 ? kSkQRows16 : BM);
+            const int QBM = cfg == 2 ? kSkQRows8 : (cfg == 0 ? kSkQRows16 : (cfg == 1 ? kSkQRows32 : BM));
             for (int32_t b = 0; b < M.nblk2; ++b)
                 for (int64_t i0 = 0; i0 < d.n; i0 += QBM)
                     for (int64_t j0 = 0; j0 < d.r; j0 += BN)
@@ -3138,7 +3141,7 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
             EDGC_LAUNCH_CHECK();
         }
         if (!P.sq[1].empty()) {
-            if ((rc = launch_skinny<1, 128, 32>((unsigned)P.sq[1].size(), st, P.d_mats, P.d_sq[1], status_dev))) return rc;
+            if ((rc = launch_skinny<1, kSkQRows32, 32>((unsigned)P.sq[1].size(), st, P.d_mats, P.d_sq[1], status_dev))) return rc;
             EDGC_LAUNCH_CHECK();
         }
         if (!P.sq[2].empty()) {
