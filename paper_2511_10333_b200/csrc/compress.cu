@@ -1648,8 +1648,10 @@ struct SkEfSmem {
 #ifndef EDGC_SKEF16_THREADS_SM
 #define EDGC_SKEF16_THREADS_SM 512
 #endif
+// FFMA2 at 16-rank blocks: bit 0 the product tiles (they spill at the 128-register cap: pass 1
+// 7.2 -> 7.6 ms), bit 1 the EF blocks (7.2 -> 7.1 ms at r = 16, 6.80 -> 6.73 at r = 12)
 #ifndef EDGC_SKEF16_FFMA2
-#define EDGC_SKEF16_FFMA2 0
+#define EDGC_SKEF16_FFMA2 2
 #endif
 #ifndef EDGC_SKEF32_THREADS_SM
 #define EDGC_SKEF32_THREADS_SM 384   // 64 x 32 tiles: 3 CTAs per SM at 168 registers (4 at 128 spill: 14.97 vs 11.65 ms at r = 32)
@@ -1669,7 +1671,8 @@ k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
     static_assert(kAV >= 1 && kBV >= 1 && kEB >= 1 && kKG % 4 == 0, "skinny EF thread layout");
     // FFMA2 tiles except at 16-rank blocks (there they spill at the 128-register cap: measured
     // r = 16 pass 1 7.05 -> 8.19 ms; r = 8 / 32 gain 2%)
-    constexpr bool kF2 = EDGC_SKINNY_FFMA2 != 0 && (BN != 16 || EDGC_SKEF16_FFMA2 != 0);
+    constexpr bool kF2 = EDGC_SKINNY_FFMA2 != 0 && (BN != 16 || (EDGC_SKEF16_FFMA2 & 1) != 0);   // product tiles
+    constexpr bool kF2E = EDGC_SKINNY_FFMA2 != 0 && (BN != 16 || (EDGC_SKEF16_FFMA2 & 2) != 0);  // EF blocks
     static_assert(KS * BM * BN * (int)sizeof(double) <= (int)sizeof(float) * 2 * BM * (kSkK + 4),
                   "K-split partials reuse the w stages");
     extern __shared__ __align__(16) unsigned char skef_raw[];
@@ -1745,7 +1748,7 @@ k_skinny_ef(const MatDev *mats, const GemmTile *tiles, int32_t *status) {
                 const float4 a4 = *reinterpret_cast<const float4 *>(&S.pt[s2][rb * 4]);
                 const float4 q4 = *reinterpret_cast<const float4 *>(&S.qt[s2][cb * 4]);
                 const float a[4] = {a4.x, a4.y, a4.z, a4.w};
-                if constexpr (kF2) {
+                if constexpr (kF2E) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const float2 lo = __ffma2_rn(make_float2(a[u], a[u]), make_float2(q4.x, q4.y),
