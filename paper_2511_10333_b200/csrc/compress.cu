@@ -907,7 +907,8 @@ __device__ void right_mul(const double *src, const double *T, int64_t m, int r, 
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, int32_t *status, double col_tol) {
+__global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, int32_t *status, double col_tol,
+                                                           int32_t *any_fb) {
     const MatDev &M = mats[blockIdx.x];
     if ((status[blockIdx.x] & 1) || M.fx) return;
     const int r = M.r;
@@ -981,7 +982,10 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, i
     // small (Z path: <= 64, which the Z trick needs anyway; otherwise <= 1000 -> < 1e-6)
     const double kappa = sqrt(rn2 * tn2);
     const bool single = kappa <= (M.zmode ? kKappaMax : 1000.0);
-    if (M.zmode && !single && tid == 0) atomicOr(status + blockIdx.x, 2);
+    if (M.zmode && !single && tid == 0) {
+        atomicOr(status + blockIdx.x, 2);
+        atomicOr(any_fb, 1);   // k_pass2 runs its tiles only if some matrix needs it
+    }
     if (single) {
         right_mul(M.p_raw, T1, m, r, nullptr, M.p_out);
         for (int e = tid; e < r * r; e += kFactorThreads) M.tmat[e] = T1[e];
@@ -2097,7 +2101,11 @@ int tc_ef_min_rank() {
 // Q partial over this tile's rows: thread owns VEC columns x RMAX ranks;
 // fp32 FMA over 32-row groups, fp64 across groups.
 template <int VEC, int RMAX>
-__global__ void __launch_bounds__(kP2Threads, VEC == 2 ? 3 : 1) k_pass2(const MatDev *mats, const Tile *tiles, const int32_t *status) {
+__global__ void __launch_bounds__(kP2Threads, VEC == 2 ? 3 : 1) k_pass2(const MatDev *mats, const Tile *tiles, const int32_t *status,
+                                                                          const int32_t *any_fb) {
+    // one independent load first: with every matrix on the Z path and none falling back (the
+    // steady state) each CTA leaves here instead of after three dependent descriptor loads
+    if (*any_fb == 0) return;
     const Tile t = tiles[blockIdx.x];
     const MatDev &M = mats[t.mat];
     const int st = status[t.mat];
@@ -2238,6 +2246,8 @@ struct Plan {
     FxTile *d_fxg = nullptr, *d_fxr = nullptr;
     int rmax4 = 0, rmax1 = 0;
     SampDev *d_samp = nullptr;          // fused sampling descriptors (workspace)
+    int32_t *d_anyfb = nullptr;         // k_pass2 gate: nonzero if some matrix needs pass 2 this step
+    bool pass2_always = false;          // some k_pass2 tile belongs to a matrix off the Z path
     std::vector<SampDev> samp_host;
     bool sample_armed = false;
     int64_t sample_slots = 0;           // partial slots per matrix (0: some matrix off the Z path)
@@ -2508,6 +2518,10 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     P.d_gw = a.take<GemmTile>(P.gw.size());
     P.d_gp = a.take<GemmTile>(P.gp.size());
     P.d_gq = a.take<GemmTile>(P.gq.size());
+    P.d_anyfb = a.take<int32_t>(1);
+    P.pass2_always = false;
+    for (int k = 0; k < n; ++k)
+        if (!P.mats[k].wide && !P.mats[k].zmode) P.pass2_always = true;
     P.bytes = a.off;
     return EDGC_OK;
 }
@@ -2629,10 +2643,10 @@ int launch_pass2(const Plan &P, bool v4, const int32_t *status, cudaStream_t st)
     if (h.empty()) return EDGC_OK;
     const unsigned grid = (unsigned)h.size();
     const int rmax = v4 ? P.rmax4 : P.rmax1;
-    if (v4 && rmax <= 4) k_pass2<4, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
-    else if (v4) k_pass2<2, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
-    else if (rmax <= 4) k_pass2<1, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
-    else k_pass2<1, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status);
+    if (v4 && rmax <= 4) k_pass2<4, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb);
+    else if (v4) k_pass2<2, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb);
+    else if (rmax <= 4) k_pass2<1, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb);
+    else k_pass2<1, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }
@@ -3114,7 +3128,8 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if ((rc = launch_gemm<0>(P, P.gp, P.d_gp, status_dev, st))) return rc;
     }
     if (phases & EDGC_PHASE_FACTOR) {
-        k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol);
+        EDGC_CUDA_TRY(cudaMemsetAsync(P.d_anyfb, P.pass2_always ? 1 : 0, sizeof(int32_t), st));
+        k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol, P.d_anyfb);
         EDGC_LAUNCH_CHECK();
         if (!P.fxg.empty()) {
             const unsigned g64 = (unsigned)P.nfxg64, gbig = (unsigned)(P.fxg.size() - P.nfxg64);
