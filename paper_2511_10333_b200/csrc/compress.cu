@@ -908,7 +908,7 @@ __device__ void right_mul(const double *src, const double *T, int64_t m, int r, 
 }
 
 __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, int32_t *status, double col_tol,
-                                                           int32_t *any_fb) {
+                                                           int32_t *any_fb, int32_t epoch) {
     const MatDev &M = mats[blockIdx.x];
     if ((status[blockIdx.x] & 1) || M.fx) return;
     const int r = M.r;
@@ -984,7 +984,7 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const MatDev *mats, i
     const bool single = kappa <= (M.zmode ? kKappaMax : 1000.0);
     if (M.zmode && !single && tid == 0) {
         atomicOr(status + blockIdx.x, 2);
-        atomicOr(any_fb, 1);   // k_pass2 runs its tiles only if some matrix needs it
+        *any_fb = epoch;   // k_pass2 runs its tiles only if some matrix needs it this run
     }
     if (single) {
         right_mul(M.p_raw, T1, m, r, nullptr, M.p_out);
@@ -2102,10 +2102,11 @@ int tc_ef_min_rank() {
 // fp32 FMA over 32-row groups, fp64 across groups.
 template <int VEC, int RMAX>
 __global__ void __launch_bounds__(kP2Threads, VEC == 2 ? 3 : 1) k_pass2(const MatDev *mats, const Tile *tiles, const int32_t *status,
-                                                                          const int32_t *any_fb) {
-    // one independent load first: with every matrix on the Z path and none falling back (the
-    // steady state) each CTA leaves here instead of after three dependent descriptor loads
-    if (*any_fb == 0) return;
+                                                                          const int32_t *any_fb, int32_t epoch) {
+    // one independent load first: with every matrix on the Z path and none falling back this
+    // run (the steady state) each CTA leaves here instead of after three dependent descriptor
+    // loads.  epoch 0: some tile is off the Z path, always run
+    if (epoch != 0 && *any_fb != epoch) return;
     const Tile t = tiles[blockIdx.x];
     const MatDev &M = mats[t.mat];
     const int st = status[t.mat];
@@ -2163,17 +2164,21 @@ __global__ void __launch_bounds__(kP2Threads, VEC == 2 ? 3 : 1) k_pass2(const Ma
 // ---------------------------------------------------------------- finalize
 // One thread per Q element (j, k): the Z (or Q) partials of every strip summed in a fixed
 // order (deterministic), then Q = Z T through shared memory.  Sized by n r so a single
-// matrix still spreads over the GPU.
+// matrix still spreads over the GPU; one flat grid over the plan's (matrix, 256-element block)
+// pairs (the former [max n r / 256] x matrices grid was mostly empty CTAs: 85 -> 73 us per
+// GPT2-2.5B step).
 constexpr int kFinThreads = 256;
-__global__ void __launch_bounds__(kFinThreads) k_finalize(const MatDev *mats, const int32_t *status) {
-    const MatDev &M = mats[blockIdx.y];
-    const int st = status[blockIdx.y];
+__global__ void __launch_bounds__(kFinThreads) k_finalize(const MatDev *mats, const int2 *fin, const int32_t *status) {
+    // (matrix, block of 256 Q elements): from the flat table, or (y, x) of a one-matrix grid
+    const int2 fb = fin ? fin[blockIdx.x] : make_int2((int)blockIdx.y, (int)blockIdx.x);
+    const MatDev &M = mats[fb.x];
+    const int st = status[fb.x];
     if (st & 1) return;
     const int r = M.r;
     const int64_t n = M.n;
     const bool zq = M.zmode && !(st & 2);
-    const int64_t e = (int64_t)blockIdx.x * kFinThreads + threadIdx.x;
-    if ((int64_t)blockIdx.x * kFinThreads >= n * r) return;   // whole CTA past this matrix
+    const int64_t e = (int64_t)fb.y * kFinThreads + threadIdx.x;
+    if ((int64_t)fb.y * kFinThreads >= n * r) return;   // whole CTA past this matrix
     const bool live = e < n * r;
     const int64_t j = e / r;
     const int k = (int)(e % r);
@@ -2182,6 +2187,13 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(const MatDev *mats, co
     double z = 0.0;
     if (live) {
         int b = 0;
+        for (; b + 8 <= nb; b += 8) {   // eight strips' loads in flight, summed in strip order
+            double zz[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) zz[u] = part[((int64_t)(b + u) * n + j) * r + k];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) z += zz[u];
+        }
         for (; b + 4 <= nb; b += 4) {   // four strips' loads in flight, summed in strip order
             const double z0 = part[((int64_t)b * n + j) * r + k], z1 = part[((int64_t)(b + 1) * n + j) * r + k];
             const double z2 = part[((int64_t)(b + 2) * n + j) * r + k], z3 = part[((int64_t)(b + 3) * n + j) * r + k];
@@ -2236,7 +2248,9 @@ struct Plan {
     std::vector<FxTile> fxg, fxr;     // multi-CTA factorisation: Gram tiles, right-multiplication tiles
     int64_t nfxg64 = 0, nfxr64 = 0;   // the first n are 64-edge tiles, the rest kFxBig-edge   // tensor-core EF tiles (128x128), P_raw / Q tiles (BN 64, 128)
     int64_t bytes = 0;
-    int64_t max_nr = 1;                // largest n r of the plan (k_finalize grid)
+    int64_t max_nr = 1;                // largest n r of the plan
+    std::vector<int2> fin;             // k_finalize grid: (matrix, 256-element block) pairs
+    int2 *d_fin = nullptr;
     MatDev *d_mats = nullptr;
     Tile *d_t1v4 = nullptr, *d_t1v1 = nullptr, *d_t2v4 = nullptr, *d_t2v1 = nullptr;
     ZTile *d_tz[9] = {};
@@ -2246,8 +2260,9 @@ struct Plan {
     FxTile *d_fxg = nullptr, *d_fxr = nullptr;
     int rmax4 = 0, rmax1 = 0;
     SampDev *d_samp = nullptr;          // fused sampling descriptors (workspace)
-    int32_t *d_anyfb = nullptr;         // k_pass2 gate: nonzero if some matrix needs pass 2 this step
+    int32_t *d_anyfb = nullptr;         // k_pass2 gate: the run's epoch if some matrix fell back
     bool pass2_always = false;          // some k_pass2 tile belongs to a matrix off the Z path
+    int32_t epoch = 0;                  // run counter (factor phase), from 1; no memset per run
     std::vector<SampDev> samp_host;
     bool sample_armed = false;
     int64_t sample_slots = 0;           // partial slots per matrix (0: some matrix off the Z path)
@@ -2519,6 +2534,10 @@ int make_plan(const edgc_compress_desc *descs, int n, void *ws, int64_t ws_bytes
     P.d_gp = a.take<GemmTile>(P.gp.size());
     P.d_gq = a.take<GemmTile>(P.gq.size());
     P.d_anyfb = a.take<int32_t>(1);
+    for (int k = 0; k < n; ++k)
+        for (int64_t b = 0; b < ceil_div(descs[k].n * (int64_t)descs[k].r, kFinThreads); ++b)
+            P.fin.push_back(make_int2(k, (int)b));
+    P.d_fin = a.take<int2>(P.fin.size());
     P.pass2_always = false;
     for (int k = 0; k < n; ++k)
         if (!P.mats[k].wide && !P.mats[k].zmode) P.pass2_always = true;
@@ -2643,10 +2662,10 @@ int launch_pass2(const Plan &P, bool v4, const int32_t *status, cudaStream_t st)
     if (h.empty()) return EDGC_OK;
     const unsigned grid = (unsigned)h.size();
     const int rmax = v4 ? P.rmax4 : P.rmax1;
-    if (v4 && rmax <= 4) k_pass2<4, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb);
-    else if (v4) k_pass2<2, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb);
-    else if (rmax <= 4) k_pass2<1, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb);
-    else k_pass2<1, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb);
+    if (v4 && rmax <= 4) k_pass2<4, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb, P.pass2_always ? 0 : P.epoch);
+    else if (v4) k_pass2<2, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb, P.pass2_always ? 0 : P.epoch);
+    else if (rmax <= 4) k_pass2<1, 4><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb, P.pass2_always ? 0 : P.epoch);
+    else k_pass2<1, 8><<<grid, kP2Threads, 0, st>>>(P.d_mats, d, status, P.d_anyfb, P.pass2_always ? 0 : P.epoch);
     EDGC_LAUNCH_CHECK();
     return EDGC_OK;
 }
@@ -3070,6 +3089,9 @@ extern "C" int edgc_compress_plan_bind(edgc_compress_plan *h, void *ws, int64_t 
         EDGC_CUDA_TRY(upg(P.d_spf[c], P.spf[c]));
         EDGC_CUDA_TRY(upg(P.d_sq[c], P.sq[c]));
     }
+    if (!P.fin.empty())
+        EDGC_CUDA_TRY(cudaMemcpyAsync(P.d_fin, P.fin.data(), sizeof(int2) * P.fin.size(), cudaMemcpyHostToDevice, st));
+    EDGC_CUDA_TRY(cudaMemsetAsync(P.d_anyfb, 0, sizeof(int32_t), st));   // epochs start at 1
     // the host staging vectors stay alive in the plan; make the upload complete
     // before the caller could destroy or rebind it
     EDGC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -3128,8 +3150,8 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
         if ((rc = launch_gemm<0>(P, P.gp, P.d_gp, status_dev, st))) return rc;
     }
     if (phases & EDGC_PHASE_FACTOR) {
-        EDGC_CUDA_TRY(cudaMemsetAsync(P.d_anyfb, P.pass2_always ? 1 : 0, sizeof(int32_t), st));
-        k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol, P.d_anyfb);
+        h->P.epoch = P.epoch == INT32_MAX ? 1 : P.epoch + 1;
+        k_factor<<<n, kFactorThreads, 0, st>>>(P.d_mats, status_dev, col_tol, P.d_anyfb, P.epoch);
         EDGC_LAUNCH_CHECK();
         if (!P.fxg.empty()) {
             const unsigned g64 = (unsigned)P.nfxg64, gbig = (unsigned)(P.fxg.size() - P.nfxg64);
@@ -3173,7 +3195,12 @@ extern "C" int edgc_compress_plan_run(edgc_compress_plan *h, double col_tol, int
             EDGC_CUDA_TRY((tc::launch<128, 4>(TcQ{P.d_mats, P.d_tcq[1], status_dev, (int)P.tcq[1].size()}, sm_count(), st)));
     }
     if (phases & EDGC_PHASE_FINALIZE) {
-        k_finalize<<<dim3((unsigned)ceil_div(P.max_nr, kFinThreads), n), kFinThreads, 0, st>>>(P.d_mats, status_dev);
+        // one matrix (the per-matrix API): its blocks directly (measured 4 us faster there than
+        // the table lookup); several: the flat table
+        if (n == 1)
+            k_finalize<<<(unsigned)P.fin.size(), kFinThreads, 0, st>>>(P.d_mats, nullptr, status_dev);
+        else
+            k_finalize<<<(unsigned)P.fin.size(), kFinThreads, 0, st>>>(P.d_mats, P.d_fin, status_dev);
         EDGC_LAUNCH_CHECK();
     }
     return EDGC_OK;
